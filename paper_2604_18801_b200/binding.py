@@ -1,0 +1,287 @@
+"""ctypes binding of libcc (include/cc.h).  Same names as the C ABI; torch tensors in, torch
+tensors out.  Marshalling only."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import asdict, dataclass
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(HERE, "libcc.so")
+
+CC_OK, CC_NOT_CONVERGED = 0, 2
+CC_ORIG, CC_DECOMP, CC_CORR = 0, 1, 2
+STOP_ACTIVE, STOP_EPS, STOP_NONE = 0, 1, 2
+CC_RUN_HOST = 1
+_STATUS = {0: "CC_OK", 2: "CC_NOT_CONVERGED", 64: "CC_E_ARG", 65: "CC_E_DATA", 66: "CC_E_BOUND",
+           67: "CC_E_OOM", 68: "CC_E_CUDA", 69: "CC_E_NCCL", 70: "CC_E_STATE"}
+
+
+class CCError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Params(C.Structure):
+    _fields_ = [("box", C.c_double), ("periodic", C.c_int), ("b", C.c_double), ("eta", C.c_double),
+                ("xi", C.c_double), ("m", C.c_int), ("alpha", C.c_double), ("beta1", C.c_double),
+                ("beta2", C.c_double), ("eps_adam", C.c_double), ("t_max", C.c_int), ("eps_loss", C.c_double),
+                ("stop_mode", C.c_int), ("optimizer", C.c_int), ("vanilla_step", C.c_double),
+                ("graph_batch", C.c_int), ("cells_per_particle", C.c_double), ("profile", C.c_int)]
+
+
+class _Dist(C.Structure):
+    _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("nccl_id_h", C.c_void_p)]
+
+
+class _VP(C.Structure):
+    _fields_ = [("n_pairs", C.c_int64), ("n_editable", C.c_int64), ("n_linked", C.c_int64),
+                ("n_violated0", C.c_int64), ("n_local", C.c_int64), ("cells_per_axis", C.c_int64),
+                ("b", C.c_double)]
+
+
+class _Corr(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("active0", C.c_int64), ("active_final", C.c_int64),
+                ("loss0", C.c_double), ("loss_final", C.c_double), ("converged", C.c_int), ("pad", C.c_int)]
+
+
+class _Mcc(C.Structure):
+    _fields_ = [("tp", C.c_uint64), ("tn", C.c_uint64), ("fp", C.c_uint64), ("fn", C.c_uint64), ("mcc", C.c_double)]
+
+
+class _Run(C.Structure):
+    _fields_ = [("vp", _VP), ("corr", _Corr)]
+
+
+EXPORTS = ["cc_default_params", "cc_nccl_unique_id", "cc_create", "cc_destroy", "cc_last_error", "cc_build_cells",
+           "cc_find_vulnerable", "cc_get_pairs", "cc_correct", "cc_get_trace", "cc_fof_label", "cc_mcc",
+           "cc_halo_sizes", "cc_hmf", "cc_kernel_stats", "cc_run"]
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def lib():
+    """Load libcc.so (building it with nvcc if it is missing).  Raises if it cannot."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        from .build import build
+        build()
+    L = C.CDLL(_LIB_PATH)
+    P = C.POINTER
+    vp, f, u32, i64, d = C.c_void_p, C.c_float, C.c_uint32, C.c_int64, C.c_double
+    L.cc_default_params.argtypes = [P(_Params)]
+    L.cc_default_params.restype = None
+    L.cc_nccl_unique_id.argtypes = [vp]
+    L.cc_create.argtypes = [P(vp), C.c_int, vp, P(_Params), P(_Dist)]
+    L.cc_destroy.argtypes = [vp]
+    L.cc_destroy.restype = None
+    L.cc_last_error.argtypes = [vp]
+    L.cc_last_error.restype = C.c_char_p
+    L.cc_build_cells.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp]
+    L.cc_find_vulnerable.argtypes = [vp, P(_VP)]
+    L.cc_get_pairs.argtypes = [vp, vp, vp, vp, i64, P(i64)]
+    L.cc_correct.argtypes = [vp, vp, vp, vp, P(_Corr)]
+    L.cc_get_trace.argtypes = [vp, P(i64), P(d), i64, P(i64)]
+    L.cc_fof_label.argtypes = [vp, C.c_int, vp, P(i64)]
+    L.cc_mcc.argtypes = [vp, C.c_int, P(_Mcc)]
+    L.cc_halo_sizes.argtypes = [vp, C.c_int, i64, P(i64), i64, P(i64)]
+    L.cc_hmf.argtypes = [P(i64), i64, d, C.c_int, d, d, P(d), P(d)]
+    L.cc_kernel_stats.argtypes = [vp, C.c_char_p, i64, P(d), P(i64), i64, P(i64), C.c_int]
+    L.cc_run.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, P(_Run)]
+    for name in EXPORTS:
+        if name not in ("cc_default_params", "cc_destroy", "cc_last_error"):
+            getattr(L, name).restype = C.c_int
+    _lib = L
+    return L
+
+
+@dataclass
+class Params:
+    """cc_params (include/cc.h): Alg. 1 REQUIRE line plus box and perf knobs."""
+    box: float = 1.0
+    periodic: int = 1
+    b: float = 0.0
+    eta: float = 0.2
+    xi: float = 0.0
+    m: int = 16
+    alpha: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps_adam: float = 1e-8
+    t_max: int = 10000
+    eps_loss: float = 1e-10
+    stop_mode: int = STOP_ACTIVE
+    optimizer: int = 0
+    vanilla_step: float = 0.0
+    graph_batch: int = 16
+    cells_per_particle: float = 8.0
+    profile: int = 0
+
+    def to_c(self) -> _Params:
+        return _Params(**{k: v for k, v in asdict(self).items()})
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _check_dev(t, dtype, name):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name}: expected a CUDA tensor (no CPU path exists)")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise TypeError(f"{name}: expected contiguous {dtype}")
+
+
+class Corrector:
+    """One context of libcc on one GPU (cc_create).  Methods map 1:1 to the C ABI."""
+
+    def __init__(self, params: Params, device: int | None = None, stream: torch.cuda.Stream | None = None,
+                 dist: tuple | None = None):
+        if not torch.cuda.is_available():
+            raise CCError(68, "no CUDA device: libcc has no CPU path")
+        self.lib = lib()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.params = params
+        self._p = params.to_c()
+        self._d = None
+        if dist is not None:
+            rank, nranks, uid = dist
+            self._uid = C.create_string_buffer(bytes(uid), 128)
+            self._d = _Dist(rank, nranks, C.cast(self._uid, C.c_void_p))
+        h = C.c_void_p()
+        st = self.lib.cc_create(C.byref(h), self.device, C.c_void_p(self.stream.cuda_stream), C.byref(self._p),
+                                None if self._d is None else C.byref(self._d))
+        if st != 0:
+            raise CCError(st, "cc_create failed")
+        self.h = h
+        self.n = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.cc_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, st, ok=(0,)):
+        if st not in ok:
+            raise CCError(st, self.lib.cc_last_error(self.h).decode(errors="replace"))
+        return st
+
+    # S1
+    def build_cells(self, x, y, z, xh, yh, zh, gid=None):
+        for nm, t in zip("x y z xh yh zh".split(), (x, y, z, xh, yh, zh)):
+            _check_dev(t, torch.float32, nm)
+        if gid is not None:
+            _check_dev(gid, torch.int32, "gid (int32 view of uint32 ids)")
+        n = x.shape[0]
+        self._inputs = (x, y, z, xh, yh, zh, gid)  # keep alive until the stream is done
+        self._chk(self.lib.cc_build_cells(self.h, n, *[_ptr(t) for t in (x, y, z, xh, yh, zh)], _ptr(gid)))
+        self.n = n
+
+    # S2 + S3
+    def find_vulnerable(self) -> dict:
+        info = _VP()
+        self._chk(self.lib.cc_find_vulnerable(self.h, C.byref(info)))
+        return {k: getattr(info, k) for k, _ in _VP._fields_}
+
+    def get_pairs(self):
+        n = C.c_int64()
+        self._chk(self.lib.cc_get_pairs(self.h, None, None, None, 0, C.byref(n)))
+        k = n.value
+        dev = torch.device("cuda", self.device)
+        gi = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+        gj = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+        fl = torch.empty(max(k, 1), dtype=torch.uint8, device=dev)
+        self._chk(self.lib.cc_get_pairs(self.h, _ptr(gi), _ptr(gj), _ptr(fl), k, C.byref(n)))
+        return gi[:k], gj[:k], fl[:k]
+
+    # S4 + S5
+    def correct(self, out=None):
+        dev = torch.device("cuda", self.device)
+        if out is None:
+            out = tuple(torch.empty(self.n, dtype=torch.float32, device=dev) for _ in range(3))
+        info = _Corr()
+        st = self._chk(self.lib.cc_correct(self.h, *[_ptr(t) for t in out], C.byref(info)), ok=(0, 2))
+        d = {k: getattr(info, k) for k, _ in _Corr._fields_ if k != "pad"}
+        d["converged"] = bool(d["converged"])
+        d["status"] = st
+        return out, d
+
+    def trace(self):
+        n = C.c_int64()
+        a = np.zeros(self.params.t_max + 2, np.int64)
+        l = np.zeros(self.params.t_max + 2, np.float64)
+        self._chk(self.lib.cc_get_trace(self.h, a.ctypes.data_as(C.POINTER(C.c_int64)),
+                                        l.ctypes.data_as(C.POINTER(C.c_double)), a.shape[0], C.byref(n)))
+        return a[: n.value], l[: n.value]
+
+    # S6
+    def fof_label(self, which=CC_ORIG, labels=None):
+        if labels is None:
+            labels = torch.empty(max(self.n, 1), dtype=torch.int32, device=torch.device("cuda", self.device))[: self.n]
+        ng = C.c_int64()
+        self._chk(self.lib.cc_fof_label(self.h, which, _ptr(labels), C.byref(ng)))
+        return labels, ng.value
+
+    # S7
+    def mcc(self, which=CC_CORR) -> dict:
+        m = _Mcc()
+        self._chk(self.lib.cc_mcc(self.h, which, C.byref(m)))
+        return {k: getattr(m, k) for k, _ in _Mcc._fields_}
+
+    def halo_sizes(self, which=CC_ORIG, min_size=20) -> np.ndarray:
+        n = C.c_int64()
+        self._chk(self.lib.cc_halo_sizes(self.h, which, min_size, None, 0, C.byref(n)))
+        out = np.zeros(max(n.value, 1), np.int64)
+        self._chk(self.lib.cc_halo_sizes(self.h, which, min_size, out.ctypes.data_as(C.POINTER(C.c_int64)),
+                                         out.shape[0], C.byref(n)))
+        return out[: n.value]
+
+    def kernel_stats(self, reset=True) -> dict:
+        names = C.create_string_buffer(8192)
+        ms = np.zeros(64, np.float64)
+        ln = np.zeros(64, np.int64)
+        n = C.c_int64()
+        self._chk(self.lib.cc_kernel_stats(self.h, names, 8192, ms.ctypes.data_as(C.POINTER(C.c_double)),
+                                           ln.ctypes.data_as(C.POINTER(C.c_int64)), 64, C.byref(n), int(reset)))
+        keys = names.value.decode().split("\n")[: n.value]
+        return {k: (float(ms[i]), int(ln[i])) for i, k in enumerate(keys)}
+
+    # end-to-end through the ABI (host or device buffers)
+    def run(self, x, y, z, xh, yh, zh, out, gid=None, host=False) -> dict:
+        info = _Run()
+        ptrs = [_ptr(t) for t in (x, y, z, xh, yh, zh)]
+        st = self._chk(self.lib.cc_run(self.h, x.shape[0], *ptrs, _ptr(gid), *[_ptr(t) for t in out],
+                                       CC_RUN_HOST if host else 0, C.byref(info)), ok=(0, 2))
+        self.n = x.shape[0]
+        vp = {k: getattr(info.vp, k) for k, _ in _VP._fields_}
+        co = {k: getattr(info.corr, k) for k, _ in _Corr._fields_ if k != "pad"}
+        return {"vp": vp, "corr": co, "status": st}
+
+
+def hmf(sizes, vol: float, n_bins: int = 50, lo: float = 0.0, hi: float = 0.0):
+    """cc_hmf: dn/dlog10 M of a halo catalogue; lo >= hi: the catalogue's range."""
+    s = np.ascontiguousarray(np.asarray(sizes, dtype=np.int64))
+    e = np.zeros(n_bins + 1, np.float64)
+    d = np.zeros(n_bins, np.float64)
+    st = lib().cc_hmf(s.ctypes.data_as(C.POINTER(C.c_int64)), s.shape[0], vol, n_bins, lo, hi,
+                      e.ctypes.data_as(C.POINTER(C.c_double)), d.ctypes.data_as(C.POINTER(C.c_double)))
+    if st != 0:
+        raise CCError(st, "cc_hmf")
+    return e, d

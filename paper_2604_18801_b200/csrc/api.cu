@@ -1,0 +1,556 @@
+// api.cu -- the C ABI of libcc (include/cc.h): context, S0 parameters, step orchestration,
+// memory management and profiling.  Host C++; every step of the path runs in the kernels of
+// bin.cu / scan.cu / pairs.cu / pgd.cu / fof.cu.  No CPU fallback exists.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "cc_internal.cuh"
+
+// ------------------------------------------------------------------------------------------
+cc_status cc_fail(cc_ctx* c, cc_status st, const std::string& msg) {
+    if (c) c->err = msg;
+    return st;
+}
+
+cc_status cc_cuda_check(cc_ctx* c, cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return cc_fail(c, CC_E_OOM, std::string("out of device memory: ") + what);
+    }
+    if (c) c->dead = true;
+    return cc_fail(c, CC_E_CUDA, std::string(cudaGetErrorString(e)) + " at " + what);
+}
+
+template <typename T>
+cc_status cc_ensure(cc_ctx* c, cc::DBuf<T>& b, size_t n, const char* name) {
+    if (n == 0) n = 1;
+    if (b.cap >= n) return CC_OK;
+    if (b.p) {
+        cudaFreeAsync(b.p, c->stream);
+        b.p = nullptr;
+        b.cap = 0;
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, n * sizeof(T), c->stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return cc_fail(c, CC_E_OOM, std::string("cudaMallocAsync failed for ") + name + " (" +
+                                        std::to_string(n * sizeof(T)) + " bytes)");
+    }
+    b.p = static_cast<T*>(p);
+    b.cap = n;
+    return CC_OK;
+}
+
+template <typename T>
+void cc_release(cc_ctx* c, cc::DBuf<T>& b) {
+    if (b.p) cudaFreeAsync(b.p, c->stream);
+    b.p = nullptr;
+    b.cap = 0;
+}
+
+#define CC_INST(T)                                                                 \
+    template cc_status cc_ensure<T>(cc_ctx*, cc::DBuf<T>&, size_t, const char*); \
+    template void cc_release<T>(cc_ctx*, cc::DBuf<T>&);
+CC_INST(float4)
+CC_INST(uint32_t)
+CC_INST(uint64_t)
+CC_INST(float)
+CC_INST(float2)
+CC_INST(double)
+CC_INST(unsigned long long)
+CC_INST(cc::Ctl)
+CC_INST(long long)
+CC_INST(unsigned char)
+
+// ------------------------------------------------------------------------------------------
+// profiling
+int cc_prof_begin(cc_ctx* c, const char* cls) {
+    if (!c->p.profile) return -1;
+    int k = -1;
+    for (size_t i = 0; i < c->prof.size(); i++)
+        if (c->prof[i].name == cls) k = (int)i;
+    if (k < 0) {
+        c->prof.push_back({cls, 0.0, 0});
+        k = (int)c->prof.size() - 1;
+    }
+    cudaEvent_t a, b;
+    if (c->ev_pool.size() >= 2) {
+        a = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        b = c->ev_pool.back();
+        c->ev_pool.pop_back();
+    } else {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+    }
+    cudaEventRecord(a, c->stream);
+    c->pend.push_back({k, a, b});
+    return (int)c->pend.size() - 1;
+}
+
+void cc_prof_end(cc_ctx* c, int token) {
+    if (token < 0) return;
+    cudaEventRecord(c->pend[(size_t)token].b, c->stream);
+}
+
+static void prof_drain(cc_ctx* c) {
+    if (c->pend.empty()) return;
+    cudaStreamSynchronize(c->stream);
+    for (auto& pe : c->pend) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, pe.a, pe.b) == cudaSuccess) {
+            c->prof[(size_t)pe.cls].ms += ms;
+            c->prof[(size_t)pe.cls].launches += 1;
+        }
+        c->ev_pool.push_back(pe.a);
+        c->ev_pool.push_back(pe.b);
+    }
+    c->pend.clear();
+}
+
+// ------------------------------------------------------------------------------------------
+// S0 -- parameters (Alg. 1 lines 1-3 P:419-421; §III-B; readings R2-R8).
+// Directed fp32 rounding of an exact double sum (via the error term of TwoSum).
+static float rd32_sum(double a, double b) {
+    double s = a + b, bb = s - a, err = (a - (s - bb)) + (b - bb);
+    float f = (float)s;
+    if ((double)f > s || ((double)f == s && err < 0)) f = std::nextafter(f, -INFINITY);
+    return f;
+}
+
+static cc_status derive_params(cc_ctx* c, int64_t n_total) {
+    const cc_params& p = c->p;
+    double b = p.b;
+    if (!(b > 0)) {
+        if (n_total <= 0) return cc_fail(c, CC_E_ARG, "b <= 0 and no particles to derive it from");
+        b = p.eta * std::cbrt(p.box * p.box * p.box / (double)n_total);  // b = eta (V/N)^(1/3)
+    }
+    c->b = b;
+    cc::Th& t = c->th;
+    t.xi_f = (float)p.xi;
+    const double xi = (double)t.xi_f;
+    c->xi_d = xi;
+    t.xip_f = rd32_sum(xi * (1.0 - std::ldexp(1.0, -p.m)), 0.0);  // xi' = xi (1 - 2^-m)
+    c->eps_q = 2.0 * xi / (std::ldexp(1.0, p.m) - 1.0);            // eps_q = 2 xi / (2^m - 1)
+    c->mu = 2.0 * std::sqrt(3.0) * c->eps_q;
+    t.c_b = (float)(b - c->mu);
+    t.c_f = (float)(b + c->mu);
+    const double s = 2.0 * std::sqrt(3.0) * xi;
+    const double lo = b - s, hi = b + s;
+    t.lo2 = lo > 0 ? (float)(lo * lo) : -1.0f;
+    t.hi2 = (float)(hi * hi);
+    t.b2 = (float)(b * b);
+    t.Lf = (float)p.box;
+    t.hLf = (float)(0.5 * p.box);
+    t.periodic = p.periodic ? 1 : 0;
+    // ghost / cell width: delta = b + 2 sqrt3 xi, never below the fp32 sqrt(hi2)
+    c->delta = std::max(hi, std::sqrt((double)t.hi2));
+    if (p.periodic && c->delta >= 0.5 * p.box)
+        return cc_fail(c, CC_E_ARG, "b + 2 sqrt3 xi must be < box/2 for minimum-image distances");
+    return CC_OK;
+}
+
+// grid: cells of side >= delta (1 + 1e-5) (margin for fp32 rounding of d2 and of positions),
+// at most K * N cells (perf knob, R25), >= 1 per axis.
+static void choose_grid(cc_ctx* c, int64_t n_local, double x_extent, double x0, int xwrap) {
+    const double L = c->p.box;
+    const double wmin = c->delta * (1.0 + 1e-5);
+    double K = c->p.cells_per_particle > 0 ? c->p.cells_per_particle : 8.0;
+    double cap = std::max(K * (double)std::max<int64_t>(n_local, 1), 27.0);
+    cap = std::min(cap, 2147483647.0);
+    int64_t nyz = std::max<int64_t>(1, (int64_t)std::floor(L / wmin));
+    int64_t nx = std::max<int64_t>(1, (int64_t)std::floor(x_extent / wmin));
+    // shrink uniformly until the cell budget holds (cells stay cubic: w = L / nyz)
+    while ((double)nx * nyz * nyz > cap && nyz > 1) {
+        nyz = std::max<int64_t>(1, (int64_t)std::floor(nyz * 0.97));
+        if (xwrap) nx = nyz;
+        else nx = std::max<int64_t>(1, (int64_t)std::ceil(x_extent * (double)nyz / L));
+    }
+    if (xwrap) nx = nyz;
+    c->g.ny = c->g.nz = (int)nyz;
+    c->g.nx = (int)nx;
+    c->g.inv_w = (double)nyz / L;
+    c->g.x0 = x0;
+    c->g.L = L;
+    c->g.xwrap = xwrap;
+    c->ncell = (int64_t)nx * nyz * nyz;
+}
+
+// ------------------------------------------------------------------------------------------
+extern "C" {
+
+void cc_default_params(cc_params* p) {
+    std::memset(p, 0, sizeof(*p));
+    p->box = 1.0;
+    p->periodic = 1;
+    p->b = 0.0;
+    p->eta = 0.2;
+    p->xi = 0.0;
+    p->m = 16;
+    p->alpha = 1e-3;
+    p->beta1 = 0.9;
+    p->beta2 = 0.999;
+    p->eps_adam = 1e-8;
+    p->t_max = 10000;
+    p->eps_loss = 1e-10;
+    p->stop_mode = CC_STOP_ACTIVE;
+    p->optimizer = CC_OPT_ADAM;
+    p->vanilla_step = 0.0;
+    p->graph_batch = 16;
+    p->cells_per_particle = 8.0;
+    p->profile = 0;
+}
+
+cc_status cc_create(cc_ctx** out, int device, void* stream, const cc_params* p, const cc_dist* dist) {
+    if (!out) return CC_E_ARG;
+    *out = nullptr;
+    if (!p) return CC_E_ARG;
+    if (!(p->box > 0) || !(p->xi >= 0) || p->m < 2 || p->m > 52 || p->t_max < 0 || p->stop_mode < 0 ||
+        p->stop_mode > 2 || p->optimizer < 0 || p->optimizer > 1)
+        return CC_E_ARG;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0 || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return CC_E_CUDA;
+    }
+    if (dist && dist->nranks > 1) return CC_E_ARG;  // multi-GPU: not in this build yet
+    cc_ctx* c = new cc_ctx();
+    c->device = device;
+    c->p = *p;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete c;
+        return CC_E_CUDA;
+    }
+    if (stream) {
+        c->stream = static_cast<cudaStream_t>(stream);
+    } else if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return CC_E_CUDA;
+    }
+    // keep freed stream-ordered allocations cached in the pool
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    if (cudaMallocHost(&c->h_ctl, sizeof(cc::Ctl)) != cudaSuccess ||
+        cudaMallocHost(&c->h_counters, 16 * sizeof(unsigned long long)) != cudaSuccess) {
+        delete c;
+        return CC_E_CUDA;
+    }
+    c->owns_stream = (stream == nullptr);
+    *out = c;
+    return CC_OK;
+}
+
+void cc_destroy(cc_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cc_release(c, c->orig4); cc_release(c, c->dec4); cc_release(c, c->cor4); cc_release(c, c->posA);
+    cc_release(c, c->posB); cc_release(c, c->origE);
+    cc_release(c, c->key); cc_release(c, c->rnk); cc_release(c, c->cell_count); cc_release(c, c->cell_start);
+    cc_release(c, c->slot_of); cc_release(c, c->deg); cc_release(c, c->eidx); cc_release(c, c->rows);
+    cc_release(c, c->slotE); cc_release(c, c->parent); cc_release(c, c->mingid); cc_release(c, c->gsize);
+    cc_release(c, c->scratch_u32); cc_release(c, c->rowoff); cc_release(c, c->rowptr); cc_release(c, c->scratch_u64);
+    cc_release(c, c->mom); cc_release(c, c->bc); cc_release(c, c->partial_d); cc_release(c, c->partial_u);
+    cc_release(c, c->counters); cc_release(c, c->ctl); cc_release(c, c->trace_a); cc_release(c, c->trace_l);
+    cc_release(c, c->tmp_bytes); cc_release(c, c->in_f); cc_release(c, c->in_gid);
+    cudaStreamSynchronize(c->stream);
+    if (c->pgd_exec) cudaGraphExecDestroy(c->pgd_exec);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    for (auto& pe : c->pend) {
+        cudaEventDestroy(pe.a);
+        cudaEventDestroy(pe.b);
+    }
+    for (auto e : c->graph_ev) cudaEventDestroy(e);
+    if (c->h_ctl) cudaFreeHost(c->h_ctl);
+    if (c->h_counters) cudaFreeHost(c->h_counters);
+    if (c->owns_stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* cc_last_error(const cc_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+cc_status cc_nccl_unique_id(void*) { return CC_E_NCCL; }
+
+#define CC_GUARD(c)                                                                          \
+    do {                                                                                     \
+        if (!(c)) return CC_E_ARG;                                                           \
+        if ((c)->dead) return cc_fail((c), CC_E_CUDA, "context unusable after a CUDA error"); \
+        cudaSetDevice((c)->device);                                                          \
+    } while (0)
+
+cc_status cc_build_cells(cc_ctx* c, int64_t n, const float* x, const float* y, const float* z, const float* xh,
+                         const float* yh, const float* zh, const uint32_t* gid) {
+    CC_GUARD(c);
+    if (n < 0) return cc_fail(c, CC_E_ARG, "n < 0");
+    if (n > 0 && (!x || !y || !z || !xh || !yh || !zh)) return cc_fail(c, CC_E_ARG, "null input pointer");
+    if (n >= cc::MAX_LOCAL) return cc_fail(c, CC_E_DATA, "n beyond the 2^30 local index space");
+    c->state = 0;
+    c->have_labels[0] = c->have_labels[1] = c->have_labels[2] = 0;
+    CC_TRY(derive_params(c, n));
+    c->n_in = n;
+    c->n = n;
+    choose_grid(c, n, c->p.box, 0.0, c->p.periodic ? 1 : 0);
+    CC_TRY(cc::bin_particles(c, x, y, z, xh, yh, zh, gid, n));
+    CC_CUDA(c, cudaMemcpyAsync(c->h_counters, c->counters.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    const unsigned long long bad = c->h_counters[0];
+    if (bad & 1ull) return cc_fail(c, CC_E_DATA, "non-finite input coordinate");
+    if (bad & 2ull) return cc_fail(c, CC_E_BOUND, "decompressed input violates |x_hat - x| <= xi (P:396)");
+    c->state = 1;
+    return CC_OK;
+}
+
+cc_status cc_find_vulnerable(cc_ctx* c, cc_vp_info* info) {
+    CC_GUARD(c);
+    if (c->state < 1) return cc_fail(c, CC_E_STATE, "cc_build_cells first");
+    const int64_t n = c->n;
+    CC_TRY(cc::pairs_count(c));
+    CC_TRY(cc_ensure(c, c->rowoff, (size_t)std::max<int64_t>(n, 1), "rowoff"));
+    CC_TRY(cc_ensure(c, c->eidx, (size_t)std::max<int64_t>(n, 1), "eidx"));
+    CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
+    unsigned long long* tot = c->counters.p + 2;  // 16-byte VDeg total at counters[2..3]
+    CC_TRY(cc::scan_deg(c, c->deg.p, c->rowoff.p, c->eidx.p, n, c->dec4.p, c->n_in, tot));
+    CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 2, tot, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->nent = (int64_t)c->h_counters[2];
+    const uint32_t w1 = (uint32_t)(c->h_counters[3] & 0xFFFFFFFFull), w2 = (uint32_t)(c->h_counters[3] >> 32);
+    c->E = w1;
+    c->E_all = (int64_t)w1 + w2;
+    if (c->E_all >= cc::MAX_LOCAL) return cc_fail(c, CC_E_DATA, "editable set beyond the 2^30 index space");
+    CC_TRY(cc::rows_finish(c));
+    c->state = 2;
+    if (info) {
+        unsigned long long* cnt = c->counters.p + 4;
+        CC_TRY(cc::mcc_run(c, CC_DECOMP, cnt));
+        CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 4, cnt, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                   c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+        const unsigned long long* h = c->h_counters + 4;
+        info->n_pairs = (int64_t)(h[0] + h[1] + h[2] + h[3]);
+        info->n_editable = c->E;
+        info->n_linked = (int64_t)(h[0] + h[3]);
+        info->n_violated0 = (int64_t)(h[2] + h[3]);
+        info->n_local = c->n;
+        info->cells_per_axis = c->g.ny;
+        info->b = c->b;
+    }
+    return CC_OK;
+}
+
+cc_status cc_get_pairs(cc_ctx* c, uint32_t* gi, uint32_t* gj, uint8_t* flags, int64_t cap, int64_t* n_out) {
+    CC_GUARD(c);
+    if (c->state < 2) return cc_fail(c, CC_E_STATE, "cc_find_vulnerable first");
+    if (cap > 0 && (!gi || !gj || !flags)) return cc_fail(c, CC_E_ARG, "null output");
+    unsigned long long* cnt = c->counters.p + 10;
+    CC_TRY(cc::get_pairs_run(c, gi, gj, flags, cap, cnt));
+    CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 10, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (n_out) *n_out = (int64_t)c->h_counters[10];
+    return CC_OK;
+}
+
+cc_status cc_correct(cc_ctx* c, float* xo, float* yo, float* zo, cc_corr_info* info) {
+    CC_GUARD(c);
+    if (c->state < 2) return cc_fail(c, CC_E_STATE, "cc_find_vulnerable first");
+    if (c->n_in > 0 && (!xo || !yo || !zo)) return cc_fail(c, CC_E_ARG, "null output");
+    if (c->p.optimizer == CC_OPT_VANILLA && !(c->p.vanilla_step > 0))
+        return cc_fail(c, CC_E_ARG, "vanilla optimizer needs vanilla_step > 0");
+    cc_corr_info local{};
+    CC_TRY(cc::pgd_run(c, &local));
+    CC_TRY(cc::write_output(c, cc::pgd_result(c), xo, yo, zo));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->state = 3;
+    c->have_labels[CC_CORR] = 0;
+    if (info) *info = local;
+    return local.converged ? CC_OK : CC_NOT_CONVERGED;
+}
+
+cc_status cc_get_trace(cc_ctx* c, int64_t* active_h, double* loss_h, int64_t cap, int64_t* n_h) {
+    CC_GUARD(c);
+    if (c->state < 3) return cc_fail(c, CC_E_STATE, "cc_correct first");
+    const int64_t n = (int64_t)c->last_iters + 1;
+    // trace[t-1] holds the stop check of iteration t; checks ran for t = 1..iters+1 unless the
+    // loop ended on T_max (then the last state was checked by the final pass only)
+    std::vector<long long> a((size_t)n, 0);
+    std::vector<double> l((size_t)n, 0.0);
+    const int64_t k = std::min<int64_t>(n, (int64_t)c->p.t_max);
+    if (k > 0) {
+        CC_CUDA(c, cudaMemcpyAsync(a.data(), c->trace_a.p, (size_t)k * sizeof(long long), cudaMemcpyDeviceToHost,
+                                   c->stream));
+        CC_CUDA(c, cudaMemcpyAsync(l.data(), c->trace_l.p, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost,
+                                   c->stream));
+    }
+    CC_CUDA(c, cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(cc::Ctl), cudaMemcpyDeviceToHost, c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    a[(size_t)n - 1] = (long long)c->h_ctl->active;  // final check of the returned state
+    l[(size_t)n - 1] = c->h_ctl->loss;
+    for (int64_t q = 0; q < n && q < cap; q++) {
+        active_h[q] = a[(size_t)q];
+        loss_h[q] = l[(size_t)q];
+    }
+    if (n_h) *n_h = n;
+    return CC_OK;
+}
+
+cc_status cc_fof_label(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
+    CC_GUARD(c);
+    if (which < CC_ORIG || which > CC_CORR) return cc_fail(c, CC_E_ARG, "which");
+    if (c->state < 1) return cc_fail(c, CC_E_STATE, "cc_build_cells first");
+    if (which == CC_CORR && c->state < 3) return cc_fail(c, CC_E_STATE, "cc_correct first");
+    int64_t ng = 0;
+    CC_TRY(cc::fof_run(c, which, labels, n_groups ? &ng : nullptr));
+    if (n_groups) *n_groups = ng;
+    c->fof_which = which;
+    return CC_OK;
+}
+
+cc_status cc_mcc(cc_ctx* c, int which, cc_mcc_info* out) {
+    CC_GUARD(c);
+    if (!out) return cc_fail(c, CC_E_ARG, "null output");
+    if (c->state < 2) return cc_fail(c, CC_E_STATE, "cc_find_vulnerable first");
+    if (which == CC_CORR && c->state < 3) return cc_fail(c, CC_E_STATE, "cc_correct first");
+    unsigned long long* cnt = c->counters.p + 4;
+    CC_TRY(cc::mcc_run(c, which, cnt));
+    CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 4, cnt, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    const unsigned long long* h = c->h_counters + 4;
+    out->tp = h[0];
+    out->tn = h[1];
+    out->fp = h[2];
+    out->fn = h[3];
+    // MCC with R21's convention; numerator exact in 128-bit integers
+    const unsigned __int128 a = (unsigned __int128)(h[0] + h[2]), b = (unsigned __int128)(h[0] + h[3]),
+                            cc_ = (unsigned __int128)(h[1] + h[2]), d = (unsigned __int128)(h[1] + h[3]);
+    if (a == 0 || b == 0 || cc_ == 0 || d == 0) {
+        out->mcc = (h[2] == 0 && h[3] == 0) ? 1.0 : 0.0;
+    } else {
+        const __int128 num = (__int128)h[0] * (__int128)h[1] - (__int128)h[2] * (__int128)h[3];
+        const unsigned __int128 den2 = a * b * cc_ * d;
+        out->mcc = (double)num / std::sqrt((double)den2);
+    }
+    return CC_OK;
+}
+
+cc_status cc_halo_sizes(cc_ctx* c, int which, int64_t min_size, int64_t* sizes_h, int64_t cap, int64_t* n_h) {
+    CC_GUARD(c);
+    if (!n_h || (cap > 0 && !sizes_h)) return cc_fail(c, CC_E_ARG, "null output");
+    if (c->fof_which != which) return cc_fail(c, CC_E_STATE, "cc_fof_label(which) must be the last FoF run");
+    return cc::halo_sizes_run(c, min_size, sizes_h, cap, n_h);
+}
+
+cc_status cc_hmf(const int64_t* sizes, int64_t n, double vol, int n_bins, double lo, double hi, double* edges,
+                 double* density) {
+    if (n < 0 || n_bins <= 0 || !(vol > 0) || !edges || !density || (n > 0 && !sizes)) return CC_E_ARG;
+    std::vector<double> lm((size_t)n);
+    double mn = INFINITY, mx = -INFINITY;
+    for (int64_t i = 0; i < n; i++) {
+        lm[(size_t)i] = std::log10((double)sizes[i]);  // M_i = N_i (unit particle mass)
+        mn = std::min(mn, lm[(size_t)i]);
+        mx = std::max(mx, lm[(size_t)i]);
+    }
+    if (!(lo < hi)) {
+        lo = n > 0 ? mn : 0.0;
+        hi = n > 0 ? mx : 1.0;
+        if (!(hi > lo)) hi = lo + 1.0;
+    }
+    const double w = (hi - lo) / n_bins;
+    for (int k = 0; k <= n_bins; k++) edges[k] = lo + w * k;
+    std::vector<double> cnt((size_t)n_bins, 0.0);
+    for (int64_t i = 0; i < n; i++) {
+        const double v = lm[(size_t)i];
+        int64_t k = (int64_t)std::floor((v - lo) / w);
+        if (v == hi) k = n_bins - 1;
+        if (k >= 0 && k < n_bins) cnt[(size_t)k] += 1.0;
+    }
+    for (int k = 0; k < n_bins; k++) density[k] = cnt[(size_t)k] / (vol * w);
+    return CC_OK;
+}
+
+cc_status cc_kernel_stats(cc_ctx* c, char* names, int64_t names_cap, double* ms, int64_t* launches, int64_t cap,
+                          int64_t* n_h, int reset) {
+    CC_GUARD(c);
+    prof_drain(c);
+    std::string all;
+    int64_t k = 0;
+    for (auto& pe : c->prof) {
+        if (k < cap) {
+            if (ms) ms[k] = pe.ms;
+            if (launches) launches[k] = pe.launches;
+        }
+        all += pe.name;
+        all += '\n';
+        k++;
+    }
+    // pseudo-class: every kernel launched through this context (profiled or not)
+    if (k < cap) {
+        if (ms) ms[k] = 0.0;
+        if (launches) launches[k] = c->launches;
+    }
+    all += "total_launches\n";
+    k++;
+    if (names && names_cap > 0) {
+        std::strncpy(names, all.c_str(), (size_t)names_cap - 1);
+        names[names_cap - 1] = 0;
+    }
+    if (n_h) *n_h = k;
+    if (reset) {
+        for (auto& pe : c->prof) {
+            pe.ms = 0;
+            pe.launches = 0;
+        }
+        c->launches = 0;
+    }
+    return CC_OK;
+}
+
+cc_status cc_run(cc_ctx* c, int64_t n, const float* x, const float* y, const float* z, const float* xh,
+                 const float* yh, const float* zh, const uint32_t* gid, float* xo, float* yo, float* zo, int flags,
+                 cc_run_info* info) {
+    CC_GUARD(c);
+    if (n < 0) return cc_fail(c, CC_E_ARG, "n < 0");
+    const float *dx = x, *dy = y, *dz = z, *dxh = xh, *dyh = yh, *dzh = zh;
+    const uint32_t* dg = gid;
+    float *ox = xo, *oy = yo, *oz = zo;
+    const size_t nn = (size_t)std::max<int64_t>(n, 1);
+    if (flags & CC_RUN_HOST) {
+        CC_TRY(cc_ensure(c, c->in_f, 9 * nn, "run staging"));
+        float* s = c->in_f.p;
+        const float* src[6] = {x, y, z, xh, yh, zh};
+        for (int k = 0; k < 6; k++)
+            if (n > 0)
+                CC_CUDA(c, cudaMemcpyAsync(s + k * nn, src[k], (size_t)n * sizeof(float), cudaMemcpyHostToDevice,
+                                           c->stream));
+        dx = s; dy = s + nn; dz = s + 2 * nn; dxh = s + 3 * nn; dyh = s + 4 * nn; dzh = s + 5 * nn;
+        ox = s + 6 * nn; oy = s + 7 * nn; oz = s + 8 * nn;
+        if (gid) {
+            CC_TRY(cc_ensure(c, c->in_gid, nn, "run gid staging"));
+            if (n > 0)
+                CC_CUDA(c, cudaMemcpyAsync(c->in_gid.p, gid, (size_t)n * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                           c->stream));
+            dg = c->in_gid.p;
+        }
+    }
+    CC_TRY(cc_build_cells(c, n, dx, dy, dz, dxh, dyh, dzh, dg));
+    cc_run_info loc{};
+    CC_TRY(cc_find_vulnerable(c, &loc.vp));
+    cc_status st = cc_correct(c, ox, oy, oz, &loc.corr);
+    if (st != CC_OK && st != CC_NOT_CONVERGED) return st;
+    if ((flags & CC_RUN_HOST) && n > 0) {
+        CC_CUDA(c, cudaMemcpyAsync(xo, ox, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaMemcpyAsync(yo, oy, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaMemcpyAsync(zo, oz, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    }
+    if (info) *info = loc;
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,290 @@
+// fof.cu -- K4 FoF labelling (S6) and K5 MCC / halo-size counters (S7).
+//
+// Paper: §II-B P:362 and Fig. 1 (edge iff d(p_i,p_j) <= b; FoF clusters = connected
+// components), §II-B-1 P:381 (cell linking, forward neighbour cells), §II-B-2 P:387 (halo mass
+// M_i ~ N_i, HMF), §IV-A P:9-15 (MCC over vulnerable pairs: FP = unlinked->linked,
+// FN = linked->broken).  The paper does not describe its own FoF code (it cites HACC's).
+//
+// B200 form: one thread per particle tests the pinned fp32 d2 <= fl32(b^2) against the
+// half-shell of its cell neighbourhood (13.5 cells) and unites on the fly with a lock-free
+// union-find (atomicCAS hooks the larger root under the smaller index, path halving), then
+// pointer jumping flattens the forest and atomicMin gives each component its min gid (R20).
+// The same cell-sorted grid serves ORIG, DECOMP and CORR positions: its cells are >= b + 2 sqrt3
+// xi wide and every position lies within xi of its original (R1).
+#include <algorithm>
+
+#include "cc_internal.cuh"
+
+namespace cc {
+namespace {
+
+constexpr int FOF_THREADS = 256;
+
+__device__ __forceinline__ uint32_t uf_find(uint32_t* par, uint32_t x) {
+    volatile uint32_t* vp = par;
+    for (;;) {
+        const uint32_t p = vp[x];
+        if (p == x) return x;
+        const uint32_t gp = vp[p];
+        if (gp != p) vp[x] = gp;  // path halving; gp is an ancestor of x (benign race)
+        x = gp;
+    }
+}
+
+__device__ __forceinline__ void uf_unite(uint32_t* par, uint32_t a, uint32_t b) {
+    a = uf_find(par, a);
+    b = uf_find(par, b);
+    while (a != b) {
+        if (a < b) {
+            const uint32_t t = a;
+            a = b;
+            b = t;
+        }
+        const uint32_t old = atomicCAS(&par[a], a, b);  // hook root a (larger) under b
+        if (old == a) return;
+        a = uf_find(par, old);
+        b = uf_find(par, b);
+    }
+}
+
+__global__ void k_iota(int64_t n, uint32_t* __restrict__ par) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < n) par[s] = (uint32_t)s;
+}
+
+// link pass: half-shell when every axis has >= 3 cells and the grid is periodic in x
+// (each unordered cell pair visited once), else the full 27-stencil with j > s
+__global__ void __launch_bounds__(FOF_THREADS)
+k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ orig4, const uint32_t* __restrict__ cs,
+           Grid g, Th t, uint32_t* __restrict__ par) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const float4 o = orig4[s];
+    const float4 p = P[s];
+    int cx, cy, cz;
+    cell_of(o.x, o.y, o.z, g, cx, cy, cz);
+    const bool periodic_yz = t.periodic != 0;
+    const bool half = g.nx >= 3 && g.ny >= 3 && g.nz >= 3 && g.xwrap && periodic_yz;
+    auto test_range = [&](uint32_t a, uint32_t b) {
+        for (uint32_t j = a; j < b; j++) {
+            const float4 q = P[j];
+            if (dist2(p, q, t) <= t.b2) uf_unite(par, (uint32_t)s, j);
+        }
+    };
+    if (!half) {
+        for_each_neighbour_range(g, cs, cx, cy, cz, periodic_yz, [&](uint32_t a, uint32_t b) {
+            if (b > (uint32_t)s + 1) test_range(a > (uint32_t)s + 1 ? a : (uint32_t)s + 1, b);
+        });
+        return;
+    }
+    // (dz=0, dy=0): own cell beyond s, then cell cx+1
+    {
+        const int64_t base = ((int64_t)cz * g.ny + cy) * g.nx;
+        const int64_t c = base + cx;
+        if (cx + 1 <= g.nx - 1) {
+            test_range((uint32_t)s + 1, cs[c + 2]);
+        } else {
+            test_range((uint32_t)s + 1, cs[c + 1]);
+            test_range(cs[base], cs[base + 1]);
+        }
+    }
+    // (dz=0, dy=+1) and (dz=+1, dy=-1..1): full x rows
+    const int rows_dz[4] = {0, 1, 1, 1};
+    const int rows_dy[4] = {1, -1, 0, 1};
+    for (int r = 0; r < 4; r++) {
+        const int zz = wrapi(cz + rows_dz[r], g.nz), yy = wrapi(cy + rows_dy[r], g.ny);
+        const int64_t base = ((int64_t)zz * g.ny + yy) * g.nx;
+        if (cx >= 1 && cx <= g.nx - 2) {
+            test_range(cs[base + cx - 1], cs[base + cx + 2]);
+        } else {
+            for (int dx = -1; dx <= 1; dx++) {
+                const int xx = wrapi(cx + dx, g.nx);
+                test_range(cs[base + xx], cs[base + xx + 1]);
+            }
+        }
+    }
+}
+
+__global__ void k_flatten(int64_t n, uint32_t* __restrict__ par) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    par[s] = uf_find(par, (uint32_t)s);
+}
+
+__global__ void k_mingid(int64_t n, const uint32_t* __restrict__ par, const float4* __restrict__ orig4,
+                         uint32_t* __restrict__ mingid, uint32_t* __restrict__ gsize,
+                         unsigned long long* __restrict__ n_roots) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned int root = 0;
+    if (s < n) {
+        const uint32_t r = par[s];
+        atomicMin(&mingid[r], __float_as_uint(orig4[s].w));
+        atomicAdd(&gsize[r], 1u);
+        root = (r == (uint32_t)s);
+    }
+    const unsigned int cnt = __syncthreads_count(root);
+    if (threadIdx.x == 0 && cnt) atomicAdd(n_roots, (unsigned long long)cnt);
+}
+
+__global__ void k_labels(int64_t n_in, const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ par,
+                         const uint32_t* __restrict__ mingid, uint32_t* __restrict__ labels) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_in) return;
+    labels[i] = mingid[par[slot_of[i]]];
+}
+
+// MCC counters over the vulnerable pairs owned here (lower-gid endpoint, R17)
+__global__ void __launch_bounds__(256)
+k_mcc(uint32_t E, const unsigned long long* __restrict__ rowptr, const uint32_t* __restrict__ rows,
+      const float4* __restrict__ W, const uint32_t* __restrict__ slotE, int via_slot, Th t,
+      unsigned long long* __restrict__ out /* tp, tn, fp, fn */) {
+    unsigned int c[4] = {0, 0, 0, 0};
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        const float4 p = via_slot ? W[slotE[e]] : W[e];
+        for (unsigned long long k = rowptr[e]; k < rowptr[e + 1]; k++) {
+            const uint32_t ent = rows[k];
+            if (!(ent & ENT_UPPER)) continue;
+            const uint32_t j = ent & ENT_IDX;
+            const float4 q = via_slot ? W[slotE[j]] : W[j];
+            const bool lk = dist2(p, q, t) <= t.b2;
+            const bool ol = (ent & ENT_OLINK) != 0;
+            c[ol ? (lk ? 0 : 3) : (lk ? 2 : 1)]++;
+        }
+    }
+    for (int q = 0; q < 4; q++) {
+        unsigned int v = c[q];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&out[q], (unsigned long long)v);
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_get_pairs(uint32_t E, const unsigned long long* __restrict__ rowptr, const uint32_t* __restrict__ rows,
+            const float4* __restrict__ posE, const float4* __restrict__ dec4, const uint32_t* __restrict__ slotE, Th t,
+            int64_t cap, uint32_t* __restrict__ gi, uint32_t* __restrict__ gj, uint8_t* __restrict__ fl,
+            unsigned long long* __restrict__ cnt) {
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        const float4 pd = dec4[slotE[e]];
+        const uint32_t g0 = __float_as_uint(posE[e].w);
+        for (unsigned long long k = rowptr[e]; k < rowptr[e + 1]; k++) {
+            const uint32_t ent = rows[k];
+            if (!(ent & ENT_UPPER)) continue;
+            const uint32_t j = ent & ENT_IDX;
+            const float4 qd = dec4[slotE[j]];
+            const uint8_t f = (uint8_t)(((ent & ENT_OLINK) ? 1 : 0) | (dist2(pd, qd, t) <= t.b2 ? 2 : 0));
+            const unsigned long long q = atomicAdd(cnt, 1ull);
+            if ((int64_t)q < cap) {
+                gi[q] = g0;
+                gj[q] = __float_as_uint(posE[j].w);
+                fl[q] = f;
+            }
+        }
+    }
+}
+
+__global__ void k_halo_collect(int64_t n, const uint32_t* __restrict__ par, const uint32_t* __restrict__ gsize,
+                               uint32_t min_size, uint32_t* __restrict__ out, unsigned long long* __restrict__ cnt) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    if (par[s] == (uint32_t)s && gsize[s] >= min_size) {
+        const unsigned long long q = atomicAdd(cnt, 1ull);
+        out[q] = gsize[s];
+    }
+}
+
+}  // namespace
+
+cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
+    const int64_t n = c->n;
+    const size_t n1 = (size_t)std::max<int64_t>(n, 1);
+    CC_TRY(cc_ensure(c, c->parent, n1, "parent"));
+    CC_TRY(cc_ensure(c, c->mingid, n1, "mingid"));
+    CC_TRY(cc_ensure(c, c->gsize, n1, "gsize"));
+    CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
+    const float4* P = which == CC_ORIG ? c->orig4.p : (which == CC_DECOMP ? c->dec4.p : c->cor4.p);
+    CC_CUDA(c, cudaMemsetAsync(c->mingid.p, 0xFF, n1 * sizeof(uint32_t), c->stream));
+    CC_CUDA(c, cudaMemsetAsync(c->gsize.p, 0, n1 * sizeof(uint32_t), c->stream));
+    CC_CUDA(c, cudaMemsetAsync(c->counters.p + 8, 0, sizeof(unsigned long long), c->stream));
+    const unsigned nb = (unsigned)((n + FOF_THREADS - 1) / FOF_THREADS);
+    int tok = cc_prof_begin(c, "K4_fof");
+    if (n > 0) {
+        CCL(c, k_iota<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p));
+        CCL(c, k_fof_link<<<nb, FOF_THREADS, 0, c->stream>>>(n, P, c->orig4.p, c->cell_start.p, c->g, c->th, c->parent.p));
+        CCL(c, k_flatten<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p));
+        CCL(c, k_mingid<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p, c->orig4.p, c->mingid.p, c->gsize.p,
+                                                    c->counters.p + 8));
+        if (labels && c->n_in > 0)
+            CCL(c, k_labels<<<(unsigned)((c->n_in + 255) / 256), 256, 0, c->stream>>>(c->n_in, c->slot_of.p, c->parent.p,
+                                                                              c->mingid.p, labels));
+    }
+    cc_prof_end(c, tok);
+    CC_CUDA(c, cudaGetLastError());
+    if (n_groups) {
+        CC_CUDA(c, cudaMemcpyAsync(c->h_counters, c->counters.p + 8, sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+        *n_groups = (int64_t)c->h_counters[0];
+    }
+    return CC_OK;
+}
+
+cc_status mcc_run(cc_ctx* c, int which, unsigned long long* counts_dev) {
+    CC_CUDA(c, cudaMemsetAsync(counts_dev, 0, 4 * sizeof(unsigned long long), c->stream));
+    if (c->E == 0) return CC_OK;
+    const float4* W;
+    int via_slot;
+    if (which == CC_DECOMP) {
+        W = c->dec4.p;
+        via_slot = 1;
+    } else if (which == CC_ORIG) {
+        W = c->orig4.p;
+        via_slot = 1;
+    } else {
+        W = pgd_result(c);
+        via_slot = 0;
+    }
+    int nb = (int)std::min<int64_t>((c->E + 255) / 256, 148 * 8);
+    int tok = cc_prof_begin(c, "K5_mcc");
+    CCL(c, k_mcc<<<nb, 256, 0, c->stream>>>((uint32_t)c->E, reinterpret_cast<const unsigned long long*>(c->rowptr.p),
+                                     c->rows.p, W, c->slotE.p, via_slot, c->th, counts_dev));
+    cc_prof_end(c, tok);
+    CC_CUDA(c, cudaGetLastError());
+    return CC_OK;
+}
+
+cc_status get_pairs_run(cc_ctx* c, uint32_t* gi, uint32_t* gj, uint8_t* flags, int64_t cap, unsigned long long* n_dev) {
+    CC_CUDA(c, cudaMemsetAsync(n_dev, 0, sizeof(unsigned long long), c->stream));
+    if (c->E == 0) return CC_OK;
+    int nb = (int)std::min<int64_t>((c->E + 255) / 256, 148 * 8);
+    CCL(c, k_get_pairs<<<nb, 256, 0, c->stream>>>((uint32_t)c->E, reinterpret_cast<const unsigned long long*>(c->rowptr.p),
+                                           c->rows.p, c->origE.p, c->dec4.p, c->slotE.p, c->th, cap, gi, gj, flags,
+                                           n_dev));
+    CC_CUDA(c, cudaGetLastError());
+    return CC_OK;
+}
+
+cc_status halo_sizes_run(cc_ctx* c, int64_t min_size, int64_t* sizes_h, int64_t cap, int64_t* n_h) {
+    const int64_t n = c->n;
+    CC_TRY(cc_ensure(c, c->scratch_u32, (size_t)std::max<int64_t>(n, 1), "halo list"));
+    CC_CUDA(c, cudaMemsetAsync(c->counters.p + 9, 0, sizeof(unsigned long long), c->stream));
+    if (n > 0)
+        CCL(c, k_halo_collect<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(
+            n, c->parent.p, c->gsize.p, (uint32_t)std::max<int64_t>(min_size, 1), c->scratch_u32.p, c->counters.p + 9));
+    CC_CUDA(c, cudaGetLastError());
+    CC_CUDA(c, cudaMemcpyAsync(c->h_counters, c->counters.p + 9, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    const int64_t k = (int64_t)c->h_counters[0];
+    std::vector<uint32_t> h((size_t)k);
+    if (k > 0) {
+        CC_CUDA(c, cudaMemcpyAsync(h.data(), c->scratch_u32.p, (size_t)k * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                   c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    }
+    std::sort(h.begin(), h.end(), [](uint32_t a, uint32_t b) { return a > b; });
+    for (int64_t q = 0; q < k && q < cap; q++) sizes_h[q] = h[(size_t)q];
+    *n_h = k;
+    return CC_OK;
+}
+
+}  // namespace cc

@@ -1,0 +1,253 @@
+// pairs.cu -- K2, vulnerable-pair search (S2) and CSR rows of the editable set (S3).
+//
+// Paper: §III-A P:396 (vulnerable pairs: original distance in (b - 2 sqrt3 xi, b + 2 sqrt3 xi];
+// editable particles = their endpoints), Alg. 1 line 3 P:421, §III-B P:442 (cell side
+// w >= b + 2 sqrt3 xi; same and adjacent cells), §III-C P:463 (two-pass count/fill, direct-address
+// map of editable particles), §IV-C P:178.
+//
+// B200 form: one thread per particle in cell-sorted order scans the 27-cell neighbourhood
+// (x-adjacent cells merged into one contiguous slot range, so 9 ranges), reading float4
+// records that neighbouring threads share through L1/L2.  Pass 1 counts each particle's band
+// partners (the row length, no atomics); an exclusive scan gives row offsets AND the editable
+// ranks (the paper's direct-address map, without atomicCAS); pass 2 writes each row's u32
+// entries (partner editable index | partner-gid-above bit | original-link bit).  Rows are then
+// sorted by partner gid so the PGD gradient sum has one defined order on any grid / rank (R14).
+// Each unordered pair is tested from both endpoints: both see the identical pinned fp32 d2.
+#include "cc_internal.cuh"
+
+namespace cc {
+namespace {
+
+constexpr int PAIR_THREADS = 256;
+
+// pass 1: deg[s] = number of band partners of slot s (owned particles only); ghost partners
+// of owned particles get bit 31 of their deg word (multi-GPU: they become ghost editables).
+__global__ void __launch_bounds__(PAIR_THREADS)
+k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
+              const uint32_t* __restrict__ cs, Grid g, Th t, uint32_t n_own, uint32_t* __restrict__ deg) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    if (__float_as_uint(dec4[s].w) >= n_own) return;  // ghost: no row
+    const float4 p = orig4[s];
+    int cx, cy, cz;
+    cell_of(p.x, p.y, p.z, g, cx, cy, cz);
+    uint32_t cnt = 0;
+    const bool multi = n_own < (uint32_t)n;
+    for_each_neighbour_range(g, cs, cx, cy, cz, t.periodic != 0, [&](uint32_t a, uint32_t b) {
+        for (uint32_t j = a; j < b; j++) {
+            if (j == (uint32_t)s) continue;
+            const float4 q = orig4[j];
+            const float d2 = dist2(p, q, t);
+            if (t.lo2 < d2 && d2 <= t.hi2) {
+                cnt++;
+                if (multi && __float_as_uint(dec4[j].w) >= n_own) atomicOr(&deg[j], 0x80000000u);
+            }
+        }
+    });
+    deg[s] = (deg[s] & 0x80000000u) | cnt;  // own word never carries the ghost bit
+}
+
+__device__ __forceinline__ uint32_t resolve_eidx(uint32_t e, uint32_t e_own) {
+    return (e & 0x80000000u) ? e_own + (e & 0x7FFFFFFFu) : e;
+}
+
+// pass 2: write the row of every owned editable slot
+__global__ void __launch_bounds__(PAIR_THREADS)
+k_pairs_fill(int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
+             const uint32_t* __restrict__ cs, Grid g, Th t, uint32_t n_own, const uint32_t* __restrict__ deg,
+             const unsigned long long* __restrict__ rowoff, const uint32_t* __restrict__ eidx, uint32_t e_own,
+             uint32_t* __restrict__ rows) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    if ((deg[s] & 0x7FFFFFFFu) == 0) return;
+    const float4 p = orig4[s];
+    const uint32_t gp = __float_as_uint(p.w);
+    int cx, cy, cz;
+    cell_of(p.x, p.y, p.z, g, cx, cy, cz);
+    unsigned long long k = rowoff[s];
+    for_each_neighbour_range(g, cs, cx, cy, cz, t.periodic != 0, [&](uint32_t a, uint32_t b) {
+        for (uint32_t j = a; j < b; j++) {
+            if (j == (uint32_t)s) continue;
+            const float4 q = orig4[j];
+            const float d2 = dist2(p, q, t);
+            if (t.lo2 < d2 && d2 <= t.hi2) {
+                uint32_t ent = resolve_eidx(eidx[j], e_own);
+                if (__float_as_uint(q.w) > gp) ent |= ENT_UPPER;
+                if (d2 <= t.b2) ent |= ENT_OLINK;
+                rows[k++] = ent;
+            }
+        }
+    });
+}
+
+// compaction: editable e -> slot, row start, original and starting position
+__global__ void __launch_bounds__(PAIR_THREADS)
+k_compact(int64_t n, const uint32_t* __restrict__ deg, const uint32_t* __restrict__ eidx,
+          const unsigned long long* __restrict__ rowoff, const float4* __restrict__ orig4,
+          const float4* __restrict__ dec4, uint32_t e_own, unsigned long long nent, uint32_t* __restrict__ slotE,
+          unsigned long long* __restrict__ rowptr, float4* __restrict__ origE, float4* __restrict__ posA) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const uint32_t e0 = eidx[s];
+    if (e0 == 0xFFFFFFFFu) return;
+    const uint32_t e = resolve_eidx(e0, e_own);
+    const float4 o = orig4[s], d = dec4[s];
+    slotE[e] = (uint32_t)s;
+    rowptr[e] = (e < e_own) ? rowoff[s] : nent;
+    origE[e] = o;
+    posA[e] = make_float4(d.x, d.y, d.z, o.w);
+}
+
+__global__ void k_rowptr_tail(unsigned long long* rowptr, uint32_t e_all, unsigned long long nent) {
+    rowptr[e_all] = nent;
+}
+
+constexpr int SHORT_ROW = 32;
+constexpr int LONG_SORT_MAX = 4096;  // block bitonic capacity (entries)
+
+__device__ __forceinline__ unsigned long long row_key(uint32_t ent, const float4* __restrict__ posA) {
+    return ((unsigned long long)__float_as_uint(posA[ent & ENT_IDX].w) << 32) | ent;
+}
+
+// sort each row by partner gid: rows <= SHORT_ROW in registers (insertion sort), longer rows
+// queued for the block kernel
+__global__ void __launch_bounds__(PAIR_THREADS)
+k_sort_short(uint32_t e_own, const unsigned long long* __restrict__ rowptr, const float4* __restrict__ posA,
+             uint32_t* __restrict__ rows, uint32_t* __restrict__ long_list, unsigned long long* __restrict__ n_long) {
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= e_own) return;
+    const unsigned long long a = rowptr[e], b = rowptr[e + 1];
+    const int len = (int)(b - a);
+    if (len <= 1) return;
+    if (len > SHORT_ROW) {
+        unsigned long long q = atomicAdd(n_long, 1ull);
+        long_list[q] = e;
+        return;
+    }
+    unsigned long long v[SHORT_ROW];
+    for (int i = 0; i < len; i++) {
+        unsigned long long x = row_key(rows[a + i], posA);
+        int j = i - 1;
+        while (j >= 0 && v[j] > x) {
+            v[j + 1] = v[j];
+            j--;
+        }
+        v[j + 1] = x;
+    }
+    for (int i = 0; i < len; i++) rows[a + i] = (uint32_t)v[i];
+}
+
+// long rows: one block per row, bitonic sort in shared memory (<= LONG_SORT_MAX entries), and
+// a serial in-place insertion sort by one thread beyond that (rare: only at xi ~ spacing)
+__global__ void __launch_bounds__(512)
+k_sort_long(const uint32_t* __restrict__ long_list, const unsigned long long* __restrict__ n_long,
+            const unsigned long long* __restrict__ rowptr, const float4* __restrict__ posA, uint32_t* __restrict__ rows) {
+    __shared__ unsigned long long sh[LONG_SORT_MAX];
+    const unsigned long long nl = *n_long;
+    for (unsigned long long q = blockIdx.x; q < nl; q += gridDim.x) {
+        const uint32_t e = long_list[q];
+        const unsigned long long a = rowptr[e], b = rowptr[e + 1];
+        const int len = (int)(b - a);
+        if (len <= LONG_SORT_MAX) {
+            int p2 = 1;
+            while (p2 < len) p2 <<= 1;
+            for (int i = threadIdx.x; i < p2; i += blockDim.x)
+                sh[i] = i < len ? row_key(rows[a + i], posA) : ~0ull;
+            __syncthreads();
+            for (int k = 2; k <= p2; k <<= 1) {
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+                        int ij = i ^ j;
+                        if (ij > i) {
+                            bool up = (i & k) == 0;
+                            unsigned long long x = sh[i], y = sh[ij];
+                            if ((x > y) == up) {
+                                sh[i] = y;
+                                sh[ij] = x;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            for (int i = threadIdx.x; i < len; i += blockDim.x) rows[a + i] = (uint32_t)sh[i];
+            __syncthreads();
+        } else if (threadIdx.x == 0) {
+            for (int i = 1; i < len; i++) {
+                uint32_t x = rows[a + i];
+                unsigned long long kx = row_key(x, posA);
+                int j = i - 1;
+                while (j >= 0 && row_key(rows[a + j], posA) > kx) {
+                    rows[a + j + 1] = rows[a + j];
+                    j--;
+                }
+                rows[a + j + 1] = x;
+            }
+        }
+    }
+}
+
+}  // namespace
+
+cc_status pairs_count(cc_ctx* c) {
+    const int64_t n = c->n;
+    CC_TRY(cc_ensure(c, c->deg, (size_t)std::max<int64_t>(n, 1), "deg"));
+    CC_CUDA(c, cudaMemsetAsync(c->deg.p, 0, (size_t)std::max<int64_t>(n, 1) * sizeof(uint32_t), c->stream));
+    if (n > 0) {
+        int tok = cc_prof_begin(c, "K2_count");
+        CCL(c, k_pairs_count<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
+            n, c->orig4.p, c->dec4.p, c->cell_start.p, c->g, c->th, (uint32_t)c->n_in, c->deg.p));
+        cc_prof_end(c, tok);
+        CC_CUDA(c, cudaGetLastError());
+    }
+    return CC_OK;
+}
+
+cc_status pairs_fill(cc_ctx* c) {
+    const int64_t n = c->n;
+    CC_TRY(cc_ensure(c, c->rows, (size_t)std::max<int64_t>(c->nent, 1), "rows"));
+    if (n > 0 && c->nent > 0) {
+        int tok = cc_prof_begin(c, "K2_fill");
+        CCL(c, k_pairs_fill<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
+            n, c->orig4.p, c->dec4.p, c->cell_start.p, c->g, c->th, (uint32_t)c->n_in, c->deg.p,
+            reinterpret_cast<const unsigned long long*>(c->rowoff.p), c->eidx.p, (uint32_t)c->E, c->rows.p));
+        cc_prof_end(c, tok);
+        CC_CUDA(c, cudaGetLastError());
+    }
+    return CC_OK;
+}
+
+cc_status rows_finish(cc_ctx* c) {
+    const int64_t n = c->n, Ea = c->E_all;
+    const size_t e1 = (size_t)std::max<int64_t>(Ea, 1);
+    CC_TRY(cc_ensure(c, c->slotE, e1, "slotE"));
+    CC_TRY(cc_ensure(c, c->rowptr, e1 + 1, "rowptr"));
+    CC_TRY(cc_ensure(c, c->origE, e1, "origE"));
+    CC_TRY(cc_ensure(c, c->posA, e1, "posA"));
+    CC_TRY(cc_ensure(c, c->posB, e1, "posB"));
+    unsigned long long* rowptr = reinterpret_cast<unsigned long long*>(c->rowptr.p);
+    int tok = cc_prof_begin(c, "K2_compact");
+    if (n > 0)
+        CCL(c, k_compact<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
+            n, c->deg.p, c->eidx.p, reinterpret_cast<const unsigned long long*>(c->rowoff.p), c->orig4.p, c->dec4.p,
+            (uint32_t)c->E, (unsigned long long)c->nent, c->slotE.p, rowptr, c->origE.p, c->posA.p));
+    CCL(c, k_rowptr_tail<<<1, 1, 0, c->stream>>>(rowptr, (uint32_t)Ea, (unsigned long long)c->nent));
+    cc_prof_end(c, tok);
+    CC_CUDA(c, cudaGetLastError());
+    CC_TRY(pairs_fill(c));
+    if (c->E > 0 && c->nent > 0) {
+        CC_TRY(cc_ensure(c, c->scratch_u32, (size_t)c->E, "long rows"));
+        CC_TRY(cc_ensure(c, c->scratch_u64, 2, "long count"));
+        CC_CUDA(c, cudaMemsetAsync(c->scratch_u64.p, 0, sizeof(uint64_t), c->stream));
+        unsigned long long* nl = reinterpret_cast<unsigned long long*>(c->scratch_u64.p);
+        int t2 = cc_prof_begin(c, "K2_sort");
+        CCL(c, k_sort_short<<<(unsigned)((c->E + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
+            (uint32_t)c->E, rowptr, c->posA.p, c->rows.p, c->scratch_u32.p, nl));
+        CCL(c, k_sort_long<<<148 * 2, 512, 0, c->stream>>>(c->scratch_u32.p, nl, rowptr, c->posA.p, c->rows.p));
+        cc_prof_end(c, t2);
+        CC_CUDA(c, cudaGetLastError());
+    }
+    return CC_OK;
+}
+
+}  // namespace cc

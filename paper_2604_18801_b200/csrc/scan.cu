@@ -1,0 +1,176 @@
+// scan.cu -- device-wide exclusive prefix sums (reduce-then-scan, 3 launches) used by S1
+// (cell histogram -> cell_start, §III-C P:461 "device-wide exclusive prefix sum") and S3
+// (degrees -> CSR row offsets and editable ranks, the paper's direct-address map P:463).
+#include "cc_internal.cuh"
+
+namespace cc {
+namespace {
+
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+struct VU32 {
+    uint32_t a;
+    __device__ static VU32 zero() { return {0u}; }
+    __device__ VU32 operator+(const VU32& o) const { return {a + o.a}; }
+    __device__ VU32 shfl_up(int d) const { return {__shfl_up_sync(0xffffffffu, a, d)}; }
+    __device__ VU32 shfl(int src) const { return {__shfl_sync(0xffffffffu, a, src)}; }
+};
+
+// degree scan value: a = row entries, b = owned editable rank, c = ghost editable rank
+struct VDeg {
+    unsigned long long a;
+    uint32_t b, c;
+    __device__ static VDeg zero() { return {0ull, 0u, 0u}; }
+    __device__ VDeg operator+(const VDeg& o) const { return {a + o.a, b + o.b, c + o.c}; }
+    __device__ VDeg shfl_up(int d) const {
+        return {__shfl_up_sync(0xffffffffu, a, d), __shfl_up_sync(0xffffffffu, b, d),
+                __shfl_up_sync(0xffffffffu, c, d)};
+    }
+    __device__ VDeg shfl(int s) const {
+        return {__shfl_sync(0xffffffffu, a, s), __shfl_sync(0xffffffffu, b, s), __shfl_sync(0xffffffffu, c, s)};
+    }
+};
+
+struct LoadU32 {
+    const uint32_t* in;
+    __device__ VU32 operator()(int64_t i) const { return {in[i]}; }
+};
+struct StoreU32 {
+    uint32_t* out;
+    __device__ void operator()(int64_t i, const VU32& v, const VU32&) const { out[i] = v.a; }
+};
+
+// deg[s] > 0 -> owned editable; deg == 0 but marked (ghost partner, dec4.w index >= n_own
+// and flagged with bit 31 of deg) -> ghost editable.
+struct LoadDeg {
+    const uint32_t* deg;
+    __device__ VDeg operator()(int64_t i) const {
+        uint32_t d = deg[i];
+        uint32_t ghost = d >> 31;
+        uint32_t k = d & 0x7FFFFFFFu;
+        return {(unsigned long long)k, (k > 0u) ? 1u : 0u, ghost};
+    }
+};
+struct StoreDeg {
+    unsigned long long* rowoff;
+    uint32_t* eidx;
+    __device__ void operator()(int64_t i, const VDeg& excl, const VDeg& self) const {
+        rowoff[i] = excl.a;
+        // owned editables take ranks [0, E_own); ghost editables get (1<<31 | ghost rank),
+        // finalised once E_own is known (rows_finish)
+        eidx[i] = self.b ? excl.b : (self.c ? (0x80000000u | excl.c) : 0xFFFFFFFFu);
+    }
+};
+
+// inclusive warp scan then block exclusive scan; returns exclusive prefix, *total = sum
+template <class V>
+__device__ V block_exclusive(V v, V* total) {
+    __shared__ V sh[SCAN_THREADS / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    V inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        V u = inc.shfl_up(o);
+        if (lane >= o) inc = inc + u;
+    }
+    if (lane == 31) sh[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        V s = lane < SCAN_THREADS / 32 ? sh[lane] : V::zero();
+        V si = s;
+        for (int o = 1; o < 32; o <<= 1) {
+            V u = si.shfl_up(o);
+            if (lane >= o) si = si + u;
+        }
+        if (lane < SCAN_THREADS / 32) sh[lane] = si;  // inclusive warp totals
+    }
+    __syncthreads();
+    V wex = (w == 0) ? V::zero() : sh[w - 1];
+    *total = sh[SCAN_THREADS / 32 - 1];
+    V ex = inc.shfl_up(1);
+    if (lane == 0) ex = V::zero();
+    __syncthreads();
+    return wex + ex;
+}
+
+template <class V, class Load>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(int64_t n, Load load, V* bsum) {
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    V s = V::zero();
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; k++)
+        if (base + k < n) s = s + load(base + k);
+    V tot;
+    (void)block_exclusive(s, &tot);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+template <class V>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_blocks(int64_t nb, V* bsum, V* total) {
+    V carry = V::zero();
+    for (int64_t off = 0; off < nb; off += SCAN_THREADS) {
+        int64_t i = off + threadIdx.x;
+        V v = i < nb ? bsum[i] : V::zero();
+        V tot;
+        V ex = block_exclusive(v, &tot);
+        if (i < nb) bsum[i] = carry + ex;
+        carry = carry + tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && total) *total = carry;
+}
+
+template <class V, class Load, class Store>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_down(int64_t n, Load load, Store store, const V* bsum) {
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    V item[SCAN_ITEMS];
+    V s = V::zero();
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; k++) {
+        item[k] = (base + k < n) ? load(base + k) : V::zero();
+        s = s + item[k];
+    }
+    V tot;
+    V run = bsum[blockIdx.x] + block_exclusive(s, &tot);
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; k++) {
+        if (base + k < n) store(base + k, run, item[k]);
+        run = run + item[k];
+    }
+}
+
+template <class V, class Load, class Store>
+cc_status scan_generic(cc_ctx* c, int64_t n, Load load, Store store, V* total_dev, const char* name) {
+    if (n <= 0) {
+        if (total_dev) CC_CUDA(c, cudaMemsetAsync(total_dev, 0, sizeof(V), c->stream));
+        return CC_OK;
+    }
+    const int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    CC_TRY(cc_ensure(c, c->tmp_bytes, (size_t)nb * sizeof(V) + 256, "scan scratch"));
+    V* bsum = reinterpret_cast<V*>(c->tmp_bytes.p);
+    int tok = cc_prof_begin(c, name);
+    CCL(c, k_scan_reduce<V, Load><<<(unsigned)nb, SCAN_THREADS, 0, c->stream>>>(n, load, bsum));
+    CCL(c, k_scan_blocks<V><<<1, SCAN_THREADS, 0, c->stream>>>(nb, bsum, total_dev));
+    CCL(c, k_scan_down<V, Load, Store><<<(unsigned)nb, SCAN_THREADS, 0, c->stream>>>(n, load, store, bsum));
+    cc_prof_end(c, tok);
+    CC_CUDA(c, cudaGetLastError());
+    return CC_OK;
+}
+
+}  // namespace
+
+cc_status scan_u32_to_u32(cc_ctx* c, const uint32_t* in, uint32_t* out, int64_t n, uint64_t* total_dev) {
+    static_assert(sizeof(VU32) == 4, "");
+    // total written as u32 into the low half of *total_dev (caller zeroes it)
+    return scan_generic<VU32>(c, n, LoadU32{in}, StoreU32{out}, reinterpret_cast<VU32*>(total_dev), "K1_scan");
+}
+
+cc_status scan_deg(cc_ctx* c, const uint32_t* deg, uint64_t* rowoff, uint32_t* eidx, int64_t n,
+                   const float4*, int64_t, unsigned long long* totals_dev) {
+    static_assert(sizeof(VDeg) == 16, "");
+    return scan_generic<VDeg>(c, n, LoadDeg{deg}, StoreDeg{reinterpret_cast<unsigned long long*>(rowoff), eidx},
+                              reinterpret_cast<VDeg*>(totals_dev), "K2_scan");
+}
+
+}  // namespace cc

@@ -1,0 +1,200 @@
+"""GPU parity tests: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded
+inputs, element by element (tests/parity.py states the bar).  Sizes span several tiles and a
+ragged tail; edge cases: empty and tiny inputs, everything in one cell, coincident particles,
+coordinates at 0 and L-, exact fp32 thresholds, all stop modes, both optimisers, and CUDA-graph
+batch sizes that force speculative overrun."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2604_18801_b200 as cc
+import synth
+from tests.parity import assert_parity, check_invariants, gpu_pipeline, oracle_pipeline
+
+pytestmark = pytest.mark.gpu
+
+
+def _arrs(w, dither=True):
+    return [t.numpy() for t in synth.make(w, dither=dither)]
+
+
+def _params(w, **kw):
+    return cc.Params(box=w.L, b=w.linking_length, xi=w.xi, **kw)
+
+
+@pytest.mark.parametrize("xi_rel,dither", [(1e-3, True), (1e-4, True), (1e-3, False), (3e-3, True)])
+def test_c1_full_pipeline_bit_exact(xi_rel, dither):
+    """configs[0]: clumped N = 65,536, b = 0.2 mean spacing."""
+    w = synth.Workload("C1", "clumped", 65_536, 1.0, xi_rel, seed=1)
+    arrs = _arrs(w, dither)
+    p = _params(w)
+    g = gpu_pipeline(arrs, p)
+    o = oracle_pipeline(arrs, p)
+    assert_parity(g, o)
+    check_invariants(arrs, g["out"], p, g["info"])
+    if g["info"]["converged"]:
+        assert g["mcc_cor"]["mcc"] == 1.0
+        assert np.array_equal(g["lab_orig"], g["lab_cor"])
+
+
+@pytest.mark.parametrize("xi_rel", [1e-4, 1e-3])
+def test_c2_lattice_bit_exact(xi_rel):
+    """configs[1]: FPM-shaped N = 196,066 quasi-uniform cloud."""
+    w = synth.Workload("C2", "lattice", 196_066, 1.0, xi_rel, seed=2)
+    arrs = _arrs(w)
+    p = _params(w)
+    assert_parity(gpu_pipeline(arrs, p), oracle_pipeline(arrs, p))
+
+
+def test_c3_fcc_bit_exact():
+    """configs[2]: EXAALT-shaped N = 2,869,440 FCC crystal, b = 0.8 a."""
+    w = synth.CONFIGS["C3"]
+    w = synth.Workload("C3", "fcc", w.n, w.L, 1e-5, b=w.b, seed=w.seed, extra=w.extra)
+    arrs = _arrs(w)
+    p = _params(w)
+    assert_parity(gpu_pipeline(arrs, p), oracle_pipeline(arrs, p))
+
+
+@pytest.mark.parametrize("mode,tmax", [(cc.STOP_NONE, 7), (cc.STOP_NONE, 40), (cc.STOP_EPS, 10000), (cc.STOP_ACTIVE, 5)])
+def test_stop_modes_bit_exact(mode, tmax):
+    """Alg. 1 stop variants: truncated (exactly t_max updates), eps_L, active-count with a cap
+    that ends the loop unconverged."""
+    w = synth.Workload("t", "clumped", 20_000, 1.0, 1e-3, seed=7)
+    arrs = _arrs(w)
+    p = _params(w, stop_mode=mode, t_max=tmax)
+    g = gpu_pipeline(arrs, p, fof=False)
+    o = oracle_pipeline(arrs, p, fof=False)
+    assert_parity(g, o, fof=False)
+    if mode == cc.STOP_NONE:
+        assert g["info"]["iterations"] == tmax
+
+
+@pytest.mark.parametrize("batch", [1, 3, 16, 64])
+def test_graph_batch_does_not_change_result(batch):
+    """The speculative device-side stop is exact for any graph batch (R11, S5)."""
+    w = synth.Workload("t", "clumped", 30_000, 1.0, 1e-3, seed=8)
+    arrs = _arrs(w)
+    p = _params(w, graph_batch=batch)
+    assert_parity(gpu_pipeline(arrs, p, fof=False), oracle_pipeline(arrs, p, fof=False), fof=False)
+
+
+def test_vanilla_pgd_bit_exact():
+    w = synth.Workload("t", "clumped", 20_000, 1.0, 1e-3, seed=9)
+    arrs = _arrs(w)
+    p = _params(w, optimizer=1, vanilla_step=2e-3, t_max=50, stop_mode=cc.STOP_NONE)
+    assert_parity(gpu_pipeline(arrs, p, fof=False), oracle_pipeline(arrs, p, fof=False), fof=False)
+
+
+@pytest.mark.parametrize("cells_per_particle", [0.05, 1.0, 64.0])
+def test_grid_resolution_does_not_change_result(cells_per_particle):
+    """The pair set is grid-independent (R1): coarse and fine grids give identical results."""
+    w = synth.Workload("t", "clumped", 25_000, 1.0, 1e-3, seed=10)
+    arrs = _arrs(w)
+    p = _params(w, cells_per_particle=cells_per_particle)
+    assert_parity(gpu_pipeline(arrs, p), oracle_pipeline(arrs, p))
+
+
+def _rand(rng, n, L=1.0):
+    p = (rng.random((n, 3)) * L).astype(np.float32)
+    p = np.where(p >= L, np.nextafter(np.float32(L), np.float32(0)), p)
+    return [p[:, 0].copy(), p[:, 1].copy(), p[:, 2].copy()]
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 255, 256, 257, 4099])
+def test_tiny_and_ragged_sizes(n):
+    rng = np.random.default_rng(n)
+    x, y, z = _rand(rng, n)
+    xi = 2e-3
+    noise = [(a + rng.uniform(-xi * 0.99, xi * 0.99, n)).astype(np.float32) for a in (x, y, z)]
+    p = cc.Params(box=1.0, b=0.06, xi=xi)
+    arrs = [x, y, z, *noise]
+    assert_parity(gpu_pipeline(arrs, p), oracle_pipeline(arrs, p))
+
+
+def test_everything_in_one_cell_and_coincident_points():
+    """A dense blob (one cell holds most particles) with exact duplicates and the coincident
+    false-pair rule (R15); coordinates at 0 and L-."""
+    rng = np.random.default_rng(5)
+    n = 3000
+    c = np.float32(0.5)
+    p = (c + rng.normal(0, 0.01, (n, 3))).astype(np.float32)
+    p[100:200] = p[0:100]          # exact duplicates
+    p[200:210] = 0.0
+    p[210:220] = np.nextafter(np.float32(1.0), np.float32(0))
+    x, y, z = p[:, 0].copy(), p[:, 1].copy(), p[:, 2].copy()
+    xi = 1e-3
+    noise = [np.clip(a + rng.uniform(-xi * 0.99, xi * 0.99, n).astype(np.float32), a - np.float32(xi * 0.99),
+                     a + np.float32(xi * 0.99)).astype(np.float32) for a in (x, y, z)]
+    pr = cc.Params(box=1.0, b=0.02, xi=xi, t_max=300)
+    arrs = [x, y, z, *noise]
+    assert_parity(gpu_pipeline(arrs, pr), oracle_pipeline(arrs, pr))
+
+
+def test_gid_permutation():
+    """User-supplied gids: results are keyed by gid (R14, R20)."""
+    w = synth.Workload("t", "clumped", 10_000, 1.0, 1e-3, seed=12)
+    arrs = _arrs(w)
+    gid = np.random.default_rng(1).permutation(10_000).astype(np.uint32) * 3 + 7
+    p = _params(w)
+    assert_parity(gpu_pipeline(arrs, p, gid=gid), oracle_pipeline(arrs, p, gid=gid))
+
+
+def test_bound_violation_rejected():
+    x = torch.rand(100, device="cuda")
+    xh = x + 0.01
+    c = cc.Corrector(cc.Params(box=1.0, b=0.05, xi=1e-3))
+    with pytest.raises(cc.CCError, match="CC_E_BOUND"):
+        c.build_cells(x, x, x, xh, x, x)
+
+
+def test_state_machine():
+    c = cc.Corrector(cc.Params(box=1.0, b=0.05, xi=1e-3))
+    with pytest.raises(cc.CCError, match="CC_E_STATE"):
+        c.find_vulnerable()
+
+
+def test_run_host_buffers_equal_device_path():
+    """cc_run with HOST buffers (the e2e call) == the step-by-step device path."""
+    w = synth.Workload("t", "clumped", 40_000, 1.0, 1e-3, seed=13)
+    arrs = _arrs(w)
+    p = _params(w)
+    g = gpu_pipeline(arrs, p, fof=False)
+    host = [torch.as_tensor(a).pin_memory() for a in arrs]
+    out = [torch.empty(w.n, dtype=torch.float32).pin_memory() for _ in range(3)]
+    c = cc.Corrector(p)
+    r = c.run(*host, out=out, host=True)
+    assert r["corr"]["iterations"] == g["info"]["iterations"]
+    for a, b in zip(out, g["out"]):
+        assert np.array_equal(a.numpy().view(np.uint32), b.view(np.uint32))
+    dev = [torch.as_tensor(a).cuda() for a in arrs]
+    dout = [torch.empty(w.n, dtype=torch.float32, device="cuda") for _ in range(3)]
+    r2 = c.run(*dev, out=dout)
+    for a, b in zip(dout, g["out"]):
+        assert np.array_equal(a.cpu().numpy().view(np.uint32), b.view(np.uint32))
+
+
+def test_repeat_runs_bit_identical():
+    w = synth.Workload("t", "clumped", 30_000, 1.0, 1e-3, seed=14)
+    arrs = _arrs(w)
+    p = _params(w)
+    a = gpu_pipeline(arrs, p, fof=False)
+    b = gpu_pipeline(arrs, p, fof=False)
+    for u, v in zip(a["out"], b["out"]):
+        assert np.array_equal(u.view(np.uint32), v.view(np.uint32))
+    assert a["info"]["loss_final"] == b["info"]["loss_final"]
+
+
+def test_hmf_on_gpu_catalogue_matches_oracle():
+    w = synth.Workload("t", "clumped", 65_536, 1.0, 1e-3, seed=1)
+    arrs = _arrs(w)
+    p = _params(w)
+    g = gpu_pipeline(arrs, p)
+    e1, d1 = cc.hmf(g["halo_orig"], 1.0, 50)
+    e2, d2 = oracle.hmf(oracle.halo_catalog(oracle.fof(*arrs[:3], oracle.cfg(L=1.0, b=w.linking_length, xi=w.xi))[0]),
+                        1.0, 50)
+    assert np.allclose(d1, d2, rtol=1e-12) and np.allclose(e1, e2, atol=1e-12)
+    lo, hi = float(np.log10(g["halo_orig"].min())), float(np.log10(g["halo_orig"].max()))
+    _, d4 = cc.hmf(g["halo_orig"], 1.0, 50, lo=lo, hi=hi)
+    _, d3 = cc.hmf(g["halo_cor"], 1.0, 50, lo=lo, hi=hi)
+    assert np.array_equal(d4, d3)   # converged -> identical HMF on the original's bins (R22)
