@@ -107,29 +107,61 @@ def oracle_sample(w: synth.Workload, n_sample: int):
     return ws
 
 
-def run_oracle(ws: synth.Workload):
+def run_oracle(ws: synth.Workload, timeout: float = 120.0):
+    """The oracle's S1-S7 on a sample, in a child process (so a slow sample cannot hang the
+    bench); returns (seconds, iterations, |V|) or None on timeout."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--_oracle", json.dumps(
+        {"name": ws.name, "kind": ws.kind, "n": ws.n, "L": ws.L, "xi_rel": ws.xi_rel, "b": ws.linking_length,
+         "seed": ws.seed, "extra": ws.extra})]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    except subprocess.TimeoutExpired:
+        return None
+    if r.returncode != 0:
+        log("oracle sample failed:", r.stderr[-500:])
+        return None
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    return d["seconds"], d["iterations"], d["pairs"]
+
+
+def _oracle_child(spec: str) -> int:
     import oracle
+    d = json.loads(spec)
+    ws = synth.Workload(d["name"], d["kind"], d["n"], d["L"], d["xi_rel"], b=d["b"], seed=d["seed"],
+                        extra=d["extra"])
     arrs = [t.numpy() for t in synth.make(ws)]
     c = oracle.cfg(L=ws.L, b=ws.linking_length, xi=ws.xi)
+    oracle.build()
     t0 = time.perf_counter()
     r = oracle.pipeline(*arrs, c)
     dt = time.perf_counter() - t0
-    return dt, r
+    print(json.dumps({"seconds": dt, "iterations": r.info["iterations"], "pairs": int(len(r.pairs[0]))}))
+    return 0
 
 
 def cpu_baseline(w: synth.Workload, target_s: float = 15.0, n_sample=None):
     """Oracle on the host cores (1 thread), a sample sized to ~target_s of CPU work."""
-    n0 = n_sample or 200_000
+    n0 = n_sample or 50_000
     ws = oracle_sample(w, n0)
-    dt, r = run_oracle(ws)
-    if n_sample is None and dt < target_s / 3:
-        n1 = int(min(n0 * target_s / max(dt, 1e-3), 4_000_000))
-        ws = oracle_sample(w, n1)
-        dt, r = run_oracle(ws)
+    r = run_oracle(ws, timeout=4 * target_s)
+    if r is None:
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": f"{w.name} recipe at N={n0}: oracle did not finish within {4 * target_s:.0f} s"}
+    if n_sample is None and r[0] < target_s / 3:
+        n1 = int(min(n0 * target_s / max(r[0], 1e-3), 4_000_000))
+        ws1 = oracle_sample(w, n1)
+        r1 = run_oracle(ws1, timeout=4 * target_s)
+        if r1 is not None:
+            ws, r = ws1, r1
+    dt, iters, npairs = r
     return {"value": ws.n / dt / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{w.name} recipe at N={ws.n} (box {ws.L:.3f}, same density, b, xi): full S1-S7 oracle run "
-                      f"{dt:.2f} s, {r.info['iterations']} iterations, |V|={len(r.pairs[0])}",
-            "seconds": dt, "n": ws.n, "iterations": r.info["iterations"]}
+                      f"{dt:.2f} s, {iters} iterations, |V|={npairs}",
+            "seconds": dt, "n": ws.n, "iterations": iters}
+
+
+def log(*a):
+    print(f"[bench {time.strftime('%H:%M:%S')}]", *a, file=sys.stderr, flush=True)
 
 
 # ------------------------------------------------------------------------------------------
@@ -138,6 +170,46 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def _workload(args):
+    w0 = synth.CONFIGS[args.config]
+    if args.xi_rel is None and args.n is None:
+        return w0
+    n = args.n or w0.n
+    L = w0.L * (n / w0.n) ** (1.0 / 3.0) if args.n else w0.L
+    return synth.Workload(w0.name, w0.kind, n, L, args.xi_rel if args.xi_rel is not None else w0.xi_rel, eta=w0.eta,
+                          b=w0.linking_length if args.n else w0.b, seed=w0.seed, extra=w0.extra)
+
+
+def reference_arm(args, w, rank):
+    """--impl reference: the CPU oracle as it stands, a bounded sample of the workload per step."""
+    if rank != 0:
+        return 0
+    n_s = args.sample_n or 30_000
+    ws = oracle_sample(w, n_s)
+    times, last = [], None
+    for k in range(args.warmup + args.steps):
+        r = run_oracle(ws, timeout=300)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": f"oracle sample N={n_s} exceeded 300 s"}))
+            return 0
+        if k >= args.warmup:
+            times.append(r[0])
+        last = r
+    dt = statistics.mean(times)
+    v = ws.n / dt / 1e6
+    sample = (f"{w.name} recipe at N={ws.n} (box {ws.L:.3f}, same density, b, xi), single-threaded C oracle, "
+              f"full S1-S7, {last[1]} iterations, |V|={last[2]}")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {**w.describe(), "workload": w.name, "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+    return 0
 
 
 def main():
@@ -149,42 +221,20 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--xi-rel", type=float, default=None)
     ap.add_argument("--n", type=int, default=None, help="override N (same density recipe)")
+    ap.add_argument("--t-max", type=int, default=10000)
     ap.add_argument("--cells-per-particle", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sample-n", type=int, default=None)
+    ap.add_argument("--_oracle", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args._oracle:
+        return _oracle_child(args._oracle)
 
     rank, world, local = dist_env()
-    w0 = synth.CONFIGS[args.config]
-    w = w0
-    if args.xi_rel is not None or args.n is not None:
-        n = args.n or w0.n
-        L = w0.L * (n / w0.n) ** (1.0 / 3.0) if args.n else w0.L
-        w = synth.Workload(w0.name, w0.kind, n, L, args.xi_rel if args.xi_rel is not None else w0.xi_rel,
-                           eta=w0.eta, b=w0.linking_length if args.n else w0.b, seed=w0.seed, extra=w0.extra)
-
+    w = _workload(args)
     if args.impl == "reference":
-        if rank != 0:
-            return 0
-        steps = []
-        for k in range(args.warmup + args.steps):
-            r = cpu_baseline(w, target_s=8.0, n_sample=args.sample_n or 300_000)
-            if k >= args.warmup:
-                steps.append(r)
-        v = statistics.mean(s["value"] for s in steps)
-        ms = statistics.mean(s["seconds"] for s in steps) * 1e3
-        cb = dict(steps[-1])
-        cb["value"] = v
-        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": w.name, **w.describe(), "sample": cb["sample"]},
-                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-                "gpu_launches": 0}
-        print(json.dumps(line), flush=True)
-        return 0
+        return reference_arm(args, w, rank)
 
     import paper_2604_18801_b200 as cc
 
@@ -193,22 +243,37 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    stream = torch.cuda.current_stream(dev)
-
-    # inputs resident in HBM (drawn on the GPU; same recipe as the parity tests)
+    stream = torch.cuda.Stream(device=dev)
+    log(f"rank {rank}/{world}: drawing {w.name} N={w.n:,} on {dev}")
     x, y, z, xh, yh, zh = synth.make(w, device=dev)
+    n_total = w.n
+    gid = None
+    if world > 1:
+        own = (cc.slab_of(x, world, w.L) == rank).nonzero().flatten()
+        x, y, z, xh, yh, zh = [a[own].contiguous() for a in (x, y, z, xh, yh, zh)]
+        gid = own.to(torch.int32)
+        del own
     torch.cuda.synchronize(dev)
-    n = w.n
-    params = cc.Params(box=w.L, b=w.linking_length, xi=w.xi, profile=1)
+    n = x.shape[0]
+    params = cc.Params(box=w.L, b=w.linking_length, xi=w.xi, profile=1, t_max=args.t_max)
     if args.cells_per_particle:
         params.cells_per_particle = args.cells_per_particle
-    c = cc.Corrector(params, device=local, stream=stream)
-    out = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(3)]
-    lab_o = torch.empty(n, dtype=torch.int32, device=dev)
-    lab_c = torch.empty(n, dtype=torch.int32, device=dev)
+    distarg = None
+    if world > 1:
+        uid = [cc.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(uid, src=0)
+        distarg = (rank, world, uid[0])
+    c = cc.Corrector(params, device=local, stream=stream, dist=distarg)
+    with torch.cuda.stream(stream):
+        out = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(3)]
+        lab_o = torch.empty(max(n, 1), dtype=torch.int32, device=dev)[:n]
+        lab_c = torch.empty(max(n, 1), dtype=torch.int32, device=dev)[:n]
+    # L2 flush buffer (only needed when the inputs fit in the 126 MB L2)
+    small = 24 * n < 512 * 2**20
+    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=dev) if small else None
 
     def step():
-        c.build_cells(x, y, z, xh, yh, zh)
+        c.build_cells(x, y, z, xh, yh, zh, gid=gid)
         vp = c.find_vulnerable()
         _, info = c.correct(out)
         _, ng_o = c.fof_label(cc.CC_ORIG, lab_o)
@@ -218,43 +283,53 @@ def main():
         m = c.mcc(cc.CC_CORR)
         return vp, info, m, ng_o, ng_c, h_o, h_c
 
-    for _ in range(args.warmup):
+    for k in range(args.warmup):
+        t0 = time.perf_counter()
         res = step()
+        log(f"warmup {k}: {time.perf_counter() - t0:.3f} s wall, |V|={res[0]['n_pairs']:,} |E|={res[0]['n_editable']:,}"
+            f" iterations={res[1]['iterations']} converged={res[1]['converged']} mcc={res[2]['mcc']:.6f}")
     c.kernel_stats(reset=True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
     clk = ClockSampler(local)
     clk.start()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
+    for k in range(args.steps):
+        if flush is not None:
+            with torch.cuda.stream(stream):
+                flush.fill_(float(k))
+        evs[k][0].record(stream)
         res = step()
-    ev1.record(stream)
+        evs[k][1].record(stream)
     torch.cuda.synchronize(dev)
-    ms_total = ev0.elapsed_time(ev1)
+    if world > 1:
+        torch.distributed.barrier()
     clocks = clk.stop()
+    ms_total = sum(a.elapsed_time(b) for a, b in evs)
     stats = c.kernel_stats(reset=True)
     if world > 1:
-        t = torch.tensor([ms_total], device=dev)
+        t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
     vp, info, m, ng_o, ng_c, h_o, h_c = res
-    value = world * n / (ms_step * 1e-3) / 1e6
+    value = n_total / (ms_step * 1e-3) / 1e6
+    log(f"timed: {ms_step:.3f} ms/step -> {value:.1f} Mparticles/s")
 
     # ---- roofline of the dominant kernel class (device time inside the timed region)
     hbm, sm_max, peak_src = _peaks()
     launches = stats.pop("total_launches", (0.0, 0))[1]
     E, nent = vp["n_editable"], 2 * vp["n_pairs"]
-    cls_ms = {k: v for k, v in stats.items()}
+    if world > 1:  # this rank's share for the per-launch byte count
+        E, nent = E / world, nent / world
+    cls_ms = dict(stats)
     dom = max(cls_ms, key=lambda k: cls_ms[k][0]) if cls_ms else None
-    # algorithmic bytes per launch (DESIGN.md §6)
+    # algorithmic bytes per launch (DESIGN.md §5)
     alg_bytes = {
         "K3_pgd": 104.0 * E + 4.0 * nent,
         "K1_key": 24.0 * n + 8.0 * n,
-        "K1_scatter": (24 + 8 + 4) * n + 36.0 * n,
+        "K1_gather": 8.0 * n + 28.0 * n + 40.0 * n,
         "K2_count": 16.0 * n + 4.0 * n,
         "K2_fill": 16.0 * n + 4.0 * n + 8.0 * n + 4.0 * nent,
         "K4_fof": 16.0 * n + 4 * 4.0 * n,
@@ -263,64 +338,74 @@ def main():
     if dom:
         d_ms, d_l = cls_ms[dom]
         avg_ms = d_ms / max(d_l, 1)
-        if dom in alg_bytes:
-            ach = alg_bytes[dom] / (avg_ms * 1e-3) / 1e9
-            roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                    "traffic": None, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
-                    "launch_ms": avg_ms, "launches": d_l}
-        else:
-            roof = {"bound": "hbm", "kernel": dom, "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
-                    "traffic": None, "launch_ms": avg_ms, "launches": d_l}
+        ach = alg_bytes[dom] / (avg_ms * 1e-3) / 1e9 if dom in alg_bytes else None
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
+                "frac": (ach / hbm) if ach is not None else None, "traffic": None,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})", "launch_ms": avg_ms, "launches": d_l}
     k3 = cls_ms.get("K3_pgd")
     k3_roof = None
     if k3 and k3[1]:
         a = alg_bytes["K3_pgd"] / (k3[0] / k3[1] * 1e-3) / 1e9
-        k3_roof = {"achieved_gbs": a, "frac": a / hbm, "launch_ms": k3[0] / k3[1], "launches": k3[1]}
+        k3_roof = {"achieved": a, "peak": hbm, "unit": "GB/s", "frac": a / hbm, "launch_ms": k3[0] / k3[1],
+                   "launches": k3[1]}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generator, drawn on the GPU)",
-        "config": {**w.describe(), "workload": w.name, "parallelism": "replicas" if world > 1 else "1 GPU",
-                   "l2": "inputs (6 x 4N B) larger than the 126 MB L2", "stop": "no L_tight-active pair (R11)",
-                   "cells_per_axis": vp["cells_per_axis"]},
-        "result": {"n_pairs": vp["n_pairs"], "n_editable": E, "violated0": vp["n_violated0"],
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded synth/ recipe, drawn on the GPU)",
+        "config": {**w.describe(), "workload": w.name,
+                   "parallelism": f"x-slabs x{world} (NCCL ghosts + per-iteration refresh/allreduce)" if world > 1
+                   else "1 GPU",
+                   "l2": "L2 flushed between steps (256 MB write)" if small else "inputs (24 N B) larger than the 126 MB L2",
+                   "stop": "no L_tight-active pair (R11)", "t_max": args.t_max, "rows_per_axis": vp["cells_per_axis"]},
+        "result": {"n_pairs": vp["n_pairs"], "n_editable": vp["n_editable"], "violated0": vp["n_violated0"],
                    "iterations": info["iterations"], "converged": info["converged"], "mcc_after": m["mcc"],
                    "fof_groups_orig": ng_o, "fof_groups_corr": ng_c, "halos_equal": bool(np.array_equal(h_o, h_c))},
         "roofline": roof, "k3_roofline": k3_roof,
-        "kernels_ms_per_step": {k: v[0] / args.steps for k, v in cls_ms.items()},
+        "kernels_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in cls_ms.items()},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
 
-    # ---- end to end through the public API with HOST buffers (pinned), copies inside
+    # ---- end to end through the public API (cc_run) with pinned HOST buffers, copies inside
     if not args.no_e2e:
         host = [t.cpu().pin_memory() for t in (x, y, z, xh, yh, zh)]
+        hgid = gid.cpu().pin_memory() if gid is not None else None
         hout = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(3)]
 
         def e2e_step():
-            r = c.run(*host, out=hout, host=True)
+            r = c.run(*host, out=hout, gid=hgid, host=True)
             c.fof_label(cc.CC_ORIG, lab_o)
             c.fof_label(cc.CC_CORR, lab_c)
-            mm = c.mcc(cc.CC_CORR)
-            return r, mm
+            return r, c.mcc(cc.CC_CORR)
 
         e2e_step()
+        ke = max(1, min(args.steps, 3))
+        if world > 1:
+            torch.distributed.barrier()
         torch.cuda.synchronize(dev)
-        ev0.record(stream)
-        for _ in range(max(1, min(args.steps, 3))):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ke):
             e2e_step()
-        ev1.record(stream)
+        e1.record(stream)
         torch.cuda.synchronize(dev)
-        e_ms = ev0.elapsed_time(ev1) / max(1, min(args.steps, 3))
-        line["e2e"] = {"value": world * n / (e_ms * 1e-3) / 1e6, "unit": UNIT, "ms_per_step": e_ms,
-                       "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 12 * n + 48}
+        e_ms = e0.elapsed_time(e1) / ke
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e_ms = float(t.item())
+        line["e2e"] = {"value": n_total / (e_ms * 1e-3) / 1e6, "unit": UNIT, "ms_per_step": e_ms,
+                       "h2d_bytes_per_step": (24 + (4 if gid is not None else 0)) * n_total,
+                       "d2h_bytes_per_step": 12 * n_total + 48}
+        log(f"e2e: {e_ms:.3f} ms/step")
         del host, hout
-    if rank == 0 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = {k: v for k, v in cpu_baseline(w).items() if k in
-                                ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        cb = cpu_baseline(w)
+        line["cpu_baseline"] = {k: v for k, v in cb.items() if k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    c.close()
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0

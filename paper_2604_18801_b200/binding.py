@@ -124,7 +124,7 @@ class Params:
     optimizer: int = 0
     vanilla_step: float = 0.0
     graph_batch: int = 16
-    cells_per_particle: float = 8.0
+    cells_per_particle: float = 2.0
     profile: int = 0
 
     def to_c(self) -> _Params:
@@ -273,6 +273,38 @@ class Corrector:
         vp = {k: getattr(info.vp, k) for k, _ in _VP._fields_}
         co = {k: getattr(info.corr, k) for k, _ in _Corr._fields_ if k != "pad"}
         return {"vp": vp, "corr": co, "status": st}
+
+
+def nccl_unique_id() -> bytes:
+    """cc_nccl_unique_id: 128 bytes for cc_dist.nccl_id_h (rank 0 creates, all ranks share)."""
+    buf = C.create_string_buffer(128)
+    st = lib().cc_nccl_unique_id(buf)
+    if st != 0:
+        raise CCError(st, "cc_nccl_unique_id")
+    return buf.raw
+
+
+def slab_of(x: torch.Tensor, nranks: int, box: float) -> torch.Tensor:
+    """Owner rank of each original x under the x-slab decomposition of cc_dist (rank r owns
+    [r L/R, (r+1) L/R)) -- the same fp64 rule the library checks."""
+    r = torch.floor(x.double() * (nranks / box)).long()
+    r = torch.clamp(r, 0, nranks - 1)
+    # guard the fp64 boundary rounding: re-test against the exact slab edges
+    lo = box * r.double() / nranks
+    hi = box * (r + 1).double() / nranks
+    xd = x.double()
+    r = torch.where(xd < lo, r - 1, torch.where(xd >= hi, r + 1, r))
+    return torch.clamp(r, 0, nranks - 1)
+
+
+def shell_masks(x: torch.Tensor, rank: int, nranks: int, box: float, gw: float):
+    """Owned particles sent as ghosts (§III-D): (to the left rank, to the right rank) =
+    (x < lo + gw, x >= hi - gw) for the slab [lo, hi) of `rank` -- the rule of dist.cu's
+    k_shell_flags, exposed for the host-side protocol tests."""
+    lo = box * rank / nranks
+    hi = box * (rank + 1) / nranks
+    xd = x.double()
+    return xd < lo + gw, xd >= hi - gw
 
 
 def hmf(sizes, vol: float, n_bins: int = 50, lo: float = 0.0, hi: float = 0.0):

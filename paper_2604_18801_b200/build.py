@@ -16,9 +16,18 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libcc.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir():
+    import nvidia.nccl  # torch's bundled NCCL 2.28 (headers + libnccl.so.2)
+    return os.path.dirname(list(nvidia.nccl.__path__)[0] + "/")
+
+
+NCCL = _nccl_dir()
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
-         f"-I{INCLUDE}"]
+         f"-I{INCLUDE}", f"-I{os.path.join(NCCL, 'include')}"]
+LDFLAGS = [f"-L{os.path.join(NCCL, 'lib')}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={os.path.join(NCCL, 'lib')}"]
 
 
 def sources():
@@ -48,7 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             subprocess.check_call(cmd)
         objs.append(obj)
     tmp = LIB + f".tmp{os.getpid()}"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, *LDFLAGS])
     os.replace(tmp, LIB)
     return LIB
 

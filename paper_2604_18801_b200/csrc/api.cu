@@ -64,6 +64,7 @@ CC_INST(unsigned long long)
 CC_INST(cc::Ctl)
 CC_INST(long long)
 CC_INST(unsigned char)
+CC_INST(uint2)
 
 // ------------------------------------------------------------------------------------------
 // profiling
@@ -148,33 +149,35 @@ static cc_status derive_params(cc_ctx* c, int64_t n_total) {
     t.periodic = p.periodic ? 1 : 0;
     // ghost / cell width: delta = b + 2 sqrt3 xi, never below the fp32 sqrt(hi2)
     c->delta = std::max(hi, std::sqrt((double)t.hi2));
+    c->r_pair = c->delta * (1.0 + 1e-5);  // search radius / ghost width (margin for fp32 rounding)
+    c->r_link = std::max(b, std::sqrt((double)t.b2)) * (1.0 + 1e-5);
     if (p.periodic && c->delta >= 0.5 * p.box)
         return cc_fail(c, CC_E_ARG, "b + 2 sqrt3 xi must be < box/2 for minimum-image distances");
     return CC_OK;
 }
 
-// grid: cells of side >= delta (1 + 1e-5) (margin for fp32 rounding of d2 and of positions),
-// at most K * N cells (perf knob, R25), >= 1 per axis.
+// Search structure (cc_internal.cuh "x-sorted rows"): rows of side >= r_pair = delta (1 + 1e-5)
+// in y and z (the margin covers fp32 rounding of d2 and of the coordinates), at most ~N rows;
+// each row cut into x-bins of width >= 2 r_pair with at most K * N cells in total (perf knob,
+// R25).  FoF on the original positions searches radius r_link = b (1 + 1e-5).
 static void choose_grid(cc_ctx* c, int64_t n_local, double x_extent, double x0, int xwrap) {
     const double L = c->p.box;
-    const double wmin = c->delta * (1.0 + 1e-5);
-    double K = c->p.cells_per_particle > 0 ? c->p.cells_per_particle : 8.0;
-    double cap = std::max(K * (double)std::max<int64_t>(n_local, 1), 27.0);
-    cap = std::min(cap, 2147483647.0);
-    int64_t nyz = std::max<int64_t>(1, (int64_t)std::floor(L / wmin));
-    int64_t nx = std::max<int64_t>(1, (int64_t)std::floor(x_extent / wmin));
-    // shrink uniformly until the cell budget holds (cells stay cubic: w = L / nyz)
-    while ((double)nx * nyz * nyz > cap && nyz > 1) {
-        nyz = std::max<int64_t>(1, (int64_t)std::floor(nyz * 0.97));
-        if (xwrap) nx = nyz;
-        else nx = std::max<int64_t>(1, (int64_t)std::ceil(x_extent * (double)nyz / L));
-    }
-    if (xwrap) nx = nyz;
+    const double K = c->p.cells_per_particle > 0 ? c->p.cells_per_particle : 2.0;
+    const double nl = (double)std::max<int64_t>(n_local, 1);
+    int64_t nyz = std::max<int64_t>(1, (int64_t)std::floor(L / c->r_pair));
+    while (nyz > 1 && (double)nyz * (double)nyz > std::max(nl, 9.0)) nyz = std::max<int64_t>(1, (int64_t)(nyz * 0.97));
+    const double rows = (double)nyz * (double)nyz;
+    int64_t nx_max = std::max<int64_t>(1, (int64_t)std::floor(x_extent / (2.0 * c->r_pair)));
+    int64_t nx = std::max<int64_t>(1, (int64_t)std::floor(K * nl / rows));
+    nx = std::min(nx, nx_max);
+    while ((double)nx * rows > 2147483647.0 && nx > 1) nx /= 2;
     c->g.ny = c->g.nz = (int)nyz;
     c->g.nx = (int)nx;
     c->g.inv_w = (double)nyz / L;
+    c->g.inv_wx = (double)nx / x_extent;
     c->g.x0 = x0;
     c->g.L = L;
+    c->g.ext_x = x_extent;
     c->g.xwrap = xwrap;
     c->ncell = (int64_t)nx * nyz * nyz;
 }
@@ -200,7 +203,7 @@ void cc_default_params(cc_params* p) {
     p->optimizer = CC_OPT_ADAM;
     p->vanilla_step = 0.0;
     p->graph_batch = 16;
-    p->cells_per_particle = 8.0;
+    p->cells_per_particle = 2.0;
     p->profile = 0;
 }
 
@@ -216,7 +219,8 @@ cc_status cc_create(cc_ctx** out, int device, void* stream, const cc_params* p, 
         cudaGetLastError();
         return CC_E_CUDA;
     }
-    if (dist && dist->nranks > 1) return CC_E_ARG;  // multi-GPU: not in this build yet
+    if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks)) return CC_E_ARG;
+    if (dist && dist->nranks > 1 && !p->periodic) return CC_E_ARG;  // slabs are periodic in x
     cc_ctx* c = new cc_ctx();
     c->device = device;
     c->p = *p;
@@ -236,12 +240,20 @@ cc_status cc_create(cc_ctx** out, int device, void* stream, const cc_params* p, 
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
+    c->owns_stream = (stream == nullptr);
     if (cudaMallocHost(&c->h_ctl, sizeof(cc::Ctl)) != cudaSuccess ||
-        cudaMallocHost(&c->h_counters, 16 * sizeof(unsigned long long)) != cudaSuccess) {
-        delete c;
+        cudaMallocHost(&c->h_counters, 16 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMallocHost(&c->h_red, 2 * sizeof(double)) != cudaSuccess) {
+        cc_destroy(c);
         return CC_E_CUDA;
     }
-    c->owns_stream = (stream == nullptr);
+    if (dist && dist->nranks > 1) {
+        cc_status st = cc::dist_init(c, dist);
+        if (st != CC_OK) {
+            cc_destroy(c);
+            return st;
+        }
+    }
     *out = c;
     return CC_OK;
 }
@@ -250,7 +262,7 @@ void cc_destroy(cc_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cc_release(c, c->orig4); cc_release(c, c->dec4); cc_release(c, c->cor4); cc_release(c, c->posA);
-    cc_release(c, c->posB); cc_release(c, c->origE);
+    cc_release(c, c->posB); cc_release(c, c->origE); cc_release(c, c->xs);
     cc_release(c, c->key); cc_release(c, c->rnk); cc_release(c, c->cell_count); cc_release(c, c->cell_start);
     cc_release(c, c->slot_of); cc_release(c, c->deg); cc_release(c, c->eidx); cc_release(c, c->rows);
     cc_release(c, c->slotE); cc_release(c, c->parent); cc_release(c, c->mingid); cc_release(c, c->gsize);
@@ -258,7 +270,17 @@ void cc_destroy(cc_ctx* c) {
     cc_release(c, c->mom); cc_release(c, c->bc); cc_release(c, c->partial_d); cc_release(c, c->partial_u);
     cc_release(c, c->counters); cc_release(c, c->ctl); cc_release(c, c->trace_a); cc_release(c, c->trace_l);
     cc_release(c, c->tmp_bytes); cc_release(c, c->in_f); cc_release(c, c->in_gid);
+    for (int d = 0; d < 2; d++) {
+        cc_release(c, c->dflag[d]); cc_release(c, c->dpos[d]); cc_release(c, c->shell[d]); cc_release(c, c->sbuf7[d]);
+        cc_release(c, c->rbuf7[d]); cc_release(c, c->req[d]); cc_release(c, c->recv_e[d]); cc_release(c, c->sreq[d]);
+        cc_release(c, c->send_e[d]); cc_release(c, c->lsb[d]); cc_release(c, c->lrb[d]); cc_release(c, c->rsb[d]);
+        cc_release(c, c->rrb[d]);
+    }
+    cc_release(c, c->stage); cc_release(c, c->gath); cc_release(c, c->dcnt); cc_release(c, c->red);
+    cc_release(c, c->bnd);
     cudaStreamSynchronize(c->stream);
+    cc::dist_destroy(c);
+    if (c->h_red) cudaFreeHost(c->h_red);
     if (c->pgd_exec) cudaGraphExecDestroy(c->pgd_exec);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     for (auto& pe : c->pend) {
@@ -274,7 +296,10 @@ void cc_destroy(cc_ctx* c) {
 
 const char* cc_last_error(const cc_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
-cc_status cc_nccl_unique_id(void*) { return CC_E_NCCL; }
+cc_status cc_nccl_unique_id(void* id) {
+    if (!id) return CC_E_ARG;
+    return cc::dist_unique_id(id);
+}
 
 #define CC_GUARD(c)                                                                          \
     do {                                                                                     \
@@ -291,11 +316,38 @@ cc_status cc_build_cells(cc_ctx* c, int64_t n, const float* x, const float* y, c
     if (n >= cc::MAX_LOCAL) return cc_fail(c, CC_E_DATA, "n beyond the 2^30 local index space");
     c->state = 0;
     c->have_labels[0] = c->have_labels[1] = c->have_labels[2] = 0;
-    CC_TRY(derive_params(c, n));
+    c->fof_which = -1;
+    int64_t n_total = n;
+    if (c->nranks > 1) {
+        if (n > 0 && !gid) return cc_fail(c, CC_E_ARG, "multi-GPU needs global particle ids (gid)");
+        CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
+        c->h_counters[7] = (unsigned long long)n;
+        CC_CUDA(c, cudaMemcpyAsync(c->counters.p + 7, c->h_counters + 7, sizeof(unsigned long long),
+                                   cudaMemcpyHostToDevice, c->stream));
+        CC_TRY(cc::dist_allreduce_u64(c, c->counters.p + 7, 1));
+        CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 7, c->counters.p + 7, sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+        n_total = (int64_t)c->h_counters[7];
+    }
+    CC_TRY(derive_params(c, n_total));
     c->n_in = n;
     c->n = n;
-    choose_grid(c, n, c->p.box, 0.0, c->p.periodic ? 1 : 0);
-    CC_TRY(cc::bin_particles(c, x, y, z, xh, yh, zh, gid, n));
+    if (c->nranks > 1) {
+        const double slab = c->slab_hi - c->slab_lo;
+        if (slab < 2.0 * c->r_pair)
+            return cc_fail(c, CC_E_ARG, "x slab narrower than two ghost widths (b + 2 sqrt3 xi); use fewer GPUs");
+        CC_TRY(cc::dist_exchange_ghosts(c, n, x, y, z, xh, yh, zh, gid));
+        const uint32_t* st = c->stage.p;
+        const size_t cap = (size_t)c->stage_cap;
+        const float* f = reinterpret_cast<const float*>(st);
+        const double x0 = std::fmod(c->slab_lo - c->r_pair + c->p.box, c->p.box);
+        choose_grid(c, c->n, slab + 2.0 * c->r_pair, x0, 0);
+        CC_TRY(cc::bin_particles(c, f, f + cap, f + 2 * cap, f + 3 * cap, f + 4 * cap, f + 5 * cap, st + 6 * cap, c->n));
+    } else {
+        choose_grid(c, n, c->p.box, 0.0, c->p.periodic ? 1 : 0);
+        CC_TRY(cc::bin_particles(c, x, y, z, xh, yh, zh, gid, n));
+    }
     CC_CUDA(c, cudaMemcpyAsync(c->h_counters, c->counters.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                c->stream));
     CC_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -325,16 +377,21 @@ cc_status cc_find_vulnerable(cc_ctx* c, cc_vp_info* info) {
     c->E_all = (int64_t)w1 + w2;
     if (c->E_all >= cc::MAX_LOCAL) return cc_fail(c, CC_E_DATA, "editable set beyond the 2^30 index space");
     CC_TRY(cc::rows_finish(c));
+    if (c->nranks > 1) CC_TRY(cc::dist_setup_refresh(c));
     c->state = 2;
     if (info) {
         unsigned long long* cnt = c->counters.p + 4;
         CC_TRY(cc::mcc_run(c, CC_DECOMP, cnt));
-        CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 4, cnt, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+        c->h_counters[8] = (unsigned long long)c->E;
+        CC_CUDA(c, cudaMemcpyAsync(c->counters.p + 8, c->h_counters + 8, sizeof(unsigned long long),
+                                   cudaMemcpyHostToDevice, c->stream));
+        CC_TRY(cc::dist_allreduce_u64(c, cnt, 5));  // tp, tn, fp, fn, |E| summed over ranks
+        CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 4, cnt, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                    c->stream));
         CC_CUDA(c, cudaStreamSynchronize(c->stream));
         const unsigned long long* h = c->h_counters + 4;
         info->n_pairs = (int64_t)(h[0] + h[1] + h[2] + h[3]);
-        info->n_editable = c->E;
+        info->n_editable = (int64_t)h[4];
         info->n_linked = (int64_t)(h[0] + h[3]);
         info->n_violated0 = (int64_t)(h[2] + h[3]);
         info->n_local = c->n;
@@ -387,10 +444,9 @@ cc_status cc_get_trace(cc_ctx* c, int64_t* active_h, double* loss_h, int64_t cap
         CC_CUDA(c, cudaMemcpyAsync(l.data(), c->trace_l.p, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost,
                                    c->stream));
     }
-    CC_CUDA(c, cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(cc::Ctl), cudaMemcpyDeviceToHost, c->stream));
     CC_CUDA(c, cudaStreamSynchronize(c->stream));
-    a[(size_t)n - 1] = (long long)c->h_ctl->active;  // final check of the returned state
-    l[(size_t)n - 1] = c->h_ctl->loss;
+    a[(size_t)n - 1] = (long long)c->final_active;  // final (global) check of the returned state
+    l[(size_t)n - 1] = c->final_loss;
     for (int64_t q = 0; q < n && q < cap; q++) {
         active_h[q] = a[(size_t)q];
         loss_h[q] = l[(size_t)q];
@@ -418,6 +474,7 @@ cc_status cc_mcc(cc_ctx* c, int which, cc_mcc_info* out) {
     if (which == CC_CORR && c->state < 3) return cc_fail(c, CC_E_STATE, "cc_correct first");
     unsigned long long* cnt = c->counters.p + 4;
     CC_TRY(cc::mcc_run(c, which, cnt));
+    CC_TRY(cc::dist_allreduce_u64(c, cnt, 4));  // owned pairs summed over ranks (R17)
     CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 4, cnt, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                c->stream));
     CC_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -443,6 +500,13 @@ cc_status cc_halo_sizes(cc_ctx* c, int which, int64_t min_size, int64_t* sizes_h
     CC_GUARD(c);
     if (!n_h || (cap > 0 && !sizes_h)) return cc_fail(c, CC_E_ARG, "null output");
     if (c->fof_which != which) return cc_fail(c, CC_E_STATE, "cc_fof_label(which) must be the last FoF run");
+    if (c->nranks > 1) {
+        std::vector<uint32_t> v;
+        CC_TRY(cc::dist_halo_sizes(c, min_size, v));
+        for (size_t q = 0; q < v.size() && (int64_t)q < cap; q++) sizes_h[q] = v[q];
+        *n_h = (int64_t)v.size();
+        return CC_OK;
+    }
     return cc::halo_sizes_run(c, min_size, sizes_h, cap, n_h);
 }
 

@@ -38,16 +38,21 @@ struct Th {
     int periodic;
 };
 
-// uniform grid on ORIGINAL positions, x fastest; ncell = nx*ny*nz.  Cell coordinate computed
-// in fp64 as floor((x - x0) * inv_w) clamped to [0, n-1] (x0 = 0 for one GPU; the slab's
-// lower ghost edge for multi-GPU, where x is first shifted by -L if it lies above the slab).
+// Search structure on ORIGINAL positions ("x-sorted rows"): the (y,z) plane is cut into
+// ny x nz rows of side >= r_max = (b + 2 sqrt3 xi)(1 + 1e-5); each row is cut along x into nx
+// bins; particles are counting-sorted by (z-row, y-row, x-bin) and sorted by x inside every bin,
+// so every row is one x-sorted slot range.  A radius-r search from a particle visits the 9
+// neighbouring rows and, in each, only the x-window [u - r, u + r] (binary search on xs[]).
+// Coordinates: u = x - x0 wrapped once into [0, L) (x0 = 0 on one GPU; the slab's lower ghost
+// edge on several); all window arithmetic in fp64.
 struct Grid {
     int nx, ny, nz;
-    double inv_w;      // cells per unit length (same on all axes)
+    double inv_w;      // rows per unit length in y and z
+    double inv_wx;     // x-bins per unit length
     double x0;         // lower x edge of the local grid
     double L;          // box
+    double ext_x;      // x extent of the local grid (L on one GPU)
     int xwrap;         // 1: x axis periodic inside this grid (single GPU)
-    double slab_hi;    // multi-GPU: x above slab_hi + ghost width belongs to the image -L
 };
 
 // per-iteration control block of the PGD loop (device resident)
@@ -111,6 +116,8 @@ struct cc_ctx {
     cc::DBuf<uint32_t> key, rnk, cell_count, cell_start, slot_of, deg, eidx, rows, slotE, parent, mingid,
         gsize, scratch_u32;
     cc::DBuf<uint64_t> rowoff, rowptr, scratch_u64;
+    cc::DBuf<float> xs;          // original x per slot (row-sorted search key)
+    double r_pair = 0, r_link = 0;   // search radii: vulnerable band / FoF on original positions
     cc::DBuf<float> mom;         // 6 * E floats: mx, my, mz, vx, vy, vz
     cc::DBuf<float2> bc;         // Adam bias corrections per iteration
     cc::DBuf<double> partial_d;  // block partials
@@ -121,6 +128,22 @@ struct cc_ctx {
     cc::DBuf<unsigned char> tmp_bytes;  // scan scratch
     cc::DBuf<float> in_f;        // cc_run host staging: 6 n floats
     cc::DBuf<uint32_t> in_gid;
+
+    // multi-GPU (dist.cu)
+    int left = 0, right = 0;
+    double slab_lo = 0, slab_hi = 0;
+    cc::DBuf<uint32_t> dflag[2], dpos[2], shell[2], stage, sbuf7[2], rbuf7[2], req[2], recv_e[2], sreq[2], send_e[2],
+        lsb[2], lrb[2], gath;
+    cc::DBuf<long long> dcnt;
+    cc::DBuf<float4> rsb[2], rrb[2];
+    cc::DBuf<double> red;
+    cc::DBuf<uint2> bnd;
+    int64_t n_shell[2] = {0, 0}, n_from_left = 0, n_from_right = 0, stage_cap = 0;
+    int64_t n_ref_send[2] = {0, 0}, n_ref_recv[2] = {0, 0};
+    int64_t launches_per_iter_tail = 0;
+    double* h_red = nullptr;
+    unsigned long long final_active = 0;
+    double final_loss = 0.0;
 
     // pinned host mirrors
     cc::Ctl* h_ctl = nullptr;
@@ -180,42 +203,97 @@ __device__ __forceinline__ double local_u(double x, const Grid& g) {
     return u;
 }
 
-// the cell of an ORIGINAL position (used identically by binning and by the searches)
-__device__ __forceinline__ void cell_of(float x, float y, float z, const Grid& g, int& cx, int& cy, int& cz) {
-    cx = cell_coord(local_u((double)x, g), 0.0, g.inv_w, g.nx);
+// the (x-bin, y-row, z-row) of an ORIGINAL position; u = its local x coordinate
+__device__ __forceinline__ void cell_of(float x, float y, float z, const Grid& g, double& u, int& cx, int& cy,
+                                        int& cz) {
+    u = local_u((double)x, g);
+    cx = cell_coord(u, 0.0, g.inv_wx, g.nx);
     cy = cell_coord((double)y, 0.0, g.inv_w, g.ny);
     cz = cell_coord((double)z, 0.0, g.inv_w, g.nz);
 }
 
+// 32-bit in-row sort key of an original x: order of u = (x < x0 ? 1 : 0, x) (x >= 0 assumed,
+// -0 folded into +0), exact -- no rounding of u is involved.
+__device__ __forceinline__ uint32_t x_sort_key(float x, const Grid& g) {
+    const float xp = __fadd_rn(x, 0.0f);
+    const uint32_t wrapped = ((double)x < g.x0) ? 0x80000000u : 0u;
+    return __float_as_uint(xp) | wrapped;
+}
+
 __device__ __forceinline__ int wrapi(int a, int n) { return a < 0 ? a + n : (a >= n ? a - n : a); }
 
-// Visit the candidate slot ranges of the 27-cell neighbourhood of cell (cx,cy,cz): the three
-// x-adjacent cells of a (y,z) row are one contiguous slot range when they do not wrap.
-// Offsets are de-duplicated when an axis has fewer than 3 cells (R1).  f(a, b) gets [a,b).
+// first slot j in [j0, j1) with u(xs[j]) >= a (u non-decreasing over the range)
+__device__ __forceinline__ uint32_t lower_bound_u(const float* __restrict__ xs, uint32_t j0, uint32_t j1, double a,
+                                                  const Grid& g) {
+    while (j0 < j1) {
+        const uint32_t m = (j0 + j1) >> 1;
+        if (local_u((double)xs[m], g) < a) j0 = m + 1;
+        else j1 = m;
+    }
+    return j0;
+}
+
+// visit every slot j of the row starting at cell index `rowbase` with a <= u_j <= b
 template <class F>
-__device__ __forceinline__ void for_each_neighbour_range(const Grid& g, const uint32_t* __restrict__ cs,
-                                                         int cx, int cy, int cz, bool periodic_yz, F&& f) {
-    const int ny_off = g.ny >= 3 ? 3 : g.ny, nz_off = g.nz >= 3 ? 3 : g.nz, nx_off = g.nx >= 3 ? 3 : g.nx;
+__device__ __forceinline__ void scan_row_window(const Grid& g, const uint32_t* __restrict__ cs,
+                                                const float* __restrict__ xs, int64_t rowbase, double a, double b,
+                                                F& f) {
+    const int ca = cell_coord(a, 0.0, g.inv_wx, g.nx), cb = cell_coord(b, 0.0, g.inv_wx, g.nx);
+    const uint32_t j1 = cs[rowbase + cb + 1];
+    uint32_t j = lower_bound_u(xs, cs[rowbase + ca], j1, a, g);
+    for (; j < j1; j++) {
+        if (local_u((double)xs[j], g) > b) break;
+        f(j);
+    }
+}
+
+// visit the x-window [u - r, u + r] (periodic in x when g.xwrap) of one row
+template <class F>
+__device__ __forceinline__ void scan_row(const Grid& g, const uint32_t* __restrict__ cs, const float* __restrict__ xs,
+                                         int64_t rowbase, double u, double r, F& f) {
+    double a = u - r, b = u + r;
+    double sa[3], sb[3];
+    int ns = 0;
+    if (g.xwrap) {
+        if (a < 0.0) {
+            sa[ns] = a + g.L;
+            sb[ns++] = g.L;
+            a = 0.0;
+        }
+        if (b >= g.L) {
+            sa[ns] = 0.0;
+            sb[ns++] = b - g.L;
+            b = g.L;
+        }
+    } else {
+        if (a < 0.0) a = 0.0;
+        if (b > g.ext_x) b = g.ext_x;
+    }
+    sa[ns] = a;
+    sb[ns++] = b;
+#pragma unroll 1
+    for (int k = 0; k < ns; k++) scan_row_window(g, cs, xs, rowbase, sa[k], sb[k], f);
+}
+
+// Radius-r candidates of a particle at local x u in row (cy, cz): the 9 neighbouring rows
+// (offsets de-duplicated when an axis has fewer than 3 rows, R1), x-window per row.  f(j).
+template <class F>
+__device__ __forceinline__ void for_each_candidate(const Grid& g, const uint32_t* __restrict__ cs,
+                                                   const float* __restrict__ xs, double u, int cy, int cz, double r,
+                                                   bool periodic_yz, F&& f) {
+    const int ny_off = g.ny >= 3 ? 3 : g.ny, nz_off = g.nz >= 3 ? 3 : g.nz;
     const int offs[3] = {0, 1, -1};
+#pragma unroll 1
     for (int kz = 0; kz < nz_off; kz++) {
         int zz = cz + offs[kz];
         if (periodic_yz) zz = wrapi(zz, g.nz);
         else if (zz < 0 || zz >= g.nz) continue;
+#pragma unroll 1
         for (int ky = 0; ky < ny_off; ky++) {
             int yy = cy + offs[ky];
             if (periodic_yz) yy = wrapi(yy, g.ny);
             else if (yy < 0 || yy >= g.ny) continue;
-            const int64_t base = ((int64_t)zz * g.ny + yy) * g.nx;
-            if (cx >= 1 && cx <= g.nx - 2) {
-                f(cs[base + cx - 1], cs[base + cx + 2]);
-            } else {
-                for (int kx = 0; kx < nx_off; kx++) {
-                    int xx = cx + offs[kx];
-                    if (g.xwrap) xx = wrapi(xx, g.nx);
-                    else if (xx < 0 || xx >= g.nx) continue;
-                    f(cs[base + xx], cs[base + xx + 1]);
-                }
-            }
+            scan_row(g, cs, xs, ((int64_t)zz * g.ny + yy) * g.nx, u, r, f);
         }
     }
 }
@@ -270,4 +348,16 @@ cc_status get_pairs_run(cc_ctx* c, uint32_t* gi, uint32_t* gj, uint8_t* flags, i
                         unsigned long long* n_dev);
 cc_status halo_sizes_run(cc_ctx* c, int64_t min_size, int64_t* sizes_h, int64_t cap, int64_t* n_h);
 const float4* pgd_result(cc_ctx* c);
+// dist.cu
+cc_status dist_init(cc_ctx* c, const cc_dist* d);
+void dist_destroy(cc_ctx* c);
+cc_status dist_unique_id(void* out);
+cc_status dist_allreduce_u64(cc_ctx* c, unsigned long long* dev, size_t count);
+cc_status dist_allreduce_f64(cc_ctx* c, double* dev, size_t count);
+cc_status dist_exchange_ghosts(cc_ctx* c, int64_t n, const float* x, const float* y, const float* z, const float* xh,
+                               const float* yh, const float* zh, const uint32_t* gid);
+cc_status dist_setup_refresh(cc_ctx* c);
+cc_status dist_iter_tail(cc_ctx* c, const float4* p0, const float4* p1);
+cc_status dist_fof_merge(cc_ctx* c, int64_t* n_groups);
+cc_status dist_halo_sizes(cc_ctx* c, int64_t min_size, std::vector<uint32_t>& out);
 }  // namespace cc

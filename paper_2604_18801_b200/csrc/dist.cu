@@ -1,0 +1,575 @@
+// dist.cu -- multi-GPU form of the hot path (§III-D; §IV-D): x-slab spatial
+// decomposition, ghost shells of width delta = b + 2 sqrt3 xi exchanged with NCCL (the paper's
+// MPI_Isend/Irecv), a per-iteration refresh of editable ghost positions (R19) and a global
+// allreduce of the L_tight-active count that drives the stop (the paper's MPI_Allreduce of the
+// loss), FoF label merging across slabs, and reductions of MCC counts and halo sizes.
+//
+// Rank r owns original x in [r L/R, (r+1) L/R); its neighbours are r-1 and r+1 (periodic).  The
+// local particle set is [owned | ghosts from the left | ghosts from the right]; the local search
+// structure spans x in [lo - gw, hi + gw) without wrap.  Every pair with an owned endpoint is
+// found locally; the pair belongs to the owner of its min-gid endpoint (R17).  Results are
+// bit-identical to one GPU: rows are summed in gid order and ghost positions are the owners'.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <unordered_map>
+#include <vector>
+
+#include "cc_internal.cuh"
+
+namespace cc {
+namespace {
+
+constexpr int DT = 256;
+
+#define CC_NCCL(c, expr)                                                                          \
+    do {                                                                                          \
+        ncclResult_t r_ = (expr);                                                                 \
+        if (r_ != ncclSuccess) return cc_fail((c), CC_E_NCCL, std::string(ncclGetErrorString(r_)) + " at " #expr); \
+    } while (0)
+
+inline ncclComm_t comm(cc_ctx* c) { return static_cast<ncclComm_t>(c->nccl_comm); }
+
+// flag owned particles inside the lower (dir 0) / upper (dir 1) ghost shell of the slab
+__global__ void k_shell_flags(int64_t n, const float* __restrict__ x, double lo, double hi, double gw, double L,
+                              uint32_t* __restrict__ f0, uint32_t* __restrict__ f1, unsigned long long* errs) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double xv = (double)x[i];
+    if (!(xv >= lo && xv < hi)) atomicOr(errs, 4ull);  // not in this rank's slab
+    f0[i] = (xv < lo + gw) ? 1u : 0u;
+    f1[i] = (xv >= hi - gw) ? 1u : 0u;
+}
+
+// list[pos[i]] = i for flagged i (pos = exclusive scan of the flags)
+__global__ void k_compact_list(int64_t n, const uint32_t* __restrict__ f, const uint32_t* __restrict__ pos,
+                               uint32_t* __restrict__ list) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (f[i]) list[pos[i]] = (uint32_t)i;
+}
+
+// pack particles of a list as 7 SoA words (x, y, z, xh, yh, zh, gid)
+__global__ void k_pack7(int64_t m, const uint32_t* __restrict__ list, const float* __restrict__ x,
+                        const float* __restrict__ y, const float* __restrict__ z, const float* __restrict__ xh,
+                        const float* __restrict__ yh, const float* __restrict__ zh, const uint32_t* __restrict__ gid,
+                        uint32_t* __restrict__ buf) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const uint32_t i = list[k];
+    buf[0 * m + k] = __float_as_uint(x[i]);
+    buf[1 * m + k] = __float_as_uint(y[i]);
+    buf[2 * m + k] = __float_as_uint(z[i]);
+    buf[3 * m + k] = __float_as_uint(xh[i]);
+    buf[4 * m + k] = __float_as_uint(yh[i]);
+    buf[5 * m + k] = __float_as_uint(zh[i]);
+    buf[6 * m + k] = gid ? gid[i] : i;
+}
+
+// copy owned arrays into the local staging (7 SoA arrays of capacity cap)
+__global__ void k_stage_owned(int64_t n, int64_t cap, const float* __restrict__ x, const float* __restrict__ y,
+                              const float* __restrict__ z, const float* __restrict__ xh, const float* __restrict__ yh,
+                              const float* __restrict__ zh, const uint32_t* __restrict__ gid, uint32_t gid_base,
+                              uint32_t* __restrict__ st) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    st[0 * cap + i] = __float_as_uint(x[i]);
+    st[1 * cap + i] = __float_as_uint(y[i]);
+    st[2 * cap + i] = __float_as_uint(z[i]);
+    st[3 * cap + i] = __float_as_uint(xh[i]);
+    st[4 * cap + i] = __float_as_uint(yh[i]);
+    st[5 * cap + i] = __float_as_uint(zh[i]);
+    st[6 * cap + i] = gid ? gid[i] : gid_base + (uint32_t)i;
+}
+
+// received block of m particles -> staging rows [off, off + m)
+__global__ void k_unstage(int64_t m, int64_t cap, int64_t off, const uint32_t* __restrict__ buf,
+                          uint32_t* __restrict__ st) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    for (int w = 0; w < 7; w++) st[w * cap + off + k] = buf[w * m + k];
+}
+
+// ghost editables: (source dir, index in the source's shell list) for each ghost editable
+__global__ void k_ghost_requests(int64_t n, const uint32_t* __restrict__ eidx, const float4* __restrict__ dec4,
+                                 uint32_t n_own, uint32_t n_from_left, uint32_t e_own, uint32_t* __restrict__ req_left,
+                                 uint32_t* __restrict__ req_left_e, unsigned long long* __restrict__ cnt_left,
+                                 uint32_t* __restrict__ req_right, uint32_t* __restrict__ req_right_e,
+                                 unsigned long long* __restrict__ cnt_right) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const uint32_t e = eidx[s];
+    if (e == 0xFFFFFFFFu || !(e & 0x80000000u)) return;
+    const uint32_t eg = e_own + (e & 0x7FFFFFFFu);
+    const uint32_t i = __float_as_uint(dec4[s].w);
+    if (i - n_own < n_from_left) {
+        const unsigned long long q = atomicAdd(cnt_left, 1ull);
+        req_left[q] = i - n_own;
+        req_left_e[q] = eg;
+    } else {
+        const unsigned long long q = atomicAdd(cnt_right, 1ull);
+        req_right[q] = i - n_own - n_from_left;
+        req_right_e[q] = eg;
+    }
+}
+
+// owner side: requested shell-list index -> owned editable index
+__global__ void k_map_requests(int64_t m, const uint32_t* __restrict__ req, const uint32_t* __restrict__ shell,
+                               const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ eidx,
+                               uint32_t* __restrict__ send_e, unsigned long long* errs) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const uint32_t e = eidx[slot_of[shell[req[k]]]];
+    if (e == 0xFFFFFFFFu || (e & 0x80000000u)) atomicOr(errs, 8ull);  // must be an owned editable
+    send_e[k] = e;
+}
+
+// per-iteration refresh: pack the updated owned positions / unpack into ghost slots
+__global__ void k_refresh_pack(int64_t m, const uint32_t* __restrict__ send_e, const Ctl* __restrict__ ctl,
+                               const float4* __restrict__ p0, const float4* __restrict__ p1, float4* __restrict__ buf) {
+    if (ctl->done) return;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const int t = ctl->t + 1;  // the iteration whose update was just written (t not yet advanced)
+    const float4* dst = (t & 1) ? p1 : p0;
+    buf[k] = dst[send_e[k]];
+}
+
+__global__ void k_refresh_unpack(int64_t m, const uint32_t* __restrict__ recv_e, const Ctl* __restrict__ ctl,
+                                 float4* __restrict__ p0, float4* __restrict__ p1, const float4* __restrict__ buf) {
+    if (ctl->done) return;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const int t = ctl->t + 1;
+    float4* dst = (t & 1) ? p1 : p0;
+    dst[recv_e[k]] = buf[k];
+}
+
+// global stop decision after the allreduce of (active, loss)
+__global__ void k_decide(Ctl* ctl, const double* __restrict__ red, int stop_mode, double eps_loss, int t_max,
+                         long long* trace_a, double* trace_l) {
+    if (ctl->done) return;
+    const int t = ctl->t + 1;
+    const unsigned long long tu = (unsigned long long)red[0];
+    const double td = red[1];
+    ctl->active = tu;
+    ctl->loss = td;
+    if (trace_a) {
+        trace_a[t - 1] = (long long)tu;
+        trace_l[t - 1] = td;
+    }
+    const bool stop = (stop_mode == CC_STOP_ACTIVE && tu == 0ull) || (stop_mode == CC_STOP_EPS && td <= eps_loss);
+    if (stop) {
+        ctl->done = 1;
+        ctl->t_res = t - 1;
+        ctl->converged = 1;
+    } else if (t >= t_max) {
+        ctl->done = 1;
+        ctl->t_res = t;
+    }
+    ctl->t = t;
+}
+
+// FoF label exchange: labels of the shell lists (owner side) ...
+__global__ void k_label_pack(int64_t m, const uint32_t* __restrict__ shell, const uint32_t* __restrict__ slot_of,
+                             const uint32_t* __restrict__ par, const uint32_t* __restrict__ mingid,
+                             uint32_t* __restrict__ buf) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    buf[k] = mingid[par[slot_of[shell[k]]]];
+}
+// ... lower the local component of each ghost to the owner's label
+__global__ void k_label_merge(int64_t m, uint32_t first_local, const uint32_t* __restrict__ slot_of,
+                              const uint32_t* __restrict__ par, uint32_t* __restrict__ mingid,
+                              const uint32_t* __restrict__ buf, unsigned long long* changed) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const uint32_t r = par[slot_of[first_local + k]];
+    const uint32_t old = atomicMin(&mingid[r], buf[k]);
+    if (buf[k] < old) atomicAdd(changed, 1ull);
+}
+
+// owned particles whose label equals their own gid = one per global component
+__global__ void k_count_label_roots(int64_t n_own, const uint32_t* __restrict__ slot_of,
+                                    const uint32_t* __restrict__ par, const uint32_t* __restrict__ mingid,
+                                    const float4* __restrict__ orig4, unsigned long long* __restrict__ cnt) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned int v = 0;
+    if (i < n_own) {
+        const uint32_t s = slot_of[i];
+        v = mingid[par[s]] == __float_as_uint(orig4[s].w);
+    }
+    const unsigned int tot = __syncthreads_count(v);
+    if (threadIdx.x == 0 && tot) atomicAdd(cnt, (unsigned long long)tot);
+}
+
+// owned members per local root, and whether the local component touches a ghost
+__global__ void k_root_counts(int64_t n, uint32_t n_own, const uint32_t* __restrict__ par,
+                              const float4* __restrict__ dec4, uint32_t* __restrict__ owned_cnt,
+                              uint32_t* __restrict__ has_ghost) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const uint32_t r = par[s];
+    if (__float_as_uint(dec4[s].w) < n_own) atomicAdd(&owned_cnt[r], 1u);
+    else has_ghost[r] = 1u;
+}
+
+__global__ void k_root_collect(int64_t n, const uint32_t* __restrict__ par, const uint32_t* __restrict__ owned_cnt,
+                               const uint32_t* __restrict__ has_ghost, const uint32_t* __restrict__ mingid,
+                               uint32_t min_size, uint32_t* __restrict__ interior, unsigned long long* n_interior,
+                               uint2* __restrict__ boundary, unsigned long long* n_boundary) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    if (par[s] != (uint32_t)s || owned_cnt[s] == 0) return;
+    if (has_ghost[s]) {
+        const unsigned long long q = atomicAdd(n_boundary, 1ull);
+        boundary[q] = make_uint2(mingid[s], owned_cnt[s]);
+    } else if (owned_cnt[s] >= min_size) {
+        const unsigned long long q = atomicAdd(n_interior, 1ull);
+        interior[q] = owned_cnt[s];
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+cc_status dist_init(cc_ctx* c, const cc_dist* d) {
+    c->rank = d->rank;
+    c->nranks = d->nranks;
+    if (d->nranks <= 1) return CC_OK;
+    if (!d->nccl_id_h || d->rank < 0 || d->rank >= d->nranks) return cc_fail(c, CC_E_ARG, "bad cc_dist");
+    ncclUniqueId id;
+    std::memcpy(&id, d->nccl_id_h, sizeof(id));
+    ncclComm_t cm;
+    CC_NCCL(c, ncclCommInitRank(&cm, d->nranks, id, d->rank));
+    c->nccl_comm = cm;
+    c->left = (d->rank + d->nranks - 1) % d->nranks;
+    c->right = (d->rank + 1) % d->nranks;
+    c->slab_lo = c->p.box * (double)d->rank / d->nranks;
+    c->slab_hi = c->p.box * (double)(d->rank + 1) / d->nranks;
+    return CC_OK;
+}
+
+void dist_destroy(cc_ctx* c) {
+    if (c->nranks > 1 && c->nccl_comm) ncclCommDestroy(comm(c));
+    c->nccl_comm = nullptr;
+}
+
+// in-place global sums of small device arrays (synchronising)
+cc_status dist_allreduce_u64(cc_ctx* c, unsigned long long* dev, size_t count) {
+    if (c->nranks <= 1) return CC_OK;
+    CC_NCCL(c, ncclAllReduce(dev, dev, count, ncclUint64, ncclSum, comm(c), c->stream));
+    return CC_OK;
+}
+cc_status dist_allreduce_f64(cc_ctx* c, double* dev, size_t count) {
+    if (c->nranks <= 1) return CC_OK;
+    CC_NCCL(c, ncclAllReduce(dev, dev, count, ncclFloat64, ncclSum, comm(c), c->stream));
+    return CC_OK;
+}
+
+// one-time ghost exchange (X1): local staging = [owned | from left | from right]
+cc_status dist_exchange_ghosts(cc_ctx* c, int64_t n, const float* x, const float* y, const float* z, const float* xh,
+                               const float* yh, const float* zh, const uint32_t* gid) {
+    const double gw = c->r_pair;  // ghost width delta (1 + 1e-5)
+    const size_t n1 = (size_t)std::max<int64_t>(n, 1);
+    CC_TRY(cc_ensure(c, c->dflag[0], n1, "shell flags"));
+    CC_TRY(cc_ensure(c, c->dflag[1], n1, "shell flags"));
+    CC_TRY(cc_ensure(c, c->dpos[0], n1 + 1, "shell positions"));
+    CC_TRY(cc_ensure(c, c->dpos[1], n1 + 1, "shell positions"));
+    CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
+    CC_CUDA(c, cudaMemsetAsync(c->counters.p, 0, 16 * sizeof(unsigned long long), c->stream));
+    const unsigned nb = (unsigned)((n + DT - 1) / DT);
+    if (n > 0)
+        CCL(c, k_shell_flags<<<nb, DT, 0, c->stream>>>(n, x, c->slab_lo, c->slab_hi, gw, c->p.box, c->dflag[0].p,
+                                                       c->dflag[1].p, c->counters.p));
+    uint64_t* tot = reinterpret_cast<uint64_t*>(c->counters.p + 1);
+    CC_TRY(scan_u32_to_u32(c, c->dflag[0].p, c->dpos[0].p, n, tot));
+    CC_TRY(scan_u32_to_u32(c, c->dflag[1].p, c->dpos[1].p, n, tot + 1));
+    CC_CUDA(c, cudaMemcpyAsync(c->h_counters, c->counters.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (c->h_counters[0] & 4ull) return cc_fail(c, CC_E_DATA, "an owned particle lies outside this rank's x slab");
+    int64_t ns[2] = {(int64_t)(c->h_counters[1] & 0xFFFFFFFFull), (int64_t)(c->h_counters[2] & 0xFFFFFFFFull)};
+    for (int d = 0; d < 2; d++) {
+        CC_TRY(cc_ensure(c, c->shell[d], (size_t)std::max<int64_t>(ns[d], 1), "shell list"));
+        if (n > 0)
+            CCL(c, k_compact_list<<<nb, DT, 0, c->stream>>>(n, c->dflag[d].p, c->dpos[d].p, c->shell[d].p));
+        c->n_shell[d] = ns[d];
+    }
+    // counts: send dir0 -> left, dir1 -> right; receive from right (their dir0), from left (their dir1)
+    CC_TRY(cc_ensure(c, c->dcnt, 4, "dist counts"));
+    {
+        long long h[4] = {ns[0], ns[1], 0, 0};
+        CC_CUDA(c, cudaMemcpyAsync(c->dcnt.p, h, 2 * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+        CC_NCCL(c, ncclGroupStart());
+        CC_NCCL(c, ncclSend(c->dcnt.p + 0, 1, ncclInt64, c->left, comm(c), c->stream));
+        CC_NCCL(c, ncclSend(c->dcnt.p + 1, 1, ncclInt64, c->right, comm(c), c->stream));
+        CC_NCCL(c, ncclRecv(c->dcnt.p + 2, 1, ncclInt64, c->right, comm(c), c->stream));
+        CC_NCCL(c, ncclRecv(c->dcnt.p + 3, 1, ncclInt64, c->left, comm(c), c->stream));
+        CC_NCCL(c, ncclGroupEnd());
+        CC_CUDA(c, cudaMemcpyAsync(h, c->dcnt.p, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+        c->n_from_right = h[2];
+        c->n_from_left = h[3];
+    }
+    const int64_t nl = n + c->n_from_left + c->n_from_right;
+    if (nl >= MAX_LOCAL) return cc_fail(c, CC_E_DATA, "local particles beyond the 2^30 index space");
+    const int64_t cap = std::max<int64_t>(nl, 1);
+    CC_TRY(cc_ensure(c, c->stage, (size_t)(7 * cap), "local staging"));
+    for (int d = 0; d < 2; d++)
+        CC_TRY(cc_ensure(c, c->sbuf7[d], (size_t)std::max<int64_t>(7 * ns[d], 1), "ghost send buffer"));
+    CC_TRY(cc_ensure(c, c->rbuf7[0], (size_t)std::max<int64_t>(7 * c->n_from_left, 1), "ghost recv buffer"));
+    CC_TRY(cc_ensure(c, c->rbuf7[1], (size_t)std::max<int64_t>(7 * c->n_from_right, 1), "ghost recv buffer"));
+    if (n > 0)
+        CCL(c, k_stage_owned<<<nb, DT, 0, c->stream>>>(n, cap, x, y, z, xh, yh, zh, gid, 0u, c->stage.p));
+    for (int d = 0; d < 2; d++)
+        if (ns[d] > 0)
+            CCL(c, k_pack7<<<(unsigned)((ns[d] + DT - 1) / DT), DT, 0, c->stream>>>(ns[d], c->shell[d].p, x, y, z, xh, yh,
+                                                                                  zh, gid, c->sbuf7[d].p));
+    CC_NCCL(c, ncclGroupStart());
+    if (ns[0] > 0) CC_NCCL(c, ncclSend(c->sbuf7[0].p, (size_t)(7 * ns[0]), ncclUint32, c->left, comm(c), c->stream));
+    if (ns[1] > 0) CC_NCCL(c, ncclSend(c->sbuf7[1].p, (size_t)(7 * ns[1]), ncclUint32, c->right, comm(c), c->stream));
+    if (c->n_from_right > 0)
+        CC_NCCL(c, ncclRecv(c->rbuf7[1].p, (size_t)(7 * c->n_from_right), ncclUint32, c->right, comm(c), c->stream));
+    if (c->n_from_left > 0)
+        CC_NCCL(c, ncclRecv(c->rbuf7[0].p, (size_t)(7 * c->n_from_left), ncclUint32, c->left, comm(c), c->stream));
+    CC_NCCL(c, ncclGroupEnd());
+    if (c->n_from_left > 0)
+        CCL(c, k_unstage<<<(unsigned)((c->n_from_left + DT - 1) / DT), DT, 0, c->stream>>>(c->n_from_left, cap, n,
+                                                                                          c->rbuf7[0].p, c->stage.p));
+    if (c->n_from_right > 0)
+        CCL(c, k_unstage<<<(unsigned)((c->n_from_right + DT - 1) / DT), DT, 0, c->stream>>>(
+                   c->n_from_right, cap, n + c->n_from_left, c->rbuf7[1].p, c->stage.p));
+    CC_CUDA(c, cudaGetLastError());
+    c->stage_cap = cap;
+    c->n = nl;
+    return CC_OK;
+}
+
+// refresh lists of ghost editables (X2), after the rows exist
+cc_status dist_setup_refresh(cc_ctx* c) {
+    const int64_t n = c->n;
+    CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
+    const int64_t ng = std::max<int64_t>(c->E_all - c->E, 1);
+    for (int d = 0; d < 2; d++) {
+        CC_TRY(cc_ensure(c, c->req[d], (size_t)ng, "ghost requests"));
+        CC_TRY(cc_ensure(c, c->recv_e[d], (size_t)ng, "ghost refresh targets"));
+    }
+    CC_CUDA(c, cudaMemsetAsync(c->counters.p + 12, 0, 3 * sizeof(unsigned long long), c->stream));
+    if (n > 0)
+        CCL(c, k_ghost_requests<<<(unsigned)((n + DT - 1) / DT), DT, 0, c->stream>>>(
+                   n, c->eidx.p, c->dec4.p, (uint32_t)c->n_in, (uint32_t)c->n_from_left, (uint32_t)c->E, c->req[0].p,
+                   c->recv_e[0].p, c->counters.p + 12, c->req[1].p, c->recv_e[1].p, c->counters.p + 13));
+    CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 12, c->counters.p + 12, 2 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    int64_t nreq[2] = {(int64_t)c->h_counters[12], (int64_t)c->h_counters[13]};  // to left, to right
+    // exchange request counts: my dir-0 requests concern the left rank's dir-1 shell, etc.
+    {
+        long long h[4] = {nreq[0], nreq[1], 0, 0};
+        CC_CUDA(c, cudaMemcpyAsync(c->dcnt.p, h, 2 * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+        CC_NCCL(c, ncclGroupStart());
+        CC_NCCL(c, ncclSend(c->dcnt.p + 0, 1, ncclInt64, c->left, comm(c), c->stream));
+        CC_NCCL(c, ncclSend(c->dcnt.p + 1, 1, ncclInt64, c->right, comm(c), c->stream));
+        CC_NCCL(c, ncclRecv(c->dcnt.p + 2, 1, ncclInt64, c->right, comm(c), c->stream));
+        CC_NCCL(c, ncclRecv(c->dcnt.p + 3, 1, ncclInt64, c->left, comm(c), c->stream));
+        CC_NCCL(c, ncclGroupEnd());
+        CC_CUDA(c, cudaMemcpyAsync(h, c->dcnt.p, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+        // from the right: requests about my dir-1 shell (sent to the right); from the left: dir-0
+        c->n_ref_send[1] = h[2];
+        c->n_ref_send[0] = h[3];
+    }
+    c->n_ref_recv[0] = nreq[0];
+    c->n_ref_recv[1] = nreq[1];
+    for (int d = 0; d < 2; d++) {
+        CC_TRY(cc_ensure(c, c->sreq[d], (size_t)std::max<int64_t>(c->n_ref_send[d], 1), "incoming requests"));
+        CC_TRY(cc_ensure(c, c->send_e[d], (size_t)std::max<int64_t>(c->n_ref_send[d], 1), "refresh sources"));
+        CC_TRY(cc_ensure(c, c->rsb[d], (size_t)std::max<int64_t>(c->n_ref_send[d], 1), "refresh send buffer"));
+        CC_TRY(cc_ensure(c, c->rrb[d], (size_t)std::max<int64_t>(c->n_ref_recv[d], 1), "refresh recv buffer"));
+    }
+    CC_NCCL(c, ncclGroupStart());
+    if (nreq[0] > 0) CC_NCCL(c, ncclSend(c->req[0].p, (size_t)nreq[0], ncclUint32, c->left, comm(c), c->stream));
+    if (nreq[1] > 0) CC_NCCL(c, ncclSend(c->req[1].p, (size_t)nreq[1], ncclUint32, c->right, comm(c), c->stream));
+    if (c->n_ref_send[1] > 0)
+        CC_NCCL(c, ncclRecv(c->sreq[1].p, (size_t)c->n_ref_send[1], ncclUint32, c->right, comm(c), c->stream));
+    if (c->n_ref_send[0] > 0)
+        CC_NCCL(c, ncclRecv(c->sreq[0].p, (size_t)c->n_ref_send[0], ncclUint32, c->left, comm(c), c->stream));
+    CC_NCCL(c, ncclGroupEnd());
+    for (int d = 0; d < 2; d++)
+        if (c->n_ref_send[d] > 0)
+            CCL(c, k_map_requests<<<(unsigned)((c->n_ref_send[d] + DT - 1) / DT), DT, 0, c->stream>>>(
+                       c->n_ref_send[d], c->sreq[d].p, c->shell[d].p, c->slot_of.p, c->eidx.p, c->send_e[d].p,
+                       c->counters.p + 14));
+    CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 14, c->counters.p + 14, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (c->h_counters[14] & 8ull) return cc_fail(c, CC_E_DATA, "ghost editable is not editable on its owner");
+    CC_TRY(cc_ensure(c, c->red, 2, "allreduce buffer"));
+    return CC_OK;
+}
+
+// per-iteration tail (X3): refresh ghosts, allreduce the stop statistics, decide
+cc_status dist_iter_tail(cc_ctx* c, const float4* p0, const float4* p1) {
+    for (int d = 0; d < 2; d++)
+        if (c->n_ref_send[d] > 0)
+            CCL(c, k_refresh_pack<<<(unsigned)((c->n_ref_send[d] + DT - 1) / DT), DT, 0, c->stream>>>(
+                       c->n_ref_send[d], c->send_e[d].p, c->ctl.p, p0, p1, c->rsb[d].p));
+    CC_NCCL(c, ncclGroupStart());
+    if (c->n_ref_send[0] > 0)
+        CC_NCCL(c, ncclSend(c->rsb[0].p, (size_t)(4 * c->n_ref_send[0]), ncclFloat32, c->left, comm(c), c->stream));
+    if (c->n_ref_send[1] > 0)
+        CC_NCCL(c, ncclSend(c->rsb[1].p, (size_t)(4 * c->n_ref_send[1]), ncclFloat32, c->right, comm(c), c->stream));
+    if (c->n_ref_recv[1] > 0)
+        CC_NCCL(c, ncclRecv(c->rrb[1].p, (size_t)(4 * c->n_ref_recv[1]), ncclFloat32, c->right, comm(c), c->stream));
+    if (c->n_ref_recv[0] > 0)
+        CC_NCCL(c, ncclRecv(c->rrb[0].p, (size_t)(4 * c->n_ref_recv[0]), ncclFloat32, c->left, comm(c), c->stream));
+    CC_NCCL(c, ncclGroupEnd());
+    for (int d = 0; d < 2; d++)
+        if (c->n_ref_recv[d] > 0)
+            CCL(c, k_refresh_unpack<<<(unsigned)((c->n_ref_recv[d] + DT - 1) / DT), DT, 0, c->stream>>>(
+                       c->n_ref_recv[d], c->recv_e[d].p, c->ctl.p, const_cast<float4*>(p0), const_cast<float4*>(p1),
+                       c->rrb[d].p));
+    CC_NCCL(c, ncclAllReduce(c->red.p, c->red.p, 2, ncclFloat64, ncclSum, comm(c), c->stream));
+    CCL(c, k_decide<<<1, 1, 0, c->stream>>>(c->ctl.p, c->red.p, c->p.stop_mode, c->p.eps_loss, c->p.t_max,
+                                            c->trace_a.p, c->trace_l.p));
+    return CC_OK;
+}
+
+// FoF label merge across slabs (X4): owners send their shell particles' labels; receivers lower
+// the ghosts' local components; repeat until no label changes anywhere.
+cc_status dist_fof_merge(cc_ctx* c, int64_t* n_groups) {
+    const int64_t ns0 = c->n_shell[0], ns1 = c->n_shell[1], nfl = c->n_from_left, nfr = c->n_from_right;
+    for (int d = 0; d < 2; d++) {
+        CC_TRY(cc_ensure(c, c->lsb[d], (size_t)std::max<int64_t>(c->n_shell[d], 1), "label send"));
+    }
+    CC_TRY(cc_ensure(c, c->lrb[0], (size_t)std::max<int64_t>(nfl, 1), "label recv"));
+    CC_TRY(cc_ensure(c, c->lrb[1], (size_t)std::max<int64_t>(nfr, 1), "label recv"));
+    CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
+    for (int round = 0; round < 4 * c->nranks + 8; round++) {
+        CC_CUDA(c, cudaMemsetAsync(c->counters.p + 15, 0, sizeof(unsigned long long), c->stream));
+        if (ns0 > 0)
+            CCL(c, k_label_pack<<<(unsigned)((ns0 + DT - 1) / DT), DT, 0, c->stream>>>(ns0, c->shell[0].p, c->slot_of.p,
+                                                                                     c->parent.p, c->mingid.p,
+                                                                                     c->lsb[0].p));
+        if (ns1 > 0)
+            CCL(c, k_label_pack<<<(unsigned)((ns1 + DT - 1) / DT), DT, 0, c->stream>>>(ns1, c->shell[1].p, c->slot_of.p,
+                                                                                     c->parent.p, c->mingid.p,
+                                                                                     c->lsb[1].p));
+        CC_NCCL(c, ncclGroupStart());
+        if (ns0 > 0) CC_NCCL(c, ncclSend(c->lsb[0].p, (size_t)ns0, ncclUint32, c->left, comm(c), c->stream));
+        if (ns1 > 0) CC_NCCL(c, ncclSend(c->lsb[1].p, (size_t)ns1, ncclUint32, c->right, comm(c), c->stream));
+        if (nfr > 0) CC_NCCL(c, ncclRecv(c->lrb[1].p, (size_t)nfr, ncclUint32, c->right, comm(c), c->stream));
+        if (nfl > 0) CC_NCCL(c, ncclRecv(c->lrb[0].p, (size_t)nfl, ncclUint32, c->left, comm(c), c->stream));
+        CC_NCCL(c, ncclGroupEnd());
+        if (nfl > 0)
+            CCL(c, k_label_merge<<<(unsigned)((nfl + DT - 1) / DT), DT, 0, c->stream>>>(
+                       nfl, (uint32_t)c->n_in, c->slot_of.p, c->parent.p, c->mingid.p, c->lrb[0].p,
+                       c->counters.p + 15));
+        if (nfr > 0)
+            CCL(c, k_label_merge<<<(unsigned)((nfr + DT - 1) / DT), DT, 0, c->stream>>>(
+                       nfr, (uint32_t)(c->n_in + nfl), c->slot_of.p, c->parent.p, c->mingid.p, c->lrb[1].p,
+                       c->counters.p + 15));
+        CC_TRY(dist_allreduce_u64(c, c->counters.p + 15, 1));
+        CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 15, c->counters.p + 15, sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+        if (c->h_counters[15] == 0) break;
+    }
+    if (n_groups) {
+        CC_CUDA(c, cudaMemsetAsync(c->counters.p + 8, 0, sizeof(unsigned long long), c->stream));
+        if (c->n_in > 0)
+            CCL(c, k_count_label_roots<<<(unsigned)((c->n_in + DT - 1) / DT), DT, 0, c->stream>>>(
+                       c->n_in, c->slot_of.p, c->parent.p, c->mingid.p, c->orig4.p, c->counters.p + 8));
+        CC_TRY(dist_allreduce_u64(c, c->counters.p + 8, 1));
+        CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 8, c->counters.p + 8, sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+        *n_groups = (int64_t)c->h_counters[8];
+    }
+    return CC_OK;
+}
+
+// global halo catalogue (X5): interior components are complete locally; boundary components
+// are merged by label across ranks on the host after an allgather.
+cc_status dist_halo_sizes(cc_ctx* c, int64_t min_size, std::vector<uint32_t>& out) {
+    const int64_t n = c->n;
+    const size_t n1 = (size_t)std::max<int64_t>(n, 1);
+    CC_TRY(cc_ensure(c, c->gsize, n1, "owned counts"));
+    CC_TRY(cc_ensure(c, c->dflag[0], n1, "ghost flags"));
+    CC_TRY(cc_ensure(c, c->scratch_u32, n1, "interior sizes"));
+    CC_TRY(cc_ensure(c, c->bnd, n1, "boundary components"));
+    CC_CUDA(c, cudaMemsetAsync(c->gsize.p, 0, n1 * sizeof(uint32_t), c->stream));
+    CC_CUDA(c, cudaMemsetAsync(c->dflag[0].p, 0, n1 * sizeof(uint32_t), c->stream));
+    CC_CUDA(c, cudaMemsetAsync(c->counters.p + 10, 0, 2 * sizeof(unsigned long long), c->stream));
+    const unsigned nb = (unsigned)((n + DT - 1) / DT);
+    if (n > 0) {
+        CCL(c, k_root_counts<<<nb, DT, 0, c->stream>>>(n, (uint32_t)c->n_in, c->parent.p, c->dec4.p, c->gsize.p,
+                                                       c->dflag[0].p));
+        CCL(c, k_root_collect<<<nb, DT, 0, c->stream>>>(n, c->parent.p, c->gsize.p, c->dflag[0].p, c->mingid.p,
+                                                        (uint32_t)std::max<int64_t>(min_size, 1), c->scratch_u32.p,
+                                                        c->counters.p + 10, c->bnd.p, c->counters.p + 11));
+    }
+    CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 10, c->counters.p + 10, 2 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    const int64_t ni = (int64_t)c->h_counters[10], nbnd = (int64_t)c->h_counters[11];
+    std::vector<uint32_t> interior((size_t)ni);
+    if (ni > 0)
+        CC_CUDA(c, cudaMemcpyAsync(interior.data(), c->scratch_u32.p, (size_t)ni * sizeof(uint32_t),
+                                   cudaMemcpyDeviceToHost, c->stream));
+    // allgather the interior sizes and the boundary (label, count) pairs
+    CC_TRY(cc_ensure(c, c->dcnt, 4 + 2 * (size_t)c->nranks, "gather counts"));
+    long long mine[2] = {ni, nbnd};
+    CC_CUDA(c, cudaMemcpyAsync(c->dcnt.p + 4 + 2 * c->rank, mine, 2 * sizeof(long long), cudaMemcpyHostToDevice,
+                               c->stream));
+    CC_NCCL(c, ncclAllGather(c->dcnt.p + 4 + 2 * c->rank, c->dcnt.p + 4, 2, ncclInt64, comm(c), c->stream));
+    std::vector<long long> all((size_t)2 * c->nranks);
+    CC_CUDA(c, cudaMemcpyAsync(all.data(), c->dcnt.p + 4, all.size() * sizeof(long long), cudaMemcpyDeviceToHost,
+                               c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    long long mi = 0, mb = 0;
+    for (int r = 0; r < c->nranks; r++) {
+        mi = std::max(mi, all[2 * r]);
+        mb = std::max(mb, all[2 * r + 1]);
+    }
+    // padded allgather: [interior sizes (mi) | boundary pairs (2 mb)] per rank
+    const size_t per = (size_t)(mi + 2 * mb);
+    CC_TRY(cc_ensure(c, c->gath, std::max<size_t>(per * (size_t)(c->nranks + 1), 1), "gather buffer"));
+    uint32_t* mineb = c->gath.p + per * (size_t)c->nranks;
+    CC_CUDA(c, cudaMemsetAsync(mineb, 0, std::max<size_t>(per, 1) * sizeof(uint32_t), c->stream));
+    if (ni > 0)
+        CC_CUDA(c, cudaMemcpyAsync(mineb, c->scratch_u32.p, (size_t)ni * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                                   c->stream));
+    if (nbnd > 0)
+        CC_CUDA(c, cudaMemcpyAsync(mineb + mi, c->bnd.p, (size_t)nbnd * sizeof(uint2), cudaMemcpyDeviceToDevice,
+                                   c->stream));
+    if (per > 0) CC_NCCL(c, ncclAllGather(mineb, c->gath.p, per, ncclUint32, comm(c), c->stream));
+    std::vector<uint32_t> h(per * (size_t)c->nranks);
+    if (!h.empty())
+        CC_CUDA(c, cudaMemcpyAsync(h.data(), c->gath.p, h.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                   c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    out.clear();
+    std::unordered_map<uint32_t, uint64_t> merged;
+    for (int r = 0; r < c->nranks; r++) {
+        const uint32_t* b = h.data() + per * (size_t)r;
+        for (long long k = 0; k < all[2 * r]; k++) out.push_back(b[k]);
+        for (long long k = 0; k < all[2 * r + 1]; k++) merged[b[mi + 2 * k]] += b[mi + 2 * k + 1];
+    }
+    for (auto& kv : merged)
+        if ((int64_t)kv.second >= min_size) out.push_back((uint32_t)kv.second);
+    std::sort(out.begin(), out.end(), [](uint32_t a, uint32_t b) { return a > b; });
+    return CC_OK;
+}
+
+cc_status dist_unique_id(void* out) {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return CC_E_NCCL;
+    std::memcpy(out, &id, sizeof(id));
+    return CC_OK;
+}
+
+}  // namespace cc

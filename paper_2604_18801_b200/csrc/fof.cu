@@ -52,56 +52,56 @@ __global__ void k_iota(int64_t n, uint32_t* __restrict__ par) {
     if (s < n) par[s] = (uint32_t)s;
 }
 
-// link pass: half-shell when every axis has >= 3 cells and the grid is periodic in x
-// (each unordered cell pair visited once), else the full 27-stencil with j > s
+// link pass over the x-sorted rows: the half-shell of rows (own row forward in slot order,
+// then rows (dz=0,dy=+1) and (dz=+1,dy=-1..1)) visits every unordered pair once; with fewer
+// than 3 periodic rows per axis it falls back to all 9 rows with j > s.  The search radius r
+// is b (ORIG) or b + 2 sqrt3 xi (DECOMP / CORR, whose positions are within xi of the original
+// ones that built the structure), with the fp32 rounding margin.
 __global__ void __launch_bounds__(FOF_THREADS)
-k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ orig4, const uint32_t* __restrict__ cs,
-           Grid g, Th t, uint32_t* __restrict__ par) {
+k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ orig4, const float* __restrict__ xs,
+           const uint32_t* __restrict__ cs, Grid g, Th t, double r, uint32_t* __restrict__ par) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
     const float4 o = orig4[s];
     const float4 p = P[s];
+    double u;
     int cx, cy, cz;
-    cell_of(o.x, o.y, o.z, g, cx, cy, cz);
+    cell_of(o.x, o.y, o.z, g, u, cx, cy, cz);
     const bool periodic_yz = t.periodic != 0;
-    const bool half = g.nx >= 3 && g.ny >= 3 && g.nz >= 3 && g.xwrap && periodic_yz;
-    auto test_range = [&](uint32_t a, uint32_t b) {
-        for (uint32_t j = a; j < b; j++) {
-            const float4 q = P[j];
-            if (dist2(p, q, t) <= t.b2) uf_unite(par, (uint32_t)s, j);
-        }
+    auto link = [&](uint32_t j) {
+        const float4 q = P[j];
+        if (dist2(p, q, t) <= t.b2) uf_unite(par, (uint32_t)s, j);
     };
+    const bool half = !periodic_yz || (g.ny >= 3 && g.nz >= 3);
     if (!half) {
-        for_each_neighbour_range(g, cs, cx, cy, cz, periodic_yz, [&](uint32_t a, uint32_t b) {
-            if (b > (uint32_t)s + 1) test_range(a > (uint32_t)s + 1 ? a : (uint32_t)s + 1, b);
-        });
+        auto fwd = [&](uint32_t j) {
+            if (j > (uint32_t)s) link(j);
+        };
+        for_each_candidate(g, cs, xs, u, cy, cz, r, periodic_yz, fwd);
         return;
     }
-    // (dz=0, dy=0): own cell beyond s, then cell cx+1
+    // own row: forward in slot (= x) order, plus the periodic wrap at the row's start
     {
-        const int64_t base = ((int64_t)cz * g.ny + cy) * g.nx;
-        const int64_t c = base + cx;
-        if (cx + 1 <= g.nx - 1) {
-            test_range((uint32_t)s + 1, cs[c + 2]);
-        } else {
-            test_range((uint32_t)s + 1, cs[c + 1]);
-            test_range(cs[base], cs[base + 1]);
+        const int64_t rowbase = ((int64_t)cz * g.ny + cy) * g.nx;
+        const double b = u + r;
+        const uint32_t row_end = cs[rowbase + g.nx];
+        for (uint32_t j = (uint32_t)s + 1; j < row_end; j++) {
+            if (local_u((double)xs[j], g) > b) break;
+            link(j);
         }
+        if (g.xwrap && b >= g.L) scan_row_window(g, cs, xs, rowbase, 0.0, b - g.L, link);
     }
-    // (dz=0, dy=+1) and (dz=+1, dy=-1..1): full x rows
     const int rows_dz[4] = {0, 1, 1, 1};
     const int rows_dy[4] = {1, -1, 0, 1};
-    for (int r = 0; r < 4; r++) {
-        const int zz = wrapi(cz + rows_dz[r], g.nz), yy = wrapi(cy + rows_dy[r], g.ny);
-        const int64_t base = ((int64_t)zz * g.ny + yy) * g.nx;
-        if (cx >= 1 && cx <= g.nx - 2) {
-            test_range(cs[base + cx - 1], cs[base + cx + 2]);
-        } else {
-            for (int dx = -1; dx <= 1; dx++) {
-                const int xx = wrapi(cx + dx, g.nx);
-                test_range(cs[base + xx], cs[base + xx + 1]);
-            }
+    for (int k = 0; k < 4; k++) {
+        int zz = cz + rows_dz[k], yy = cy + rows_dy[k];
+        if (periodic_yz) {
+            zz = wrapi(zz, g.nz);
+            yy = wrapi(yy, g.ny);
+        } else if (zz < 0 || zz >= g.nz || yy < 0 || yy >= g.ny) {
+            continue;
         }
+        scan_row(g, cs, xs, ((int64_t)zz * g.ny + yy) * g.nx, u, r, link);
     }
 }
 
@@ -209,17 +209,18 @@ cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
     int tok = cc_prof_begin(c, "K4_fof");
     if (n > 0) {
         CCL(c, k_iota<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p));
-        CCL(c, k_fof_link<<<nb, FOF_THREADS, 0, c->stream>>>(n, P, c->orig4.p, c->cell_start.p, c->g, c->th, c->parent.p));
+        CCL(c, k_fof_link<<<nb, FOF_THREADS, 0, c->stream>>>(n, P, c->orig4.p, c->xs.p, c->cell_start.p, c->g, c->th, which == CC_ORIG ? c->r_link : c->r_pair, c->parent.p));
         CCL(c, k_flatten<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p));
         CCL(c, k_mingid<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p, c->orig4.p, c->mingid.p, c->gsize.p,
                                                     c->counters.p + 8));
-        if (labels && c->n_in > 0)
-            CCL(c, k_labels<<<(unsigned)((c->n_in + 255) / 256), 256, 0, c->stream>>>(c->n_in, c->slot_of.p, c->parent.p,
-                                                                              c->mingid.p, labels));
     }
+    if (c->nranks > 1) CC_TRY(dist_fof_merge(c, n_groups));  // global labels across slabs (X4)
+    if (n > 0 && labels && c->n_in > 0)
+        CCL(c, k_labels<<<(unsigned)((c->n_in + 255) / 256), 256, 0, c->stream>>>(c->n_in, c->slot_of.p, c->parent.p,
+                                                                                  c->mingid.p, labels));
     cc_prof_end(c, tok);
     CC_CUDA(c, cudaGetLastError());
-    if (n_groups) {
+    if (n_groups && c->nranks == 1) {
         CC_CUDA(c, cudaMemcpyAsync(c->h_counters, c->counters.p + 8, sizeof(unsigned long long),
                                    cudaMemcpyDeviceToHost, c->stream));
         CC_CUDA(c, cudaStreamSynchronize(c->stream));

@@ -24,27 +24,28 @@ constexpr int PAIR_THREADS = 256;
 // of owned particles get bit 31 of their deg word (multi-GPU: they become ghost editables).
 __global__ void __launch_bounds__(PAIR_THREADS)
 k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
-              const uint32_t* __restrict__ cs, Grid g, Th t, uint32_t n_own, uint32_t* __restrict__ deg) {
+              const float* __restrict__ xs, const uint32_t* __restrict__ cs, Grid g, Th t, double r, uint32_t n_own,
+              uint32_t* __restrict__ deg) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
     if (__float_as_uint(dec4[s].w) >= n_own) return;  // ghost: no row
     const float4 p = orig4[s];
+    double u;
     int cx, cy, cz;
-    cell_of(p.x, p.y, p.z, g, cx, cy, cz);
+    cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
     uint32_t cnt = 0;
     const bool multi = n_own < (uint32_t)n;
-    for_each_neighbour_range(g, cs, cx, cy, cz, t.periodic != 0, [&](uint32_t a, uint32_t b) {
-        for (uint32_t j = a; j < b; j++) {
-            if (j == (uint32_t)s) continue;
-            const float4 q = orig4[j];
-            const float d2 = dist2(p, q, t);
-            if (t.lo2 < d2 && d2 <= t.hi2) {
-                cnt++;
-                if (multi && __float_as_uint(dec4[j].w) >= n_own) atomicOr(&deg[j], 0x80000000u);
-            }
+    auto test = [&](uint32_t j) {
+        if (j == (uint32_t)s) return;
+        const float4 q = orig4[j];
+        const float d2 = dist2(p, q, t);
+        if (t.lo2 < d2 && d2 <= t.hi2) {
+            cnt++;
+            if (multi && __float_as_uint(dec4[j].w) >= n_own) atomicOr(&deg[j], 0x80000000u);
         }
-    });
-    deg[s] = (deg[s] & 0x80000000u) | cnt;  // own word never carries the ghost bit
+    };
+    for_each_candidate(g, cs, xs, u, cy, cz, r, t.periodic != 0, test);
+    deg[s] = cnt;  // an owned slot never carries the ghost bit
 }
 
 __device__ __forceinline__ uint32_t resolve_eidx(uint32_t e, uint32_t e_own) {
@@ -53,8 +54,8 @@ __device__ __forceinline__ uint32_t resolve_eidx(uint32_t e, uint32_t e_own) {
 
 // pass 2: write the row of every owned editable slot
 __global__ void __launch_bounds__(PAIR_THREADS)
-k_pairs_fill(int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
-             const uint32_t* __restrict__ cs, Grid g, Th t, uint32_t n_own, const uint32_t* __restrict__ deg,
+k_pairs_fill(int64_t n, const float4* __restrict__ orig4, const float* __restrict__ xs,
+             const uint32_t* __restrict__ cs, Grid g, Th t, double r, const uint32_t* __restrict__ deg,
              const unsigned long long* __restrict__ rowoff, const uint32_t* __restrict__ eidx, uint32_t e_own,
              uint32_t* __restrict__ rows) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -62,22 +63,22 @@ k_pairs_fill(int64_t n, const float4* __restrict__ orig4, const float4* __restri
     if ((deg[s] & 0x7FFFFFFFu) == 0) return;
     const float4 p = orig4[s];
     const uint32_t gp = __float_as_uint(p.w);
+    double u;
     int cx, cy, cz;
-    cell_of(p.x, p.y, p.z, g, cx, cy, cz);
+    cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
     unsigned long long k = rowoff[s];
-    for_each_neighbour_range(g, cs, cx, cy, cz, t.periodic != 0, [&](uint32_t a, uint32_t b) {
-        for (uint32_t j = a; j < b; j++) {
-            if (j == (uint32_t)s) continue;
-            const float4 q = orig4[j];
-            const float d2 = dist2(p, q, t);
-            if (t.lo2 < d2 && d2 <= t.hi2) {
-                uint32_t ent = resolve_eidx(eidx[j], e_own);
-                if (__float_as_uint(q.w) > gp) ent |= ENT_UPPER;
-                if (d2 <= t.b2) ent |= ENT_OLINK;
-                rows[k++] = ent;
-            }
+    auto emit = [&](uint32_t j) {
+        if (j == (uint32_t)s) return;
+        const float4 q = orig4[j];
+        const float d2 = dist2(p, q, t);
+        if (t.lo2 < d2 && d2 <= t.hi2) {
+            uint32_t ent = resolve_eidx(eidx[j], e_own);
+            if (__float_as_uint(q.w) > gp) ent |= ENT_UPPER;
+            if (d2 <= t.b2) ent |= ENT_OLINK;
+            rows[k++] = ent;
         }
-    });
+    };
+    for_each_candidate(g, cs, xs, u, cy, cz, r, t.periodic != 0, emit);
 }
 
 // compaction: editable e -> slot, row start, original and starting position
@@ -196,7 +197,7 @@ cc_status pairs_count(cc_ctx* c) {
     if (n > 0) {
         int tok = cc_prof_begin(c, "K2_count");
         CCL(c, k_pairs_count<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
-            n, c->orig4.p, c->dec4.p, c->cell_start.p, c->g, c->th, (uint32_t)c->n_in, c->deg.p));
+            n, c->orig4.p, c->dec4.p, c->xs.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in, c->deg.p));
         cc_prof_end(c, tok);
         CC_CUDA(c, cudaGetLastError());
     }
@@ -209,7 +210,7 @@ cc_status pairs_fill(cc_ctx* c) {
     if (n > 0 && c->nent > 0) {
         int tok = cc_prof_begin(c, "K2_fill");
         CCL(c, k_pairs_fill<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
-            n, c->orig4.p, c->dec4.p, c->cell_start.p, c->g, c->th, (uint32_t)c->n_in, c->deg.p,
+            n, c->orig4.p, c->xs.p, c->cell_start.p, c->g, c->th, c->r_pair, c->deg.p,
             reinterpret_cast<const unsigned long long*>(c->rowoff.p), c->eidx.p, (uint32_t)c->E, c->rows.p));
         cc_prof_end(c, tok);
         CC_CUDA(c, cudaGetLastError());

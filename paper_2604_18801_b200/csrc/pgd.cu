@@ -47,6 +47,7 @@ struct PgdArgs {
     long long* trace_a;
     double* trace_l;
     int count_only;
+    double* red;  // multi-GPU: local (active, loss) for the allreduce, else nullptr
 };
 
 __device__ __forceinline__ float adam_coord(float x, float g, float* __restrict__ m, float* __restrict__ v,
@@ -211,7 +212,10 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
         ctl->active = tu;
         ctl->loss = td;
         ctl->ticket = 0;
-        if (!a.count_only) {
+        if (a.red) {  // multi-GPU: the decision waits for the allreduce (dist.cu k_decide)
+            a.red[0] = (double)tu;
+            a.red[1] = td;
+        } else if (!a.count_only) {
             if (a.trace_a) {
                 a.trace_a[t - 1] = (long long)tu;
                 a.trace_l[t - 1] = td;
@@ -306,6 +310,7 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.trace_a = c->trace_a.p;
     a.trace_l = c->trace_l.p;
     a.count_only = count_only;
+    a.red = c->nranks > 1 ? c->red.p : nullptr;
     return a;
 }
 
@@ -319,6 +324,23 @@ int pgd_blocks(int64_t E) {
 }  // namespace
 
 const float4* pgd_result(cc_ctx* c) { return (c->last_iters & 1) ? c->posB.p : c->posA.p; }
+
+// (active, loss) of the count-only pass just enqueued, summed over ranks (synchronising)
+static cc_status global_check(cc_ctx* c, double* al) {
+    if (c->nranks > 1) {
+        CC_TRY(dist_allreduce_f64(c, c->red.p, 2));
+        CC_CUDA(c, cudaMemcpyAsync(c->h_red, c->red.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+        al[0] = c->h_red[0];
+        al[1] = c->h_red[1];
+    } else {
+        CC_CUDA(c, cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+        al[0] = (double)c->h_ctl->active;
+        al[1] = c->h_ctl->loss;
+    }
+    return CC_OK;
+}
 
 cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     const int64_t E = c->E, Ea = c->E_all;
@@ -358,10 +380,12 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     PgdArgs a0 = make_args(c, 1);
     CCL(c, k_pgd<<<nb, PGD_THREADS, 0, c->stream>>>(a0));
     CC_CUDA(c, cudaGetLastError());
-    CC_CUDA(c, cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
-    CC_CUDA(c, cudaStreamSynchronize(c->stream));
-    info->active0 = (int64_t)c->h_ctl->active;
-    info->loss0 = c->h_ctl->loss;
+    {
+        double al[2];
+        CC_TRY(global_check(c, al));
+        info->active0 = (int64_t)al[0];
+        info->loss0 = al[1];
+    }
     CCL(c, k_ctl_reset<<<1, 1, 0, c->stream>>>(c->ctl.p));
 
     int iters = 0;
@@ -387,6 +411,18 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
                 CCL(c, k_pgd<<<nb, PGD_THREADS, 0, c->stream>>>(a));
                 if (c->p.profile)
                     cudaEventRecordWithFlags(c->graph_ev[2 * k + 1], c->stream, cudaEventRecordExternal);
+                if (c->nranks > 1) {
+                    const int64_t l0 = c->launches;
+                    cc_status st = dist_iter_tail(c, c->posA.p, c->posB.p);
+                    if (st != CC_OK) {
+                        cudaGraph_t g2;
+                        cudaStreamEndCapture(c->stream, &g2);
+                        if (g2) cudaGraphDestroy(g2);
+                        return st;
+                    }
+                    c->launches_per_iter_tail = c->launches - l0;
+                    c->launches = l0;
+                }
             }
             c->launches -= batch;  // captured, not launched
             cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
@@ -400,7 +436,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
         int t_before = 0;
         for (;;) {
             CC_CUDA(c, cudaGraphLaunch(c->pgd_exec, c->stream));
-            c->launches += batch;
+            c->launches += batch * (1 + c->launches_per_iter_tail);
             CC_CUDA(c, cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
             CC_CUDA(c, cudaStreamSynchronize(c->stream));
             const Ctl h = *c->h_ctl;
@@ -436,12 +472,14 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     CCL(c, k_pgd<<<nb, PGD_THREADS, 0, c->stream>>>(af));
     cc_prof_end(c, tok);
     CC_CUDA(c, cudaGetLastError());
-    CC_CUDA(c, cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
-    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    double al[2];
+    CC_TRY(global_check(c, al));
     info->iterations = iters;
-    info->active_final = (int64_t)c->h_ctl->active;
-    info->loss_final = c->h_ctl->loss;
-    info->converged = c->p.stop_mode == CC_STOP_EPS ? (c->h_ctl->loss <= c->p.eps_loss) : (c->h_ctl->active == 0);
+    info->active_final = (int64_t)al[0];
+    info->loss_final = al[1];
+    info->converged = c->p.stop_mode == CC_STOP_EPS ? (al[1] <= c->p.eps_loss) : (al[0] == 0.0);
+    c->final_active = (unsigned long long)al[0];
+    c->final_loss = al[1];
     return CC_OK;
 }
 
