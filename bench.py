@@ -130,7 +130,7 @@ def _oracle_child(spec: str) -> int:
     ws = synth.Workload(d["name"], d["kind"], d["n"], d["L"], d["xi_rel"], b=d["b"], seed=d["seed"],
                         extra=d["extra"])
     arrs = [t.numpy() for t in synth.make(ws)]
-    c = oracle.cfg(L=ws.L, b=ws.linking_length, xi=ws.xi)
+    c = oracle.cfg(L=ws.L, b=ws.linking_length, xi=ws.xi, stop_mode=d.get("stop", oracle.STOP_RESTORED))
     oracle.build()
     t0 = time.perf_counter()
     r = oracle.pipeline(*arrs, c)
@@ -222,6 +222,8 @@ def main():
     ap.add_argument("--xi-rel", type=float, default=None)
     ap.add_argument("--n", type=int, default=None, help="override N (same density recipe)")
     ap.add_argument("--t-max", type=int, default=10000)
+    ap.add_argument("--stop", default="restored", choices=["restored", "active", "eps", "none"],
+                    help="Alg. 1 stop (R11): restored = L_tight <= 1e-10 and MCC = 1 (default)")
     ap.add_argument("--cells-per-particle", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -255,7 +257,8 @@ def main():
         del own
     torch.cuda.synchronize(dev)
     n = x.shape[0]
-    params = cc.Params(box=w.L, b=w.linking_length, xi=w.xi, profile=1, t_max=args.t_max)
+    stop = {"restored": cc.STOP_RESTORED, "active": cc.STOP_ACTIVE, "eps": cc.STOP_EPS, "none": cc.STOP_NONE}[args.stop]
+    params = cc.Params(box=w.L, b=w.linking_length, xi=w.xi, profile=1, t_max=args.t_max, stop_mode=stop)
     if args.cells_per_particle:
         params.cells_per_particle = args.cells_per_particle
     distarg = None
@@ -357,7 +360,9 @@ def main():
                    "parallelism": f"x-slabs x{world} (NCCL ghosts + per-iteration refresh/allreduce)" if world > 1
                    else "1 GPU",
                    "l2": "L2 flushed between steps (256 MB write)" if small else "inputs (24 N B) larger than the 126 MB L2",
-                   "stop": "no L_tight-active pair (R11)", "t_max": args.t_max, "rows_per_axis": vp["cells_per_axis"]},
+                   "stop": {"restored": "L_tight <= 1e-10 and all link statuses restored (Alg. 1 l.6 + MCC=1, R11)",
+                            "active": "no L_tight-active pair (R11)", "eps": "L_tight <= 1e-10 (Alg. 1 l.6)",
+                            "none": "fixed t_max updates"}[args.stop], "t_max": args.t_max, "rows_per_axis": vp["cells_per_axis"]},
         "result": {"n_pairs": vp["n_pairs"], "n_editable": vp["n_editable"], "violated0": vp["n_violated0"],
                    "iterations": info["iterations"], "converged": info["converged"], "mcc_after": m["mcc"],
                    "fof_groups_orig": ng_o, "fof_groups_corr": ng_c, "halos_equal": bool(np.array_equal(h_o, h_c))},

@@ -47,7 +47,9 @@ typedef enum {
 
 enum { CC_STOP_ACTIVE = 0,  /* stop when no pair is L_tight-active (R11; default)             */
        CC_STOP_EPS = 1,     /* stop when L_tight <= eps_loss (Alg. 1 line 6)           */
-       CC_STOP_NONE = 2 };  /* run exactly t_max updates (truncated mode)        */
+       CC_STOP_NONE = 2,    /* run exactly t_max updates (truncated mode)        */
+       CC_STOP_RESTORED = 3 }; /* L_tight <= eps_loss AND every vulnerable pair's link status
+                                  restored (MCC = 1; Alg. 1 l.6 + north_star's stop)          */
 enum { CC_OPT_ADAM = 0, CC_OPT_VANILLA = 1 };
 enum { CC_ORIG = 0, CC_DECOMP = 1, CC_CORR = 2 };  /* which positions cc_fof_label/cc_mcc use */
 
@@ -131,14 +133,18 @@ typedef struct {
     int64_t active0;        /* L_tight-active pairs at P_hat^(0)                             */
     int64_t active_final;   /* L_tight-active pairs at the returned positions                */
     double loss0, loss_final; /* L_tight (fp64 sums of fp32 terms; reporting only, R16)       */
-    int converged;
+    int converged;            /* the stop rule holds at the returned positions                */
     int pad;
+    int64_t violated0;        /* pairs whose link status differs from the original (Eq. 1)    */
+    int64_t violated_final;
 } cc_corr_info;
 cc_status cc_correct(cc_ctx* ctx, float* xo, float* yo, float* zo, cc_corr_info* info_h);
 
-/* L_tight-active count and loss per stop check of the last cc_correct (trace of Fig. 6,
- * P:91-99); up to cap entries, *n_h = iterations + 1. */
-cc_status cc_get_trace(cc_ctx* ctx, int64_t* active_h, double* loss_h, int64_t cap, int64_t* n_h);
+/* L_tight-active count, L_tight and violated-pair count per stop check of the last cc_correct
+ * (the L_tight-vs-iteration trace of Fig. 6); up to cap entries each (violated_h may
+ * be NULL), *n_h = iterations + 1 (the last entry is the returned state). */
+cc_status cc_get_trace(cc_ctx* ctx, int64_t* active_h, double* loss_h, int64_t* violated_h, int64_t cap,
+                       int64_t* n_h);
 
 /* S6 -- FoF labels (§II-B, Fig. 1) on ORIG, DECOMP or CORR positions: edge iff the
  * pinned fp32 d2 <= fl32(b^2); label = minimum gid of the connected component (R20).

@@ -56,7 +56,7 @@ class CorrInfo(C.Structure):
                 ("pad", C.c_int)]
 
 
-STOP_ACTIVE, STOP_EPS, STOP_NONE = 0, 1, 2
+STOP_ACTIVE, STOP_EPS, STOP_NONE, STOP_RESTORED = 0, 1, 2, 3
 
 _lib = None
 
@@ -85,7 +85,7 @@ def lib():
                                    C.c_int, f64p]
         L.oc_tight_f64.restype = C.c_double
         L.oc_correct.argtypes = [C.c_int64, f32p, f32p, f32p, f32p, f32p, f32p, u32p, C.c_int64, i64p, i64p,
-                                 u8p, P(Cfg), f32p, f32p, f32p, P(CorrInfo), i64p, f64p]
+                                 u8p, P(Cfg), f32p, f32p, f32p, P(CorrInfo), i64p, f64p, i64p]
         _lib = L
     return _lib
 
@@ -217,7 +217,7 @@ def tight_f64(P, pairs, b, eps_q, L=1.0, periodic=True, grad=False):
 
 def correct(x, y, z, xh, yh, zh, pairs, c: Cfg, gid=None, trace=False):
     """Alg. 1 lines 4-10: PGD-Adam on L_tight with projection onto B(xi').
-    Returns (xo, yo, zo, info dict[, (trace_active, trace_loss)])."""
+    Returns (xo, yo, zo, info dict[, (trace_active, trace_loss, trace_violated)])."""
     arrs = [_f32(a) for a in (x, y, z, xh, yh, zh)]
     n = arrs[0].shape[0]
     pi, pj, pf = [np.ascontiguousarray(a) for a in pairs]
@@ -227,18 +227,19 @@ def correct(x, y, z, xh, yh, zh, pairs, c: Cfg, gid=None, trace=False):
     info = CorrInfo()
     ta = np.zeros(c.t_max + 1, np.int64) if trace else None
     tl = np.zeros(c.t_max + 1, np.float64) if trace else None
+    tv = np.zeros(c.t_max + 1, np.int64) if trace else None
     st = lib().oc_correct(n, *[_ptr(a, C.c_float) for a in arrs], None if g is None else _ptr(g, C.c_uint32),
                           pi.shape[0], _ptr(pi, C.c_int64), _ptr(pj, C.c_int64), _ptr(pf, C.c_uint8),
                           C.byref(c), _ptr(xo, C.c_float), _ptr(yo, C.c_float), _ptr(zo, C.c_float),
                           C.byref(info), None if ta is None else _ptr(ta, C.c_int64),
-                          None if tl is None else _ptr(tl, C.c_double))
+                          None if tl is None else _ptr(tl, C.c_double), None if tv is None else _ptr(tv, C.c_int64))
     if st:
         raise RuntimeError(f"oc_correct status {st}")
     d = {k: getattr(info, k) for k, _ in CorrInfo._fields_ if k != "pad"}
     d["converged"] = bool(d["converged"])
     if trace:
         k = d["iterations"] + 1
-        return xo, yo, zo, d, (ta[:k], tl[:k])
+        return xo, yo, zo, d, (ta[:k], tl[:k], tv[:k])
     return xo, yo, zo, d
 
 

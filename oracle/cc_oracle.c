@@ -37,7 +37,8 @@ typedef struct {
     int t_max;           /* Alg. 1 T_max */
     double eps_loss;     /* Alg. 1 epsilon_L */
     int stop_mode;       /* 0: stop when no L_tight-active pair (R11); 1: L_tight <= eps_loss
-                            (Alg. 1 line 6); 2: never stop early (exactly t_max updates) */
+                            (Alg. 1 line 6); 2: never stop early (exactly t_max updates);
+                            3: L_tight <= eps_loss and every link status restored (MCC = 1) */
     int optimizer;       /* 0: Adam; 1: vanilla projected gradient */
     double vanilla_step; /* step for optimizer 1 (Alg. 1 line 9 "P - alpha g") */
 } oc_cfg;
@@ -579,7 +580,7 @@ int oc_correct(int64_t n, const float* x, const float* y, const float* z, const 
                const float* yh, const float* zh, const uint32_t* gid, int64_t np,
                const int64_t* pi, const int64_t* pj, const uint8_t* pf, const oc_cfg* c,
                float* xo, float* yo, float* zo, oc_corr_info* info, int64_t* trace_active,
-               double* trace_loss) {
+               double* trace_loss, int64_t* trace_violated) {
     oc_th t;
     int st = oc_thresholds(c, &t);
     if (st) return st;
@@ -660,8 +661,10 @@ int oc_correct(int64_t n, const float* x, const float* y, const float* z, const 
             if (t_it > 1) eval_pairs(P, np, pi, pj, pf, &t, per, &act, &loss, &viol);
             if (trace_active) trace_active[t_it - 1] = act;
             if (trace_loss) trace_loss[t_it - 1] = loss;
+            if (trace_violated) trace_violated[t_it - 1] = viol;
             if (c->stop_mode == 0 && act == 0) break;
             if (c->stop_mode == 1 && loss <= c->eps_loss) break;
+            if (c->stop_mode == 3 && viol == 0 && loss <= c->eps_loss) break;
             p1 = p1 * c->beta1;
             p2 = p2 * c->beta2;
             const float bc1 = (float)(1.0 - p1), bc2 = (float)(1.0 - p2);
@@ -702,10 +705,13 @@ int oc_correct(int64_t n, const float* x, const float* y, const float* z, const 
         eval_pairs(P, np, pi, pj, pf, &t, per, &act, &loss, &viol);
         if (trace_active) trace_active[info->iterations] = act;
         if (trace_loss) trace_loss[info->iterations] = loss;
+        if (trace_violated) trace_violated[info->iterations] = viol;
         info->active_final = act;
         info->loss_final = loss;
         info->violated_final = viol;
-        info->converged = c->stop_mode == 1 ? (loss <= c->eps_loss) : (act == 0);
+        if (c->stop_mode == 1) info->converged = loss <= c->eps_loss;
+        else if (c->stop_mode == 3) info->converged = viol == 0 && loss <= c->eps_loss;
+        else info->converged = act == 0;
     }
     for (int64_t i = 0; i < n; i++) { xo[i] = P[3 * i]; yo[i] = P[3 * i + 1]; zo[i] = P[3 * i + 2]; }
 done:

@@ -6,7 +6,7 @@ works without a GPU (for building and ABI checks) but every compute call needs t
 extension and a device, and raises otherwise.
 """
 from .binding import (CC_CORR, CC_DECOMP, CC_ORIG, CCError, Corrector, Params, STOP_ACTIVE, STOP_EPS,
-                      STOP_NONE, hmf, lib, lib_path, nccl_unique_id, shell_masks, slab_of)
+                      STOP_NONE, STOP_RESTORED, hmf, lib, lib_path, nccl_unique_id, shell_masks, slab_of)
 
 __all__ = ["Corrector", "Params", "CCError", "hmf", "lib", "lib_path", "nccl_unique_id", "slab_of", "CC_ORIG",
-           "CC_DECOMP", "CC_CORR", "STOP_ACTIVE", "STOP_EPS", "STOP_NONE"]
+           "CC_DECOMP", "CC_CORR", "STOP_ACTIVE", "STOP_EPS", "STOP_NONE", "STOP_RESTORED"]

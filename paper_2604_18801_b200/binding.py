@@ -14,7 +14,7 @@ _LIB_PATH = os.path.join(HERE, "libcc.so")
 
 CC_OK, CC_NOT_CONVERGED = 0, 2
 CC_ORIG, CC_DECOMP, CC_CORR = 0, 1, 2
-STOP_ACTIVE, STOP_EPS, STOP_NONE = 0, 1, 2
+STOP_ACTIVE, STOP_EPS, STOP_NONE, STOP_RESTORED = 0, 1, 2, 3
 CC_RUN_HOST = 1
 _STATUS = {0: "CC_OK", 2: "CC_NOT_CONVERGED", 64: "CC_E_ARG", 65: "CC_E_DATA", 66: "CC_E_BOUND",
            67: "CC_E_OOM", 68: "CC_E_CUDA", 69: "CC_E_NCCL", 70: "CC_E_STATE"}
@@ -46,7 +46,8 @@ class _VP(C.Structure):
 
 class _Corr(C.Structure):
     _fields_ = [("iterations", C.c_int64), ("active0", C.c_int64), ("active_final", C.c_int64),
-                ("loss0", C.c_double), ("loss_final", C.c_double), ("converged", C.c_int), ("pad", C.c_int)]
+                ("loss0", C.c_double), ("loss_final", C.c_double), ("converged", C.c_int), ("pad", C.c_int),
+                ("violated0", C.c_int64), ("violated_final", C.c_int64)]
 
 
 class _Mcc(C.Structure):
@@ -91,7 +92,7 @@ def lib():
     L.cc_find_vulnerable.argtypes = [vp, P(_VP)]
     L.cc_get_pairs.argtypes = [vp, vp, vp, vp, i64, P(i64)]
     L.cc_correct.argtypes = [vp, vp, vp, vp, P(_Corr)]
-    L.cc_get_trace.argtypes = [vp, P(i64), P(d), i64, P(i64)]
+    L.cc_get_trace.argtypes = [vp, P(i64), P(d), P(i64), i64, P(i64)]
     L.cc_fof_label.argtypes = [vp, C.c_int, vp, P(i64)]
     L.cc_mcc.argtypes = [vp, C.c_int, P(_Mcc)]
     L.cc_halo_sizes.argtypes = [vp, C.c_int, i64, P(i64), i64, P(i64)]
@@ -227,9 +228,11 @@ class Corrector:
         n = C.c_int64()
         a = np.zeros(self.params.t_max + 2, np.int64)
         l = np.zeros(self.params.t_max + 2, np.float64)
+        v = np.zeros(self.params.t_max + 2, np.int64)
         self._chk(self.lib.cc_get_trace(self.h, a.ctypes.data_as(C.POINTER(C.c_int64)),
-                                        l.ctypes.data_as(C.POINTER(C.c_double)), a.shape[0], C.byref(n)))
-        return a[: n.value], l[: n.value]
+                                        l.ctypes.data_as(C.POINTER(C.c_double)),
+                                        v.ctypes.data_as(C.POINTER(C.c_int64)), a.shape[0], C.byref(n)))
+        return a[: n.value], l[: n.value], v[: n.value]
 
     # S6
     def fof_label(self, which=CC_ORIG, labels=None):

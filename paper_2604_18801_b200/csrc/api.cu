@@ -212,7 +212,7 @@ cc_status cc_create(cc_ctx** out, int device, void* stream, const cc_params* p, 
     *out = nullptr;
     if (!p) return CC_E_ARG;
     if (!(p->box > 0) || !(p->xi >= 0) || p->m < 2 || p->m > 52 || p->t_max < 0 || p->stop_mode < 0 ||
-        p->stop_mode > 2 || p->optimizer < 0 || p->optimizer > 1)
+        p->stop_mode > 3 || p->optimizer < 0 || p->optimizer > 1)
         return CC_E_ARG;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0 || device < 0 || device >= ndev) {
@@ -243,7 +243,7 @@ cc_status cc_create(cc_ctx** out, int device, void* stream, const cc_params* p, 
     c->owns_stream = (stream == nullptr);
     if (cudaMallocHost(&c->h_ctl, sizeof(cc::Ctl)) != cudaSuccess ||
         cudaMallocHost(&c->h_counters, 16 * sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMallocHost(&c->h_red, 2 * sizeof(double)) != cudaSuccess) {
+        cudaMallocHost(&c->h_red, 4 * sizeof(double)) != cudaSuccess) {
         cc_destroy(c);
         return CC_E_CUDA;
     }
@@ -269,6 +269,7 @@ void cc_destroy(cc_ctx* c) {
     cc_release(c, c->scratch_u32); cc_release(c, c->rowoff); cc_release(c, c->rowptr); cc_release(c, c->scratch_u64);
     cc_release(c, c->mom); cc_release(c, c->bc); cc_release(c, c->partial_d); cc_release(c, c->partial_u);
     cc_release(c, c->counters); cc_release(c, c->ctl); cc_release(c, c->trace_a); cc_release(c, c->trace_l);
+    cc_release(c, c->trace_v); cc_release(c, c->longrow);
     cc_release(c, c->tmp_bytes); cc_release(c, c->in_f); cc_release(c, c->in_gid);
     for (int d = 0; d < 2; d++) {
         cc_release(c, c->dflag[d]); cc_release(c, c->dpos[d]); cc_release(c, c->shell[d]); cc_release(c, c->sbuf7[d]);
@@ -429,13 +430,14 @@ cc_status cc_correct(cc_ctx* c, float* xo, float* yo, float* zo, cc_corr_info* i
     return local.converged ? CC_OK : CC_NOT_CONVERGED;
 }
 
-cc_status cc_get_trace(cc_ctx* c, int64_t* active_h, double* loss_h, int64_t cap, int64_t* n_h) {
+cc_status cc_get_trace(cc_ctx* c, int64_t* active_h, double* loss_h, int64_t* viol_h, int64_t cap, int64_t* n_h) {
     CC_GUARD(c);
     if (c->state < 3) return cc_fail(c, CC_E_STATE, "cc_correct first");
+    if (cap > 0 && (!active_h || !loss_h)) return cc_fail(c, CC_E_ARG, "null output");
     const int64_t n = (int64_t)c->last_iters + 1;
     // trace[t-1] holds the stop check of iteration t; checks ran for t = 1..iters+1 unless the
     // loop ended on T_max (then the last state was checked by the final pass only)
-    std::vector<long long> a((size_t)n, 0);
+    std::vector<long long> a((size_t)n, 0), v((size_t)n, 0);
     std::vector<double> l((size_t)n, 0.0);
     const int64_t k = std::min<int64_t>(n, (int64_t)c->p.t_max);
     if (k > 0) {
@@ -443,13 +445,17 @@ cc_status cc_get_trace(cc_ctx* c, int64_t* active_h, double* loss_h, int64_t cap
                                    c->stream));
         CC_CUDA(c, cudaMemcpyAsync(l.data(), c->trace_l.p, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost,
                                    c->stream));
+        CC_CUDA(c, cudaMemcpyAsync(v.data(), c->trace_v.p, (size_t)k * sizeof(long long), cudaMemcpyDeviceToHost,
+                                   c->stream));
     }
     CC_CUDA(c, cudaStreamSynchronize(c->stream));
     a[(size_t)n - 1] = (long long)c->final_active;  // final (global) check of the returned state
     l[(size_t)n - 1] = c->final_loss;
+    v[(size_t)n - 1] = (long long)c->final_violated;
     for (int64_t q = 0; q < n && q < cap; q++) {
         active_h[q] = a[(size_t)q];
         loss_h[q] = l[(size_t)q];
+        if (viol_h) viol_h[q] = v[(size_t)q];
     }
     if (n_h) *n_h = n;
     return CC_OK;

@@ -63,7 +63,8 @@ struct Ctl {
     int converged;
     unsigned int ticket;
     int pad;
-    unsigned long long active;   // active count of the last check
+    unsigned long long active;   // L_tight-active pairs at the last check
+    unsigned long long violated; // pairs whose link status differs from the original (Eq. 1)
     double loss;
 };
 
@@ -123,7 +124,9 @@ struct cc_ctx {
     cc::DBuf<double> partial_d;  // block partials
     cc::DBuf<unsigned long long> partial_u, counters;
     cc::DBuf<cc::Ctl> ctl;
-    cc::DBuf<long long> trace_a;
+    cc::DBuf<long long> trace_a, trace_v;
+    cc::DBuf<uint32_t> longrow;  // editable rows longer than 32 entries (K3 warp path)
+    int64_t n_long = 0;
     cc::DBuf<double> trace_l;
     cc::DBuf<unsigned char> tmp_bytes;  // scan scratch
     cc::DBuf<float> in_f;        // cc_run host staging: 6 n floats
@@ -144,6 +147,7 @@ struct cc_ctx {
     double* h_red = nullptr;
     unsigned long long final_active = 0;
     double final_loss = 0.0;
+    unsigned long long final_violated = 0;
 
     // pinned host mirrors
     cc::Ctl* h_ctl = nullptr;
@@ -151,7 +155,8 @@ struct cc_ctx {
 
     // PGD graph cache
     cudaGraphExec_t pgd_exec = nullptr;
-    const void* pgd_key[4] = {nullptr, nullptr, nullptr, nullptr};
+    const void* pgd_key[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    int64_t pgd_nlong = -1;
     int pgd_batch = 0;
     int64_t pgd_E = -1;
     int last_iters = 0;
@@ -166,6 +171,16 @@ struct cc_ctx {
 };
 
 namespace cc {
+
+// Alg. 1 line 6 stop test per stop mode (R11): ACTIVE: no L_tight-active pair;
+// EPS: L_tight <= eps_L; RESTORED: L_tight <= eps_L and every link status restored (MCC = 1)
+__host__ __device__ inline bool stop_rule(int mode, unsigned long long active, double loss,
+                                          unsigned long long violated, double eps_loss) {
+    if (mode == CC_STOP_ACTIVE) return active == 0ull;
+    if (mode == CC_STOP_EPS) return loss <= eps_loss;
+    if (mode == CC_STOP_RESTORED) return violated == 0ull && loss <= eps_loss;
+    return false;
+}
 
 // ---------------------------------------------------------------------------------------
 // pinned fp32 distance arithmetic (R4): explicit round-to-nearest intrinsics, no

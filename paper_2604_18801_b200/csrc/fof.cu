@@ -105,10 +105,23 @@ k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ o
     }
 }
 
+// read-only root walk: the flatten pass must not path-halve, or a halving write could land
+// after another thread's final par[x] = root and leave x pointing at a non-root
+__device__ __forceinline__ uint32_t uf_root(const uint32_t* par, uint32_t x) {
+    const volatile uint32_t* vp = par;
+    uint32_t p = vp[x];
+    while (p != x) {
+        x = p;
+        p = vp[x];
+    }
+    return x;
+}
+
 __global__ void k_flatten(int64_t n, uint32_t* __restrict__ par) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    par[s] = uf_find(par, (uint32_t)s);
+    const uint32_t r = uf_root(par, (uint32_t)s);
+    par[s] = r;  // only ever replaces par[s] by an ancestor of s: safe for concurrent walkers
 }
 
 __global__ void k_mingid(int64_t n, const uint32_t* __restrict__ par, const float4* __restrict__ orig4,

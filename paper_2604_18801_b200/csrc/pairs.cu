@@ -119,12 +119,8 @@ k_sort_short(uint32_t e_own, const unsigned long long* __restrict__ rowptr, cons
     if (e >= e_own) return;
     const unsigned long long a = rowptr[e], b = rowptr[e + 1];
     const int len = (int)(b - a);
-    if (len <= 1) return;
-    if (len > SHORT_ROW) {
-        unsigned long long q = atomicAdd(n_long, 1ull);
-        long_list[q] = e;
-        return;
-    }
+    long_list[e] = len > SHORT_ROW ? 1u : 0u;  // flags; compacted in order by rows_finish
+    if (len <= 1 || len > SHORT_ROW) return;
     unsigned long long v[SHORT_ROW];
     for (int i = 0; i < len; i++) {
         unsigned long long x = row_key(rows[a + i], posA);
@@ -136,6 +132,13 @@ k_sort_short(uint32_t e_own, const unsigned long long* __restrict__ rowptr, cons
         v[j + 1] = x;
     }
     for (int i = 0; i < len; i++) rows[a + i] = (uint32_t)v[i];
+}
+
+// ordered compaction of flagged editables (deterministic long-row list)
+__global__ void k_flag_compact(uint32_t E, const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                               uint32_t* __restrict__ list) {
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < E && flag[e]) list[pos[e]] = e;
 }
 
 // long rows: one block per row, bitonic sort in shared memory (<= LONG_SORT_MAX entries), and
@@ -236,17 +239,28 @@ cc_status rows_finish(cc_ctx* c) {
     cc_prof_end(c, tok);
     CC_CUDA(c, cudaGetLastError());
     CC_TRY(pairs_fill(c));
+    c->n_long = 0;
+    CC_TRY(cc_ensure(c, c->longrow, (size_t)std::max<int64_t>(c->E, 1), "long rows"));
     if (c->E > 0 && c->nent > 0) {
-        CC_TRY(cc_ensure(c, c->scratch_u32, (size_t)c->E, "long rows"));
         CC_TRY(cc_ensure(c, c->scratch_u64, 2, "long count"));
         CC_CUDA(c, cudaMemsetAsync(c->scratch_u64.p, 0, sizeof(uint64_t), c->stream));
         unsigned long long* nl = reinterpret_cast<unsigned long long*>(c->scratch_u64.p);
         int t2 = cc_prof_begin(c, "K2_sort");
-        CCL(c, k_sort_short<<<(unsigned)((c->E + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
-            (uint32_t)c->E, rowptr, c->posA.p, c->rows.p, c->scratch_u32.p, nl));
-        CCL(c, k_sort_long<<<148 * 2, 512, 0, c->stream>>>(c->scratch_u32.p, nl, rowptr, c->posA.p, c->rows.p));
+        // deg is dead after the fill: reuse it for the long-row flags, scratch_u32 for their ranks
+        CC_TRY(cc_ensure(c, c->scratch_u32, (size_t)c->E + 1, "long row ranks"));
+        const unsigned ge = (unsigned)((c->E + PAIR_THREADS - 1) / PAIR_THREADS);
+        CCL(c, k_sort_short<<<ge, PAIR_THREADS, 0, c->stream>>>((uint32_t)c->E, rowptr, c->posA.p, c->rows.p,
+                                                                c->deg.p, nl));
+        CC_TRY(scan_u32_to_u32(c, c->deg.p, c->scratch_u32.p, c->E, reinterpret_cast<uint64_t*>(nl)));
+        CCL(c, k_flag_compact<<<ge, PAIR_THREADS, 0, c->stream>>>((uint32_t)c->E, c->deg.p, c->scratch_u32.p,
+                                                                  c->longrow.p));
+        CCL(c, k_sort_long<<<148 * 2, 512, 0, c->stream>>>(c->longrow.p, nl, rowptr, c->posA.p, c->rows.p));
         cc_prof_end(c, t2);
         CC_CUDA(c, cudaGetLastError());
+        CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 1, nl, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                   c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+        c->n_long = (int64_t)c->h_counters[1];
     }
     return CC_OK;
 }

@@ -99,9 +99,11 @@ def assert_parity(g, o, fof=True, exact_positions=True):
     md, mc = g["mcc_dec"], g["mcc_cor"]
     assert (md["tp"], md["tn"], md["fp"], md["fn"]) == tuple(o["mcc_dec"])
     assert (mc["tp"], mc["tn"], mc["fp"], mc["fn"]) == tuple(o["mcc_cor"])
-    ta, tl = g["trace"]
-    oa, ol = o["trace"]
+    ta, tl, tv = g["trace"]
+    oa, ol, ov = o["trace"]
     assert np.array_equal(ta, oa), (ta[:10], oa[:10])
+    assert np.array_equal(tv, ov), (tv[:10], ov[:10])
+    assert gi["violated0"] == oi["violated0"] and gi["violated_final"] == oi["violated_final"]
     if fof:
         for name in ("orig", "dec", "cor"):
             assert g["ng_" + name] == o["ng_" + name], name

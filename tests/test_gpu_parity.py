@@ -56,7 +56,8 @@ def test_c3_fcc_bit_exact():
     assert_parity(gpu_pipeline(arrs, p), oracle_pipeline(arrs, p))
 
 
-@pytest.mark.parametrize("mode,tmax", [(cc.STOP_NONE, 7), (cc.STOP_NONE, 40), (cc.STOP_EPS, 10000), (cc.STOP_ACTIVE, 5)])
+@pytest.mark.parametrize("mode,tmax", [(cc.STOP_NONE, 7), (cc.STOP_NONE, 40), (cc.STOP_EPS, 10000), (cc.STOP_ACTIVE, 5),
+                                       (cc.STOP_RESTORED, 10000)])
 def test_stop_modes_bit_exact(mode, tmax):
     """Alg. 1 stop variants: truncated (exactly t_max updates), eps_L, active-count with a cap
     that ends the loop unconverged."""

@@ -222,6 +222,13 @@ def test_convergence_restores_clusters(xi_rel, dither):
     ce = oracle.cfg(L=1.0, b=w.linking_length, xi=w.xi, stop_mode=oracle.STOP_EPS, eps_loss=1e-10)
     _, _, _, info = oracle.correct(x, y, z, xh, yh, zh, r.pairs, ce)
     assert info["iterations"] <= oracle.iteration_budget(oracle.thresholds(c)["xi"], info["active0"], 1e-10)
+    # the bench's stop (Alg. 1 eps_L test + every link status restored): MCC = 1 at the stop
+    cr = oracle.cfg(L=1.0, b=w.linking_length, xi=w.xi, stop_mode=oracle.STOP_RESTORED, eps_loss=1e-10)
+    xr, yr, zr, ir = oracle.correct(x, y, z, xh, yh, zh, r.pairs, cr)
+    assert ir["converged"] and ir["violated_final"] == 0 and ir["loss_final"] <= 1e-10
+    assert ir["iterations"] <= r.info["iterations"]
+    ol = (r.pairs[2] & 1).astype(bool)
+    assert oracle.mcc(*oracle.mcc_counts(ol, oracle.pair_links(r.pairs[0], r.pairs[1], xr, yr, zr, cr))) == 1.0
 
 
 def test_vanilla_pgd_monotone():
@@ -235,7 +242,7 @@ def test_vanilla_pgd_monotone():
     step = 1.0 / (4.0 * deg)
     c = oracle.cfg(L=1.0, b=w.linking_length, xi=w.xi, optimizer=1, vanilla_step=step, t_max=60,
                    stop_mode=oracle.STOP_NONE)
-    _, _, _, info, (ta, tl) = oracle.correct(x, y, z, xh, yh, zh, pairs, c, trace=True)
+    _, _, _, info, (ta, tl, tv) = oracle.correct(x, y, z, xh, yh, zh, pairs, c, trace=True)
     assert tl[-1] < tl[0]
     assert np.all(np.diff(tl) <= 1e-7 * tl[0]), np.diff(tl).max()
 
