@@ -65,6 +65,7 @@ CC_INST(cc::Ctl)
 CC_INST(long long)
 CC_INST(unsigned char)
 CC_INST(uint2)
+CC_INST(uint4)
 
 // ------------------------------------------------------------------------------------------
 // profiling
@@ -151,6 +152,9 @@ static cc_status derive_params(cc_ctx* c, int64_t n_total) {
     c->delta = std::max(hi, std::sqrt((double)t.hi2));
     c->r_pair = c->delta * (1.0 + 1e-5);  // search radius / ghost width (margin for fp32 rounding)
     c->r_link = std::max(b, std::sqrt((double)t.b2)) * (1.0 + 1e-5);
+    // corrected positions lie within xi' < xi_f of the original: a stable link (d2 <= lo2) keeps
+    // d_hat <= b - 2 sqrt3 (xi_f - xi'), safely below b when that margin >> fp32 rounding of d
+    c->corr_base_ok = 2.0 * std::sqrt(3.0) * ((double)t.xi_f - (double)t.xip_f) > 1e-6 * b;
     if (p.periodic && c->delta >= 0.5 * p.box)
         return cc_fail(c, CC_E_ARG, "b + 2 sqrt3 xi must be < box/2 for minimum-image distances");
     return CC_OK;
@@ -269,7 +273,7 @@ void cc_destroy(cc_ctx* c) {
     cc_release(c, c->scratch_u32); cc_release(c, c->rowoff); cc_release(c, c->rowptr); cc_release(c, c->scratch_u64);
     cc_release(c, c->mom); cc_release(c, c->bc); cc_release(c, c->partial_d); cc_release(c, c->partial_u);
     cc_release(c, c->counters); cc_release(c, c->ctl); cc_release(c, c->trace_a); cc_release(c, c->trace_l);
-    cc_release(c, c->trace_v); cc_release(c, c->longrow);
+    cc_release(c, c->trace_v); cc_release(c, c->longrow); cc_release(c, c->parent_base); cc_release(c, c->rec32);
     cc_release(c, c->tmp_bytes); cc_release(c, c->in_f); cc_release(c, c->in_gid);
     for (int d = 0; d < 2; d++) {
         cc_release(c, c->dflag[d]); cc_release(c, c->dpos[d]); cc_release(c, c->shell[d]); cc_release(c, c->sbuf7[d]);
@@ -318,6 +322,7 @@ cc_status cc_build_cells(cc_ctx* c, int64_t n, const float* x, const float* y, c
     c->state = 0;
     c->have_labels[0] = c->have_labels[1] = c->have_labels[2] = 0;
     c->fof_which = -1;
+    c->base_valid = false;
     int64_t n_total = n;
     if (c->nranks > 1) {
         if (n > 0 && !gid) return cc_fail(c, CC_E_ARG, "multi-GPU needs global particle ids (gid)");

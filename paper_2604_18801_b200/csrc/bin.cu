@@ -3,13 +3,16 @@
 // converts these counts into cell-start offsets, after which a scatter kernel places each
 // particle into a cell-sorted array using atomic index reservations."
 //
-// B200 form (the x-sorted-row structure of cc_internal.cuh): a fused key + histogram kernel
-// (coalesced SoA reads; the u32 atomic's return value is the particle's provisional rank in its
-// cell; it also checks the input contract), the reduce-then-scan of scan.cu, a scatter of
-// 8-byte (x-key, index) records, an in-cell sort of those records by x (cells hold ~1/K
-// particles on average: thread-per-cell insertion sort, block bitonic for crowded cells), and
-// a coalesced gather writing the float4 (x,y,z,gid) / (xh,yh,zh,i) records every later kernel
-// reads.  The slot order is therefore fully determined by the data (x ties by input index).
+// B200 form (the x-sorted-row structure of cc_internal.cuh):
+//  1. key + histogram: coalesced SoA reads, one u32 atomic per particle whose return value is
+//     its provisional rank inside the cell; checks the input contract (finite, |x_hat-x|<=xi).
+//  2. reduce-then-scan of the counts (scan.cu) -> cell_start.
+//  3. scatter of one full 32-byte record (x,y,z,x_hat,y_hat,z_hat,gid,i) per particle: one
+//     aligned full-sector write each, instead of re-gathering six arrays later.
+//  4. per-cell finish: each cell (~1/K particles on average) sorts its records by x in
+//     registers (crowded cells: a block bitonic) and writes the float4 records, xs and slot_of.
+//     Consecutive threads own consecutive cells, so reads and writes stream.
+// The slot order is fully determined by the data (x ties broken by input index).
 #include <cmath>
 
 #include "cc_internal.cuh"
@@ -18,8 +21,14 @@ namespace cc {
 namespace {
 
 constexpr int BIN_THREADS = 256;
-constexpr int CELL_SHORT = 32;
+constexpr int CELL_SHORT = 16;
 constexpr int CELL_LONG_MAX = 4096;
+
+struct __align__(16) Rec {
+    float x, y, z, xh;
+    float yh, zh;
+    uint32_t gid, i;
+};
 
 __global__ void __launch_bounds__(BIN_THREADS)
 k_bin_key(int64_t n, const float* __restrict__ x, const float* __restrict__ y, const float* __restrict__ z,
@@ -45,45 +54,88 @@ k_bin_key(int64_t n, const float* __restrict__ x, const float* __restrict__ y, c
 }
 
 __global__ void __launch_bounds__(BIN_THREADS)
-k_bin_scatter(int64_t n, const float* __restrict__ x, const uint32_t* __restrict__ key, const uint32_t* __restrict__ rnk,
-              const uint32_t* __restrict__ cell_start, Grid g, unsigned long long* __restrict__ rec) {
+k_bin_scatter(int64_t n, const float* __restrict__ x, const float* __restrict__ y, const float* __restrict__ z,
+              const float* __restrict__ xh, const float* __restrict__ yh, const float* __restrict__ zh,
+              const uint32_t* __restrict__ gid, const uint32_t* __restrict__ key, const uint32_t* __restrict__ rnk,
+              const uint32_t* __restrict__ cell_start, Rec* __restrict__ rec) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t s = cell_start[key[i]] + rnk[i];
-    rec[s] = ((unsigned long long)x_sort_key(x[i], g) << 32) | (unsigned long long)(uint32_t)i;
+    Rec r;
+    r.x = x[i];
+    r.y = y[i];
+    r.z = z[i];
+    r.xh = xh[i];
+    r.yh = yh[i];
+    r.zh = zh[i];
+    r.gid = gid ? gid[i] : (uint32_t)i;
+    r.i = (uint32_t)i;
+    reinterpret_cast<uint4*>(rec)[2 * s] = *reinterpret_cast<const uint4*>(&r.x);
+    reinterpret_cast<uint4*>(rec)[2 * s + 1] = *reinterpret_cast<const uint4*>(&r.yh);
 }
 
-// sort each cell's records: short cells in registers, crowded ones queued for a block
+__device__ __forceinline__ void emit(const Rec& r, uint32_t s, float4* __restrict__ orig4, float4* __restrict__ dec4,
+                                     float* __restrict__ xs, uint32_t* __restrict__ slot_of) {
+    orig4[s] = make_float4(r.x, r.y, r.z, __uint_as_float(r.gid));
+    dec4[s] = make_float4(r.xh, r.yh, r.zh, __uint_as_float(r.i));
+    xs[s] = r.x;
+    slot_of[r.i] = s;
+}
+
+__device__ __forceinline__ Rec load_rec(const Rec* __restrict__ rec, uint32_t s) {
+    Rec r;
+    *reinterpret_cast<uint4*>(&r.x) = reinterpret_cast<const uint4*>(rec)[2 * s];
+    *reinterpret_cast<uint4*>(&r.yh) = reinterpret_cast<const uint4*>(rec)[2 * s + 1];
+    return r;
+}
+
+// sort key inside a row: (u-order key of x, input index)
+__device__ __forceinline__ unsigned long long rec_key(const Rec& r, const Grid& g) {
+    return ((unsigned long long)x_sort_key(r.x, g) << 32) | r.i;
+}
+
+// per-cell finish: sort the cell's records by x and write the slot-ordered arrays
 __global__ void __launch_bounds__(BIN_THREADS)
-k_cell_sort_short(int64_t ncell, const uint32_t* __restrict__ cs, unsigned long long* __restrict__ rec,
-                  uint32_t* __restrict__ long_list, unsigned long long* __restrict__ n_long) {
+k_cell_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restrict__ rec, Grid g,
+              float4* __restrict__ orig4, float4* __restrict__ dec4, float* __restrict__ xs,
+              uint32_t* __restrict__ slot_of, uint32_t* __restrict__ long_list, unsigned long long* __restrict__ n_long) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= ncell) return;
     const uint32_t a = cs[c], b = cs[c + 1];
     const int len = (int)(b - a);
-    if (len <= 1) return;
+    if (len == 0) return;
+    if (len == 1) {
+        emit(load_rec(rec, a), a, orig4, dec4, xs, slot_of);
+        return;
+    }
     if (len > CELL_SHORT) {
         const unsigned long long q = atomicAdd(n_long, 1ull);
         long_list[q] = (uint32_t)c;
         return;
     }
-    unsigned long long v[CELL_SHORT];
-    for (int i = 0; i < len; i++) {
-        const unsigned long long xk = rec[a + i];
-        int j = i - 1;
+    unsigned long long v[CELL_SHORT];  // (x key << 32 | input index): unique, data-determined order
+    int off[CELL_SHORT];               // local offset of the record, moved along
+    for (int k = 0; k < len; k++) {
+        const unsigned long long xk = rec_key(load_rec(rec, a + k), g);
+        int j = k - 1;
         while (j >= 0 && v[j] > xk) {
             v[j + 1] = v[j];
+            off[j + 1] = off[j];
             j--;
         }
         v[j + 1] = xk;
+        off[j + 1] = k;
     }
-    for (int i = 0; i < len; i++) rec[a + i] = v[i];
+    for (int k = 0; k < len; k++) emit(load_rec(rec, a + off[k]), a + k, orig4, dec4, xs, slot_of);
 }
 
+// crowded cells: one block per cell, bitonic sort of (key, local offset) in shared memory
 __global__ void __launch_bounds__(512)
-k_cell_sort_long(const uint32_t* __restrict__ long_list, const unsigned long long* __restrict__ n_long,
-                 const uint32_t* __restrict__ cs, unsigned long long* __restrict__ rec) {
+k_cell_finish_long(const uint32_t* __restrict__ long_list, const unsigned long long* __restrict__ n_long,
+                   const uint32_t* __restrict__ cs, const Rec* __restrict__ rec, Grid g, float4* __restrict__ orig4,
+                   float4* __restrict__ dec4, float* __restrict__ xs, uint32_t* __restrict__ slot_of) {
     __shared__ unsigned long long sh[CELL_LONG_MAX];
+    __shared__ unsigned short so[CELL_LONG_MAX];
     const unsigned long long nl = *n_long;
     for (unsigned long long q = blockIdx.x; q < nl; q += gridDim.x) {
         const uint32_t c = long_list[q];
@@ -92,7 +144,10 @@ k_cell_sort_long(const uint32_t* __restrict__ long_list, const unsigned long lon
         if (len <= CELL_LONG_MAX) {
             int p2 = 1;
             while (p2 < len) p2 <<= 1;
-            for (int i = threadIdx.x; i < p2; i += blockDim.x) sh[i] = i < len ? rec[a + i] : ~0ull;
+            for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+                sh[i] = i < len ? rec_key(load_rec(rec, a + i), g) : ~0ull;  // unique keys (input index)
+                so[i] = (unsigned short)i;
+            }
             __syncthreads();
             for (int k = 2; k <= p2; k <<= 1) {
                 for (int j = k >> 1; j > 0; j >>= 1) {
@@ -104,42 +159,37 @@ k_cell_sort_long(const uint32_t* __restrict__ long_list, const unsigned long lon
                             if ((x0 > x1) == up) {
                                 sh[i] = x1;
                                 sh[ij] = x0;
+                                const unsigned short t0 = so[i];
+                                so[i] = so[ij];
+                                so[ij] = t0;
                             }
                         }
                     }
                     __syncthreads();
                 }
             }
-            for (int i = threadIdx.x; i < len; i += blockDim.x) rec[a + i] = sh[i];
+            for (int k = threadIdx.x; k < len; k += blockDim.x)
+                emit(load_rec(rec, a + so[k]), a + k, orig4, dec4, xs, slot_of);
             __syncthreads();
-        } else if (threadIdx.x == 0) {  // pathological crowding: serial insertion sort (correct, slow)
-            for (int i = 1; i < len; i++) {
-                const unsigned long long xk = rec[a + i];
-                int j = i - 1;
-                while (j >= 0 && rec[a + j] > xk) {
-                    rec[a + j + 1] = rec[a + j];
-                    j--;
+        } else if (threadIdx.x == 0) {
+            // pathological crowding: selection by repeated minimum (correct, slow)
+            unsigned long long prev = 0;
+            for (int k = 0; k < len; k++) {
+                unsigned long long best = ~0ull;
+                uint32_t bq = 0;
+                for (int q2 = 0; q2 < len; q2++) {
+                    const Rec r = load_rec(rec, a + q2);
+                    const unsigned long long kk = ((unsigned long long)x_sort_key(r.x, g) << 32) | r.i;
+                    if ((k == 0 || kk > prev) && kk < best) {
+                        best = kk;
+                        bq = q2;
+                    }
                 }
-                rec[a + j + 1] = xk;
+                emit(load_rec(rec, a + bq), a + k, orig4, dec4, xs, slot_of);
+                prev = best;
             }
         }
     }
-}
-
-__global__ void __launch_bounds__(BIN_THREADS)
-k_bin_gather(int64_t n, const float* __restrict__ x, const float* __restrict__ y, const float* __restrict__ z,
-             const float* __restrict__ xh, const float* __restrict__ yh, const float* __restrict__ zh,
-             const uint32_t* __restrict__ gid, const unsigned long long* __restrict__ rec, float4* __restrict__ orig4,
-             float4* __restrict__ dec4, float* __restrict__ xs, uint32_t* __restrict__ slot_of) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
-    const uint32_t i = (uint32_t)(rec[s] & 0xFFFFFFFFull);
-    const float xi_ = x[i];
-    const uint32_t gi = gid ? gid[i] : i;
-    orig4[s] = make_float4(xi_, y[i], z[i], __uint_as_float(gi));
-    dec4[s] = make_float4(xh[i], yh[i], zh[i], __uint_as_float(i));
-    xs[s] = xi_;
-    slot_of[i] = (uint32_t)s;
 }
 
 }  // namespace
@@ -156,13 +206,13 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
     CC_TRY(cc_ensure(c, c->dec4, n1, "dec4"));
     CC_TRY(cc_ensure(c, c->xs, n1, "xs"));
     CC_TRY(cc_ensure(c, c->slot_of, n1, "slot_of"));
-    CC_TRY(cc_ensure(c, c->rowoff, n1 + 1, "records"));  // reused: sort records now, row offsets later
+    CC_TRY(cc_ensure(c, c->rec32, 2 * n1, "binning records"));  // 32 B per particle
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
     CC_TRY(cc_ensure(c, c->scratch_u64, 2, "long count"));
     CC_CUDA(c, cudaMemsetAsync(c->cell_count.p, 0, (size_t)nc * sizeof(uint32_t), c->stream));
     CC_CUDA(c, cudaMemsetAsync(c->counters.p, 0, 16 * sizeof(unsigned long long), c->stream));
     CC_CUDA(c, cudaMemsetAsync(c->scratch_u64.p, 0, sizeof(uint64_t), c->stream));
-    unsigned long long* rec = reinterpret_cast<unsigned long long*>(c->rowoff.p);
+    Rec* rec = reinterpret_cast<Rec*>(c->rec32.p);
     const unsigned nb = (unsigned)((n + BIN_THREADS - 1) / BIN_THREADS);
     if (n > 0) {
         int tok = cc_prof_begin(c, "K1_key");
@@ -176,16 +226,16 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
                            reinterpret_cast<uint64_t*>(c->cell_start.p + nc)));
     if (n > 0) {
         CC_TRY(cc_ensure(c, c->scratch_u32, (size_t)std::max<int64_t>(std::min<int64_t>(nc, n), 1), "crowded cells"));
-        int tok = cc_prof_begin(c, "K1_scatter_sort");
-        CCL(c, k_bin_scatter<<<nb, BIN_THREADS, 0, c->stream>>>(n, x, c->key.p, c->rnk.p, c->cell_start.p, c->g, rec));
-        unsigned long long* nl = reinterpret_cast<unsigned long long*>(c->scratch_u64.p);
-        CCL(c, k_cell_sort_short<<<(unsigned)((nc + BIN_THREADS - 1) / BIN_THREADS), BIN_THREADS, 0, c->stream>>>(
-                   nc, c->cell_start.p, rec, c->scratch_u32.p, nl));
-        CCL(c, k_cell_sort_long<<<148 * 2, 512, 0, c->stream>>>(c->scratch_u32.p, nl, c->cell_start.p, rec));
+        int tok = cc_prof_begin(c, "K1_scatter");
+        CCL(c, k_bin_scatter<<<nb, BIN_THREADS, 0, c->stream>>>(n, x, y, z, xh, yh, zh, gid, c->key.p, c->rnk.p,
+                                                                 c->cell_start.p, rec));
         cc_prof_end(c, tok);
-        int t2 = cc_prof_begin(c, "K1_gather");
-        CCL(c, k_bin_gather<<<nb, BIN_THREADS, 0, c->stream>>>(n, x, y, z, xh, yh, zh, gid, rec, c->orig4.p, c->dec4.p,
-                                                                c->xs.p, c->slot_of.p));
+        unsigned long long* nl = reinterpret_cast<unsigned long long*>(c->scratch_u64.p);
+        int t2 = cc_prof_begin(c, "K1_finish");
+        CCL(c, k_cell_finish<<<(unsigned)((nc + BIN_THREADS - 1) / BIN_THREADS), BIN_THREADS, 0, c->stream>>>(
+                   nc, c->cell_start.p, rec, c->g, c->orig4.p, c->dec4.p, c->xs.p, c->slot_of.p, c->scratch_u32.p, nl));
+        CCL(c, k_cell_finish_long<<<148 * 2, 512, 0, c->stream>>>(c->scratch_u32.p, nl, c->cell_start.p, rec, c->g,
+                                                                  c->orig4.p, c->dec4.p, c->xs.p, c->slot_of.p));
         cc_prof_end(c, t2);
         CC_CUDA(c, cudaGetLastError());
     }

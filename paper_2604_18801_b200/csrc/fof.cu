@@ -59,7 +59,7 @@ __global__ void k_iota(int64_t n, uint32_t* __restrict__ par) {
 // ones that built the structure), with the fp32 rounding margin.
 __global__ void __launch_bounds__(FOF_THREADS)
 k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ orig4, const float* __restrict__ xs,
-           const uint32_t* __restrict__ cs, Grid g, Th t, double r, uint32_t* __restrict__ par) {
+           const uint32_t* __restrict__ cs, Grid g, Th t, double r, float thr2, uint32_t* __restrict__ par) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
     const float4 o = orig4[s];
@@ -70,7 +70,7 @@ k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ o
     const bool periodic_yz = t.periodic != 0;
     auto link = [&](uint32_t j) {
         const float4 q = P[j];
-        if (dist2(p, q, t) <= t.b2) uf_unite(par, (uint32_t)s, j);
+        if (dist2(p, q, t) <= thr2) uf_unite(par, (uint32_t)s, j);
     };
     const bool half = !periodic_yz || (g.ny >= 3 && g.nz >= 3);
     if (!half) {
@@ -207,6 +207,51 @@ __global__ void k_halo_collect(int64_t n, const uint32_t* __restrict__ par, cons
 
 }  // namespace
 
+// vulnerable-pair links on top of the stable forest: pair (e, j) is linked in the positions W
+// (ORIG: its original-link bit; CORR: the pinned d2 <= b2 on the result positions)
+__global__ void __launch_bounds__(256)
+k_union_rows(uint32_t E, const unsigned long long* __restrict__ rowptr, const uint32_t* __restrict__ rows,
+             const uint32_t* __restrict__ slotE, const float4* __restrict__ W, int use_orig_bit, Th t,
+             uint32_t* __restrict__ par) {
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        const unsigned long long k0 = rowptr[e], k1 = rowptr[e + 1];
+        if (k0 == k1) continue;
+        const uint32_t se = slotE[e];
+        const float4 p = use_orig_bit ? make_float4(0.f, 0.f, 0.f, 0.f) : W[e];
+        for (unsigned long long k = k0; k < k1; k++) {
+            const uint32_t ent = rows[k];
+            const uint32_t j = ent & ENT_IDX;
+            if (!(ent & ENT_UPPER) && j < E) continue;  // each owned pair once; ghost partners always
+            const bool lk = use_orig_bit ? (ent & ENT_OLINK) != 0 : dist2(p, W[j], t) <= t.b2;
+            if (lk) uf_unite(par, se, slotE[j]);
+        }
+    }
+}
+
+// The stable forest: links with original d2 <= lo2 (d <= b - 2 sqrt3 xi) exist in the original,
+// decompressed and corrected positions alike (R1/DESIGN.md §5), so they are searched ONCE; each
+// FoF labelling then adds only the vulnerable pairs from the CSR rows.
+static cc_status fof_base(cc_ctx* c) {
+    const int64_t n = c->n;
+    const size_t n1 = (size_t)std::max<int64_t>(n, 1);
+    CC_TRY(cc_ensure(c, c->parent_base, n1, "stable forest"));
+    const unsigned nb = (unsigned)((n + FOF_THREADS - 1) / FOF_THREADS);
+    int tok = cc_prof_begin(c, "K4_fof_base");
+    if (n > 0) {
+        CCL(c, k_iota<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent_base.p));
+        if (c->th.lo2 >= 0.0f) {
+            const double r = std::sqrt((double)c->th.lo2) * (1.0 + 1e-5);
+            CCL(c, k_fof_link<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->orig4.p, c->orig4.p, c->xs.p, c->cell_start.p,
+                                                                 c->g, c->th, r, c->th.lo2, c->parent_base.p));
+        }
+        CCL(c, k_flatten<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent_base.p));
+    }
+    cc_prof_end(c, tok);
+    CC_CUDA(c, cudaGetLastError());
+    c->base_valid = true;
+    return CC_OK;
+}
+
 cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
     const int64_t n = c->n;
     const size_t n1 = (size_t)std::max<int64_t>(n, 1);
@@ -215,14 +260,31 @@ cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
     CC_TRY(cc_ensure(c, c->gsize, n1, "gsize"));
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
     const float4* P = which == CC_ORIG ? c->orig4.p : (which == CC_DECOMP ? c->dec4.p : c->cor4.p);
+    // ORIG always, CORR when the xi - xi' margin dominates fp32 rounding: stable forest + rows
+    const bool via_base = c->state >= 2 && (which == CC_ORIG || (which == CC_CORR && c->corr_base_ok));
+    if (via_base && !c->base_valid) CC_TRY(fof_base(c));
     CC_CUDA(c, cudaMemsetAsync(c->mingid.p, 0xFF, n1 * sizeof(uint32_t), c->stream));
     CC_CUDA(c, cudaMemsetAsync(c->gsize.p, 0, n1 * sizeof(uint32_t), c->stream));
     CC_CUDA(c, cudaMemsetAsync(c->counters.p + 8, 0, sizeof(unsigned long long), c->stream));
     const unsigned nb = (unsigned)((n + FOF_THREADS - 1) / FOF_THREADS);
     int tok = cc_prof_begin(c, "K4_fof");
     if (n > 0) {
-        CCL(c, k_iota<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p));
-        CCL(c, k_fof_link<<<nb, FOF_THREADS, 0, c->stream>>>(n, P, c->orig4.p, c->xs.p, c->cell_start.p, c->g, c->th, which == CC_ORIG ? c->r_link : c->r_pair, c->parent.p));
+        if (via_base) {
+            CC_CUDA(c, cudaMemcpyAsync(c->parent.p, c->parent_base.p, (size_t)n * sizeof(uint32_t),
+                                       cudaMemcpyDeviceToDevice, c->stream));
+            if (c->E > 0) {
+                const int nbe = (int)std::min<int64_t>((c->E + 255) / 256, 148 * 8);
+                CCL(c, k_union_rows<<<nbe, 256, 0, c->stream>>>(
+                           (uint32_t)c->E, reinterpret_cast<const unsigned long long*>(c->rowptr.p), c->rows.p,
+                           c->slotE.p, which == CC_ORIG ? nullptr : pgd_result(c), which == CC_ORIG ? 1 : 0, c->th,
+                           c->parent.p));
+            }
+        } else {
+            CCL(c, k_iota<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p));
+            CCL(c, k_fof_link<<<nb, FOF_THREADS, 0, c->stream>>>(n, P, c->orig4.p, c->xs.p, c->cell_start.p, c->g,
+                                                                 c->th, which == CC_ORIG ? c->r_link : c->r_pair,
+                                                                 c->th.b2, c->parent.p));
+        }
         CCL(c, k_flatten<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p));
         CCL(c, k_mingid<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p, c->orig4.p, c->mingid.p, c->gsize.p,
                                                     c->counters.p + 8));
