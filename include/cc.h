@@ -70,6 +70,8 @@ typedef struct {
     int graph_batch;       /* PGD iterations per CUDA-graph launch (perf only; 0 = default)  */
     double cells_per_particle; /* grid budget K: at most K*N cells (perf only; 0 = default)  */
     int profile;           /* 1: time each kernel class with CUDA events (cc_kernel_stats)   */
+    int frontier;          /* 1: skip particles whose state provably cannot change (exact;   */
+                           /*    perf only, results identical; 0 = sweep every editable)    */
 } cc_params;
 
 /* fill *p with the paper's defaults (eta 0.2, m 16, Adam 1e-3/.9/.999/1e-8, t_max 10000,

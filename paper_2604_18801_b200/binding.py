@@ -31,7 +31,8 @@ class _Params(C.Structure):
                 ("xi", C.c_double), ("m", C.c_int), ("alpha", C.c_double), ("beta1", C.c_double),
                 ("beta2", C.c_double), ("eps_adam", C.c_double), ("t_max", C.c_int), ("eps_loss", C.c_double),
                 ("stop_mode", C.c_int), ("optimizer", C.c_int), ("vanilla_step", C.c_double),
-                ("graph_batch", C.c_int), ("cells_per_particle", C.c_double), ("profile", C.c_int)]
+                ("graph_batch", C.c_int), ("cells_per_particle", C.c_double), ("profile", C.c_int),
+                ("frontier", C.c_int)]
 
 
 class _Dist(C.Structure):
@@ -127,6 +128,7 @@ class Params:
     graph_batch: int = 16
     cells_per_particle: float = 2.0
     profile: int = 0
+    frontier: int = 1
 
     def to_c(self) -> _Params:
         return _Params(**{k: v for k, v in asdict(self).items()})

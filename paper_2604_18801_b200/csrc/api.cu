@@ -209,6 +209,7 @@ void cc_default_params(cc_params* p) {
     p->graph_batch = 16;
     p->cells_per_particle = 2.0;
     p->profile = 0;
+    p->frontier = 1;
 }
 
 cc_status cc_create(cc_ctx** out, int device, void* stream, const cc_params* p, const cc_dist* dist) {
@@ -274,6 +275,7 @@ void cc_destroy(cc_ctx* c) {
     cc_release(c, c->mom); cc_release(c, c->bc); cc_release(c, c->partial_d); cc_release(c, c->partial_u);
     cc_release(c, c->counters); cc_release(c, c->ctl); cc_release(c, c->trace_a); cc_release(c, c->trace_l);
     cc_release(c, c->trace_v); cc_release(c, c->longrow); cc_release(c, c->parent_base); cc_release(c, c->rec32);
+    cc_release(c, c->frozen); cc_release(c, c->touch);
     cc_release(c, c->tmp_bytes); cc_release(c, c->in_f); cc_release(c, c->in_gid);
     for (int d = 0; d < 2; d++) {
         cc_release(c, c->dflag[d]); cc_release(c, c->dpos[d]); cc_release(c, c->shell[d]); cc_release(c, c->sbuf7[d]);

@@ -130,6 +130,7 @@ struct cc_ctx {
     cc::DBuf<cc::Ctl> ctl;
     cc::DBuf<long long> trace_a, trace_v;
     cc::DBuf<uint32_t> longrow;  // editable rows longer than 32 entries (K3 warp path)
+    cc::DBuf<uint32_t> frozen, touch;  // K3 frontier state (pgd.cu)
     int64_t n_long = 0;
     cc::DBuf<double> trace_l;
     cc::DBuf<unsigned char> tmp_bytes;  // scan scratch

@@ -58,7 +58,17 @@ struct PgdArgs {
     long long* trace_v;
     int count_only;
     double* red;  // multi-GPU: local (active, loss, violated) for the allreduce, else nullptr
+    // frontier (exact active-set skipping): frozen[e] = 0 awake, FZ_NEVER never frozen (has a
+    // ghost partner), else the last iteration e was processed; touch0/1[e] = iteration at which a
+    // partner's move requires processing e (parity double-buffered); errs counts unsafe freezes
+    int frontier;
+    uint32_t* frozen;
+    uint32_t* touch0;
+    uint32_t* touch1;
+    unsigned long long* errs;
 };
+
+constexpr uint32_t FZ_NEVER = 0xFFFFFFFFu;
 
 // one pair term, pinned (R4, R13, R14, R15): r = minimg(p - q), d_hat = sqrt_rn(r.r);
 // kind 0: inactive, 1: add (px,py,pz) to the gradient, 2: coincident -> add px to g.x only
@@ -113,19 +123,6 @@ __device__ __forceinline__ void accumulate(float& gx, float& gy, float& gz, cons
     }
 }
 
-__device__ __forceinline__ float adam_coord(float x, float g, float* __restrict__ m, float* __restrict__ v,
-                                            const PgdArgs& a, float bc1, float bc2) {
-    const float mm = __fadd_rn(__fmul_rn(a.b1, *m), __fmul_rn(a.omb1, g));
-    const float vv = __fadd_rn(__fmul_rn(a.b2, *v), __fmul_rn(a.omb2, __fmul_rn(g, g)));
-    *m = mm;
-    *v = vv;
-    const float mh = __fdiv_rn(mm, bc1);
-    const float vh = __fdiv_rn(vv, bc2);
-    const float den = __fadd_rn(__fsqrt_rn(vh), a.eps);
-    const float step = __fmul_rn(a.alpha, __fdiv_rn(mh, den));
-    return __fsub_rn(x, step);
-}
-
 __device__ __forceinline__ float project(float x, float o, float xip) {
     const float lo = __fsub_ru(o, xip);
     const float hi = __fadd_rd(o, xip);
@@ -135,25 +132,78 @@ __device__ __forceinline__ float project(float x, float o, float xip) {
 }
 
 // Adam (or vanilla) step + projection of editable e, written to dst
-__device__ __forceinline__ void update(const PgdArgs& a, uint32_t e, const float4& p, float gx, float gy, float gz,
-                                       float bc1, float bc2, float4* __restrict__ dst) {
+// one coordinate's Adam step in registers (R9); returns the new coordinate, sets |step|
+__device__ __forceinline__ float adam_reg(float x, float g, float& m, float& v, const PgdArgs& a, float bc1, float bc2,
+                                          float& step_abs) {
+    m = __fadd_rn(__fmul_rn(a.b1, m), __fmul_rn(a.omb1, g));
+    v = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(a.omb2, __fmul_rn(g, g)));
+    const float mh = __fdiv_rn(m, bc1);
+    const float vh = __fdiv_rn(v, bc2);
+    const float den = __fadd_rn(__fsqrt_rn(vh), a.eps);
+    const float step = __fmul_rn(a.alpha, __fdiv_rn(mh, den));
+    step_abs = fabsf(step);
+    return __fsub_rn(x, step);
+}
+
+// |step| far below the coordinate's ulp: the particle cannot move while its gradient stays 0
+// (the Adam step then shrinks by ~10% per iteration), the frontier's freeze condition
+__device__ __forceinline__ bool negligible(float step_abs, float x) { return step_abs <= fabsf(x) * 1.4901161e-8f; }
+
+// Adam (or vanilla) step + projection of editable e, written to dst.  `replay` zero-gradient
+// iterations missed while e was frozen (frontier) are first re-run exactly, in order.
+// Returns bit0 = moved, bit1 = freeze-eligible step (negligible on all coordinates).
+__device__ __forceinline__ int update(const PgdArgs& a, uint32_t e, const float4& p, float gx, float gy, float gz,
+                                      int t, int replay_from, float4* __restrict__ dst) {
     const float4 o = a.origE[e];
     float x = p.x, y = p.y, z = p.z;
+    int flags = 0;
     if (a.optimizer == CC_OPT_ADAM) {
-        float* m = a.mom;
+        float* M = a.mom;
         const size_t E = a.E;
-        x = adam_coord(x, gx, m + e, m + 3 * E + e, a, bc1, bc2);
-        y = adam_coord(y, gy, m + E + e, m + 4 * E + e, a, bc1, bc2);
-        z = adam_coord(z, gz, m + 2 * E + e, m + 5 * E + e, a, bc1, bc2);
+        float mx = M[e], my = M[E + e], mz = M[2 * E + e], vx = M[3 * E + e], vy = M[4 * E + e], vz = M[5 * E + e];
+        float sx, sy, sz;
+        for (int tt = replay_from; tt < t; tt++) {  // frozen iterations: gradient exactly 0
+            const float2 b = a.bc[tt - 1];
+            const float nx = project(adam_reg(x, 0.0f, mx, vx, a, b.x, b.y, sx), o.x, a.t.xip_f);
+            const float ny = project(adam_reg(y, 0.0f, my, vy, a, b.x, b.y, sy), o.y, a.t.xip_f);
+            const float nz = project(adam_reg(z, 0.0f, mz, vz, a, b.x, b.y, sz), o.z, a.t.xip_f);
+            if (nx != x || ny != y || nz != z) atomicAdd(a.errs, 1ull);  // freeze was unsafe
+            x = nx;
+            y = ny;
+            z = nz;
+        }
+        const float2 b = a.bc[t - 1];
+        const float nx = project(adam_reg(x, gx, mx, vx, a, b.x, b.y, sx), o.x, a.t.xip_f);
+        const float ny = project(adam_reg(y, gy, my, vy, a, b.x, b.y, sy), o.y, a.t.xip_f);
+        const float nz = project(adam_reg(z, gz, mz, vz, a, b.x, b.y, sz), o.z, a.t.xip_f);
+        M[e] = mx;
+        M[E + e] = my;
+        M[2 * E + e] = mz;
+        M[3 * E + e] = vx;
+        M[4 * E + e] = vy;
+        M[5 * E + e] = vz;
+        if (negligible(sx, x) && negligible(sy, y) && negligible(sz, z)) flags |= 2;
+        x = nx;
+        y = ny;
+        z = nz;
     } else {
-        x = __fsub_rn(x, __fmul_rn(a.vstep, gx));
-        y = __fsub_rn(y, __fmul_rn(a.vstep, gy));
-        z = __fsub_rn(z, __fmul_rn(a.vstep, gz));
+        const float sx = __fmul_rn(a.vstep, gx), sy = __fmul_rn(a.vstep, gy), sz = __fmul_rn(a.vstep, gz);
+        if (sx == 0.0f && sy == 0.0f && sz == 0.0f) flags |= 2;
+        x = project(__fsub_rn(x, sx), o.x, a.t.xip_f);
+        y = project(__fsub_rn(y, sy), o.y, a.t.xip_f);
+        z = project(__fsub_rn(z, sz), o.z, a.t.xip_f);
     }
-    x = project(x, o.x, a.t.xip_f);
-    y = project(y, o.y, a.t.xip_f);
-    z = project(z, o.z, a.t.xip_f);
+    if (x != p.x || y != p.y || z != p.z) flags |= 1;
     dst[e] = make_float4(x, y, z, p.w);
+    return flags;
+}
+
+// frontier bookkeeping after e was processed at iteration t (one thread per e)
+__device__ __forceinline__ void frontier_after(const PgdArgs& a, uint32_t e, int t, int flags, bool any_active,
+                                               uint32_t fz) {
+    if (fz == FZ_NEVER) return;
+    const bool freeze = !(flags & 1) && (flags & 2) && !any_active;
+    a.frozen[e] = freeze ? (uint32_t)t : 0u;
 }
 
 __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
@@ -169,23 +219,31 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
         src = ((t - 1) & 1) ? a.pos1 : a.pos0;
         dst = (t & 1) ? a.pos1 : a.pos0;
     }
-    float bc1 = 1.0f, bc2 = 1.0f;
-    if (!a.count_only && a.optimizer == CC_OPT_ADAM) {
-        const float2 bcv = a.bc[t - 1];
-        bc1 = bcv.x;
-        bc2 = bcv.y;
-    }
     const Th th = a.t;
     unsigned int cnt = 0, nviol = 0;
     double loss = 0.0;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 
     // ---- long rows: one warp per row, 32 entries per round, row-order accumulation via shuffles
+    // frontier (exact skipping of frozen particles from iteration 3 on): see frontier_after
+    const bool skip_frozen = a.frontier && !a.count_only && t >= 3;
+    const uint32_t* __restrict__ tcur = (t & 1) ? a.touch1 : a.touch0;
+    uint32_t* __restrict__ tnext = (t & 1) ? a.touch0 : a.touch1;
     const uint32_t gw = blockIdx.x * (PGD_THREADS / 32) + w, nw = gridDim.x * (PGD_THREADS / 32);
     for (uint32_t q = gw; q < a.n_long; q += nw) {
         const uint32_t e = a.long_list[q];
+        uint32_t fz = 0;
+        int replay_from = t;
+        if (a.frontier && !a.count_only) {
+            fz = a.frozen[e];
+            if (skip_frozen && fz != 0u && fz != FZ_NEVER) {
+                if (tcur[e] != (uint32_t)t) continue;  // warp-uniform
+                replay_from = (int)fz + 1;
+            }
+        }
         const float4 p = src[e];
         const unsigned long long k0 = a.rowptr[e], k1 = a.rowptr[e + 1];
+        bool any_active = false;
         float gx = 0.0f, gy = 0.0f, gz = 0.0f;
         for (unsigned long long kb = k0; kb < k1; kb += 32) {
             const unsigned long long k = kb + lane;
@@ -203,6 +261,7 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
                 }
             }
             const int m = (int)min((unsigned long long)32, k1 - kb);
+            any_active |= __any_sync(0xffffffffu, tm.kind != 0);
             for (int i = 0; i < m; i++) {  // the pinned sequential order, identical on all lanes
                 Term u;
                 u.kind = __shfl_sync(0xffffffffu, tm.kind, i);
@@ -212,15 +271,37 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
                 accumulate(gx, gy, gz, u);
             }
         }
-        if (!a.count_only && lane == 0) update(a, e, p, gx, gy, gz, bc1, bc2, dst);
+        if (!a.count_only) {
+            int flags = 0;
+            if (lane == 0) {
+                flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);
+                if (a.frontier) frontier_after(a, e, t, flags, any_active, fz);
+            }
+            flags = __shfl_sync(0xffffffffu, flags, 0);
+            if (a.frontier && (flags & 1))  // moved: wake every partner for the next iteration
+                for (unsigned long long k = k0 + lane; k < k1; k += 32) {
+                    const uint32_t j = a.rows[k] & ENT_IDX;
+                    if (j < a.E) tnext[j] = (uint32_t)(t + 1);
+                }
+        }
     }
 
     // ---- short rows: one thread each, partner loads batched ahead of the sequential sum
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < a.E; e += stride) {
+        uint32_t fz = 0;
+        int replay_from = t;
+        if (a.frontier && !a.count_only) {
+            fz = a.frozen[e];
+            if (skip_frozen && fz != 0u && fz != FZ_NEVER) {
+                if (tcur[e] != (uint32_t)t) continue;  // frozen and no partner moved: nothing changes
+                replay_from = (int)fz + 1;
+            }
+        }
         const unsigned long long k0 = a.rowptr[e], k1 = a.rowptr[e + 1];
         if (k1 - k0 > (unsigned long long)LONG_ROW) continue;  // warp path
         const float4 p = src[e];
+        bool any_active = false;
         float gx = 0.0f, gy = 0.0f, gz = 0.0f;
         for (unsigned long long kb = k0; kb < k1; kb += BATCH) {
             uint32_t ent[BATCH];
@@ -241,11 +322,22 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
                         }
                         nviol += tm.viol;
                     }
+                    any_active |= tm.kind != 0;
                     accumulate(gx, gy, gz, tm);
                 }
             }
         }
-        if (!a.count_only) update(a, e, p, gx, gy, gz, bc1, bc2, dst);
+        if (!a.count_only) {
+            const int flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);
+            if (a.frontier) {
+                frontier_after(a, e, t, flags, any_active, fz);
+                if (flags & 1)
+                    for (unsigned long long k = k0; k < k1; k++) {
+                        const uint32_t j = a.rows[k] & ENT_IDX;
+                        if (j < a.E) tnext[j] = (uint32_t)(t + 1);
+                    }
+            }
+        }
     }
 
     // ---- deterministic block reduction (fixed shuffle tree + fixed warp order)
@@ -417,7 +509,26 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.trace_v = c->trace_v.p;
     a.count_only = count_only;
     a.red = c->nranks > 1 ? c->red.p : nullptr;
+    a.frontier = c->p.frontier ? 1 : 0;
+    a.frozen = c->frozen.p;
+    a.touch0 = c->touch.p;
+    a.touch1 = c->touch.p + std::max<int64_t>(c->E, 1);
+    a.errs = c->counters.p + 15;
     return a;
+}
+
+// frontier state at the start of cc_correct: everyone awake; rows with a ghost partner
+// (multi-GPU) are never frozen, so moves of ghosts (refreshed each iteration) are always seen
+__global__ void k_frontier_init(uint32_t E, const unsigned long long* __restrict__ rowptr,
+                                const uint32_t* __restrict__ rows, uint32_t* __restrict__ frozen,
+                                uint32_t* __restrict__ touch0, uint32_t* __restrict__ touch1) {
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    bool ghost = false;
+    for (unsigned long long k = rowptr[e]; k < rowptr[e + 1]; k++) ghost |= (rows[k] & ENT_IDX) >= E;
+    frozen[e] = ghost ? FZ_NEVER : 0u;
+    touch0[e] = 0u;
+    touch1[e] = 0u;
 }
 
 int pgd_blocks(int64_t E) {
@@ -460,6 +571,14 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     CC_TRY(cc_ensure(c, c->trace_l, (size_t)tmax + 1, "trace"));
     CC_TRY(cc_ensure(c, c->trace_v, (size_t)tmax + 1, "trace"));
     if (c->nranks > 1) CC_TRY(cc_ensure(c, c->red, 4, "allreduce buffer"));
+    CC_TRY(cc_ensure(c, c->frozen, (size_t)std::max<int64_t>(E, 1), "frontier state"));
+    CC_TRY(cc_ensure(c, c->touch, 2 * (size_t)std::max<int64_t>(E, 1), "frontier touches"));
+    CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
+    CC_CUDA(c, cudaMemsetAsync(c->counters.p + 15, 0, sizeof(unsigned long long), c->stream));
+    if (E > 0)
+        CCL(c, k_frontier_init<<<(unsigned)((E + 255) / 256), 256, 0, c->stream>>>(
+                   (uint32_t)E, reinterpret_cast<const unsigned long long*>(c->rowptr.p), c->rows.p, c->frozen.p,
+                   c->touch.p, c->touch.p + std::max<int64_t>(E, 1)));
     // restart from P_hat^(0) (a previous cc_correct may have overwritten posA)
     if (Ea > 0)
         CCL(c, k_reset_pos<<<(unsigned)((Ea + 255) / 256), 256, 0, c->stream>>>(Ea, c->slotE.p, c->dec4.p,
@@ -595,6 +714,14 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     c->final_active = (unsigned long long)al[0];
     c->final_loss = al[1];
     c->final_violated = (unsigned long long)al[2];
+    if (c->p.frontier) {
+        CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 15, c->counters.p + 15, sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+        if (c->h_counters[15] != 0)  // a frozen particle would have moved: the skip was not exact
+            return cc_fail(c, CC_E_DATA, "frontier: " + std::to_string(c->h_counters[15]) +
+                                             " unsafe freezes (rerun with params.frontier = 0)");
+    }
     return CC_OK;
 }
 

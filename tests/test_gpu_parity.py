@@ -71,6 +71,16 @@ def test_stop_modes_bit_exact(mode, tmax):
         assert g["info"]["iterations"] == tmax
 
 
+@pytest.mark.parametrize("frontier,mode", [(0, cc.STOP_ACTIVE), (0, cc.STOP_RESTORED), (1, cc.STOP_RESTORED)])
+def test_frontier_is_exact(frontier, mode):
+    """K3's frontier skipping (frozen particles replayed lazily) changes no result: both
+    settings equal the oracle bit-exactly (the oracle sweeps every editable every iteration)."""
+    w = synth.Workload("t", "clumped", 40_000, 1.0, 3e-3, seed=15)
+    arrs = _arrs(w)
+    p = _params(w, frontier=frontier, stop_mode=mode)
+    assert_parity(gpu_pipeline(arrs, p, fof=False), oracle_pipeline(arrs, p, fof=False), fof=False)
+
+
 @pytest.mark.parametrize("batch", [1, 3, 16, 64])
 def test_graph_batch_does_not_change_result(batch):
     """The speculative device-side stop is exact for any graph batch (R11, S5)."""
