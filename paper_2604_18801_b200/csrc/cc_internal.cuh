@@ -131,6 +131,8 @@ struct cc_ctx {
     cc::DBuf<long long> trace_a, trace_v;
     cc::DBuf<uint32_t> longrow;  // editable rows longer than 32 entries (K3 warp path)
     cc::DBuf<uint32_t> frozen, touch;  // K3 frontier state (pgd.cu)
+    cc::DBuf<uint32_t> midrow;   // editables with 5..16 then 17..32 row entries (K3 lists)
+    int64_t n_mid[2] = {0, 0};
     int64_t n_long = 0;
     cc::DBuf<double> trace_l;
     cc::DBuf<unsigned char> tmp_bytes;  // scan scratch
@@ -162,6 +164,8 @@ struct cc_ctx {
     cudaGraphExec_t pgd_exec = nullptr;
     const void* pgd_key[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     int64_t pgd_nlong = -1;
+    const void* pgd_mid = nullptr;
+    const void* pgd_frozen = nullptr;
     int pgd_batch = 0;
     int64_t pgd_E = -1;
     int last_iters = 0;
@@ -207,6 +211,35 @@ __device__ __forceinline__ float dist2(const float4& a, const float4& b, const T
     s = __fadd_rn(s, __fmul_rn(dy, dy));
     s = __fadd_rn(s, __fmul_rn(dz, dz));
     return s;
+}
+
+// lock-free union-find (FoF, K2's stable links): roots are hooked larger-under-smaller with
+// atomicCAS, finds path-halve (every write replaces a parent by one of its ancestors)
+__device__ __forceinline__ uint32_t uf_find(uint32_t* par, uint32_t x) {
+    volatile uint32_t* vp = par;
+    for (;;) {
+        const uint32_t p = vp[x];
+        if (p == x) return x;
+        const uint32_t gp = vp[p];
+        if (gp != p) vp[x] = gp;
+        x = gp;
+    }
+}
+
+__device__ __forceinline__ void uf_unite(uint32_t* par, uint32_t a, uint32_t b) {
+    a = uf_find(par, a);
+    b = uf_find(par, b);
+    while (a != b) {
+        if (a < b) {
+            const uint32_t t = a;
+            a = b;
+            b = t;
+        }
+        const uint32_t old = atomicCAS(&par[a], a, b);  // hook root a (larger) under b
+        if (old == a) return;
+        a = uf_find(par, old);
+        b = uf_find(par, b);
+    }
 }
 
 __device__ __forceinline__ int cell_coord(double x, double x0, double inv_w, int n) {
@@ -368,6 +401,8 @@ cc_status get_pairs_run(cc_ctx* c, uint32_t* gi, uint32_t* gj, uint8_t* flags, i
                         unsigned long long* n_dev);
 cc_status halo_sizes_run(cc_ctx* c, int64_t min_size, int64_t* sizes_h, int64_t cap, int64_t* n_h);
 const float4* pgd_result(cc_ctx* c);
+cc_status fof_base_begin(cc_ctx* c);
+cc_status fof_base_end(cc_ctx* c);
 // dist.cu
 cc_status dist_init(cc_ctx* c, const cc_dist* d);
 void dist_destroy(cc_ctx* c);

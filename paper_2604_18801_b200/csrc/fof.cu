@@ -20,33 +20,6 @@ namespace {
 
 constexpr int FOF_THREADS = 256;
 
-__device__ __forceinline__ uint32_t uf_find(uint32_t* par, uint32_t x) {
-    volatile uint32_t* vp = par;
-    for (;;) {
-        const uint32_t p = vp[x];
-        if (p == x) return x;
-        const uint32_t gp = vp[p];
-        if (gp != p) vp[x] = gp;  // path halving; gp is an ancestor of x (benign race)
-        x = gp;
-    }
-}
-
-__device__ __forceinline__ void uf_unite(uint32_t* par, uint32_t a, uint32_t b) {
-    a = uf_find(par, a);
-    b = uf_find(par, b);
-    while (a != b) {
-        if (a < b) {
-            const uint32_t t = a;
-            a = b;
-            b = t;
-        }
-        const uint32_t old = atomicCAS(&par[a], a, b);  // hook root a (larger) under b
-        if (old == a) return;
-        a = uf_find(par, old);
-        b = uf_find(par, b);
-    }
-}
-
 __global__ void k_iota(int64_t n, uint32_t* __restrict__ par) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s < n) par[s] = (uint32_t)s;
@@ -129,21 +102,30 @@ __global__ void k_mingid(int64_t n, const uint32_t* __restrict__ par, const floa
                          unsigned long long* __restrict__ n_roots) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned int root = 0;
+    // neighbouring slots mostly share a root (halo cores): one atomic per distinct root per warp
+    const uint32_t r = s < n ? par[s] : 0xFFFFFFFFu;
+    const uint32_t gid = s < n ? __float_as_uint(orig4[s].w) : 0xFFFFFFFFu;
+    const unsigned int same = __match_any_sync(0xffffffffu, r);
+    const uint32_t mn = __reduce_min_sync(same, gid);
     if (s < n) {
-        const uint32_t r = par[s];
-        atomicMin(&mingid[r], __float_as_uint(orig4[s].w));
-        atomicAdd(&gsize[r], 1u);
+        if ((threadIdx.x & 31) == (unsigned)(__ffs(same) - 1)) {
+            atomicMin(&mingid[r], mn);
+            atomicAdd(&gsize[r], (uint32_t)__popc(same));
+        }
         root = (r == (uint32_t)s);
     }
     const unsigned int cnt = __syncthreads_count(root);
     if (threadIdx.x == 0 && cnt) atomicAdd(n_roots, (unsigned long long)cnt);
 }
 
-__global__ void k_labels(int64_t n_in, const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ par,
+// labels in input order, written from slot order (one random store instead of three
+// dependent random loads per particle)
+__global__ void k_labels(int64_t n, uint32_t n_in, const float4* __restrict__ dec4, const uint32_t* __restrict__ par,
                          const uint32_t* __restrict__ mingid, uint32_t* __restrict__ labels) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_in) return;
-    labels[i] = mingid[par[slot_of[i]]];
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const uint32_t i = __float_as_uint(dec4[s].w);
+    if (i < n_in) labels[i] = mingid[par[s]];
 }
 
 // MCC counters over the vulnerable pairs owned here (lower-gid endpoint, R17)
@@ -252,6 +234,26 @@ static cc_status fof_base(cc_ctx* c) {
     return CC_OK;
 }
 
+// the count sweep of K2 (pairs.cu) unites the stable links it meets; these bracket it
+cc_status fof_base_begin(cc_ctx* c) {
+    const int64_t n = c->n;
+    CC_TRY(cc_ensure(c, c->parent_base, (size_t)std::max<int64_t>(n, 1), "stable forest"));
+    c->base_valid = false;
+    if (n > 0) CCL(c, k_iota<<<(unsigned)((n + FOF_THREADS - 1) / FOF_THREADS), FOF_THREADS, 0, c->stream>>>(
+                          n, c->parent_base.p));
+    CC_CUDA(c, cudaGetLastError());
+    return CC_OK;
+}
+
+cc_status fof_base_end(cc_ctx* c) {
+    const int64_t n = c->n;
+    if (n > 0) CCL(c, k_flatten<<<(unsigned)((n + FOF_THREADS - 1) / FOF_THREADS), FOF_THREADS, 0, c->stream>>>(
+                          n, c->parent_base.p));
+    CC_CUDA(c, cudaGetLastError());
+    c->base_valid = true;
+    return CC_OK;
+}
+
 cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
     const int64_t n = c->n;
     const size_t n1 = (size_t)std::max<int64_t>(n, 1);
@@ -291,8 +293,8 @@ cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
     }
     if (c->nranks > 1) CC_TRY(dist_fof_merge(c, n_groups));  // global labels across slabs (X4)
     if (n > 0 && labels && c->n_in > 0)
-        CCL(c, k_labels<<<(unsigned)((c->n_in + 255) / 256), 256, 0, c->stream>>>(c->n_in, c->slot_of.p, c->parent.p,
-                                                                                  c->mingid.p, labels));
+        CCL(c, k_labels<<<nb, FOF_THREADS, 0, c->stream>>>(n, (uint32_t)c->n_in, c->dec4.p, c->parent.p, c->mingid.p,
+                                                           labels));
     cc_prof_end(c, tok);
     CC_CUDA(c, cudaGetLastError());
     if (n_groups && c->nranks == 1) {

@@ -25,7 +25,7 @@ constexpr int PAIR_THREADS = 256;
 __global__ void __launch_bounds__(PAIR_THREADS)
 k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
               const float* __restrict__ xs, const uint32_t* __restrict__ cs, Grid g, Th t, double r, uint32_t n_own,
-              uint32_t* __restrict__ deg) {
+              uint32_t* __restrict__ deg, uint32_t* __restrict__ par_base) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
     if (__float_as_uint(dec4[s].w) >= n_own) return;  // ghost: no row
@@ -42,6 +42,10 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
         if (t.lo2 < d2 && d2 <= t.hi2) {
             cnt++;
             if (multi && __float_as_uint(dec4[j].w) >= n_own) atomicOr(&deg[j], 0x80000000u);
+        } else if (d2 <= t.lo2 && j > (uint32_t)s) {
+            // a stable FoF link (linked in original, decompressed and corrected positions alike,
+            // fof.cu): united here, in the same candidate sweep, once per pair
+            uf_unite(par_base, (uint32_t)s, j);
         }
     };
     for_each_candidate(g, cs, xs, u, cy, cz, r, t.periodic != 0, test);
@@ -134,6 +138,14 @@ k_sort_short(uint32_t e_own, const unsigned long long* __restrict__ rowptr, cons
     for (int i = 0; i < len; i++) rows[a + i] = (uint32_t)v[i];
 }
 
+__global__ void k_class_flags(uint32_t E, const unsigned long long* __restrict__ rowptr, unsigned lo, unsigned hi,
+                              uint32_t* __restrict__ flag) {
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    const unsigned long long len = rowptr[e + 1] - rowptr[e];
+    flag[e] = (len >= lo && len <= hi) ? 1u : 0u;
+}
+
 // ordered compaction of flagged editables (deterministic long-row list)
 __global__ void k_flag_compact(uint32_t E, const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
                                uint32_t* __restrict__ list) {
@@ -197,14 +209,16 @@ cc_status pairs_count(cc_ctx* c) {
     const int64_t n = c->n;
     CC_TRY(cc_ensure(c, c->deg, (size_t)std::max<int64_t>(n, 1), "deg"));
     CC_CUDA(c, cudaMemsetAsync(c->deg.p, 0, (size_t)std::max<int64_t>(n, 1) * sizeof(uint32_t), c->stream));
+    CC_TRY(fof_base_begin(c));  // the stable FoF forest is built inside the count sweep
     if (n > 0) {
         int tok = cc_prof_begin(c, "K2_count");
         CCL(c, k_pairs_count<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
-            n, c->orig4.p, c->dec4.p, c->xs.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in, c->deg.p));
+            n, c->orig4.p, c->dec4.p, c->xs.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in, c->deg.p,
+            c->parent_base.p));
         cc_prof_end(c, tok);
         CC_CUDA(c, cudaGetLastError());
     }
-    return CC_OK;
+    return fof_base_end(c);
 }
 
 cc_status pairs_fill(cc_ctx* c) {
@@ -261,6 +275,25 @@ cc_status rows_finish(cc_ctx* c) {
                                    c->stream));
         CC_CUDA(c, cudaStreamSynchronize(c->stream));
         c->n_long = (int64_t)c->h_counters[1];
+        // K3 work classes by row length (uniform trip counts per warp): rows of 5..16 and 17..32
+        // entries get ordered index lists; rows <= 4 are swept in place, rows > 32 use warps
+        CC_TRY(cc_ensure(c, c->midrow, (size_t)std::max<int64_t>(c->E, 1), "mid rows"));
+        int64_t off = 0;
+        const unsigned lo[2] = {5u, 17u}, hi[2] = {16u, 32u};
+        for (int k = 0; k < 2; k++) {
+            CC_CUDA(c, cudaMemsetAsync(nl, 0, sizeof(uint64_t), c->stream));
+            CCL(c, k_class_flags<<<ge, PAIR_THREADS, 0, c->stream>>>((uint32_t)c->E, rowptr, lo[k], hi[k], c->deg.p));
+            CC_TRY(scan_u32_to_u32(c, c->deg.p, c->scratch_u32.p, c->E, reinterpret_cast<uint64_t*>(nl)));
+            CCL(c, k_flag_compact<<<ge, PAIR_THREADS, 0, c->stream>>>((uint32_t)c->E, c->deg.p, c->scratch_u32.p,
+                                                                      c->midrow.p + off));
+            CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 1, nl, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                       c->stream));
+            CC_CUDA(c, cudaStreamSynchronize(c->stream));
+            c->n_mid[k] = (int64_t)c->h_counters[1];
+            off += c->n_mid[k];
+        }
+    } else {
+        c->n_mid[0] = c->n_mid[1] = 0;
     }
     return CC_OK;
 }

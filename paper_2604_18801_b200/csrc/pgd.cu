@@ -32,6 +32,7 @@ constexpr int PGD_THREADS = 256;
 constexpr int PGD_MAX_BLOCKS = 148 * 8;
 constexpr int LONG_ROW = 32;  // rows longer than this take the warp path (rows_finish's long list)
 constexpr int BATCH = 4;
+constexpr int SHORT_MAX = 4;  // rows swept in place; 5..32 via the mid lists (pairs.cu)
 
 struct PgdArgs {
     uint32_t E;  // editable particles with rows (owned)
@@ -40,6 +41,8 @@ struct PgdArgs {
     const float4* __restrict__ origE;
     const uint32_t* __restrict__ long_list;
     uint32_t n_long;
+    const uint32_t* __restrict__ mid_list;  // rows of 5..16 then 17..32 entries
+    uint32_t n_mid;
     float4* pos0;
     float4* pos1;
     float* __restrict__ mom;  // 6 x E SoA
@@ -287,19 +290,18 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
     }
 
     // ---- short rows: one thread each, partner loads batched ahead of the sequential sum
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < a.E; e += stride) {
+    // rows of <= SHORT_MAX entries are swept in place (one batch each); rows of 5..32 come from
+    // length-class lists (rows_finish) so a warp's threads run the same number of batches
+    auto process = [&](uint32_t e, unsigned long long k0, unsigned long long k1) {
         uint32_t fz = 0;
         int replay_from = t;
         if (a.frontier && !a.count_only) {
             fz = a.frozen[e];
             if (skip_frozen && fz != 0u && fz != FZ_NEVER) {
-                if (tcur[e] != (uint32_t)t) continue;  // frozen and no partner moved: nothing changes
+                if (tcur[e] != (uint32_t)t) return;  // frozen and no partner moved: nothing changes
                 replay_from = (int)fz + 1;
             }
         }
-        const unsigned long long k0 = a.rowptr[e], k1 = a.rowptr[e + 1];
-        if (k1 - k0 > (unsigned long long)LONG_ROW) continue;  // warp path
         const float4 p = src[e];
         bool any_active = false;
         float gx = 0.0f, gy = 0.0f, gz = 0.0f;
@@ -338,6 +340,15 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
                     }
             }
         }
+    };
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < a.E; e += stride) {
+        const unsigned long long k0 = a.rowptr[e], k1 = a.rowptr[e + 1];
+        if (k1 - k0 <= (unsigned long long)SHORT_MAX) process(e, k0, k1);
+    }
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < a.n_mid; q += stride) {
+        const uint32_t e = a.mid_list[q];
+        process(e, a.rowptr[e], a.rowptr[e + 1]);
     }
 
     // ---- deterministic block reduction (fixed shuffle tree + fixed warp order)
@@ -485,6 +496,8 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.origE = c->origE.p;
     a.long_list = c->longrow.p;
     a.n_long = (uint32_t)c->n_long;
+    a.mid_list = c->midrow.p;
+    a.n_mid = (uint32_t)(c->n_mid[0] + c->n_mid[1]);
     a.pos0 = c->posA.p;
     a.pos1 = c->posB.p;
     a.mom = c->mom.p;
@@ -619,8 +632,11 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     int iters = 0;
     if (tmax > 0) {
         // (re)capture a graph of `batch` iterations, each bracketed by event records
+        // the graph bakes in every argument of k_pgd: re-capture when any of them changed
         const void* key[5] = {c->posA.p, c->rows.p, c->mom.p, c->ctl.p, c->longrow.p};
-        bool same = c->pgd_exec && c->pgd_batch == batch && c->pgd_E == E && c->pgd_nlong == c->n_long;
+        const int64_t shape = c->n_long * 1000003 + (c->n_mid[0] + c->n_mid[1]) * 7 + (int64_t)(c->midrow.p != nullptr);
+        bool same = c->pgd_exec && c->pgd_batch == batch && c->pgd_E == E && c->pgd_nlong == shape &&
+                    c->pgd_mid == (const void*)c->midrow.p && c->pgd_frozen == (const void*)c->frozen.p;
         for (int k = 0; k < 5; k++) same = same && key[k] == c->pgd_key[k];
         if (!same) {
             if (c->pgd_exec) cudaGraphExecDestroy(c->pgd_exec);
@@ -660,7 +676,9 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
             for (int k = 0; k < 5; k++) c->pgd_key[k] = key[k];
             c->pgd_batch = batch;
             c->pgd_E = E;
-            c->pgd_nlong = c->n_long;
+            c->pgd_nlong = shape;
+            c->pgd_mid = c->midrow.p;
+            c->pgd_frozen = c->frozen.p;
         }
         int t_before = 0;
         for (;;) {

@@ -21,6 +21,8 @@ import synth  # noqa: E402
 
 
 def main():
+    import faulthandler
+    faulthandler.dump_traceback_later(int(os.environ.get("MG_WATCHDOG", "240")), exit=True)
     n = int(os.environ.get("MG_N", "60000"))
     xi_rel = float(os.environ.get("MG_XI", "1e-3"))
     seed = int(os.environ.get("MG_SEED", "3"))
@@ -39,11 +41,19 @@ def main():
     uid = [cc.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     p = cc.Params(box=w.L, b=w.linking_length, xi=w.xi)
+    def log(*a):
+        print(f"[rank {rank}]", *a, file=sys.stderr, flush=True)
+
     c = cc.Corrector(p, device=local, dist=(rank, world, uid[0]))
+    log("created, owned", int(mine.sum()))
     c.build_cells(*loc, gid=gid)
+    log("cells built")
     vp = c.find_vulnerable()
+    log("pairs", vp)
     out, info = c.correct()
+    log("corrected", info)
     lab_o, ng_o = c.fof_label(cc.CC_ORIG)
+    log("fof orig", ng_o)
     h_o = c.halo_sizes(cc.CC_ORIG, 20)
     lab_c, ng_c = c.fof_label(cc.CC_CORR)
     h_c = c.halo_sizes(cc.CC_CORR, 20)
