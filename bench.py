@@ -323,6 +323,8 @@ def main():
     # ---- roofline of the dominant kernel class (device time inside the timed region)
     hbm, sm_max, peak_src = _peaks()
     launches = stats.pop("total_launches", (0.0, 0))[1]
+    k3_we = stats.pop("K3_work_editables", (0.0, 0))[1]   # editables updated (frontier skips the rest)
+    k3_wn = stats.pop("K3_work_entries", (0.0, 0))[1]     # row entries evaluated
     E, nent = vp["n_editable"], 2 * vp["n_pairs"]
     if world > 1:  # this rank's share for the per-launch byte count
         E, nent = E / world, nent / world
@@ -330,7 +332,9 @@ def main():
     dom = max(cls_ms, key=lambda k: cls_ms[k][0]) if cls_ms else None
     # algorithmic bytes per launch
     alg_bytes = {
-        "K3_pgd": 104.0 * E + 4.0 * nent,
+        # per launch: 104 B per editable actually updated + 4 B per row entry evaluated
+        "K3_pgd": (104.0 * k3_we + 4.0 * k3_wn) / max(cls_ms.get("K3_pgd", (0, 1))[1], 1) if k3_we
+        else 104.0 * E + 4.0 * nent,
         "K1_key": 24.0 * n + 8.0 * n,
         "K1_gather": 8.0 * n + 28.0 * n + 40.0 * n,
         "K2_count": 16.0 * n + 4.0 * n,
@@ -350,7 +354,8 @@ def main():
     if k3 and k3[1]:
         a = alg_bytes["K3_pgd"] / (k3[0] / k3[1] * 1e-3) / 1e9
         k3_roof = {"achieved": a, "peak": hbm, "unit": "GB/s", "frac": a / hbm, "launch_ms": k3[0] / k3[1],
-                   "launches": k3[1]}
+                   "launches": k3[1], "editables_updated_per_launch": k3_we / k3[1],
+                   "entries_per_launch": k3_wn / k3[1], "editables_total": E}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

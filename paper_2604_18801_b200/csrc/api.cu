@@ -274,8 +274,9 @@ void cc_destroy(cc_ctx* c) {
     cc_release(c, c->scratch_u32); cc_release(c, c->rowoff); cc_release(c, c->rowptr); cc_release(c, c->scratch_u64);
     cc_release(c, c->mom); cc_release(c, c->bc); cc_release(c, c->partial_d); cc_release(c, c->partial_u);
     cc_release(c, c->counters); cc_release(c, c->ctl); cc_release(c, c->trace_a); cc_release(c, c->trace_l);
-    cc_release(c, c->trace_v); cc_release(c, c->longrow); cc_release(c, c->parent_base); cc_release(c, c->rec32);
-    cc_release(c, c->frozen); cc_release(c, c->touch); cc_release(c, c->midrow);
+    cc_release(c, c->trace_v); cc_release(c, c->parent_base); cc_release(c, c->rec32);
+    cc_release(c, c->frozen); cc_release(c, c->touch); cc_release(c, c->k3work);
+    cc_release(c, c->ggroup);
     cc_release(c, c->tmp_bytes); cc_release(c, c->in_f); cc_release(c, c->in_gid);
     for (int d = 0; d < 2; d++) {
         cc_release(c, c->dflag[d]); cc_release(c, c->dpos[d]); cc_release(c, c->shell[d]); cc_release(c, c->sbuf7[d]);
@@ -286,9 +287,12 @@ void cc_destroy(cc_ctx* c) {
     cc_release(c, c->stage); cc_release(c, c->gath); cc_release(c, c->dcnt); cc_release(c, c->red);
     cc_release(c, c->bnd);
     cudaStreamSynchronize(c->stream);
+    // the PGD graph holds NCCL work (multi-GPU): release it before the communicator
+    if (c->pgd_exec) cudaGraphExecDestroy(c->pgd_exec);
+    c->pgd_exec = nullptr;
+    cudaDeviceSynchronize();
     cc::dist_destroy(c);
     if (c->h_red) cudaFreeHost(c->h_red);
-    if (c->pgd_exec) cudaGraphExecDestroy(c->pgd_exec);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     for (auto& pe : c->pend) {
         cudaEventDestroy(pe.a);
@@ -374,15 +378,15 @@ cc_status cc_find_vulnerable(cc_ctx* c, cc_vp_info* info) {
     CC_TRY(cc_ensure(c, c->rowoff, (size_t)std::max<int64_t>(n, 1), "rowoff"));
     CC_TRY(cc_ensure(c, c->eidx, (size_t)std::max<int64_t>(n, 1), "eidx"));
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
-    unsigned long long* tot = c->counters.p + 2;  // 16-byte VDeg total at counters[2..3]
-    CC_TRY(cc::scan_deg(c, c->deg.p, c->rowoff.p, c->eidx.p, n, c->dec4.p, c->n_in, tot));
-    CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 2, tot, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+    CC_TRY(cc_ensure(c, c->key, (size_t)std::max<int64_t>(n, 1), "row class"));  // key is dead after K1
+    unsigned long long* tot = c->counters.p + 2;  // 56-byte VDeg total at counters[2..8]
+    CC_TRY(cc::scan_deg(c, c->deg.p, c->rowoff.p, c->eidx.p, c->key.p, n, tot));
+    CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 2, tot, 7 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                c->stream));
     CC_CUDA(c, cudaStreamSynchronize(c->stream));
-    c->nent = (int64_t)c->h_counters[2];
-    const uint32_t w1 = (uint32_t)(c->h_counters[3] & 0xFFFFFFFFull), w2 = (uint32_t)(c->h_counters[3] >> 32);
-    c->E = w1;
-    c->E_all = (int64_t)w1 + w2;
+    unsigned long long totals[7];
+    std::memcpy(totals, c->h_counters + 2, sizeof(totals));
+    CC_TRY(cc::rows_resolve(c, totals));
     if (c->E_all >= cc::MAX_LOCAL) return cc_fail(c, CC_E_DATA, "editable set beyond the 2^30 index space");
     CC_TRY(cc::rows_finish(c));
     if (c->nranks > 1) CC_TRY(cc::dist_setup_refresh(c));
@@ -573,6 +577,22 @@ cc_status cc_kernel_stats(cc_ctx* c, char* names, int64_t names_cap, double* ms,
     }
     all += "total_launches\n";
     k++;
+    // pseudo-classes: K3 work actually done (the frontier skips frozen particles)
+    unsigned long long wk[2] = {0, 0};
+    if (c->k3work.p) {
+        CC_CUDA(c, cudaMemcpyAsync(wk, c->k3work.p, sizeof(wk), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+        if (reset) CC_CUDA(c, cudaMemsetAsync(c->k3work.p, 0, sizeof(wk), c->stream));
+    }
+    const char* wn[2] = {"K3_work_editables\n", "K3_work_entries\n"};
+    for (int q = 0; q < 2; q++) {
+        if (k < cap) {
+            if (ms) ms[k] = 0.0;
+            if (launches) launches[k] = (int64_t)wk[q];
+        }
+        all += wn[q];
+        k++;
+    }
     if (names && names_cap > 0) {
         std::strncpy(names, all.c_str(), (size_t)names_cap - 1);
         names[names_cap - 1] = 0;

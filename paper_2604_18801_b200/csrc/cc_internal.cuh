@@ -129,11 +129,9 @@ struct cc_ctx {
     cc::DBuf<unsigned long long> partial_u, counters;
     cc::DBuf<cc::Ctl> ctl;
     cc::DBuf<long long> trace_a, trace_v;
-    cc::DBuf<uint32_t> longrow;  // editable rows longer than 32 entries (K3 warp path)
-    cc::DBuf<uint32_t> frozen, touch;  // K3 frontier state (pgd.cu)
-    cc::DBuf<uint32_t> midrow;   // editables with 5..16 then 17..32 row entries (K3 lists)
-    int64_t n_mid[2] = {0, 0};
-    int64_t n_long = 0;
+    cc::DBuf<uint32_t> frozen, touch, ggroup;  // K3 frontier state (pgd.cu)
+    cc::DBuf<unsigned long long> k3work;  // K3 work totals (editables updated, entries evaluated)
+    int64_t E_cls[4] = {0, 0, 0, 0};  // editables per K3 work class (row_class), numbered class-major
     cc::DBuf<double> trace_l;
     cc::DBuf<unsigned char> tmp_bytes;  // scan scratch
     cc::DBuf<float> in_f;        // cc_run host staging: 6 n floats
@@ -162,12 +160,7 @@ struct cc_ctx {
 
     // PGD graph cache
     cudaGraphExec_t pgd_exec = nullptr;
-    const void* pgd_key[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    int64_t pgd_nlong = -1;
-    const void* pgd_mid = nullptr;
-    const void* pgd_frozen = nullptr;
-    int pgd_batch = 0;
-    int64_t pgd_E = -1;
+    std::vector<unsigned char> pgd_sig;  // arguments baked into pgd_exec (re-capture on change)
     int last_iters = 0;
     int fof_which = -1;
     int have_labels[3] = {0, 0, 0};
@@ -180,6 +173,11 @@ struct cc_ctx {
 };
 
 namespace cc {
+
+// K3 work classes by row length (editables are numbered class-major, slot order inside a
+// class): 0: 1..4 entries (thread, one batch), 1: 5..16, 2: 17..32 (thread, uniform trip
+// counts per warp), 3: > 32 (one warp per row)
+__host__ __device__ inline int row_class(uint32_t len) { return len <= 4u ? 0 : (len <= 16u ? 1 : (len <= 32u ? 2 : 3)); }
 
 // Alg. 1 line 6 stop test per stop mode (R11): ACTIVE: no L_tight-active pair;
 // EPS: L_tight <= eps_L; RESTORED: L_tight <= eps_L and every link status restored (MCC = 1)
@@ -226,7 +224,8 @@ __device__ __forceinline__ uint32_t uf_find(uint32_t* par, uint32_t x) {
     }
 }
 
-__device__ __forceinline__ void uf_unite(uint32_t* par, uint32_t a, uint32_t b) {
+// returns a root the two sets shared when the call ended (an ancestor of both from then on)
+__device__ __forceinline__ uint32_t uf_unite(uint32_t* par, uint32_t a, uint32_t b) {
     a = uf_find(par, a);
     b = uf_find(par, b);
     while (a != b) {
@@ -236,10 +235,21 @@ __device__ __forceinline__ void uf_unite(uint32_t* par, uint32_t a, uint32_t b) 
             b = t;
         }
         const uint32_t old = atomicCAS(&par[a], a, b);  // hook root a (larger) under b
-        if (old == a) return;
+        if (old == a) return b;
         a = uf_find(par, old);
         b = uf_find(par, b);
     }
+    return a;
+}
+
+// Link s with j unless they are visibly in one set already: rs is a cached ancestor of s (sets
+// only merge, so a stale parent/grandparent of j equal to rs proves it); dense halo cores meet
+// mostly redundant links, which this filter turns from two L2 root walks into L1 loads.
+__device__ __forceinline__ void uf_link(uint32_t* par, uint32_t s, uint32_t j, uint32_t& rs) {
+    const uint32_t pj = par[j];
+    if (pj == rs) return;
+    if (par[pj] == rs) return;
+    rs = uf_unite(par, s, j);
 }
 
 __device__ __forceinline__ int cell_coord(double x, double x0, double inv_w, int n) {
@@ -386,8 +396,9 @@ void cc_prof_end(cc_ctx* c, int token);
 // launch wrappers (each .cu file)
 namespace cc {
 cc_status scan_u32_to_u32(cc_ctx* c, const uint32_t* in, uint32_t* out, int64_t n, uint64_t* total_dev);
-cc_status scan_deg(cc_ctx* c, const uint32_t* deg, uint64_t* rowoff, uint32_t* eidx, int64_t n,
-                   const float4* dec4, int64_t n_own, unsigned long long* totals_dev);
+cc_status scan_deg(cc_ctx* c, const uint32_t* deg, uint64_t* rowoff, uint32_t* eidx, uint32_t* cls, int64_t n,
+                   unsigned long long* totals_dev);
+cc_status rows_resolve(cc_ctx* c, const unsigned long long* totals_h);
 cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* z, const float* xh,
                         const float* yh, const float* zh, const uint32_t* gid, int64_t n);
 cc_status pairs_count(cc_ctx* c);

@@ -100,9 +100,8 @@ __global__ void k_ghost_requests(int64_t n, const uint32_t* __restrict__ eidx, c
                                  unsigned long long* __restrict__ cnt_right) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    const uint32_t e = eidx[s];
-    if (e == 0xFFFFFFFFu || !(e & 0x80000000u)) return;
-    const uint32_t eg = e_own + (e & 0x7FFFFFFFu);
+    const uint32_t eg = eidx[s];
+    if (eg == 0xFFFFFFFFu || eg < e_own) return;  // ghost editables are numbered after all owned ones
     const uint32_t i = __float_as_uint(dec4[s].w);
     if (i - n_own < n_from_left) {
         const unsigned long long q = atomicAdd(cnt_left, 1ull);
@@ -118,11 +117,11 @@ __global__ void k_ghost_requests(int64_t n, const uint32_t* __restrict__ eidx, c
 // owner side: requested shell-list index -> owned editable index
 __global__ void k_map_requests(int64_t m, const uint32_t* __restrict__ req, const uint32_t* __restrict__ shell,
                                const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ eidx,
-                               uint32_t* __restrict__ send_e, unsigned long long* errs) {
+                               uint32_t e_own, uint32_t* __restrict__ send_e, unsigned long long* errs) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= m) return;
     const uint32_t e = eidx[slot_of[shell[req[k]]]];
-    if (e == 0xFFFFFFFFu || (e & 0x80000000u)) atomicOr(errs, 8ull);  // must be an owned editable
+    if (e >= e_own) atomicOr(errs, 8ull);  // must be an owned editable
     send_e[k] = e;
 }
 
@@ -403,7 +402,7 @@ cc_status dist_setup_refresh(cc_ctx* c) {
     for (int d = 0; d < 2; d++)
         if (c->n_ref_send[d] > 0)
             CCL(c, k_map_requests<<<(unsigned)((c->n_ref_send[d] + DT - 1) / DT), DT, 0, c->stream>>>(
-                       c->n_ref_send[d], c->sreq[d].p, c->shell[d].p, c->slot_of.p, c->eidx.p, c->send_e[d].p,
+                       c->n_ref_send[d], c->sreq[d].p, c->shell[d].p, c->slot_of.p, c->eidx.p, (uint32_t)c->E, c->send_e[d].p,
                        c->counters.p + 14));
     CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 14, c->counters.p + 14, sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, c->stream));

@@ -41,9 +41,10 @@ k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ o
     int cx, cy, cz;
     cell_of(o.x, o.y, o.z, g, u, cx, cy, cz);
     const bool periodic_yz = t.periodic != 0;
+    uint32_t rs = (uint32_t)s;  // cached ancestor of s (uf_link)
     auto link = [&](uint32_t j) {
         const float4 q = P[j];
-        if (dist2(p, q, t) <= thr2) uf_unite(par, (uint32_t)s, j);
+        if (dist2(p, q, t) <= thr2) uf_link(par, (uint32_t)s, j, rs);
     };
     const bool half = !periodic_yz || (g.ny >= 3 && g.nz >= 3);
     if (!half) {
@@ -199,13 +200,14 @@ k_union_rows(uint32_t E, const unsigned long long* __restrict__ rowptr, const ui
         const unsigned long long k0 = rowptr[e], k1 = rowptr[e + 1];
         if (k0 == k1) continue;
         const uint32_t se = slotE[e];
+        uint32_t rs = se;
         const float4 p = use_orig_bit ? make_float4(0.f, 0.f, 0.f, 0.f) : W[e];
         for (unsigned long long k = k0; k < k1; k++) {
             const uint32_t ent = rows[k];
             const uint32_t j = ent & ENT_IDX;
             if (!(ent & ENT_UPPER) && j < E) continue;  // each owned pair once; ghost partners always
             const bool lk = use_orig_bit ? (ent & ENT_OLINK) != 0 : dist2(p, W[j], t) <= t.b2;
-            if (lk) uf_unite(par, se, slotE[j]);
+            if (lk) uf_link(par, se, slotE[j], rs);
         }
     }
 }

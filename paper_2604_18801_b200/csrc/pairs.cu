@@ -13,6 +13,8 @@
 // entries (partner editable index | partner-gid-above bit | original-link bit).  Rows are then
 // sorted by partner gid so the PGD gradient sum has one defined order on any grid / rank (R14).
 // Each unordered pair is tested from both endpoints: both see the identical pinned fp32 d2.
+#include <cstring>
+
 #include "cc_internal.cuh"
 
 namespace cc {
@@ -34,6 +36,7 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
     int cx, cy, cz;
     cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
     uint32_t cnt = 0;
+    uint32_t rs = (uint32_t)s;  // cached ancestor of s in the stable forest (uf_link)
     const bool multi = n_own < (uint32_t)n;
     auto test = [&](uint32_t j) {
         if (j == (uint32_t)s) return;
@@ -45,15 +48,32 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
         } else if (d2 <= t.lo2 && j > (uint32_t)s) {
             // a stable FoF link (linked in original, decompressed and corrected positions alike,
             // fof.cu): united here, in the same candidate sweep, once per pair
-            uf_unite(par_base, (uint32_t)s, j);
+            uf_link(par_base, (uint32_t)s, j, rs);
         }
     };
     for_each_candidate(g, cs, xs, u, cy, cz, r, t.periodic != 0, test);
     deg[s] = cnt;  // an owned slot never carries the ghost bit
 }
 
-__device__ __forceinline__ uint32_t resolve_eidx(uint32_t e, uint32_t e_own) {
-    return (e & 0x80000000u) ? e_own + (e & 0x7FFFFFFFu) : e;
+// after the scan: editable ranks and row offsets become global (class-major numbering: class
+// bases first, ghost editables after all owned ones)
+struct ClassBases {
+    uint32_t e[4];
+    unsigned long long off[4];
+};
+__global__ void k_resolve(int64_t n, const uint32_t* __restrict__ cls, ClassBases cb, uint32_t e_own,
+                          uint32_t* __restrict__ eidx, unsigned long long* __restrict__ rowoff) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const uint32_t k = cls[s];
+    if (k <= 3u) {
+        eidx[s] += cb.e[k];
+        rowoff[s] += cb.off[k];
+    } else if (k == 4u) {
+        eidx[s] += e_own;
+    } else {
+        eidx[s] = 0xFFFFFFFFu;
+    }
 }
 
 // pass 2: write the row of every owned editable slot
@@ -76,7 +96,7 @@ k_pairs_fill(int64_t n, const float4* __restrict__ orig4, const float* __restric
         const float4 q = orig4[j];
         const float d2 = dist2(p, q, t);
         if (t.lo2 < d2 && d2 <= t.hi2) {
-            uint32_t ent = resolve_eidx(eidx[j], e_own);
+            uint32_t ent = eidx[j];
             if (__float_as_uint(q.w) > gp) ent |= ENT_UPPER;
             if (d2 <= t.b2) ent |= ENT_OLINK;
             rows[k++] = ent;
@@ -93,9 +113,8 @@ k_compact(int64_t n, const uint32_t* __restrict__ deg, const uint32_t* __restric
           unsigned long long* __restrict__ rowptr, float4* __restrict__ origE, float4* __restrict__ posA) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    const uint32_t e0 = eidx[s];
-    if (e0 == 0xFFFFFFFFu) return;
-    const uint32_t e = resolve_eidx(e0, e_own);
+    const uint32_t e = eidx[s];
+    if (e == 0xFFFFFFFFu) return;
     const float4 o = orig4[s], d = dec4[s];
     slotE[e] = (uint32_t)s;
     rowptr[e] = (e < e_own) ? rowoff[s] : nent;
@@ -114,16 +133,15 @@ __device__ __forceinline__ unsigned long long row_key(uint32_t ent, const float4
     return ((unsigned long long)__float_as_uint(posA[ent & ENT_IDX].w) << 32) | ent;
 }
 
-// sort each row by partner gid: rows <= SHORT_ROW in registers (insertion sort), longer rows
-// queued for the block kernel
+// sort each row by partner gid: rows of classes 0-2 (<= 32 entries) in registers (insertion
+// sort); class-3 rows by the block kernel
 __global__ void __launch_bounds__(PAIR_THREADS)
-k_sort_short(uint32_t e_own, const unsigned long long* __restrict__ rowptr, const float4* __restrict__ posA,
-             uint32_t* __restrict__ rows, uint32_t* __restrict__ long_list, unsigned long long* __restrict__ n_long) {
+k_sort_short(uint32_t e_end, const unsigned long long* __restrict__ rowptr, const float4* __restrict__ posA,
+             uint32_t* __restrict__ rows) {
     const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= e_own) return;
+    if (e >= e_end) return;
     const unsigned long long a = rowptr[e], b = rowptr[e + 1];
     const int len = (int)(b - a);
-    long_list[e] = len > SHORT_ROW ? 1u : 0u;  // flags; compacted in order by rows_finish
     if (len <= 1 || len > SHORT_ROW) return;
     unsigned long long v[SHORT_ROW];
     for (int i = 0; i < len; i++) {
@@ -138,30 +156,13 @@ k_sort_short(uint32_t e_own, const unsigned long long* __restrict__ rowptr, cons
     for (int i = 0; i < len; i++) rows[a + i] = (uint32_t)v[i];
 }
 
-__global__ void k_class_flags(uint32_t E, const unsigned long long* __restrict__ rowptr, unsigned lo, unsigned hi,
-                              uint32_t* __restrict__ flag) {
-    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= E) return;
-    const unsigned long long len = rowptr[e + 1] - rowptr[e];
-    flag[e] = (len >= lo && len <= hi) ? 1u : 0u;
-}
-
-// ordered compaction of flagged editables (deterministic long-row list)
-__global__ void k_flag_compact(uint32_t E, const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
-                               uint32_t* __restrict__ list) {
-    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < E && flag[e]) list[pos[e]] = e;
-}
-
 // long rows: one block per row, bitonic sort in shared memory (<= LONG_SORT_MAX entries), and
 // a serial in-place insertion sort by one thread beyond that (rare: only at xi ~ spacing)
 __global__ void __launch_bounds__(512)
-k_sort_long(const uint32_t* __restrict__ long_list, const unsigned long long* __restrict__ n_long,
-            const unsigned long long* __restrict__ rowptr, const float4* __restrict__ posA, uint32_t* __restrict__ rows) {
+k_sort_long(uint32_t e_lo, uint32_t e_hi, const unsigned long long* __restrict__ rowptr,
+            const float4* __restrict__ posA, uint32_t* __restrict__ rows) {
     __shared__ unsigned long long sh[LONG_SORT_MAX];
-    const unsigned long long nl = *n_long;
-    for (unsigned long long q = blockIdx.x; q < nl; q += gridDim.x) {
-        const uint32_t e = long_list[q];
+    for (uint32_t e = e_lo + blockIdx.x; e < e_hi; e += gridDim.x) {
         const unsigned long long a = rowptr[e], b = rowptr[e + 1];
         const int len = (int)(b - a);
         if (len <= LONG_SORT_MAX) {
@@ -221,6 +222,32 @@ cc_status pairs_count(cc_ctx* c) {
     return fof_base_end(c);
 }
 
+// totals_h = the 56-byte VDeg total (scan.cu): entries per class, editables per class, ghosts
+cc_status rows_resolve(cc_ctx* c, const unsigned long long* totals_h) {
+    uint32_t cnt[4], ghosts;
+    std::memcpy(cnt, totals_h + 4, sizeof(cnt));
+    std::memcpy(&ghosts, totals_h + 6, sizeof(ghosts));
+    int64_t e = 0, ent = 0;
+    ClassBases cb;
+    for (int k = 0; k < 4; k++) {
+        cb.e[k] = (uint32_t)e;
+        cb.off[k] = (unsigned long long)ent;
+        c->E_cls[k] = cnt[k];
+        e += cnt[k];
+        ent += (int64_t)totals_h[k];
+    }
+    c->E = e;
+    c->E_all = e + ghosts;
+    c->nent = ent;
+    if (c->E_all >= MAX_LOCAL) return CC_OK;  // caller reports
+    const int64_t n = c->n;
+    if (n > 0)
+        CCL(c, k_resolve<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(
+            n, c->key.p, cb, (uint32_t)e, c->eidx.p, reinterpret_cast<unsigned long long*>(c->rowoff.p)));
+    CC_CUDA(c, cudaGetLastError());
+    return CC_OK;
+}
+
 cc_status pairs_fill(cc_ctx* c) {
     const int64_t n = c->n;
     CC_TRY(cc_ensure(c, c->rows, (size_t)std::max<int64_t>(c->nent, 1), "rows"));
@@ -253,47 +280,17 @@ cc_status rows_finish(cc_ctx* c) {
     cc_prof_end(c, tok);
     CC_CUDA(c, cudaGetLastError());
     CC_TRY(pairs_fill(c));
-    c->n_long = 0;
-    CC_TRY(cc_ensure(c, c->longrow, (size_t)std::max<int64_t>(c->E, 1), "long rows"));
+    const uint32_t e_short = (uint32_t)(c->E_cls[0] + c->E_cls[1] + c->E_cls[2]);
     if (c->E > 0 && c->nent > 0) {
-        CC_TRY(cc_ensure(c, c->scratch_u64, 2, "long count"));
-        CC_CUDA(c, cudaMemsetAsync(c->scratch_u64.p, 0, sizeof(uint64_t), c->stream));
-        unsigned long long* nl = reinterpret_cast<unsigned long long*>(c->scratch_u64.p);
         int t2 = cc_prof_begin(c, "K2_sort");
-        // deg is dead after the fill: reuse it for the long-row flags, scratch_u32 for their ranks
-        CC_TRY(cc_ensure(c, c->scratch_u32, (size_t)c->E + 1, "long row ranks"));
-        const unsigned ge = (unsigned)((c->E + PAIR_THREADS - 1) / PAIR_THREADS);
-        CCL(c, k_sort_short<<<ge, PAIR_THREADS, 0, c->stream>>>((uint32_t)c->E, rowptr, c->posA.p, c->rows.p,
-                                                                c->deg.p, nl));
-        CC_TRY(scan_u32_to_u32(c, c->deg.p, c->scratch_u32.p, c->E, reinterpret_cast<uint64_t*>(nl)));
-        CCL(c, k_flag_compact<<<ge, PAIR_THREADS, 0, c->stream>>>((uint32_t)c->E, c->deg.p, c->scratch_u32.p,
-                                                                  c->longrow.p));
-        CCL(c, k_sort_long<<<148 * 2, 512, 0, c->stream>>>(c->longrow.p, nl, rowptr, c->posA.p, c->rows.p));
+        if (e_short > 0)
+            CCL(c, k_sort_short<<<(e_short + PAIR_THREADS - 1) / PAIR_THREADS, PAIR_THREADS, 0, c->stream>>>(
+                e_short, rowptr, c->posA.p, c->rows.p));
+        if (c->E_cls[3] > 0)
+            CCL(c, k_sort_long<<<(unsigned)std::min<int64_t>(c->E_cls[3], 148 * 8), 512, 0, c->stream>>>(
+                e_short, (uint32_t)c->E, rowptr, c->posA.p, c->rows.p));
         cc_prof_end(c, t2);
         CC_CUDA(c, cudaGetLastError());
-        CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 1, nl, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                                   c->stream));
-        CC_CUDA(c, cudaStreamSynchronize(c->stream));
-        c->n_long = (int64_t)c->h_counters[1];
-        // K3 work classes by row length (uniform trip counts per warp): rows of 5..16 and 17..32
-        // entries get ordered index lists; rows <= 4 are swept in place, rows > 32 use warps
-        CC_TRY(cc_ensure(c, c->midrow, (size_t)std::max<int64_t>(c->E, 1), "mid rows"));
-        int64_t off = 0;
-        const unsigned lo[2] = {5u, 17u}, hi[2] = {16u, 32u};
-        for (int k = 0; k < 2; k++) {
-            CC_CUDA(c, cudaMemsetAsync(nl, 0, sizeof(uint64_t), c->stream));
-            CCL(c, k_class_flags<<<ge, PAIR_THREADS, 0, c->stream>>>((uint32_t)c->E, rowptr, lo[k], hi[k], c->deg.p));
-            CC_TRY(scan_u32_to_u32(c, c->deg.p, c->scratch_u32.p, c->E, reinterpret_cast<uint64_t*>(nl)));
-            CCL(c, k_flag_compact<<<ge, PAIR_THREADS, 0, c->stream>>>((uint32_t)c->E, c->deg.p, c->scratch_u32.p,
-                                                                      c->midrow.p + off));
-            CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 1, nl, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                                       c->stream));
-            CC_CUDA(c, cudaStreamSynchronize(c->stream));
-            c->n_mid[k] = (int64_t)c->h_counters[1];
-            off += c->n_mid[k];
-        }
-    } else {
-        c->n_mid[0] = c->n_mid[1] = 0;
     }
     return CC_OK;
 }

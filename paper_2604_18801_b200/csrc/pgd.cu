@@ -21,6 +21,7 @@
 // Algorithmic bytes per launch: 104 B per editable (pos r/w 32, orig 16, m,v r/w 48, rowptr 8)
 // + 4 B per directed row entry; partner positions are gathers (L2 when local).
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "cc_internal.cuh"
@@ -30,19 +31,15 @@ namespace {
 
 constexpr int PGD_THREADS = 256;
 constexpr int PGD_MAX_BLOCKS = 148 * 8;
-constexpr int LONG_ROW = 32;  // rows longer than this take the warp path (rows_finish's long list)
 constexpr int BATCH = 4;
-constexpr int SHORT_MAX = 4;  // rows swept in place; 5..32 via the mid lists (pairs.cu)
 
 struct PgdArgs {
     uint32_t E;  // editable particles with rows (owned)
     const unsigned long long* __restrict__ rowptr;
     const uint32_t* __restrict__ rows;
     const float4* __restrict__ origE;
-    const uint32_t* __restrict__ long_list;
-    uint32_t n_long;
-    const uint32_t* __restrict__ mid_list;  // rows of 5..16 then 17..32 entries
-    uint32_t n_mid;
+    uint32_t e_short;  // editables are numbered class-major by row length (pairs.cu): [0, e_short)
+                       // have <= 32 entries (thread path), [e_short, E) more (warp path)
     float4* pos0;
     float4* pos1;
     float* __restrict__ mom;  // 6 x E SoA
@@ -68,7 +65,11 @@ struct PgdArgs {
     uint32_t* frozen;
     uint32_t* touch0;
     uint32_t* touch1;
+    uint32_t* gawake;   // per 32-editable group: members not frozen
+    uint32_t* gtouch0;  // per group: touch stamps (parity double-buffered like touch0/1)
+    uint32_t* gtouch1;
     unsigned long long* errs;
+    unsigned long long* work;  // running totals: [0] editables updated, [1] row entries evaluated
 };
 
 constexpr uint32_t FZ_NEVER = 0xFFFFFFFFu;
@@ -207,6 +208,16 @@ __device__ __forceinline__ void frontier_after(const PgdArgs& a, uint32_t e, int
     if (fz == FZ_NEVER) return;
     const bool freeze = !(flags & 1) && (flags & 2) && !any_active;
     a.frozen[e] = freeze ? (uint32_t)t : 0u;
+    // awake-member count of e's 32-editable group (the warp-level pre-filter of the sweep)
+    if (fz == 0u && freeze) atomicSub(&a.gawake[e >> 5], 1u);
+    else if (fz != 0u && !freeze) atomicAdd(&a.gawake[e >> 5], 1u);
+}
+
+// a moved particle wakes partner j for iteration t+1 (and j's group)
+__device__ __forceinline__ void touch(const PgdArgs& a, uint32_t* __restrict__ tnext, uint32_t* __restrict__ gnext,
+                                      uint32_t j, int t) {
+    tnext[j] = (uint32_t)(t + 1);
+    gnext[j >> 5] = (uint32_t)(t + 1);
 }
 
 __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
@@ -224,6 +235,7 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
     }
     const Th th = a.t;
     unsigned int cnt = 0, nviol = 0;
+    unsigned long long wk_e = 0, wk_n = 0;  // work done: editables updated, row entries evaluated
     double loss = 0.0;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 
@@ -232,9 +244,10 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
     const bool skip_frozen = a.frontier && !a.count_only && t >= 3;
     const uint32_t* __restrict__ tcur = (t & 1) ? a.touch1 : a.touch0;
     uint32_t* __restrict__ tnext = (t & 1) ? a.touch0 : a.touch1;
+    const uint32_t* __restrict__ gcur = (t & 1) ? a.gtouch1 : a.gtouch0;
+    uint32_t* __restrict__ gnext = (t & 1) ? a.gtouch0 : a.gtouch1;
     const uint32_t gw = blockIdx.x * (PGD_THREADS / 32) + w, nw = gridDim.x * (PGD_THREADS / 32);
-    for (uint32_t q = gw; q < a.n_long; q += nw) {
-        const uint32_t e = a.long_list[q];
+    for (uint32_t e = a.e_short + gw; e < a.E; e += nw) {
         uint32_t fz = 0;
         int replay_from = t;
         if (a.frontier && !a.count_only) {
@@ -246,6 +259,10 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
         }
         const float4 p = src[e];
         const unsigned long long k0 = a.rowptr[e], k1 = a.rowptr[e + 1];
+        if (lane == 0) {
+            wk_e++;
+            wk_n += k1 - k0;
+        }
         bool any_active = false;
         float gx = 0.0f, gy = 0.0f, gz = 0.0f;
         for (unsigned long long kb = k0; kb < k1; kb += 32) {
@@ -284,14 +301,13 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
             if (a.frontier && (flags & 1))  // moved: wake every partner for the next iteration
                 for (unsigned long long k = k0 + lane; k < k1; k += 32) {
                     const uint32_t j = a.rows[k] & ENT_IDX;
-                    if (j < a.E) tnext[j] = (uint32_t)(t + 1);
+                    if (j < a.E) touch(a, tnext, gnext, j, t);
                 }
         }
     }
 
-    // ---- short rows: one thread each, partner loads batched ahead of the sequential sum
-    // rows of <= SHORT_MAX entries are swept in place (one batch each); rows of 5..32 come from
-    // length-class lists (rows_finish) so a warp's threads run the same number of batches
+    // ---- short rows: one thread each, partner loads batched ahead of the sequential sum; the
+    // class-major numbering keeps a warp's rows in one length class (uniform batch counts)
     auto process = [&](uint32_t e, unsigned long long k0, unsigned long long k1) {
         uint32_t fz = 0;
         int replay_from = t;
@@ -303,6 +319,8 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
             }
         }
         const float4 p = src[e];
+        wk_e++;
+        wk_n += k1 - k0;
         bool any_active = false;
         float gx = 0.0f, gy = 0.0f, gz = 0.0f;
         for (unsigned long long kb = k0; kb < k1; kb += BATCH) {
@@ -336,19 +354,29 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
                 if (flags & 1)
                     for (unsigned long long k = k0; k < k1; k++) {
                         const uint32_t j = a.rows[k] & ENT_IDX;
-                        if (j < a.E) tnext[j] = (uint32_t)(t + 1);
+                        if (j < a.E) touch(a, tnext, gnext, j, t);
                     }
             }
         }
     };
     const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < a.E; e += stride) {
-        const unsigned long long k0 = a.rowptr[e], k1 = a.rowptr[e + 1];
-        if (k1 - k0 <= (unsigned long long)SHORT_MAX) process(e, k0, k1);
-    }
-    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < a.n_mid; q += stride) {
-        const uint32_t e = a.mid_list[q];
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < a.e_short; e += stride) {
+        // warp pre-filter: a group of 32 editables with no awake member and no touch is skipped
+        // with one load (stride and block size are multiples of 32: one group per warp)
+        if (skip_frozen && a.gawake[e >> 5] == 0u && gcur[e >> 5] != (uint32_t)t) continue;
         process(e, a.rowptr[e], a.rowptr[e + 1]);
+    }
+
+    // ---- work counters (integers: order-free), one atomic per warp
+    if (!a.count_only) {
+        for (int o = 16; o > 0; o >>= 1) {
+            wk_e += __shfl_down_sync(0xffffffffu, wk_e, o);
+            wk_n += __shfl_down_sync(0xffffffffu, wk_n, o);
+        }
+        if (lane == 0 && wk_e) {
+            atomicAdd(&a.work[0], wk_e);
+            atomicAdd(&a.work[1], wk_n);
+        }
     }
 
     // ---- deterministic block reduction (fixed shuffle tree + fixed warp order)
@@ -465,10 +493,9 @@ __global__ void k_cor4(int64_t n, const float4* __restrict__ dec4, const uint32_
                        uint32_t e_own, const float4* __restrict__ res, float4* __restrict__ cor4) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    const uint32_t e0 = eidx[s];
+    const uint32_t e = eidx[s];
     float4 d = dec4[s];
-    if (e0 != 0xFFFFFFFFu) {
-        const uint32_t e = (e0 & 0x80000000u) ? e_own + (e0 & 0x7FFFFFFFu) : e0;
+    if (e != 0xFFFFFFFFu) {
         const float4 r = res[e];
         d.x = r.x;
         d.y = r.y;
@@ -489,15 +516,13 @@ __global__ void k_output(int64_t n_in, const uint32_t* __restrict__ slot_of, con
 }
 
 PgdArgs make_args(cc_ctx* c, int count_only) {
-    PgdArgs a{};
+    PgdArgs a;
+    std::memset(&a, 0, sizeof(a));  // padding too: the bytes are the graph signature
     a.E = (uint32_t)c->E;
     a.rowptr = reinterpret_cast<const unsigned long long*>(c->rowptr.p);
     a.rows = c->rows.p;
     a.origE = c->origE.p;
-    a.long_list = c->longrow.p;
-    a.n_long = (uint32_t)c->n_long;
-    a.mid_list = c->midrow.p;
-    a.n_mid = (uint32_t)(c->n_mid[0] + c->n_mid[1]);
+    a.e_short = (uint32_t)(c->E_cls[0] + c->E_cls[1] + c->E_cls[2]);
     a.pos0 = c->posA.p;
     a.pos1 = c->posB.p;
     a.mom = c->mom.p;
@@ -527,6 +552,11 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.touch0 = c->touch.p;
     a.touch1 = c->touch.p + std::max<int64_t>(c->E, 1);
     a.errs = c->counters.p + 15;
+    a.work = c->k3work.p;
+    const int64_t ng = (std::max<int64_t>(c->E, 1) + 31) / 32;
+    a.gawake = c->ggroup.p;
+    a.gtouch0 = c->ggroup.p + ng;
+    a.gtouch1 = c->ggroup.p + 2 * ng;
     return a;
 }
 
@@ -534,8 +564,14 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
 // (multi-GPU) are never frozen, so moves of ghosts (refreshed each iteration) are always seen
 __global__ void k_frontier_init(uint32_t E, const unsigned long long* __restrict__ rowptr,
                                 const uint32_t* __restrict__ rows, uint32_t* __restrict__ frozen,
-                                uint32_t* __restrict__ touch0, uint32_t* __restrict__ touch1) {
+                                uint32_t* __restrict__ touch0, uint32_t* __restrict__ touch1,
+                                uint32_t* __restrict__ ggroup, uint32_t ng) {
     const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < ng) {  // group counters: every member starts awake
+        ggroup[e] = min(32u, E - 32u * e);
+        ggroup[ng + e] = 0u;
+        ggroup[2 * ng + e] = 0u;
+    }
     if (e >= E) return;
     bool ghost = false;
     for (unsigned long long k = rowptr[e]; k < rowptr[e + 1]; k++) ghost |= (rows[k] & ENT_IDX) >= E;
@@ -584,14 +620,20 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     CC_TRY(cc_ensure(c, c->trace_l, (size_t)tmax + 1, "trace"));
     CC_TRY(cc_ensure(c, c->trace_v, (size_t)tmax + 1, "trace"));
     if (c->nranks > 1) CC_TRY(cc_ensure(c, c->red, 4, "allreduce buffer"));
+    if (!c->k3work.p) {
+        CC_TRY(cc_ensure(c, c->k3work, 2, "K3 work counters"));
+        CC_CUDA(c, cudaMemsetAsync(c->k3work.p, 0, 2 * sizeof(unsigned long long), c->stream));
+    }
     CC_TRY(cc_ensure(c, c->frozen, (size_t)std::max<int64_t>(E, 1), "frontier state"));
     CC_TRY(cc_ensure(c, c->touch, 2 * (size_t)std::max<int64_t>(E, 1), "frontier touches"));
+    CC_TRY(cc_ensure(c, c->ggroup, 3 * (size_t)((std::max<int64_t>(E, 1) + 31) / 32), "frontier groups"));
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
     CC_CUDA(c, cudaMemsetAsync(c->counters.p + 15, 0, sizeof(unsigned long long), c->stream));
     if (E > 0)
         CCL(c, k_frontier_init<<<(unsigned)((E + 255) / 256), 256, 0, c->stream>>>(
                    (uint32_t)E, reinterpret_cast<const unsigned long long*>(c->rowptr.p), c->rows.p, c->frozen.p,
-                   c->touch.p, c->touch.p + std::max<int64_t>(E, 1)));
+                   c->touch.p, c->touch.p + std::max<int64_t>(E, 1), c->ggroup.p,
+                   (uint32_t)((std::max<int64_t>(E, 1) + 31) / 32)));
     // restart from P_hat^(0) (a previous cc_correct may have overwritten posA)
     if (Ea > 0)
         CCL(c, k_reset_pos<<<(unsigned)((Ea + 255) / 256), 256, 0, c->stream>>>(Ea, c->slotE.p, c->dec4.p,
@@ -613,7 +655,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
         CC_CUDA(c, cudaStreamSynchronize(c->stream));  // h goes out of scope
     }
     CCL(c, k_ctl_reset<<<1, 1, 0, c->stream>>>(c->ctl.p));
-    const int nb = pgd_blocks(std::max<int64_t>(E, (int64_t)c->n_long * 32));
+    const int nb = pgd_blocks(std::max<int64_t>(E, c->E_cls[3] * 32));
     const int batch = c->p.graph_batch > 0 ? c->p.graph_batch : 16;
     PgdArgs a = make_args(c, 0);
     // initial statistics of P_hat^(0) for the report
@@ -633,11 +675,26 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     if (tmax > 0) {
         // (re)capture a graph of `batch` iterations, each bracketed by event records
         // the graph bakes in every argument of k_pgd: re-capture when any of them changed
-        const void* key[5] = {c->posA.p, c->rows.p, c->mom.p, c->ctl.p, c->longrow.p};
-        const int64_t shape = c->n_long * 1000003 + (c->n_mid[0] + c->n_mid[1]) * 7 + (int64_t)(c->midrow.p != nullptr);
-        bool same = c->pgd_exec && c->pgd_batch == batch && c->pgd_E == E && c->pgd_nlong == shape &&
-                    c->pgd_mid == (const void*)c->midrow.p && c->pgd_frozen == (const void*)c->frozen.p;
-        for (int k = 0; k < 5; k++) same = same && key[k] == c->pgd_key[k];
+        // signature: every byte k_pgd and the multi-GPU tail bake in
+        std::vector<unsigned char> sig;
+        auto put = [&sig](const void* v, size_t sz) {
+            const unsigned char* b = static_cast<const unsigned char*>(v);
+            sig.insert(sig.end(), b, b + sz);
+        };
+        put(&a, sizeof(a));
+        put(&nb, sizeof(nb));
+        put(&batch, sizeof(batch));
+        if (c->nranks > 1) {
+            for (int d = 0; d < 2; d++) {
+                const void* ptrs[4] = {c->send_e[d].p, c->recv_e[d].p, c->rsb[d].p, c->rrb[d].p};
+                put(ptrs, sizeof(ptrs));
+                put(&c->n_ref_send[d], sizeof(int64_t));
+                put(&c->n_ref_recv[d], sizeof(int64_t));
+            }
+            const void* r = c->red.p;
+            put(&r, sizeof(r));
+        }
+        const bool same = c->pgd_exec && sig == c->pgd_sig;
         if (!same) {
             if (c->pgd_exec) cudaGraphExecDestroy(c->pgd_exec);
             c->pgd_exec = nullptr;
@@ -673,12 +730,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
             CC_CUDA(c, ce);
             CC_CUDA(c, cudaGraphInstantiate(&c->pgd_exec, graph, 0));
             cudaGraphDestroy(graph);
-            for (int k = 0; k < 5; k++) c->pgd_key[k] = key[k];
-            c->pgd_batch = batch;
-            c->pgd_E = E;
-            c->pgd_nlong = shape;
-            c->pgd_mid = c->midrow.p;
-            c->pgd_frozen = c->frozen.p;
+            c->pgd_sig = sig;
         }
         int t_before = 0;
         for (;;) {

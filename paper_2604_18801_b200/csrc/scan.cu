@@ -18,18 +18,41 @@ struct VU32 {
     __device__ VU32 shfl(int src) const { return {__shfl_sync(0xffffffffu, a, src)}; }
 };
 
-// degree scan value: a = row entries, b = owned editable rank, c = ghost editable rank
+// degree scan value, per row-length class k (K3 work classes, cc_internal.cuh row_class):
+// a[k] = row entries, b[k] = editable rank; g = ghost editable rank
 struct VDeg {
-    unsigned long long a;
-    uint32_t b, c;
-    __device__ static VDeg zero() { return {0ull, 0u, 0u}; }
-    __device__ VDeg operator+(const VDeg& o) const { return {a + o.a, b + o.b, c + o.c}; }
-    __device__ VDeg shfl_up(int d) const {
-        return {__shfl_up_sync(0xffffffffu, a, d), __shfl_up_sync(0xffffffffu, b, d),
-                __shfl_up_sync(0xffffffffu, c, d)};
+    unsigned long long a[4];
+    uint32_t b[4];
+    uint32_t g, pad;
+    __device__ static VDeg zero() {
+        VDeg v;
+        for (int k = 0; k < 4; k++) {
+            v.a[k] = 0ull;
+            v.b[k] = 0u;
+        }
+        v.g = 0u;
+        v.pad = 0u;
+        return v;
     }
-    __device__ VDeg shfl(int s) const {
-        return {__shfl_sync(0xffffffffu, a, s), __shfl_sync(0xffffffffu, b, s), __shfl_sync(0xffffffffu, c, s)};
+    __device__ VDeg operator+(const VDeg& o) const {
+        VDeg v;
+        for (int k = 0; k < 4; k++) {
+            v.a[k] = a[k] + o.a[k];
+            v.b[k] = b[k] + o.b[k];
+        }
+        v.g = g + o.g;
+        v.pad = 0u;
+        return v;
+    }
+    __device__ VDeg shfl_up(int d) const {
+        VDeg v;
+        for (int k = 0; k < 4; k++) {
+            v.a[k] = __shfl_up_sync(0xffffffffu, a[k], d);
+            v.b[k] = __shfl_up_sync(0xffffffffu, b[k], d);
+        }
+        v.g = __shfl_up_sync(0xffffffffu, g, d);
+        v.pad = 0u;
+        return v;
     }
 };
 
@@ -47,20 +70,40 @@ struct StoreU32 {
 struct LoadDeg {
     const uint32_t* deg;
     __device__ VDeg operator()(int64_t i) const {
-        uint32_t d = deg[i];
-        uint32_t ghost = d >> 31;
-        uint32_t k = d & 0x7FFFFFFFu;
-        return {(unsigned long long)k, (k > 0u) ? 1u : 0u, ghost};
+        const uint32_t d = deg[i];
+        const uint32_t len = d & 0x7FFFFFFFu;
+        VDeg v = VDeg::zero();
+        if (len > 0u) {
+            const int k = row_class(len);
+            v.a[k] = len;
+            v.b[k] = 1u;
+        } else {
+            v.g = d >> 31;
+        }
+        return v;
     }
 };
+// provisional (class, rank-in-class, row offset in class); rows_resolve adds the class bases
 struct StoreDeg {
     unsigned long long* rowoff;
     uint32_t* eidx;
+    uint32_t* cls;
     __device__ void operator()(int64_t i, const VDeg& excl, const VDeg& self) const {
-        rowoff[i] = excl.a;
-        // owned editables take ranks [0, E_own); ghost editables get (1<<31 | ghost rank),
-        // finalised once E_own is known (rows_finish)
-        eidx[i] = self.b ? excl.b : (self.c ? (0x80000000u | excl.c) : 0xFFFFFFFFu);
+        uint32_t k = 0xFFu, r = 0xFFFFFFFFu;
+        unsigned long long o = 0ull;
+        for (int q = 0; q < 4; q++)
+            if (self.b[q]) {
+                k = (uint32_t)q;
+                r = excl.b[q];
+                o = excl.a[q];
+            }
+        if (self.g) {
+            k = 4u;
+            r = excl.g;
+        }
+        cls[i] = k;
+        eidx[i] = r;
+        rowoff[i] = o;
     }
 };
 
@@ -166,10 +209,11 @@ cc_status scan_u32_to_u32(cc_ctx* c, const uint32_t* in, uint32_t* out, int64_t 
     return scan_generic<VU32>(c, n, LoadU32{in}, StoreU32{out}, reinterpret_cast<VU32*>(total_dev), "K1_scan");
 }
 
-cc_status scan_deg(cc_ctx* c, const uint32_t* deg, uint64_t* rowoff, uint32_t* eidx, int64_t n,
-                   const float4*, int64_t, unsigned long long* totals_dev) {
-    static_assert(sizeof(VDeg) == 16, "");
-    return scan_generic<VDeg>(c, n, LoadDeg{deg}, StoreDeg{reinterpret_cast<unsigned long long*>(rowoff), eidx},
+cc_status scan_deg(cc_ctx* c, const uint32_t* deg, uint64_t* rowoff, uint32_t* eidx, uint32_t* cls, int64_t n,
+                   unsigned long long* totals_dev) {
+    static_assert(sizeof(VDeg) == 56, "");
+    return scan_generic<VDeg>(c, n, LoadDeg{deg},
+                              StoreDeg{reinterpret_cast<unsigned long long*>(rowoff), eidx, cls},
                               reinterpret_cast<VDeg*>(totals_dev), "K2_scan");
 }
 

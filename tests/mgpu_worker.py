@@ -112,6 +112,9 @@ def main():
         check(seen == n, "ownership partition")
         print(json.dumps({"ok": ok, "fail": msg, "world": world, "n": n, "pairs": vp1["n_pairs"],
                           "iterations": info1["iterations"], "groups": ngo1}), flush=True)
+    c.close()  # collective teardown of libcc's NCCL communicator on every rank
+    if rank == 0:
+        s.close()
     okt = torch.tensor([1 if ok else 0], device=dev)
     dist.broadcast(okt, src=0)
     dist.destroy_process_group()

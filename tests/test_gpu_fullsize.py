@@ -73,12 +73,26 @@ def test_c4_full_size_sampled_parity():
     th = oracle.thresholds(c_or)
     rad = max(th["band_hi"], math.sqrt(th["hi2"])) * (1 + 1e-5)
 
+    xorder = np.argsort(H[0], kind="stable")
+    xsorted = H[0][xorder]
+
+    def xwindow(lo, hi):
+        return xorder[np.searchsorted(xsorted, lo, "left"):np.searchsorted(xsorted, hi, "right")]
+
     def partners_oracle(i):
-        """brute force over all N: candidates within the band radius per axis (min image), then
-        the oracle's own pair test on {i} U candidates"""
-        d = [np.abs(H[k] - H[k][i]) for k in range(3)]
+        """all N particles within the band radius per axis (min image; an x-sorted index only
+        narrows the scan, every candidate is tested), then the oracle's own brute-force pair
+        test on {i} U candidates"""
+        xi_ = float(H[0][i])
+        cand = [xwindow(xi_ - rad, xi_ + rad)]
+        if xi_ - rad < 0:
+            cand.append(xwindow(xi_ - rad + w.L, w.L))
+        if xi_ + rad >= w.L:
+            cand.append(xwindow(0.0, xi_ + rad - w.L))
+        cand = np.unique(np.concatenate(cand))
+        d = [np.abs(H[k][cand] - H[k][i]) for k in range(3)]
         d = [np.minimum(dk, w.L - dk) for dk in d]
-        cand = np.nonzero((d[0] <= rad) & (d[1] <= rad) & (d[2] <= rad))[0]
+        cand = cand[(d[0] <= rad) & (d[1] <= rad) & (d[2] <= rad)]
         idx = np.concatenate([[i], cand[cand != i]])
         pi, pj, pf = oracle.find_pairs(*(h[idx] for h in H), c_or, gid=idx.astype(np.uint32), brute=True)
         a, b = idx[pi], idx[pj]
