@@ -69,15 +69,21 @@ def test_c4_full_size_sampled_parity():
         assert np.array_equal(O[k][~ed].view(np.uint32), H[3 + k][~ed].view(np.uint32))
     order = np.argsort(gi, kind="stable")
     gi_s, gj_s, fl_s = gi[order], gj[order], fl[order]
+    order_j = np.argsort(gj, kind="stable")
+    gj_j, gi_j, fl_j = gj[order_j], gi[order_j], fl[order_j]
     c_or = oracle.cfg(L=w.L, b=w.linking_length, xi=w.xi, t_max=T, stop_mode=oracle.STOP_NONE)
     th = oracle.thresholds(c_or)
     rad = max(th["band_hi"], math.sqrt(th["hi2"])) * (1 + 1e-5)
 
-    xorder = np.argsort(H[0], kind="stable")
-    xsorted = H[0][xorder]
+    xs_t, xo_t = torch.sort(arrs[0], stable=True)  # the index only narrows the scan (device sort)
+    xsorted, xorder = xs_t.cpu().numpy(), xo_t.cpu().numpy()
+    del xs_t, xo_t
 
     def xwindow(lo, hi):
-        return xorder[np.searchsorted(xsorted, lo, "left"):np.searchsorted(xsorted, hi, "right")]
+        # fp32 keys widened outward by one ulp (a float64 key would make numpy cast the array)
+        lo32 = np.nextafter(np.float32(lo), np.float32(-np.inf))
+        hi32 = np.nextafter(np.float32(hi), np.float32(np.inf))
+        return xorder[np.searchsorted(xsorted, lo32, "left"):np.searchsorted(xsorted, hi32, "right")]
 
     def partners_oracle(i):
         """all N particles within the band radius per axis (min image; an x-sorted index only
@@ -104,9 +110,9 @@ def test_c4_full_size_sampled_parity():
         s, e = np.searchsorted(gi_s, i), np.searchsorted(gi_s, i, side="right")
         for k in range(s, e):
             res[(int(i), int(gj_s[k]))] = int(fl_s[k])
-        sel = np.nonzero(gj == i)[0]
-        for k in sel:
-            res[(int(gi[k]), int(i))] = int(fl[k])
+        s, e = np.searchsorted(gj_j, i), np.searchsorted(gj_j, i, side="right")
+        for k in range(s, e):
+            res[(int(gi_j[k]), int(i))] = int(fl_j[k])
         return res
 
     rng = np.random.default_rng(0)
