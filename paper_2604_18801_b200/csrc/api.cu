@@ -248,7 +248,7 @@ cc_status cc_create(cc_ctx** out, int device, void* stream, const cc_params* p, 
     c->owns_stream = (stream == nullptr);
     if (cudaMallocHost(&c->h_ctl, sizeof(cc::Ctl)) != cudaSuccess ||
         cudaMallocHost(&c->h_counters, 16 * sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMallocHost(&c->h_red, 4 * sizeof(double)) != cudaSuccess) {
+        cudaMallocHost(&c->h_red, cc::LFX_STATS * sizeof(unsigned long long)) != cudaSuccess) {
         cc_destroy(c);
         return CC_E_CUDA;
     }
@@ -272,11 +272,11 @@ void cc_destroy(cc_ctx* c) {
     cc_release(c, c->slot_of); cc_release(c, c->deg); cc_release(c, c->eidx); cc_release(c, c->rows);
     cc_release(c, c->slotE); cc_release(c, c->parent); cc_release(c, c->mingid); cc_release(c, c->gsize);
     cc_release(c, c->scratch_u32); cc_release(c, c->rowoff); cc_release(c, c->rowptr); cc_release(c, c->scratch_u64);
-    cc_release(c, c->mom); cc_release(c, c->bc); cc_release(c, c->partial_d); cc_release(c, c->partial_u);
+    cc_release(c, c->mom); cc_release(c, c->bc); 
     cc_release(c, c->counters); cc_release(c, c->ctl); cc_release(c, c->trace_a); cc_release(c, c->trace_l);
     cc_release(c, c->trace_v); cc_release(c, c->parent_base); cc_release(c, c->rec32);
-    cc_release(c, c->frozen); cc_release(c, c->touch); cc_release(c, c->k3work);
-    cc_release(c, c->ggroup);
+    cc_release(c, c->frozen); cc_release(c, c->inl); cc_release(c, c->k3work);
+    cc_release(c, c->wlist);
     cc_release(c, c->tmp_bytes); cc_release(c, c->in_f); cc_release(c, c->in_gid);
     for (int d = 0; d < 2; d++) {
         cc_release(c, c->dflag[d]); cc_release(c, c->dpos[d]); cc_release(c, c->shell[d]); cc_release(c, c->sbuf7[d]);

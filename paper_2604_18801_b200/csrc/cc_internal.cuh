@@ -66,7 +66,57 @@ struct Ctl {
     unsigned long long active;   // L_tight-active pairs at the last check
     unsigned long long violated; // pairs whose link status differs from the original (Eq. 1)
     double loss;
+    unsigned int wn[2];  // frontier work-list lengths, by iteration parity (pgd.cu)
+    unsigned int pad2[2];
+    unsigned long long acc[8];  // K3 launch statistics being summed (LossFx layout, below)
 };
+
+// ---------------------------------------------------------------------------------------
+// exact, order-independent L_tight sum (R28).  Every term ee^2 (ee fp32, so ee^2 is
+// exact in fp64) is truncated to a multiple of 2^-LFX_UNIT and added as 32-bit digits into
+// 64-bit limbs: integer sums, so any summation order -- threads, blocks, ranks -- gives the
+// same loss, and the stop decision (R11) is bit-identical for any grid or rank count.
+// Statistics words: [0] active pairs, [1] violated pairs, [2..7] loss limbs (limb k weighs
+// 2^(32k - LFX_UNIT)); range [2^-140, 2^52).
+constexpr int LFX_UNIT = 140;
+constexpr int LFX_STATS = 8;
+
+__device__ __forceinline__ void lfx_add(unsigned long long* l, double d) {
+    if (!(d > 0.0)) return;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(d);
+    const int ex = (int)((bits >> 52) & 0x7FF);
+    unsigned long long m = (bits & 0xFFFFFFFFFFFFFull) | (ex ? (1ull << 52) : 0ull);
+    int s = (ex ? ex : 1) - 1075 + LFX_UNIT;  // d = m * 2^(s - LFX_UNIT)
+    if (s < 0) {
+        if (s <= -64) return;
+        m >>= -s;
+        s = 0;
+    }
+    const int k0 = s >> 5, off = s & 31;
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+        unsigned long long part = 0ull;
+        if (k == k0) part = (m << off) & 0xFFFFFFFFull;
+        else if (k == k0 + 1) part = (m >> (32 - off)) & 0xFFFFFFFFull;
+        else if (k == k0 + 2 && off) part = (m >> (64 - off)) & 0xFFFFFFFFull;
+        l[k] += part;
+    }
+}
+
+// value of the limbs: carries normalised, then summed from the top in fp64 (fixed order)
+__host__ __device__ inline double lfx_value(const unsigned long long* l) {
+    unsigned long long d[6], carry = 0ull;
+    for (int k = 0; k < 6; k++) {
+        const unsigned long long v = l[k] + carry;  // < 2^64: carry < 2^32 and l[k] < 2^63
+        d[k] = v & 0xFFFFFFFFull;
+        carry = v >> 32;
+    }
+    double r = (double)carry;
+    for (int k = 5; k >= 0; k--) r = r * 4294967296.0 + (double)d[k];
+    // scale by 2^-LFX_UNIT in two exact steps
+    const double s70 = 8.470329472543003e-22;  // 2^-70
+    return r * s70 * s70;
+}
 
 template <typename T>
 struct DBuf {
@@ -125,11 +175,10 @@ struct cc_ctx {
     double r_pair = 0, r_link = 0;   // search radii: vulnerable band / FoF on original positions
     cc::DBuf<float> mom;         // 6 * E floats: mx, my, mz, vx, vy, vz
     cc::DBuf<float2> bc;         // Adam bias corrections per iteration
-    cc::DBuf<double> partial_d;  // block partials
-    cc::DBuf<unsigned long long> partial_u, counters;
+    cc::DBuf<unsigned long long> counters;
     cc::DBuf<cc::Ctl> ctl;
     cc::DBuf<long long> trace_a, trace_v;
-    cc::DBuf<uint32_t> frozen, touch, ggroup;  // K3 frontier state (pgd.cu)
+    cc::DBuf<uint32_t> frozen, inl, wlist;  // K3 frontier state and work lists (pgd.cu)
     cc::DBuf<unsigned long long> k3work;  // K3 work totals (editables updated, entries evaluated)
     int64_t E_cls[4] = {0, 0, 0, 0};  // editables per K3 work class (row_class), numbered class-major
     cc::DBuf<double> trace_l;
@@ -144,12 +193,12 @@ struct cc_ctx {
         lsb[2], lrb[2], gath;
     cc::DBuf<long long> dcnt;
     cc::DBuf<float4> rsb[2], rrb[2];
-    cc::DBuf<double> red;
+    cc::DBuf<unsigned long long> red;  // K3 stop statistics (LFX_STATS words) for the allreduce
     cc::DBuf<uint2> bnd;
     int64_t n_shell[2] = {0, 0}, n_from_left = 0, n_from_right = 0, stage_cap = 0;
     int64_t n_ref_send[2] = {0, 0}, n_ref_recv[2] = {0, 0};
     int64_t launches_per_iter_tail = 0;
-    double* h_red = nullptr;
+    unsigned long long* h_red = nullptr;
     unsigned long long final_active = 0;
     double final_loss = 0.0;
     unsigned long long final_violated = 0;

@@ -147,13 +147,13 @@ __global__ void k_refresh_unpack(int64_t m, const uint32_t* __restrict__ recv_e,
 }
 
 // global stop decision after the allreduce of (active, loss)
-__global__ void k_decide(Ctl* ctl, const double* __restrict__ red, int stop_mode, double eps_loss, int t_max,
-                         long long* trace_a, double* trace_l, long long* trace_v) {
+__global__ void k_decide(Ctl* ctl, const unsigned long long* __restrict__ red, int stop_mode, double eps_loss,
+                         int t_max, long long* trace_a, double* trace_l, long long* trace_v) {
     if (ctl->done) return;
     const int t = ctl->t + 1;
-    const unsigned long long tu = (unsigned long long)red[0];
-    const double td = red[1];
-    const unsigned long long tv = (unsigned long long)red[2];
+    const unsigned long long tu = red[0];
+    const double td = lfx_value(red + 2);  // exact integer sums over ranks: rank-count invariant
+    const unsigned long long tv = red[1];
     ctl->active = tu;
     ctl->loss = td;
     ctl->violated = tv;
@@ -408,7 +408,7 @@ cc_status dist_setup_refresh(cc_ctx* c) {
                                cudaMemcpyDeviceToHost, c->stream));
     CC_CUDA(c, cudaStreamSynchronize(c->stream));
     if (c->h_counters[14] & 8ull) return cc_fail(c, CC_E_DATA, "ghost editable is not editable on its owner");
-    CC_TRY(cc_ensure(c, c->red, 4, "allreduce buffer"));
+    CC_TRY(cc_ensure(c, c->red, LFX_STATS, "allreduce buffer"));
     return CC_OK;
 }
 
@@ -433,7 +433,7 @@ cc_status dist_iter_tail(cc_ctx* c, const float4* p0, const float4* p1) {
             CCL(c, k_refresh_unpack<<<(unsigned)((c->n_ref_recv[d] + DT - 1) / DT), DT, 0, c->stream>>>(
                        c->n_ref_recv[d], c->recv_e[d].p, c->ctl.p, const_cast<float4*>(p0), const_cast<float4*>(p1),
                        c->rrb[d].p));
-    CC_NCCL(c, ncclAllReduce(c->red.p, c->red.p, 3, ncclFloat64, ncclSum, comm(c), c->stream));
+    CC_NCCL(c, ncclAllReduce(c->red.p, c->red.p, LFX_STATS, ncclUint64, ncclSum, comm(c), c->stream));
     CCL(c, k_decide<<<1, 1, 0, c->stream>>>(c->ctl.p, c->red.p, c->p.stop_mode, c->p.eps_loss, c->p.t_max,
                                             c->trace_a.p, c->trace_l.p, c->trace_v.p));
     return CC_OK;

@@ -24,7 +24,11 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "cc_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace cc {
 namespace {
@@ -51,23 +55,20 @@ struct PgdArgs {
     int stop_mode;
     double eps_loss;
     Ctl* ctl;
-    unsigned long long* part_u;  // 2 per block: active, violated
-    double* part_d;
     long long* trace_a;
     double* trace_l;
     long long* trace_v;
     int count_only;
-    double* red;  // multi-GPU: local (active, loss, violated) for the allreduce, else nullptr
+    unsigned long long* red;  // multi-GPU: local statistics (LFX_STATS words) for the allreduce, else nullptr
     // frontier (exact active-set skipping): frozen[e] = 0 awake, FZ_NEVER never frozen (has a
-    // ghost partner), else the last iteration e was processed; touch0/1[e] = iteration at which a
-    // partner's move requires processing e (parity double-buffered); errs counts unsafe freezes
+    // ghost partner), else the last iteration e was processed.  Iteration t (>= 3) processes
+    // only its work list: the editables awake after t-1 and the partners of those that moved
+    // at t-1 (built by t-1); errs counts unsafe freezes
     int frontier;
     uint32_t* frozen;
-    uint32_t* touch0;
-    uint32_t* touch1;
-    uint32_t* gawake;   // per 32-editable group: members not frozen
-    uint32_t* gtouch0;  // per group: touch stamps (parity double-buffered like touch0/1)
-    uint32_t* gtouch1;
+    uint32_t* inl;    // inl[e] = iteration whose work list holds e (dedupe stamp)
+    uint32_t* wl0;    // work lists by iteration parity (E entries each)
+    uint32_t* wl1;
     unsigned long long* errs;
     unsigned long long* work;  // running totals: [0] editables updated, [1] row entries evaluated
 };
@@ -202,25 +203,29 @@ __device__ __forceinline__ int update(const PgdArgs& a, uint32_t e, const float4
     return flags;
 }
 
-// frontier bookkeeping after e was processed at iteration t (one thread per e)
-__device__ __forceinline__ void frontier_after(const PgdArgs& a, uint32_t e, int t, int flags, bool any_active,
+// frontier bookkeeping after e was processed at iteration t; returns whether e stays awake
+__device__ __forceinline__ bool frontier_after(const PgdArgs& a, uint32_t e, int t, int flags, bool any_active,
                                                uint32_t fz) {
-    if (fz == FZ_NEVER) return;
+    if (fz == FZ_NEVER) return true;
     const bool freeze = !(flags & 1) && (flags & 2) && !any_active;
     a.frozen[e] = freeze ? (uint32_t)t : 0u;
-    // awake-member count of e's 32-editable group (the warp-level pre-filter of the sweep)
-    if (fz == 0u && freeze) atomicSub(&a.gawake[e >> 5], 1u);
-    else if (fz != 0u && !freeze) atomicAdd(&a.gawake[e >> 5], 1u);
+    return !freeze;
 }
 
-// a moved particle wakes partner j for iteration t+1 (and j's group)
-__device__ __forceinline__ void touch(const PgdArgs& a, uint32_t* __restrict__ tnext, uint32_t* __restrict__ gnext,
-                                      uint32_t j, int t) {
-    tnext[j] = (uint32_t)(t + 1);
-    gnext[j >> 5] = (uint32_t)(t + 1);
+// queue editable j for iteration t+1 (once: the stamp dedupes), warp-aggregated append
+__device__ __forceinline__ void enqueue(const PgdArgs& a, uint32_t* __restrict__ wnext, unsigned int* __restrict__ nnext,
+                                        uint32_t j, int t) {
+    const uint32_t stamp = (uint32_t)(t + 1);
+    if (*((volatile uint32_t*)&a.inl[j]) == stamp) return;
+    if (atomicExch(&a.inl[j], stamp) == stamp) return;
+    cg::coalesced_group g = cg::coalesced_threads();
+    unsigned int base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(nnext, g.size());
+    base = g.shfl(base, 0);
+    wnext[base + g.thread_rank()] = j;
 }
 
-__global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
+__global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
     Ctl* ctl = a.ctl;
     if (!a.count_only && *((volatile int*)&ctl->done)) return;
     const int t = a.count_only ? 0 : ctl->t + 1;
@@ -234,91 +239,41 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
         dst = (t & 1) ? a.pos1 : a.pos0;
     }
     const Th th = a.t;
-    unsigned int cnt = 0, nviol = 0;
+    unsigned long long st[LFX_STATS];  // active pairs, violated pairs, loss limbs (exact sums)
+#pragma unroll
+    for (int k = 0; k < LFX_STATS; k++) st[k] = 0ull;
     unsigned long long wk_e = 0, wk_n = 0;  // work done: editables updated, row entries evaluated
-    double loss = 0.0;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 
-    // ---- long rows: one warp per row, 32 entries per round, row-order accumulation via shuffles
-    // frontier (exact skipping of frozen particles from iteration 3 on): see frontier_after
-    const bool skip_frozen = a.frontier && !a.count_only && t >= 3;
-    const uint32_t* __restrict__ tcur = (t & 1) ? a.touch1 : a.touch0;
-    uint32_t* __restrict__ tnext = (t & 1) ? a.touch0 : a.touch1;
-    const uint32_t* __restrict__ gcur = (t & 1) ? a.gtouch1 : a.gtouch0;
-    uint32_t* __restrict__ gnext = (t & 1) ? a.gtouch0 : a.gtouch1;
-    const uint32_t gw = blockIdx.x * (PGD_THREADS / 32) + w, nw = gridDim.x * (PGD_THREADS / 32);
-    for (uint32_t e = a.e_short + gw; e < a.E; e += nw) {
-        uint32_t fz = 0;
-        int replay_from = t;
-        if (a.frontier && !a.count_only) {
-            fz = a.frozen[e];
-            if (skip_frozen && fz != 0u && fz != FZ_NEVER) {
-                if (tcur[e] != (uint32_t)t) continue;  // warp-uniform
-                replay_from = (int)fz + 1;
+    // frontier: iteration t >= 3 walks only its work list (built by t-1); t >= 2 builds the next
+    const bool front = a.frontier && !a.count_only;
+    const bool lists = front && t >= 3;
+    const bool build = front && t >= 2;
+    const uint32_t* __restrict__ wcur = (t & 1) ? a.wl1 : a.wl0;
+    uint32_t* __restrict__ wnext = (t & 1) ? a.wl0 : a.wl1;
+    unsigned int* nnext = &ctl->wn[(t + 1) & 1];
+    const uint32_t n_items = lists ? ctl->wn[t & 1] : a.E;
+
+    auto count = [&](const Term& tm, uint32_t ent) {  // each pair once, at its lower-gid endpoint
+        if (ent & ENT_UPPER) {
+            if (tm.kind) {
+                st[0]++;
+                lfx_add(st + 2, (double)tm.ee * (double)tm.ee);
             }
+            st[1] += tm.viol;
         }
+    };
+    auto replay_start = [&](uint32_t e, uint32_t& fz) {
+        fz = front ? a.frozen[e] : 0u;
+        return (fz != 0u && fz != FZ_NEVER) ? (int)fz + 1 : t;  // zero-gradient steps missed while frozen
+    };
+
+    // ---- a row of <= 32 entries: one thread, partner loads batched ahead of the sequential sum
+    auto process_thread = [&](uint32_t e) {
+        uint32_t fz;
+        const int replay_from = replay_start(e, fz);
         const float4 p = src[e];
         const unsigned long long k0 = a.rowptr[e], k1 = a.rowptr[e + 1];
-        if (lane == 0) {
-            wk_e++;
-            wk_n += k1 - k0;
-        }
-        bool any_active = false;
-        float gx = 0.0f, gy = 0.0f, gz = 0.0f;
-        for (unsigned long long kb = k0; kb < k1; kb += 32) {
-            const unsigned long long k = kb + lane;
-            Term tm;
-            tm.kind = 0;
-            if (k < k1) {
-                const uint32_t ent = a.rows[k];
-                tm = pair_term(p, src[ent & ENT_IDX], ent, th);
-                if (ent & ENT_UPPER) {
-                    if (tm.kind) {
-                        cnt++;
-                        loss += (double)tm.ee * (double)tm.ee;
-                    }
-                    nviol += tm.viol;
-                }
-            }
-            const int m = (int)min((unsigned long long)32, k1 - kb);
-            any_active |= __any_sync(0xffffffffu, tm.kind != 0);
-            for (int i = 0; i < m; i++) {  // the pinned sequential order, identical on all lanes
-                Term u;
-                u.kind = __shfl_sync(0xffffffffu, tm.kind, i);
-                u.px = __shfl_sync(0xffffffffu, tm.px, i);
-                u.py = __shfl_sync(0xffffffffu, tm.py, i);
-                u.pz = __shfl_sync(0xffffffffu, tm.pz, i);
-                accumulate(gx, gy, gz, u);
-            }
-        }
-        if (!a.count_only) {
-            int flags = 0;
-            if (lane == 0) {
-                flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);
-                if (a.frontier) frontier_after(a, e, t, flags, any_active, fz);
-            }
-            flags = __shfl_sync(0xffffffffu, flags, 0);
-            if (a.frontier && (flags & 1))  // moved: wake every partner for the next iteration
-                for (unsigned long long k = k0 + lane; k < k1; k += 32) {
-                    const uint32_t j = a.rows[k] & ENT_IDX;
-                    if (j < a.E) touch(a, tnext, gnext, j, t);
-                }
-        }
-    }
-
-    // ---- short rows: one thread each, partner loads batched ahead of the sequential sum; the
-    // class-major numbering keeps a warp's rows in one length class (uniform batch counts)
-    auto process = [&](uint32_t e, unsigned long long k0, unsigned long long k1) {
-        uint32_t fz = 0;
-        int replay_from = t;
-        if (a.frontier && !a.count_only) {
-            fz = a.frozen[e];
-            if (skip_frozen && fz != 0u && fz != FZ_NEVER) {
-                if (tcur[e] != (uint32_t)t) return;  // frozen and no partner moved: nothing changes
-                replay_from = (int)fz + 1;
-            }
-        }
-        const float4 p = src[e];
         wk_e++;
         wk_n += k1 - k0;
         bool any_active = false;
@@ -335,13 +290,7 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
             for (int i = 0; i < BATCH; i++) {
                 if (kb + i < k1) {
                     const Term tm = pair_term(p, qq[i], ent[i], th);
-                    if (ent[i] & ENT_UPPER) {
-                        if (tm.kind) {
-                            cnt++;
-                            loss += (double)tm.ee * (double)tm.ee;
-                        }
-                        nviol += tm.viol;
-                    }
+                    count(tm, ent[i]);
                     any_active |= tm.kind != 0;
                     accumulate(gx, gy, gz, tm);
                 }
@@ -350,21 +299,84 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
         if (!a.count_only) {
             const int flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);
             if (a.frontier) {
-                frontier_after(a, e, t, flags, any_active, fz);
-                if (flags & 1)
-                    for (unsigned long long k = k0; k < k1; k++) {
-                        const uint32_t j = a.rows[k] & ENT_IDX;
-                        if (j < a.E) touch(a, tnext, gnext, j, t);
-                    }
+                const bool awake = frontier_after(a, e, t, flags, any_active, fz);
+                if (build) {
+                    if (awake) enqueue(a, wnext, nnext, e, t);
+                    if (flags & 1)  // moved: every partner must be looked at in t+1
+                        for (unsigned long long k = k0; k < k1; k++) {
+                            const uint32_t j = a.rows[k] & ENT_IDX;
+                            if (j < a.E) enqueue(a, wnext, nnext, j, t);
+                        }
+                }
             }
         }
     };
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < a.e_short; e += stride) {
-        // warp pre-filter: a group of 32 editables with no awake member and no touch is skipped
-        // with one load (stride and block size are multiples of 32: one group per warp)
-        if (skip_frozen && a.gawake[e >> 5] == 0u && gcur[e >> 5] != (uint32_t)t) continue;
-        process(e, a.rowptr[e], a.rowptr[e + 1]);
+
+    // ---- a row of > 32 entries: the whole warp, 32 entries per round, row-order accumulation
+    // through shuffles (the pinned order, identical on all lanes)
+    auto process_warp = [&](uint32_t e) {
+        uint32_t fz;
+        const int replay_from = replay_start(e, fz);
+        const float4 p = src[e];
+        const unsigned long long k0 = a.rowptr[e], k1 = a.rowptr[e + 1];
+        if (lane == 0) {
+            wk_e++;
+            wk_n += k1 - k0;
+        }
+        bool any_active = false;
+        float gx = 0.0f, gy = 0.0f, gz = 0.0f;
+        for (unsigned long long kb = k0; kb < k1; kb += 32) {
+            const unsigned long long k = kb + lane;
+            Term tm;
+            tm.kind = 0;
+            if (k < k1) {
+                const uint32_t ent = a.rows[k];
+                tm = pair_term(p, src[ent & ENT_IDX], ent, th);
+                count(tm, ent);
+            }
+            const int m = (int)min((unsigned long long)32, k1 - kb);
+            any_active |= __any_sync(0xffffffffu, tm.kind != 0);
+            for (int i = 0; i < m; i++) {
+                Term u;
+                u.kind = __shfl_sync(0xffffffffu, tm.kind, i);
+                u.px = __shfl_sync(0xffffffffu, tm.px, i);
+                u.py = __shfl_sync(0xffffffffu, tm.py, i);
+                u.pz = __shfl_sync(0xffffffffu, tm.pz, i);
+                accumulate(gx, gy, gz, u);
+            }
+        }
+        if (!a.count_only) {
+            int flags = 0;
+            bool awake = false;
+            if (lane == 0) {
+                flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);
+                if (a.frontier) awake = frontier_after(a, e, t, flags, any_active, fz);
+                if (build && awake) enqueue(a, wnext, nnext, e, t);
+            }
+            flags = __shfl_sync(0xffffffffu, flags, 0);
+            if (build && (flags & 1))
+                for (unsigned long long k = k0 + lane; k < k1; k += 32) {
+                    const uint32_t j = a.rows[k] & ENT_IDX;
+                    if (j < a.E) enqueue(a, wnext, nnext, j, t);
+                }
+        }
+    };
+
+    // ---- items: editables 0..E-1 (sweep) or the work list; a warp takes 32 consecutive items,
+    // short rows by their own lane, then each long row (numbered last, pairs.cu) by the warp
+    const uint32_t gw = blockIdx.x * (PGD_THREADS / 32) + w, nw = gridDim.x * (PGD_THREADS / 32);
+    for (uint32_t base = gw * 32u; base < n_items; base += nw * 32u) {
+        const uint32_t idx = base + lane;
+        uint32_t e = 0xFFFFFFFFu;
+        if (idx < n_items) e = lists ? wcur[idx] : idx;
+        const bool lng = e != 0xFFFFFFFFu && e >= a.e_short;
+        if (e != 0xFFFFFFFFu && !lng) process_thread(e);
+        unsigned lm = __ballot_sync(0xffffffffu, lng);
+        while (lm) {
+            const int sl = __ffs(lm) - 1;
+            process_warp(__shfl_sync(0xffffffffu, e, sl));
+            lm &= lm - 1;
+        }
     }
 
     // ---- work counters (integers: order-free), one atomic per warp
@@ -379,94 +391,62 @@ __global__ void __launch_bounds__(PGD_THREADS) k_pgd(PgdArgs a) {
         }
     }
 
-    // ---- deterministic block reduction (fixed shuffle tree + fixed warp order)
-    __shared__ unsigned long long sh_u[PGD_THREADS / 32], sh_v[PGD_THREADS / 32];
-    __shared__ double sh_d[PGD_THREADS / 32];
+    // ---- statistics: integer sums (LossFx), so the order of warps, blocks and ranks is free
+    __shared__ unsigned long long sh[PGD_THREADS / 32][LFX_STATS];
     __shared__ bool am_last;
-    unsigned long long cu = cnt, cv = nviol;
-    for (int o = 16; o > 0; o >>= 1) {
-        cu += __shfl_down_sync(0xffffffffu, cu, o);
-        cv += __shfl_down_sync(0xffffffffu, cv, o);
-        loss += __shfl_down_sync(0xffffffffu, loss, o);
+#pragma unroll
+    for (int k = 0; k < LFX_STATS; k++) {
+        unsigned long long v = st[k];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0) sh[w][k] = v;
     }
-    if (lane == 0) {
-        sh_u[w] = cu;
-        sh_v[w] = cv;
-        sh_d[w] = loss;
+    __syncthreads();
+    if (threadIdx.x < LFX_STATS) {
+        unsigned long long v = 0ull;
+        for (int k = 0; k < PGD_THREADS / 32; k++) v += sh[k][threadIdx.x];
+        if (v) atomicAdd(&ctl->acc[threadIdx.x], v);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned long long bu = 0, bv = 0;
-        double bd = 0.0;
-        for (int k = 0; k < PGD_THREADS / 32; k++) {
-            bu += sh_u[k];
-            bv += sh_v[k];
-            bd += sh_d[k];
-        }
-        a.part_u[2 * blockIdx.x] = bu;
-        a.part_u[2 * blockIdx.x + 1] = bv;
-        a.part_d[blockIdx.x] = bd;
         __threadfence();
         const unsigned int tk = atomicAdd(&ctl->ticket, 1u);
         am_last = (tk == gridDim.x - 1);
     }
     __syncthreads();
-    if (!am_last) return;
-    // last block: fixed-order sum of the block partials
+    if (!am_last || threadIdx.x != 0) return;
+    // last block: every other block's sums are in ctl->acc
     __threadfence();
-    unsigned long long su = 0, sv = 0;
-    double sd = 0.0;
-    for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-        su += ((volatile unsigned long long*)a.part_u)[2 * b];
-        sv += ((volatile unsigned long long*)a.part_u)[2 * b + 1];
-        sd += ((volatile double*)a.part_d)[b];
+    unsigned long long tot[LFX_STATS];
+    for (int k = 0; k < LFX_STATS; k++) {
+        tot[k] = ((volatile unsigned long long*)ctl->acc)[k];
+        ctl->acc[k] = 0ull;
     }
-    for (int o = 16; o > 0; o >>= 1) {
-        su += __shfl_down_sync(0xffffffffu, su, o);
-        sv += __shfl_down_sync(0xffffffffu, sv, o);
-        sd += __shfl_down_sync(0xffffffffu, sd, o);
-    }
-    __syncthreads();
-    if (lane == 0) {
-        sh_u[w] = su;
-        sh_v[w] = sv;
-        sh_d[w] = sd;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long tu = 0, tv = 0;
-        double td = 0.0;
-        for (int k = 0; k < PGD_THREADS / 32; k++) {
-            tu += sh_u[k];
-            tv += sh_v[k];
-            td += sh_d[k];
+    const unsigned long long tu = tot[0], tv = tot[1];
+    const double td = lfx_value(tot + 2);
+    ctl->active = tu;
+    ctl->violated = tv;
+    ctl->loss = td;
+    ctl->ticket = 0;
+    if (lists) ctl->wn[t & 1] = 0u;  // consumed: iteration t+1 fills it for t+2
+    if (a.red) {  // multi-GPU: the decision waits for the allreduce (dist.cu k_decide)
+        for (int k = 0; k < LFX_STATS; k++) a.red[k] = tot[k];
+    } else if (!a.count_only) {
+        if (a.trace_a) {
+            a.trace_a[t - 1] = (long long)tu;
+            a.trace_l[t - 1] = td;
+            a.trace_v[t - 1] = (long long)tv;
         }
-        ctl->active = tu;
-        ctl->violated = tv;
-        ctl->loss = td;
-        ctl->ticket = 0;
-        if (a.red) {  // multi-GPU: the decision waits for the allreduce (dist.cu k_decide)
-            a.red[0] = (double)tu;
-            a.red[1] = td;
-            a.red[2] = (double)tv;
-        } else if (!a.count_only) {
-            if (a.trace_a) {
-                a.trace_a[t - 1] = (long long)tu;
-                a.trace_l[t - 1] = td;
-                a.trace_v[t - 1] = (long long)tv;
-            }
-            if (stop_rule(a.stop_mode, tu, td, tv, a.eps_loss)) {
-                ctl->done = 1;
-                ctl->t_res = t - 1;  // the state this launch read
-                ctl->converged = 1;
-            } else if (t >= a.t_max) {
-                ctl->done = 1;
-                ctl->t_res = t;      // the state this launch wrote
-            }
-            ctl->t = t;
+        if (stop_rule(a.stop_mode, tu, td, tv, a.eps_loss)) {
+            ctl->done = 1;
+            ctl->t_res = t - 1;  // the state this launch read
+            ctl->converged = 1;
+        } else if (t >= a.t_max) {
+            ctl->done = 1;
+            ctl->t_res = t;      // the state this launch wrote
         }
-        __threadfence();
+        ctl->t = t;
     }
+    __threadfence();
 }
 
 __global__ void k_ctl_reset(Ctl* ctl) {
@@ -478,6 +458,8 @@ __global__ void k_ctl_reset(Ctl* ctl) {
     ctl->active = 0;
     ctl->violated = 0;
     ctl->loss = 0.0;
+    ctl->wn[0] = ctl->wn[1] = 0u;
+    for (int k = 0; k < LFX_STATS; k++) ctl->acc[k] = 0ull;
 }
 
 __global__ void k_reset_pos(int64_t Ea, const uint32_t* __restrict__ slotE, const float4* __restrict__ dec4,
@@ -540,8 +522,6 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.stop_mode = c->p.stop_mode;
     a.eps_loss = c->p.eps_loss;
     a.ctl = c->ctl.p;
-    a.part_u = c->partial_u.p;
-    a.part_d = c->partial_d.p;
     a.trace_a = c->trace_a.p;
     a.trace_l = c->trace_l.p;
     a.trace_v = c->trace_v.p;
@@ -549,14 +529,11 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.red = c->nranks > 1 ? c->red.p : nullptr;
     a.frontier = c->p.frontier ? 1 : 0;
     a.frozen = c->frozen.p;
-    a.touch0 = c->touch.p;
-    a.touch1 = c->touch.p + std::max<int64_t>(c->E, 1);
     a.errs = c->counters.p + 15;
     a.work = c->k3work.p;
-    const int64_t ng = (std::max<int64_t>(c->E, 1) + 31) / 32;
-    a.gawake = c->ggroup.p;
-    a.gtouch0 = c->ggroup.p + ng;
-    a.gtouch1 = c->ggroup.p + 2 * ng;
+    a.inl = c->inl.p;
+    a.wl0 = c->wlist.p;
+    a.wl1 = c->wlist.p + std::max<int64_t>(c->E, 1);
     return a;
 }
 
@@ -564,20 +541,13 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
 // (multi-GPU) are never frozen, so moves of ghosts (refreshed each iteration) are always seen
 __global__ void k_frontier_init(uint32_t E, const unsigned long long* __restrict__ rowptr,
                                 const uint32_t* __restrict__ rows, uint32_t* __restrict__ frozen,
-                                uint32_t* __restrict__ touch0, uint32_t* __restrict__ touch1,
-                                uint32_t* __restrict__ ggroup, uint32_t ng) {
+                                uint32_t* __restrict__ inl) {
     const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < ng) {  // group counters: every member starts awake
-        ggroup[e] = min(32u, E - 32u * e);
-        ggroup[ng + e] = 0u;
-        ggroup[2 * ng + e] = 0u;
-    }
     if (e >= E) return;
     bool ghost = false;
     for (unsigned long long k = rowptr[e]; k < rowptr[e + 1]; k++) ghost |= (rows[k] & ENT_IDX) >= E;
     frozen[e] = ghost ? FZ_NEVER : 0u;
-    touch0[e] = 0u;
-    touch1[e] = 0u;
+    inl[e] = 0u;
 }
 
 int pgd_blocks(int64_t E) {
@@ -594,10 +564,13 @@ const float4* pgd_result(cc_ctx* c) { return (c->last_iters & 1) ? c->posB.p : c
 // (active, loss, violated) of the count-only pass just enqueued, summed over ranks (synchronising)
 static cc_status global_check(cc_ctx* c, double* al) {
     if (c->nranks > 1) {
-        CC_TRY(dist_allreduce_f64(c, c->red.p, 3));
-        CC_CUDA(c, cudaMemcpyAsync(c->h_red, c->red.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CC_TRY(dist_allreduce_u64(c, c->red.p, LFX_STATS));
+        CC_CUDA(c, cudaMemcpyAsync(c->h_red, c->red.p, LFX_STATS * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                   c->stream));
         CC_CUDA(c, cudaStreamSynchronize(c->stream));
-        for (int k = 0; k < 3; k++) al[k] = c->h_red[k];
+        al[0] = (double)c->h_red[0];
+        al[1] = lfx_value(c->h_red + 2);
+        al[2] = (double)c->h_red[1];
     } else {
         CC_CUDA(c, cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
         CC_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -613,27 +586,24 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     const int tmax = c->p.t_max;
     CC_TRY(cc_ensure(c, c->mom, (size_t)std::max<int64_t>(6 * E, 1), "adam moments"));
     CC_TRY(cc_ensure(c, c->bc, (size_t)std::max(tmax, 1), "bias corrections"));
-    CC_TRY(cc_ensure(c, c->partial_u, 2 * PGD_MAX_BLOCKS, "partials"));
-    CC_TRY(cc_ensure(c, c->partial_d, PGD_MAX_BLOCKS, "partials"));
     CC_TRY(cc_ensure(c, c->ctl, 1, "ctl"));
     CC_TRY(cc_ensure(c, c->trace_a, (size_t)tmax + 1, "trace"));
     CC_TRY(cc_ensure(c, c->trace_l, (size_t)tmax + 1, "trace"));
     CC_TRY(cc_ensure(c, c->trace_v, (size_t)tmax + 1, "trace"));
-    if (c->nranks > 1) CC_TRY(cc_ensure(c, c->red, 4, "allreduce buffer"));
+    if (c->nranks > 1) CC_TRY(cc_ensure(c, c->red, LFX_STATS, "allreduce buffer"));
     if (!c->k3work.p) {
         CC_TRY(cc_ensure(c, c->k3work, 2, "K3 work counters"));
         CC_CUDA(c, cudaMemsetAsync(c->k3work.p, 0, 2 * sizeof(unsigned long long), c->stream));
     }
     CC_TRY(cc_ensure(c, c->frozen, (size_t)std::max<int64_t>(E, 1), "frontier state"));
-    CC_TRY(cc_ensure(c, c->touch, 2 * (size_t)std::max<int64_t>(E, 1), "frontier touches"));
-    CC_TRY(cc_ensure(c, c->ggroup, 3 * (size_t)((std::max<int64_t>(E, 1) + 31) / 32), "frontier groups"));
+    CC_TRY(cc_ensure(c, c->inl, (size_t)std::max<int64_t>(E, 1), "frontier stamps"));
+    CC_TRY(cc_ensure(c, c->wlist, 2 * (size_t)std::max<int64_t>(E, 1), "frontier work lists"));
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
     CC_CUDA(c, cudaMemsetAsync(c->counters.p + 15, 0, sizeof(unsigned long long), c->stream));
     if (E > 0)
         CCL(c, k_frontier_init<<<(unsigned)((E + 255) / 256), 256, 0, c->stream>>>(
                    (uint32_t)E, reinterpret_cast<const unsigned long long*>(c->rowptr.p), c->rows.p, c->frozen.p,
-                   c->touch.p, c->touch.p + std::max<int64_t>(E, 1), c->ggroup.p,
-                   (uint32_t)((std::max<int64_t>(E, 1) + 31) / 32)));
+                   c->inl.p));
     // restart from P_hat^(0) (a previous cc_correct may have overwritten posA)
     if (Ea > 0)
         CCL(c, k_reset_pos<<<(unsigned)((Ea + 255) / 256), 256, 0, c->stream>>>(Ea, c->slotE.p, c->dec4.p,
@@ -655,7 +625,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
         CC_CUDA(c, cudaStreamSynchronize(c->stream));  // h goes out of scope
     }
     CCL(c, k_ctl_reset<<<1, 1, 0, c->stream>>>(c->ctl.p));
-    const int nb = pgd_blocks(std::max<int64_t>(E, c->E_cls[3] * 32));
+    const int nb = pgd_blocks(E);
     const int batch = c->p.graph_batch > 0 ? c->p.graph_batch : 16;
     PgdArgs a = make_args(c, 0);
     // initial statistics of P_hat^(0) for the report
