@@ -62,13 +62,13 @@ struct Ctl {
     int t_res;         // updates contained in the result buffer
     int converged;
     unsigned int ticket;
-    int pad;
+    int mode;          // K3 schedule of the next launch: 0 sweep, 1 sweep + build list, 2 list (pgd.cu)
     unsigned long long active;   // L_tight-active pairs at the last check
     unsigned long long violated; // pairs whose link status differs from the original (Eq. 1)
     double loss;
     unsigned int wn[2];  // frontier work-list lengths, by iteration parity (pgd.cu)
     unsigned int pad2[2];
-    unsigned long long acc[8];  // K3 launch statistics being summed (LossFx layout, below)
+    unsigned long long acc[10];  // K3 launch statistics being summed (LFX layout + schedule counts)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -81,6 +81,7 @@ struct Ctl {
 constexpr int LFX_UNIT = 140;
 constexpr int LFX_STATS = 8;
 
+template <int STRIDE = 1>
 __device__ __forceinline__ void lfx_add(unsigned long long* l, double d) {
     if (!(d > 0.0)) return;
     const unsigned long long bits = (unsigned long long)__double_as_longlong(d);
@@ -99,7 +100,7 @@ __device__ __forceinline__ void lfx_add(unsigned long long* l, double d) {
         if (k == k0) part = (m << off) & 0xFFFFFFFFull;
         else if (k == k0 + 1) part = (m >> (32 - off)) & 0xFFFFFFFFull;
         else if (k == k0 + 2 && off) part = (m >> (64 - off)) & 0xFFFFFFFFull;
-        l[k] += part;
+        if (part) l[k * STRIDE] += part;
     }
 }
 

@@ -36,6 +36,7 @@ namespace {
 constexpr int PGD_THREADS = 256;
 constexpr int PGD_MAX_BLOCKS = 148 * 8;
 constexpr int BATCH = 4;
+constexpr int NSTAT = LFX_STATS + 2;
 
 struct PgdArgs {
     uint32_t E;  // editable particles with rows (owned)
@@ -239,16 +240,24 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
         dst = (t & 1) ? a.pos1 : a.pos0;
     }
     const Th th = a.t;
-    unsigned long long st[LFX_STATS];  // active pairs, violated pairs, loss limbs (exact sums)
+    // active pairs, violated pairs, loss limbs (exact sums, LFX layout), then the schedule
+    // counts: editables left awake, row entries of editables that moved
+    // (per-thread counters live in shared memory: they are touched rarely and would otherwise
+    // cost 20 registers in this latency-bound kernel)
+    __shared__ unsigned long long st_sh[NSTAT][PGD_THREADS];
 #pragma unroll
-    for (int k = 0; k < LFX_STATS; k++) st[k] = 0ull;
+    for (int k = 0; k < NSTAT; k++) st_sh[k][threadIdx.x] = 0ull;
+    unsigned long long* st = &st_sh[0][threadIdx.x];  // st[k * PGD_THREADS] = counter k
     unsigned long long wk_e = 0, wk_n = 0;  // work done: editables updated, row entries evaluated
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 
-    // frontier: iteration t >= 3 walks only its work list (built by t-1); t >= 2 builds the next
+    // frontier schedule (ctl->mode, chosen by the previous launch): sweep all editables in index
+    // order while much of the set is awake; once little is, sweep once more while building the
+    // work list, then walk only the list (rebuilt every launch)
     const bool front = a.frontier && !a.count_only;
-    const bool lists = front && t >= 3;
-    const bool build = front && t >= 2;
+    const int mode = front ? ctl->mode : 0;
+    const bool lists = mode == 2;
+    const bool build = mode >= 1;
     const uint32_t* __restrict__ wcur = (t & 1) ? a.wl1 : a.wl0;
     uint32_t* __restrict__ wnext = (t & 1) ? a.wl0 : a.wl1;
     unsigned int* nnext = &ctl->wn[(t + 1) & 1];
@@ -258,9 +267,9 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
         if (ent & ENT_UPPER) {
             if (tm.kind) {
                 st[0]++;
-                lfx_add(st + 2, (double)tm.ee * (double)tm.ee);
+                lfx_add<PGD_THREADS>(st + 2 * PGD_THREADS, (double)tm.ee * (double)tm.ee);
             }
-            st[1] += tm.viol;
+            if (tm.viol) st[PGD_THREADS]++;
         }
     };
     auto replay_start = [&](uint32_t e, uint32_t& fz) {
@@ -300,6 +309,8 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
             const int flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);
             if (a.frontier) {
                 const bool awake = frontier_after(a, e, t, flags, any_active, fz);
+                if (awake) st[LFX_STATS * PGD_THREADS]++;
+                if (flags & 1) st[(LFX_STATS + 1) * PGD_THREADS] += k1 - k0;
                 if (build) {
                     if (awake) enqueue(a, wnext, nnext, e, t);
                     if (flags & 1)  // moved: every partner must be looked at in t+1
@@ -351,6 +362,8 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
             if (lane == 0) {
                 flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);
                 if (a.frontier) awake = frontier_after(a, e, t, flags, any_active, fz);
+                if (awake) st[LFX_STATS * PGD_THREADS]++;
+                if (flags & 1) st[(LFX_STATS + 1) * PGD_THREADS] += k1 - k0;
                 if (build && awake) enqueue(a, wnext, nnext, e, t);
             }
             flags = __shfl_sync(0xffffffffu, flags, 0);
@@ -392,19 +405,13 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
     }
 
     // ---- statistics: integer sums (LossFx), so the order of warps, blocks and ranks is free
-    __shared__ unsigned long long sh[PGD_THREADS / 32][LFX_STATS];
     __shared__ bool am_last;
-#pragma unroll
-    for (int k = 0; k < LFX_STATS; k++) {
-        unsigned long long v = st[k];
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-        if (lane == 0) sh[w][k] = v;
-    }
     __syncthreads();
-    if (threadIdx.x < LFX_STATS) {
+    for (int k = w; k < NSTAT; k += PGD_THREADS / 32) {  // warp w sums counters w, w+8, ...
         unsigned long long v = 0ull;
-        for (int k = 0; k < PGD_THREADS / 32; k++) v += sh[k][threadIdx.x];
-        if (v) atomicAdd(&ctl->acc[threadIdx.x], v);
+        for (int i = lane; i < PGD_THREADS; i += 32) v += st_sh[k][i];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0 && v) atomicAdd(&ctl->acc[k], v);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -416,8 +423,8 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
     if (!am_last || threadIdx.x != 0) return;
     // last block: every other block's sums are in ctl->acc
     __threadfence();
-    unsigned long long tot[LFX_STATS];
-    for (int k = 0; k < LFX_STATS; k++) {
+    unsigned long long tot[NSTAT];
+    for (int k = 0; k < NSTAT; k++) {
         tot[k] = ((volatile unsigned long long*)ctl->acc)[k];
         ctl->acc[k] = 0ull;
     }
@@ -427,7 +434,15 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
     ctl->violated = tv;
     ctl->loss = td;
     ctl->ticket = 0;
-    if (lists) ctl->wn[t & 1] = 0u;  // consumed: iteration t+1 fills it for t+2
+    if (front) {
+        // next schedule: lists pay off once the awake editables plus the partners of movers
+        // (what a list would hold) are a small part of E; any schedule gives the same result
+        const bool few = tot[LFX_STATS] + tot[LFX_STATS + 1] <= (unsigned long long)(a.E >> 3);
+        const int next = few ? (build ? 2 : 1) : 0;
+        ctl->mode = next;
+        if (lists) ctl->wn[t & 1] = 0u;               // consumed
+        if (next != 2) ctl->wn[(t + 1) & 1] = 0u;     // built but not used
+    }
     if (a.red) {  // multi-GPU: the decision waits for the allreduce (dist.cu k_decide)
         for (int k = 0; k < LFX_STATS; k++) a.red[k] = tot[k];
     } else if (!a.count_only) {
@@ -459,7 +474,8 @@ __global__ void k_ctl_reset(Ctl* ctl) {
     ctl->violated = 0;
     ctl->loss = 0.0;
     ctl->wn[0] = ctl->wn[1] = 0u;
-    for (int k = 0; k < LFX_STATS; k++) ctl->acc[k] = 0ull;
+    ctl->mode = 0;
+    for (int k = 0; k < 10; k++) ctl->acc[k] = 0ull;
 }
 
 __global__ void k_reset_pos(int64_t Ea, const uint32_t* __restrict__ slotE, const float4* __restrict__ dec4,
