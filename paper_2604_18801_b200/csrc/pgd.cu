@@ -35,8 +35,16 @@ namespace {
 
 constexpr int PGD_THREADS = 256;
 constexpr int PGD_MAX_BLOCKS = 148 * 8;
-constexpr int BATCH = 4;
 constexpr int NSTAT = LFX_STATS + 2;
+constexpr int NB = 4;         // row entries per lane per chunk
+constexpr int CH = 32 * NB;   // flattened row entries per warp chunk
+
+struct WarpSh {               // per-warp staging of K3's flattened row evaluation
+    float4 t[CH];             // term (px, py, pz, kind bits) of each chunk entry
+    float4 p[32];             // positions of the warp's 32 editables
+    unsigned long long k0[32];
+    uint32_t off[33];         // exclusive scan of the row lengths, off[32] = total
+};
 
 struct PgdArgs {
     uint32_t E;  // editable particles with rows (owned)
@@ -226,7 +234,7 @@ __device__ __forceinline__ void enqueue(const PgdArgs& a, uint32_t* __restrict__
     wnext[base + g.thread_rank()] = j;
 }
 
-__global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
+__global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
     Ctl* ctl = a.ctl;
     if (!a.count_only && *((volatile int*)&ctl->done)) return;
     const int t = a.count_only ? 0 : ctl->t + 1;
@@ -248,6 +256,7 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
 #pragma unroll
     for (int k = 0; k < NSTAT; k++) st_sh[k][threadIdx.x] = 0ull;
     unsigned long long* st = &st_sh[0][threadIdx.x];  // st[k * PGD_THREADS] = counter k
+    __shared__ WarpSh wsh[PGD_THREADS / 32];
     unsigned long long wk_e = 0, wk_n = 0;  // work done: editables updated, row entries evaluated
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 
@@ -277,119 +286,109 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
         return (fz != 0u && fz != FZ_NEVER) ? (int)fz + 1 : t;  // zero-gradient steps missed while frozen
     };
 
-    // ---- a row of <= 32 entries: one thread, partner loads batched ahead of the sequential sum
-    auto process_thread = [&](uint32_t e) {
-        uint32_t fz;
-        const int replay_from = replay_start(e, fz);
-        const float4 p = src[e];
-        const unsigned long long k0 = a.rowptr[e], k1 = a.rowptr[e + 1];
-        wk_e++;
-        wk_n += k1 - k0;
+    // ---- a warp takes 32 work items (editables 0..E-1 in order, or the work list), one per
+    // lane, and evaluates the concatenation of their rows flattened across the lanes: CH
+    // entries per chunk, NB independent row/partner loads per lane in flight, the terms parked
+    // in shared memory; then each lane sums its own row's terms in row order (the pinned order,
+    // R14) and applies Adam + projection to its editable.
+    WarpSh& ws = wsh[w];
+    const uint32_t gw = blockIdx.x * (PGD_THREADS / 32) + w, nw = gridDim.x * (PGD_THREADS / 32);
+    for (uint32_t base = gw * 32u; base < n_items; base += nw * 32u) {
+        const uint32_t idx = base + lane;
+        const bool valid = idx < n_items;
+        const uint32_t e = valid ? (lists ? wcur[idx] : idx) : 0u;
+        unsigned long long k0 = 0ull;
+        uint32_t len = 0u;
+        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) {
+            k0 = a.rowptr[e];
+            len = (uint32_t)(a.rowptr[e + 1] - k0);
+            p = src[e];
+        }
+        uint32_t off = len;  // exclusive scan of the row lengths over the warp
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, off, o);
+            if (lane >= o) off += v;
+        }
+        const uint32_t T = __shfl_sync(0xffffffffu, off, 31);
+        off -= len;
+        ws.off[lane] = off;
+        ws.k0[lane] = k0;
+        ws.p[lane] = p;
+        if (lane == 0) ws.off[32] = T;
+        __syncwarp();
+        if (valid) {
+            wk_e++;
+            wk_n += len;
+        }
         bool any_active = false;
         float gx = 0.0f, gy = 0.0f, gz = 0.0f;
-        for (unsigned long long kb = k0; kb < k1; kb += BATCH) {
-            uint32_t ent[BATCH];
-            float4 qq[BATCH];
+        for (uint32_t c = 0; c < T; c += CH) {
+            // evaluate entries c .. c+CH-1 of the flattened rows
+            uint32_t ent[NB];
+            int sg[NB];
 #pragma unroll
-            for (int i = 0; i < BATCH; i++) ent[i] = (kb + i < k1) ? a.rows[kb + i] : 0u;
-#pragma unroll
-            for (int i = 0; i < BATCH; i++)
-                if (kb + i < k1) qq[i] = src[ent[i] & ENT_IDX];
-#pragma unroll
-            for (int i = 0; i < BATCH; i++) {
-                if (kb + i < k1) {
-                    const Term tm = pair_term(p, qq[i], ent[i], th);
-                    count(tm, ent[i]);
-                    any_active |= tm.kind != 0;
-                    accumulate(gx, gy, gz, tm);
+            for (int j = 0; j < NB; j++) {
+                const uint32_t f = c + lane + 32u * j;
+                sg[j] = -1;
+                ent[j] = 0u;
+                if (f < T) {
+                    int lo = 0, hi = 31;  // the row holding f: largest s with off[s] <= f
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (ws.off[mid] <= f) lo = mid;
+                        else hi = mid - 1;
+                    }
+                    sg[j] = lo;
+                    ent[j] = a.rows[ws.k0[lo] + (f - ws.off[lo])];
                 }
             }
+            float4 q[NB];
+#pragma unroll
+            for (int j = 0; j < NB; j++)
+                if (sg[j] >= 0) q[j] = src[ent[j] & ENT_IDX];
+#pragma unroll
+            for (int j = 0; j < NB; j++) {
+                if (sg[j] >= 0) {
+                    const Term tm = pair_term(ws.p[sg[j]], q[j], ent[j], th);
+                    count(tm, ent[j]);
+                    ws.t[lane + 32 * j] = make_float4(tm.px, tm.py, tm.pz, __int_as_float(tm.kind));
+                }
+            }
+            __syncwarp();
+            // this lane's own row: its entries inside the chunk, in row order
+            const uint32_t f0 = max(off, c), f1 = min(off + len, c + CH);
+            for (uint32_t f = f0; f < f1; f++) {
+                const float4 u = ws.t[f - c];
+                Term tm;
+                tm.px = u.x;
+                tm.py = u.y;
+                tm.pz = u.z;
+                tm.kind = __float_as_int(u.w);
+                any_active |= tm.kind != 0;
+                accumulate(gx, gy, gz, tm);
+            }
+            __syncwarp();
         }
-        if (!a.count_only) {
+        if (valid && !a.count_only) {
+            uint32_t fz;
+            const int replay_from = replay_start(e, fz);
             const int flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);
             if (a.frontier) {
                 const bool awake = frontier_after(a, e, t, flags, any_active, fz);
                 if (awake) st[LFX_STATS * PGD_THREADS]++;
-                if (flags & 1) st[(LFX_STATS + 1) * PGD_THREADS] += k1 - k0;
+                if (flags & 1) st[(LFX_STATS + 1) * PGD_THREADS] += len;
                 if (build) {
                     if (awake) enqueue(a, wnext, nnext, e, t);
                     if (flags & 1)  // moved: every partner must be looked at in t+1
-                        for (unsigned long long k = k0; k < k1; k++) {
+                        for (unsigned long long k = k0; k < k0 + len; k++) {
                             const uint32_t j = a.rows[k] & ENT_IDX;
                             if (j < a.E) enqueue(a, wnext, nnext, j, t);
                         }
                 }
             }
         }
-    };
-
-    // ---- a row of > 32 entries: the whole warp, 32 entries per round, row-order accumulation
-    // through shuffles (the pinned order, identical on all lanes)
-    auto process_warp = [&](uint32_t e) {
-        uint32_t fz;
-        const int replay_from = replay_start(e, fz);
-        const float4 p = src[e];
-        const unsigned long long k0 = a.rowptr[e], k1 = a.rowptr[e + 1];
-        if (lane == 0) {
-            wk_e++;
-            wk_n += k1 - k0;
-        }
-        bool any_active = false;
-        float gx = 0.0f, gy = 0.0f, gz = 0.0f;
-        for (unsigned long long kb = k0; kb < k1; kb += 32) {
-            const unsigned long long k = kb + lane;
-            Term tm;
-            tm.kind = 0;
-            if (k < k1) {
-                const uint32_t ent = a.rows[k];
-                tm = pair_term(p, src[ent & ENT_IDX], ent, th);
-                count(tm, ent);
-            }
-            const int m = (int)min((unsigned long long)32, k1 - kb);
-            any_active |= __any_sync(0xffffffffu, tm.kind != 0);
-            for (int i = 0; i < m; i++) {
-                Term u;
-                u.kind = __shfl_sync(0xffffffffu, tm.kind, i);
-                u.px = __shfl_sync(0xffffffffu, tm.px, i);
-                u.py = __shfl_sync(0xffffffffu, tm.py, i);
-                u.pz = __shfl_sync(0xffffffffu, tm.pz, i);
-                accumulate(gx, gy, gz, u);
-            }
-        }
-        if (!a.count_only) {
-            int flags = 0;
-            bool awake = false;
-            if (lane == 0) {
-                flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);
-                if (a.frontier) awake = frontier_after(a, e, t, flags, any_active, fz);
-                if (awake) st[LFX_STATS * PGD_THREADS]++;
-                if (flags & 1) st[(LFX_STATS + 1) * PGD_THREADS] += k1 - k0;
-                if (build && awake) enqueue(a, wnext, nnext, e, t);
-            }
-            flags = __shfl_sync(0xffffffffu, flags, 0);
-            if (build && (flags & 1))
-                for (unsigned long long k = k0 + lane; k < k1; k += 32) {
-                    const uint32_t j = a.rows[k] & ENT_IDX;
-                    if (j < a.E) enqueue(a, wnext, nnext, j, t);
-                }
-        }
-    };
-
-    // ---- items: editables 0..E-1 (sweep) or the work list; a warp takes 32 consecutive items,
-    // short rows by their own lane, then each long row (numbered last, pairs.cu) by the warp
-    const uint32_t gw = blockIdx.x * (PGD_THREADS / 32) + w, nw = gridDim.x * (PGD_THREADS / 32);
-    for (uint32_t base = gw * 32u; base < n_items; base += nw * 32u) {
-        const uint32_t idx = base + lane;
-        uint32_t e = 0xFFFFFFFFu;
-        if (idx < n_items) e = lists ? wcur[idx] : idx;
-        const bool lng = e != 0xFFFFFFFFu && e >= a.e_short;
-        if (e != 0xFFFFFFFFu && !lng) process_thread(e);
-        unsigned lm = __ballot_sync(0xffffffffu, lng);
-        while (lm) {
-            const int sl = __ffs(lm) - 1;
-            process_warp(__shfl_sync(0xffffffffu, e, sl));
-            lm &= lm - 1;
-        }
+        __syncwarp();
     }
 
     // ---- work counters (integers: order-free), one atomic per warp
