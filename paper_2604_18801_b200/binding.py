@@ -60,7 +60,7 @@ class _Run(C.Structure):
 
 
 EXPORTS = ["cc_default_params", "cc_nccl_unique_id", "cc_create", "cc_destroy", "cc_last_error", "cc_build_cells",
-           "cc_find_vulnerable", "cc_get_pairs", "cc_correct", "cc_get_trace", "cc_fof_label", "cc_mcc",
+           "cc_find_vulnerable", "cc_get_pairs", "cc_correct", "cc_get_trace", "cc_get_schedule", "cc_fof_label", "cc_mcc",
            "cc_halo_sizes", "cc_hmf", "cc_kernel_stats", "cc_run"]
 
 _lib = None
@@ -94,6 +94,7 @@ def lib():
     L.cc_get_pairs.argtypes = [vp, vp, vp, vp, i64, P(i64)]
     L.cc_correct.argtypes = [vp, vp, vp, vp, P(_Corr)]
     L.cc_get_trace.argtypes = [vp, P(i64), P(d), P(i64), i64, P(i64)]
+    L.cc_get_schedule.argtypes = [vp, P(i64), i64, P(i64)]
     L.cc_fof_label.argtypes = [vp, C.c_int, vp, P(i64)]
     L.cc_mcc.argtypes = [vp, C.c_int, P(_Mcc)]
     L.cc_halo_sizes.argtypes = [vp, C.c_int, i64, P(i64), i64, P(i64)]
@@ -235,6 +236,13 @@ class Corrector:
                                         l.ctypes.data_as(C.POINTER(C.c_double)),
                                         v.ctypes.data_as(C.POINTER(C.c_int64)), a.shape[0], C.byref(n)))
         return a[: n.value], l[: n.value], v[: n.value]
+
+    def schedule(self):
+        """K3 schedule per iteration: (items processed, editables left awake, moved row entries)."""
+        n = C.c_int64()
+        a = np.zeros((self.params.t_max + 1, 3), np.int64)
+        self._chk(self.lib.cc_get_schedule(self.h, a.ctypes.data_as(C.POINTER(C.c_int64)), a.shape[0], C.byref(n)))
+        return a[: n.value]
 
     # S6
     def fof_label(self, which=CC_ORIG, labels=None):

@@ -274,7 +274,7 @@ void cc_destroy(cc_ctx* c) {
     cc_release(c, c->scratch_u32); cc_release(c, c->rowoff); cc_release(c, c->rowptr); cc_release(c, c->scratch_u64);
     cc_release(c, c->mom); cc_release(c, c->bc); 
     cc_release(c, c->counters); cc_release(c, c->ctl); cc_release(c, c->trace_a); cc_release(c, c->trace_l);
-    cc_release(c, c->trace_v); cc_release(c, c->parent_base); cc_release(c, c->rec32);
+    cc_release(c, c->trace_v); cc_release(c, c->trace_s); cc_release(c, c->parent_base); cc_release(c, c->rec32);
     cc_release(c, c->frozen); cc_release(c, c->inl); cc_release(c, c->k3work);
     cc_release(c, c->wlist);
     cc_release(c, c->tmp_bytes); cc_release(c, c->in_f); cc_release(c, c->in_gid);
@@ -439,6 +439,21 @@ cc_status cc_correct(cc_ctx* c, float* xo, float* yo, float* zo, cc_corr_info* i
     c->have_labels[CC_CORR] = 0;
     if (info) *info = local;
     return local.converged ? CC_OK : CC_NOT_CONVERGED;
+}
+
+cc_status cc_get_schedule(cc_ctx* c, int64_t* sched_h, int64_t cap, int64_t* n_h) {
+    CC_GUARD(c);
+    if (c->state < 3) return cc_fail(c, CC_E_STATE, "cc_correct first");
+    if (cap > 0 && !sched_h) return cc_fail(c, CC_E_ARG, "null output");
+    const int64_t n = std::min<int64_t>((int64_t)c->last_iters, (int64_t)c->p.t_max);
+    const int64_t k = std::min(n, cap);
+    if (k > 0) {
+        CC_CUDA(c, cudaMemcpyAsync(sched_h, c->trace_s.p, (size_t)(3 * k) * sizeof(long long), cudaMemcpyDeviceToHost,
+                                   c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    }
+    if (n_h) *n_h = n;
+    return CC_OK;
 }
 
 cc_status cc_get_trace(cc_ctx* c, int64_t* active_h, double* loss_h, int64_t* viol_h, int64_t cap, int64_t* n_h) {

@@ -44,6 +44,7 @@ struct WarpSh {               // per-warp staging of K3's flattened row evaluati
     float4 p[32];             // positions of the warp's 32 editables
     unsigned long long k0[32];
     uint32_t off[33];         // exclusive scan of the row lengths, off[32] = total
+    unsigned char seg[CH];    // owning lane of each chunk entry
 };
 
 struct PgdArgs {
@@ -67,6 +68,7 @@ struct PgdArgs {
     long long* trace_a;
     double* trace_l;
     long long* trace_v;
+    long long* trace_s;  // schedule per iteration: items, awake, moved entries
     int count_only;
     unsigned long long* red;  // multi-GPU: local statistics (LFX_STATS words) for the allreduce, else nullptr
     // frontier (exact active-set skipping): frozen[e] = 0 awake, FZ_NEVER never frozen (has a
@@ -145,16 +147,24 @@ __device__ __forceinline__ float project(float x, float o, float xip) {
     return x;
 }
 
+// IEEE a / b (round to nearest) with the zero-dividend case answered directly: the exact
+// result is a signed zero, and __fdiv_rn would take its slow path for it (frequent here: the
+// Adam moments of particles without active pairs are exactly 0).  b is finite and non-zero.
+__device__ __forceinline__ float div_rn(float a, float b) {
+    if (a == 0.0f) return __int_as_float((__float_as_int(a) ^ __float_as_int(b)) & 0x80000000);
+    return __fdiv_rn(a, b);
+}
+
 // Adam (or vanilla) step + projection of editable e, written to dst
 // one coordinate's Adam step in registers (R9); returns the new coordinate, sets |step|
 __device__ __forceinline__ float adam_reg(float x, float g, float& m, float& v, const PgdArgs& a, float bc1, float bc2,
                                           float& step_abs) {
     m = __fadd_rn(__fmul_rn(a.b1, m), __fmul_rn(a.omb1, g));
     v = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(a.omb2, __fmul_rn(g, g)));
-    const float mh = __fdiv_rn(m, bc1);
-    const float vh = __fdiv_rn(v, bc2);
-    const float den = __fadd_rn(__fsqrt_rn(vh), a.eps);
-    const float step = __fmul_rn(a.alpha, __fdiv_rn(mh, den));
+    const float mh = div_rn(m, bc1);
+    const float vh = div_rn(v, bc2);
+    const float den = __fadd_rn(vh == 0.0f ? vh : __fsqrt_rn(vh), a.eps);
+    const float step = __fmul_rn(a.alpha, div_rn(mh, den));
     step_abs = fabsf(step);
     return __fsub_rn(x, step);
 }
@@ -324,6 +334,10 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
         bool any_active = false;
         float gx = 0.0f, gy = 0.0f, gz = 0.0f;
         for (uint32_t c = 0; c < T; c += CH) {
+            // this lane's own row inside the chunk: mark which lane owns each position
+            const uint32_t f0 = max(off, c), f1 = min(off + len, c + CH);
+            for (uint32_t f = f0; f < f1; f++) ws.seg[f - c] = (unsigned char)lane;
+            __syncwarp();
             // evaluate entries c .. c+CH-1 of the flattened rows
             uint32_t ent[NB];
             int sg[NB];
@@ -333,14 +347,9 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
                 sg[j] = -1;
                 ent[j] = 0u;
                 if (f < T) {
-                    int lo = 0, hi = 31;  // the row holding f: largest s with off[s] <= f
-                    while (lo < hi) {
-                        const int mid = (lo + hi + 1) >> 1;
-                        if (ws.off[mid] <= f) lo = mid;
-                        else hi = mid - 1;
-                    }
-                    sg[j] = lo;
-                    ent[j] = a.rows[ws.k0[lo] + (f - ws.off[lo])];
+                    const int o = ws.seg[f - c];
+                    sg[j] = o;
+                    ent[j] = a.rows[ws.k0[o] + (f - ws.off[o])];
                 }
             }
             float4 q[NB];
@@ -357,7 +366,6 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
             }
             __syncwarp();
             // this lane's own row: its entries inside the chunk, in row order
-            const uint32_t f0 = max(off, c), f1 = min(off + len, c + CH);
             for (uint32_t f = f0; f < f1; f++) {
                 const float4 u = ws.t[f - c];
                 Term tm;
@@ -433,6 +441,11 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
     ctl->violated = tv;
     ctl->loss = td;
     ctl->ticket = 0;
+    if (!a.count_only && a.trace_s && t >= 1 && t <= a.t_max) {
+        a.trace_s[3 * (t - 1)] = (long long)n_items;
+        a.trace_s[3 * (t - 1) + 1] = (long long)tot[LFX_STATS];
+        a.trace_s[3 * (t - 1) + 2] = (long long)tot[LFX_STATS + 1];
+    }
     if (front) {
         // next schedule: lists pay off once the awake editables plus the partners of movers
         // (what a list would hold) are a small part of E; any schedule gives the same result
@@ -540,6 +553,7 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.trace_a = c->trace_a.p;
     a.trace_l = c->trace_l.p;
     a.trace_v = c->trace_v.p;
+    a.trace_s = c->trace_s.p;
     a.count_only = count_only;
     a.red = c->nranks > 1 ? c->red.p : nullptr;
     a.frontier = c->p.frontier ? 1 : 0;
@@ -605,6 +619,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     CC_TRY(cc_ensure(c, c->trace_a, (size_t)tmax + 1, "trace"));
     CC_TRY(cc_ensure(c, c->trace_l, (size_t)tmax + 1, "trace"));
     CC_TRY(cc_ensure(c, c->trace_v, (size_t)tmax + 1, "trace"));
+    CC_TRY(cc_ensure(c, c->trace_s, 3 * ((size_t)tmax + 1), "trace"));
     if (c->nranks > 1) CC_TRY(cc_ensure(c, c->red, LFX_STATS, "allreduce buffer"));
     if (!c->k3work.p) {
         CC_TRY(cc_ensure(c, c->k3work, 2, "K3 work counters"));

@@ -37,6 +37,13 @@ a, l, v = c.trace()
 idx = sorted(set([0, 1, 2, 5, 10, 20, 50, 100, 150, 200, 300, 500, 1000, 2000, 5000, len(a) - 1]))
 print("trace (t, active, loss, violated)", [(i, int(a[i]), float(l[i]), int(v[i])) for i in idx if i < len(a)],
       flush=True)
+sch = c.schedule()
+print("schedule (t, items, awake, moved entries):")
+for t in sorted(set(list(range(0, 12)) + list(range(12, len(sch), max(1, len(sch) // 40))) + [len(sch) - 1])):
+    if t < len(sch):
+        print("  ", t + 1, *sch[t].tolist())
+if os.environ.get("DIAG_ONLY_K3"):
+    sys.exit(0)
 m = c.mcc(cc.CC_CORR)
 md = c.mcc(cc.CC_DECOMP)
 print("mcc corr", m, "dec", md, flush=True)
