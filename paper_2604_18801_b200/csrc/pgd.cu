@@ -78,6 +78,8 @@ struct PgdArgs {
     int frontier;
     uint32_t* frozen;
     uint32_t* inl;    // inl[e] = iteration whose work list holds e (dedupe stamp)
+    uint32_t* mbits;  // 3 bitmaps of nwords words: editables that moved at iteration t (t % 3)
+    uint32_t nwords;
     uint32_t* wl0;    // work lists by iteration parity (E entries each)
     uint32_t* wl1;
     unsigned long long* errs;
@@ -129,14 +131,12 @@ __device__ __forceinline__ Term pair_term(const float4& p, const float4& q, uint
     return o;
 }
 
+// branch-free: an inactive term is (+0, +0, +0) (kind 2 has py = pz = +0), and g + 0 == g
+// exactly because g is never -0 (it starts at +0, and x + (-x) rounds to +0)
 __device__ __forceinline__ void accumulate(float& gx, float& gy, float& gz, const Term& tm) {
-    if (tm.kind == 1) {
-        gx = __fadd_rn(gx, tm.px);
-        gy = __fadd_rn(gy, tm.py);
-        gz = __fadd_rn(gz, tm.pz);
-    } else if (tm.kind == 2) {
-        gx = __fadd_rn(gx, tm.px);
-    }
+    gx = __fadd_rn(gx, tm.px);
+    gy = __fadd_rn(gy, tm.py);
+    gz = __fadd_rn(gz, tm.pz);
 }
 
 __device__ __forceinline__ float project(float x, float o, float xip) {
@@ -291,10 +291,13 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
             if (tm.viol) st[PGD_THREADS]++;
         }
     };
-    auto replay_start = [&](uint32_t e, uint32_t& fz) {
-        fz = front ? a.frozen[e] : 0u;
-        return (fz != 0u && fz != FZ_NEVER) ? (int)fz + 1 : t;  // zero-gradient steps missed while frozen
-    };
+    // moved-bitmaps: t writes mbits[t % 3], reads mbits[(t-1) % 3], clears mbits[(t+1) % 3]
+    uint32_t* __restrict__ mcur = a.mbits + (size_t)(t % 3) * a.nwords;
+    const uint32_t* __restrict__ mprev = a.mbits + (size_t)((t + 2) % 3) * a.nwords;
+    if (front) {
+        uint32_t* mclr = a.mbits + (size_t)((t + 1) % 3) * a.nwords;
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.nwords; i += gridDim.x * blockDim.x) mclr[i] = 0u;
+    }
 
     // ---- a warp takes 32 work items (editables 0..E-1 in order, or the work list), one per
     // lane, and evaluates the concatenation of their rows flattened across the lanes: CH
@@ -305,16 +308,31 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
     const uint32_t gw = blockIdx.x * (PGD_THREADS / 32) + w, nw = gridDim.x * (PGD_THREADS / 32);
     for (uint32_t base = gw * 32u; base < n_items; base += nw * 32u) {
         const uint32_t idx = base + lane;
-        const bool valid = idx < n_items;
+        bool valid = idx < n_items;
         const uint32_t e = valid ? (lists ? wcur[idx] : idx) : 0u;
         unsigned long long k0 = 0ull;
         uint32_t len = 0u;
-        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint32_t fz = 0u;
         if (valid) {
             k0 = a.rowptr[e];
             len = (uint32_t)(a.rowptr[e + 1] - k0);
-            p = src[e];
+            if (front) fz = a.frozen[e];
+            // sweep: a frozen editable none of whose partners moved at t-1 cannot change (its
+            // replay happens whenever it is next processed): skip it
+            if (!lists && fz != 0u && fz != FZ_NEVER) {
+                bool need = false;
+                for (unsigned long long k = k0; k < k0 + len && !need; k++) {
+                    const uint32_t j = a.rows[k] & ENT_IDX;
+                    need = (mprev[j >> 5] >> (j & 31)) & 1u;
+                }
+                if (!need) {
+                    valid = false;
+                    len = 0u;
+                }
+            }
         }
+        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) p = src[e];
         uint32_t off = len;  // exclusive scan of the row lengths over the warp
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t v = __shfl_up_sync(0xffffffffu, off, o);
@@ -378,10 +396,11 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
             }
             __syncwarp();
         }
+        int flags = 0;
         if (valid && !a.count_only) {
-            uint32_t fz;
-            const int replay_from = replay_start(e, fz);
-            const int flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);
+            const int replay_from = (fz != 0u && fz != FZ_NEVER) ? (int)fz + 1 : t;  // zero-gradient
+                                                                                      // steps missed while frozen
+            flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);
             if (a.frontier) {
                 const bool awake = frontier_after(a, e, t, flags, any_active, fz);
                 if (awake) st[LFX_STATS * PGD_THREADS]++;
@@ -394,6 +413,14 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
                             if (j < a.E) enqueue(a, wnext, nnext, j, t);
                         }
                 }
+            }
+        }
+        if (front) {  // movers of iteration t (read by the next sweep's frozen check)
+            const unsigned mv = __ballot_sync(0xffffffffu, (flags & 1) != 0);
+            if (!lists) {  // items base..base+31 are one whole bitmap word
+                if (lane == 0 && base < a.E) mcur[base >> 5] = mv;
+            } else if (flags & 1) {
+                atomicOr(&mcur[e >> 5], 1u << (e & 31));
             }
         }
         __syncwarp();
@@ -561,6 +588,8 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.errs = c->counters.p + 15;
     a.work = c->k3work.p;
     a.inl = c->inl.p;
+    a.mbits = c->mbits.p;
+    a.nwords = (uint32_t)((std::max<int64_t>(c->E, 1) + 31) / 32);
     a.wl0 = c->wlist.p;
     a.wl1 = c->wlist.p + std::max<int64_t>(c->E, 1);
     return a;
@@ -627,6 +656,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     }
     CC_TRY(cc_ensure(c, c->frozen, (size_t)std::max<int64_t>(E, 1), "frontier state"));
     CC_TRY(cc_ensure(c, c->inl, (size_t)std::max<int64_t>(E, 1), "frontier stamps"));
+    CC_TRY(cc_ensure(c, c->mbits, 3 * (size_t)((std::max<int64_t>(E, 1) + 31) / 32), "moved bitmaps"));
     CC_TRY(cc_ensure(c, c->wlist, 2 * (size_t)std::max<int64_t>(E, 1), "frontier work lists"));
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
     CC_CUDA(c, cudaMemsetAsync(c->counters.p + 15, 0, sizeof(unsigned long long), c->stream));
