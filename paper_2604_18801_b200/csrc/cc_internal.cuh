@@ -62,13 +62,11 @@ struct Ctl {
     int t_res;         // updates contained in the result buffer
     int converged;
     unsigned int ticket;
-    int mode;          // K3 schedule of the next launch: 0 sweep, 1 sweep + build list, 2 list (pgd.cu)
+    int pad;
     unsigned long long active;   // L_tight-active pairs at the last check
     unsigned long long violated; // pairs whose link status differs from the original (Eq. 1)
     double loss;
-    unsigned int wn[2];  // frontier work-list lengths, by iteration parity (pgd.cu)
-    unsigned int pad2[2];
-    unsigned long long acc[10];  // K3 launch statistics being summed (LFX layout + schedule counts)
+    unsigned long long acc[12];  // K3 launch statistics being summed (LFX layout + schedule counts)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -179,7 +177,7 @@ struct cc_ctx {
     cc::DBuf<unsigned long long> counters;
     cc::DBuf<cc::Ctl> ctl;
     cc::DBuf<long long> trace_a, trace_v, trace_s;
-    cc::DBuf<uint32_t> frozen, inl, wlist, mbits;  // K3 frontier state, work lists, moved bitmaps (pgd.cu)
+    cc::DBuf<uint32_t> frozen, fbits;  // K3 frontier: last-processed iteration, awake/touched bitmaps (pgd.cu)
     cc::DBuf<unsigned long long> k3work;  // K3 work totals (editables updated, entries evaluated)
     int64_t E_cls[4] = {0, 0, 0, 0};  // editables per K3 work class (row_class), numbered class-major
     cc::DBuf<double> trace_l;

@@ -35,7 +35,7 @@ namespace {
 
 constexpr int PGD_THREADS = 256;
 constexpr int PGD_MAX_BLOCKS = 148 * 8;
-constexpr int NSTAT = LFX_STATS + 2;
+constexpr int NSTAT = LFX_STATS + 3;
 constexpr int NB = 4;         // row entries per lane per chunk
 constexpr int CH = 32 * NB;   // flattened row entries per warp chunk
 
@@ -43,8 +43,9 @@ struct WarpSh {               // per-warp staging of K3's flattened row evaluati
     float4 t[CH];             // term (px, py, pz, kind bits) of each chunk entry
     float4 p[32];             // positions of the warp's 32 editables
     unsigned long long k0[32];
-    uint32_t off[33];         // exclusive scan of the row lengths, off[32] = total
+    uint32_t off[32];         // exclusive scan of the row lengths
     unsigned char seg[CH];    // owning lane of each chunk entry
+    uint32_t aw[32];          // awake bits of the current 32-word range
 };
 
 struct PgdArgs {
@@ -77,11 +78,9 @@ struct PgdArgs {
     // at t-1 (built by t-1); errs counts unsafe freezes
     int frontier;
     uint32_t* frozen;
-    uint32_t* inl;    // inl[e] = iteration whose work list holds e (dedupe stamp)
-    uint32_t* mbits;  // 3 bitmaps of nwords words: editables that moved at iteration t (t % 3)
+    uint32_t* abits;  // 2 bitmaps of nwords words: editables awake after an iteration
+    uint32_t* ubits;  // 3 bitmaps: editables touched (a partner moved) in an iteration
     uint32_t nwords;
-    uint32_t* wl0;    // work lists by iteration parity (E entries each)
-    uint32_t* wl1;
     unsigned long long* errs;
     unsigned long long* work;  // running totals: [0] editables updated, [1] row entries evaluated
 };
@@ -231,17 +230,10 @@ __device__ __forceinline__ bool frontier_after(const PgdArgs& a, uint32_t e, int
     return !freeze;
 }
 
-// queue editable j for iteration t+1 (once: the stamp dedupes), warp-aggregated append
-__device__ __forceinline__ void enqueue(const PgdArgs& a, uint32_t* __restrict__ wnext, unsigned int* __restrict__ nnext,
-                                        uint32_t j, int t) {
-    const uint32_t stamp = (uint32_t)(t + 1);
-    if (*((volatile uint32_t*)&a.inl[j]) == stamp) return;
-    if (atomicExch(&a.inl[j], stamp) == stamp) return;
-    cg::coalesced_group g = cg::coalesced_threads();
-    unsigned int base = 0;
-    if (g.thread_rank() == 0) base = atomicAdd(nnext, g.size());
-    base = g.shfl(base, 0);
-    wnext[base + g.thread_rank()] = j;
+// a moved editable marks partner j (owned) for iteration t+1 in the touched bitmap
+__device__ __forceinline__ void touch(uint32_t* __restrict__ unext, uint32_t j) {
+    const uint32_t bit = 1u << (j & 31);
+    if (!(*((volatile uint32_t*)&unext[j >> 5]) & bit)) atomicOr(&unext[j >> 5], bit);
 }
 
 __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
@@ -258,10 +250,10 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
         dst = (t & 1) ? a.pos1 : a.pos0;
     }
     const Th th = a.t;
-    // active pairs, violated pairs, loss limbs (exact sums, LFX layout), then the schedule
-    // counts: editables left awake, row entries of editables that moved
-    // (per-thread counters live in shared memory: they are touched rarely and would otherwise
-    // cost 20 registers in this latency-bound kernel)
+    // statistics: active pairs, violated pairs, loss limbs (exact sums, LFX layout), then the
+    // schedule counts: editables left awake, row entries of editables that moved, editables
+    // processed.  Per-thread counters live in shared memory (touched rarely; registers are the
+    // occupancy limit of this latency-bound kernel).
     __shared__ unsigned long long st_sh[NSTAT][PGD_THREADS];
 #pragma unroll
     for (int k = 0; k < NSTAT; k++) st_sh[k][threadIdx.x] = 0ull;
@@ -269,18 +261,23 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
     __shared__ WarpSh wsh[PGD_THREADS / 32];
     unsigned long long wk_e = 0, wk_n = 0;  // work done: editables updated, row entries evaluated
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    WarpSh& ws = wsh[w];
 
-    // frontier schedule (ctl->mode, chosen by the previous launch): sweep all editables in index
-    // order while much of the set is awake; once little is, sweep once more while building the
-    // work list, then walk only the list (rebuilt every launch)
+    // frontier (exact active-set skipping): from iteration 2 on, only the editables awake after
+    // t-1 or touched (a partner moved at t-1) are processed.  Bitmaps over the E editables:
+    // awake A[t & 1] read / A[(t+1) & 1] written whole words; touched U[t % 3] read /
+    // U[(t+1) % 3] set by atomics / U[(t+2) % 3] cleared for the next launch.
     const bool front = a.frontier && !a.count_only;
-    const int mode = front ? ctl->mode : 0;
-    const bool lists = mode == 2;
-    const bool build = mode >= 1;
-    const uint32_t* __restrict__ wcur = (t & 1) ? a.wl1 : a.wl0;
-    uint32_t* __restrict__ wnext = (t & 1) ? a.wl0 : a.wl1;
-    unsigned int* nnext = &ctl->wn[(t + 1) & 1];
-    const uint32_t n_items = lists ? ctl->wn[t & 1] : a.E;
+    const bool select = front && t >= 2;
+    const uint32_t nw32 = a.nwords;
+    const uint32_t* __restrict__ acur = a.abits + (size_t)(t & 1) * nw32;
+    uint32_t* __restrict__ anext = a.abits + (size_t)((t + 1) & 1) * nw32;
+    const uint32_t* __restrict__ ucur = a.ubits + (size_t)(t % 3) * nw32;
+    uint32_t* __restrict__ unext = a.ubits + (size_t)((t + 1) % 3) * nw32;
+    if (front) {
+        uint32_t* uclr = a.ubits + (size_t)((t + 2) % 3) * nw32;
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nw32; i += gridDim.x * blockDim.x) uclr[i] = 0u;
+    }
 
     auto count = [&](const Term& tm, uint32_t ent) {  // each pair once, at its lower-gid endpoint
         if (ent & ENT_UPPER) {
@@ -291,48 +288,25 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
             if (tm.viol) st[PGD_THREADS]++;
         }
     };
-    // moved-bitmaps: t writes mbits[t % 3], reads mbits[(t-1) % 3], clears mbits[(t+1) % 3]
-    uint32_t* __restrict__ mcur = a.mbits + (size_t)(t % 3) * a.nwords;
-    const uint32_t* __restrict__ mprev = a.mbits + (size_t)((t + 2) % 3) * a.nwords;
-    if (front) {
-        uint32_t* mclr = a.mbits + (size_t)((t + 1) % 3) * a.nwords;
-        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.nwords; i += gridDim.x * blockDim.x) mclr[i] = 0u;
-    }
 
-    // ---- a warp takes 32 work items (editables 0..E-1 in order, or the work list), one per
-    // lane, and evaluates the concatenation of their rows flattened across the lanes: CH
-    // entries per chunk, NB independent row/partner loads per lane in flight, the terms parked
-    // in shared memory; then each lane sums its own row's terms in row order (the pinned order,
-    // R14) and applies Adam + projection to its editable.
-    WarpSh& ws = wsh[w];
-    const uint32_t gw = blockIdx.x * (PGD_THREADS / 32) + w, nw = gridDim.x * (PGD_THREADS / 32);
-    for (uint32_t base = gw * 32u; base < n_items; base += nw * 32u) {
-        const uint32_t idx = base + lane;
-        bool valid = idx < n_items;
-        const uint32_t e = valid ? (lists ? wcur[idx] : idx) : 0u;
+    // ---- one batch: up to 32 editables (one per lane, `valid`).  The concatenation of their
+    // rows is evaluated flattened across the lanes: CH entries per chunk, NB independent
+    // row/partner loads per lane in flight, the terms parked in shared memory; then each lane
+    // sums its own row's terms in row order (the pinned order, R14) and applies Adam + the
+    // projection to its editable.  Returns whether the lane's editable stays awake.
+    auto process_batch = [&](const uint32_t e, const bool valid) -> bool {
         unsigned long long k0 = 0ull;
-        uint32_t len = 0u;
-        uint32_t fz = 0u;
+        uint32_t len = 0u, fz = 0u;
+        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
         if (valid) {
             k0 = a.rowptr[e];
             len = (uint32_t)(a.rowptr[e + 1] - k0);
+            p = src[e];
             if (front) fz = a.frozen[e];
-            // sweep: a frozen editable none of whose partners moved at t-1 cannot change (its
-            // replay happens whenever it is next processed): skip it
-            if (!lists && fz != 0u && fz != FZ_NEVER) {
-                bool need = false;
-                for (unsigned long long k = k0; k < k0 + len && !need; k++) {
-                    const uint32_t j = a.rows[k] & ENT_IDX;
-                    need = (mprev[j >> 5] >> (j & 31)) & 1u;
-                }
-                if (!need) {
-                    valid = false;
-                    len = 0u;
-                }
-            }
+            wk_e++;
+            wk_n += len;
+            st[(LFX_STATS + 2) * PGD_THREADS]++;
         }
-        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid) p = src[e];
         uint32_t off = len;  // exclusive scan of the row lengths over the warp
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t v = __shfl_up_sync(0xffffffffu, off, o);
@@ -343,12 +317,7 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
         ws.off[lane] = off;
         ws.k0[lane] = k0;
         ws.p[lane] = p;
-        if (lane == 0) ws.off[32] = T;
         __syncwarp();
-        if (valid) {
-            wk_e++;
-            wk_n += len;
-        }
         bool any_active = false;
         float gx = 0.0f, gy = 0.0f, gz = 0.0f;
         for (uint32_t c = 0; c < T; c += CH) {
@@ -356,7 +325,6 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
             const uint32_t f0 = max(off, c), f1 = min(off + len, c + CH);
             for (uint32_t f = f0; f < f1; f++) ws.seg[f - c] = (unsigned char)lane;
             __syncwarp();
-            // evaluate entries c .. c+CH-1 of the flattened rows
             uint32_t ent[NB];
             int sg[NB];
 #pragma unroll
@@ -383,8 +351,7 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
                 }
             }
             __syncwarp();
-            // this lane's own row: its entries inside the chunk, in row order
-            for (uint32_t f = f0; f < f1; f++) {
+            for (uint32_t f = f0; f < f1; f++) {  // own row, row order
                 const float4 u = ws.t[f - c];
                 Term tm;
                 tm.px = u.x;
@@ -397,32 +364,83 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
             __syncwarp();
         }
         int flags = 0;
+        bool awake = false;
         if (valid && !a.count_only) {
             const int replay_from = (fz != 0u && fz != FZ_NEVER) ? (int)fz + 1 : t;  // zero-gradient
-                                                                                      // steps missed while frozen
-            flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);
+            flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);               // steps missed while frozen
             if (a.frontier) {
-                const bool awake = frontier_after(a, e, t, flags, any_active, fz);
+                awake = frontier_after(a, e, t, flags, any_active, fz);
                 if (awake) st[LFX_STATS * PGD_THREADS]++;
                 if (flags & 1) st[(LFX_STATS + 1) * PGD_THREADS] += len;
-                if (build) {
-                    if (awake) enqueue(a, wnext, nnext, e, t);
-                    if (flags & 1)  // moved: every partner must be looked at in t+1
-                        for (unsigned long long k = k0; k < k0 + len; k++) {
-                            const uint32_t j = a.rows[k] & ENT_IDX;
-                            if (j < a.E) enqueue(a, wnext, nnext, j, t);
-                        }
+            }
+        }
+        if (front) {  // a mover touches its owned partners for t+1
+            const bool moved = (flags & 1) != 0;
+            if (moved && len <= 32u)
+                for (unsigned long long k = k0; k < k0 + len; k++) {
+                    const uint32_t j = a.rows[k] & ENT_IDX;
+                    if (j < a.E) touch(unext, j);
+                }
+            unsigned lm = __ballot_sync(0xffffffffu, moved && len > 32u);
+            while (lm) {  // long rows: the whole warp
+                const int sl = __ffs(lm) - 1;
+                lm &= lm - 1;
+                const unsigned long long kb = __shfl_sync(0xffffffffu, k0, sl);
+                const uint32_t ln = __shfl_sync(0xffffffffu, len, sl);
+                for (uint32_t i = lane; i < ln; i += 32) {
+                    const uint32_t j = a.rows[kb + i] & ENT_IDX;
+                    if (j < a.E) touch(unext, j);
                 }
             }
         }
-        if (front) {  // movers of iteration t (read by the next sweep's frozen check)
-            const unsigned mv = __ballot_sync(0xffffffffu, (flags & 1) != 0);
-            if (!lists) {  // items base..base+31 are one whole bitmap word
-                if (lane == 0 && base < a.E) mcur[base >> 5] = mv;
-            } else if (flags & 1) {
-                atomicOr(&mcur[e >> 5], 1u << (e & 31));
+        return awake;
+    };
+
+    // ---- work items: a warp takes a range of 32 bitmap words (1024 editables) at a time and
+    // processes its selected editables in index order, 32 per batch
+    const uint32_t gw = blockIdx.x * (PGD_THREADS / 32) + w, nwarps = gridDim.x * (PGD_THREADS / 32);
+    const uint32_t nranges = (nw32 + 31) / 32;
+    for (uint32_t r = gw; r < nranges; r += nwarps) {
+        const uint32_t wi = r * 32u + lane;
+        uint32_t mask = 0u;
+        if (wi < nw32) {
+            if (select) {
+                mask = acur[wi] | ucur[wi];
+            } else {
+                const uint32_t e0 = wi * 32u;
+                mask = (a.E - e0 >= 32u) ? 0xFFFFFFFFu : ((1u << (a.E - e0)) - 1u);
             }
         }
+        const uint32_t cnt = __popc(mask);
+        uint32_t pre = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += v;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, pre, 31);
+        pre -= cnt;
+        ws.aw[lane] = 0u;
+        __syncwarp();
+        for (uint32_t b0 = 0; b0 < total; b0 += 32u) {
+            const uint32_t k = b0 + lane;
+            int lo = 0, hi = 31;  // the word holding selected item k: largest s with pre[s] <= k
+#pragma unroll
+            for (int it = 0; it < 5; it++) {
+                const int mid = (lo + hi + 1) >> 1;
+                const uint32_t pm = __shfl_sync(0xffffffffu, pre, mid);
+                if (pm <= k) lo = mid;
+                else hi = mid - 1;
+            }
+            const uint32_t ms = __shfl_sync(0xffffffffu, mask, lo);
+            const uint32_t ps = __shfl_sync(0xffffffffu, pre, lo);
+            const bool valid = k < total;
+            uint32_t e = 0u;
+            if (valid) e = (r * 32u + (uint32_t)lo) * 32u + __fns(ms, 0u, (int)(k - ps) + 1);
+            const bool awake = process_batch(e, valid);
+            if (front && awake) atomicOr(&ws.aw[lo], 1u << (e & 31));
+            __syncwarp();
+        }
+        if (front && wi < nw32) anext[wi] = ws.aw[lane];
         __syncwarp();
     }
 
@@ -438,7 +456,7 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
         }
     }
 
-    // ---- statistics: integer sums (LossFx), so the order of warps, blocks and ranks is free
+    // ---- statistics: integer sums (LFX), so the order of warps, blocks and ranks is free
     __shared__ bool am_last;
     __syncthreads();
     for (int k = w; k < NSTAT; k += PGD_THREADS / 32) {  // warp w sums counters w, w+8, ...
@@ -469,18 +487,9 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
     ctl->loss = td;
     ctl->ticket = 0;
     if (!a.count_only && a.trace_s && t >= 1 && t <= a.t_max) {
-        a.trace_s[3 * (t - 1)] = (long long)n_items;
+        a.trace_s[3 * (t - 1)] = (long long)tot[LFX_STATS + 2];
         a.trace_s[3 * (t - 1) + 1] = (long long)tot[LFX_STATS];
         a.trace_s[3 * (t - 1) + 2] = (long long)tot[LFX_STATS + 1];
-    }
-    if (front) {
-        // next schedule: lists pay off once the awake editables plus the partners of movers
-        // (what a list would hold) are a small part of E; any schedule gives the same result
-        const bool few = tot[LFX_STATS] + tot[LFX_STATS + 1] <= (unsigned long long)(a.E >> 3);
-        const int next = few ? (build ? 2 : 1) : 0;
-        ctl->mode = next;
-        if (lists) ctl->wn[t & 1] = 0u;               // consumed
-        if (next != 2) ctl->wn[(t + 1) & 1] = 0u;     // built but not used
     }
     if (a.red) {  // multi-GPU: the decision waits for the allreduce (dist.cu k_decide)
         for (int k = 0; k < LFX_STATS; k++) a.red[k] = tot[k];
@@ -512,9 +521,7 @@ __global__ void k_ctl_reset(Ctl* ctl) {
     ctl->active = 0;
     ctl->violated = 0;
     ctl->loss = 0.0;
-    ctl->wn[0] = ctl->wn[1] = 0u;
-    ctl->mode = 0;
-    for (int k = 0; k < 10; k++) ctl->acc[k] = 0ull;
+    for (int k = 0; k < 12; k++) ctl->acc[k] = 0ull;
 }
 
 __global__ void k_reset_pos(int64_t Ea, const uint32_t* __restrict__ slotE, const float4* __restrict__ dec4,
@@ -587,25 +594,21 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.frozen = c->frozen.p;
     a.errs = c->counters.p + 15;
     a.work = c->k3work.p;
-    a.inl = c->inl.p;
-    a.mbits = c->mbits.p;
     a.nwords = (uint32_t)((std::max<int64_t>(c->E, 1) + 31) / 32);
-    a.wl0 = c->wlist.p;
-    a.wl1 = c->wlist.p + std::max<int64_t>(c->E, 1);
+    a.abits = c->fbits.p;
+    a.ubits = c->fbits.p + 2 * (size_t)a.nwords;
     return a;
 }
 
 // frontier state at the start of cc_correct: everyone awake; rows with a ghost partner
 // (multi-GPU) are never frozen, so moves of ghosts (refreshed each iteration) are always seen
 __global__ void k_frontier_init(uint32_t E, const unsigned long long* __restrict__ rowptr,
-                                const uint32_t* __restrict__ rows, uint32_t* __restrict__ frozen,
-                                uint32_t* __restrict__ inl) {
+                                const uint32_t* __restrict__ rows, uint32_t* __restrict__ frozen) {
     const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
     bool ghost = false;
     for (unsigned long long k = rowptr[e]; k < rowptr[e + 1]; k++) ghost |= (rows[k] & ENT_IDX) >= E;
     frozen[e] = ghost ? FZ_NEVER : 0u;
-    inl[e] = 0u;
 }
 
 int pgd_blocks(int64_t E) {
@@ -655,15 +658,14 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
         CC_CUDA(c, cudaMemsetAsync(c->k3work.p, 0, 2 * sizeof(unsigned long long), c->stream));
     }
     CC_TRY(cc_ensure(c, c->frozen, (size_t)std::max<int64_t>(E, 1), "frontier state"));
-    CC_TRY(cc_ensure(c, c->inl, (size_t)std::max<int64_t>(E, 1), "frontier stamps"));
-    CC_TRY(cc_ensure(c, c->mbits, 3 * (size_t)((std::max<int64_t>(E, 1) + 31) / 32), "moved bitmaps"));
-    CC_TRY(cc_ensure(c, c->wlist, 2 * (size_t)std::max<int64_t>(E, 1), "frontier work lists"));
+    const size_t nwords = (size_t)((std::max<int64_t>(E, 1) + 31) / 32);
+    CC_TRY(cc_ensure(c, c->fbits, 5 * nwords, "frontier bitmaps"));
+    CC_CUDA(c, cudaMemsetAsync(c->fbits.p, 0, 5 * nwords * sizeof(uint32_t), c->stream));
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
     CC_CUDA(c, cudaMemsetAsync(c->counters.p + 15, 0, sizeof(unsigned long long), c->stream));
     if (E > 0)
         CCL(c, k_frontier_init<<<(unsigned)((E + 255) / 256), 256, 0, c->stream>>>(
-                   (uint32_t)E, reinterpret_cast<const unsigned long long*>(c->rowptr.p), c->rows.p, c->frozen.p,
-                   c->inl.p));
+                   (uint32_t)E, reinterpret_cast<const unsigned long long*>(c->rowptr.p), c->rows.p, c->frozen.p));
     // restart from P_hat^(0) (a previous cc_correct may have overwritten posA)
     if (Ea > 0)
         CCL(c, k_reset_pos<<<(unsigned)((Ea + 255) / 256), 256, 0, c->stream>>>(Ea, c->slotE.p, c->dec4.p,
