@@ -62,7 +62,9 @@ struct Ctl {
     int t_res;         // updates contained in the result buffer
     int converged;
     unsigned int ticket;
-    int pad;
+    int sel;           // K3: this launch processes only the bitmap-selected editables (pgd.cu)
+    int bld;           // K3: this launch builds the awake/touched bitmaps
+    int pad3;
     unsigned long long active;   // L_tight-active pairs at the last check
     unsigned long long violated; // pairs whose link status differs from the original (Eq. 1)
     double loss;

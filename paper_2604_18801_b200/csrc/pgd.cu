@@ -130,13 +130,6 @@ __device__ __forceinline__ Term pair_term(const float4& p, const float4& q, uint
     return o;
 }
 
-// branch-free: an inactive term is (+0, +0, +0) (kind 2 has py = pz = +0), and g + 0 == g
-// exactly because g is never -0 (it starts at +0, and x + (-x) rounds to +0)
-__device__ __forceinline__ void accumulate(float& gx, float& gy, float& gz, const Term& tm) {
-    gx = __fadd_rn(gx, tm.px);
-    gy = __fadd_rn(gy, tm.py);
-    gz = __fadd_rn(gz, tm.pz);
-}
 
 __device__ __forceinline__ float project(float x, float o, float xip) {
     const float lo = __fsub_ru(o, xip);
@@ -267,14 +260,18 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
     // t-1 or touched (a partner moved at t-1) are processed.  Bitmaps over the E editables:
     // awake A[t & 1] read / A[(t+1) & 1] written whole words; touched U[t % 3] read /
     // U[(t+1) % 3] set by atomics / U[(t+2) % 3] cleared for the next launch.
+    // Building the bitmaps costs a random atomic per partner of every mover, so launch t builds
+    // them only when the previous launch saw few awake editables and movers (ctl->bld); launch
+    // t+1 selects iff launch t built (ctl->sel), else it processes every editable.
     const bool front = a.frontier && !a.count_only;
-    const bool select = front && t >= 2;
+    const bool select = front && ctl->sel;
+    const bool build = front && ctl->bld;
     const uint32_t nw32 = a.nwords;
     const uint32_t* __restrict__ acur = a.abits + (size_t)(t & 1) * nw32;
     uint32_t* __restrict__ anext = a.abits + (size_t)((t + 1) & 1) * nw32;
     const uint32_t* __restrict__ ucur = a.ubits + (size_t)(t % 3) * nw32;
     uint32_t* __restrict__ unext = a.ubits + (size_t)((t + 1) % 3) * nw32;
-    if (front) {
+    if (front) {  // (cleared even when not building: a later build must start from zero)
         uint32_t* uclr = a.ubits + (size_t)((t + 2) % 3) * nw32;
         for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nw32; i += gridDim.x * blockDim.x) uclr[i] = 0u;
     }
@@ -321,9 +318,13 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
         bool any_active = false;
         float gx = 0.0f, gy = 0.0f, gz = 0.0f;
         for (uint32_t c = 0; c < T; c += CH) {
-            // this lane's own row inside the chunk: mark which lane owns each position
+            // this lane's own row inside the chunk: mark which lane owns each position (unless one
+            // row covers the whole chunk, the long-row case)
             const uint32_t f0 = max(off, c), f1 = min(off + len, c + CH);
-            for (uint32_t f = f0; f < f1; f++) ws.seg[f - c] = (unsigned char)lane;
+            const unsigned cover = __ballot_sync(0xffffffffu, f0 == c && f1 == min(c + CH, T) && f1 > f0);
+            const int whole = cover ? __ffs(cover) - 1 : -1;
+            if (whole < 0)
+                for (uint32_t f = f0; f < f1; f++) ws.seg[f - c] = (unsigned char)lane;
             __syncwarp();
             uint32_t ent[NB];
             int sg[NB];
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
                 sg[j] = -1;
                 ent[j] = 0u;
                 if (f < T) {
-                    const int o = ws.seg[f - c];
+                    const int o = whole >= 0 ? whole : ws.seg[f - c];
                     sg[j] = o;
                     ent[j] = a.rows[ws.k0[o] + (f - ws.off[o])];
                 }
@@ -351,15 +352,28 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
                 }
             }
             __syncwarp();
-            for (uint32_t f = f0; f < f1; f++) {  // own row, row order
+            // own row, in row order (R14).  Branch-free: an inactive term is (+0, +0, +0) and a
+            // coincident one (+-2e, +0, +0); g + 0 == g exactly since g is never -0 (it starts at
+            // +0 and x + (-x) rounds to +0).  Loads of 4 terms are issued ahead of the sums.
+            uint32_t f = f0;
+            for (; f + 4 <= f1; f += 4) {
+                float4 u[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) u[i] = ws.t[f + i - c];
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    any_active |= __float_as_int(u[i].w) != 0;
+                    gx = __fadd_rn(gx, u[i].x);
+                    gy = __fadd_rn(gy, u[i].y);
+                    gz = __fadd_rn(gz, u[i].z);
+                }
+            }
+            for (; f < f1; f++) {
                 const float4 u = ws.t[f - c];
-                Term tm;
-                tm.px = u.x;
-                tm.py = u.y;
-                tm.pz = u.z;
-                tm.kind = __float_as_int(u.w);
-                any_active |= tm.kind != 0;
-                accumulate(gx, gy, gz, tm);
+                any_active |= __float_as_int(u.w) != 0;
+                gx = __fadd_rn(gx, u.x);
+                gy = __fadd_rn(gy, u.y);
+                gz = __fadd_rn(gz, u.z);
             }
             __syncwarp();
         }
@@ -374,7 +388,7 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
                 if (flags & 1) st[(LFX_STATS + 1) * PGD_THREADS] += len;
             }
         }
-        if (front) {  // a mover touches its owned partners for t+1
+        if (build) {  // a mover touches its owned partners for t+1
             const bool moved = (flags & 1) != 0;
             if (moved && len <= 32u)
                 for (unsigned long long k = k0; k < k0 + len; k++) {
@@ -437,10 +451,10 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
             uint32_t e = 0u;
             if (valid) e = (r * 32u + (uint32_t)lo) * 32u + __fns(ms, 0u, (int)(k - ps) + 1);
             const bool awake = process_batch(e, valid);
-            if (front && awake) atomicOr(&ws.aw[lo], 1u << (e & 31));
+            if (build && awake) atomicOr(&ws.aw[lo], 1u << (e & 31));
             __syncwarp();
         }
-        if (front && wi < nw32) anext[wi] = ws.aw[lane];
+        if (build && wi < nw32) anext[wi] = ws.aw[lane];
         __syncwarp();
     }
 
@@ -491,6 +505,10 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
         a.trace_s[3 * (t - 1) + 1] = (long long)tot[LFX_STATS];
         a.trace_s[3 * (t - 1) + 2] = (long long)tot[LFX_STATS + 1];
     }
+    if (front) {
+        ctl->sel = build ? 1 : 0;
+        ctl->bld = (tot[LFX_STATS] + tot[LFX_STATS + 1] <= (unsigned long long)(a.E >> 2)) ? 1 : 0;
+    }
     if (a.red) {  // multi-GPU: the decision waits for the allreduce (dist.cu k_decide)
         for (int k = 0; k < LFX_STATS; k++) a.red[k] = tot[k];
     } else if (!a.count_only) {
@@ -522,6 +540,8 @@ __global__ void k_ctl_reset(Ctl* ctl) {
     ctl->violated = 0;
     ctl->loss = 0.0;
     for (int k = 0; k < 12; k++) ctl->acc[k] = 0ull;
+    ctl->sel = 0;
+    ctl->bld = 0;
 }
 
 __global__ void k_reset_pos(int64_t Ea, const uint32_t* __restrict__ slotE, const float4* __restrict__ dec4,
