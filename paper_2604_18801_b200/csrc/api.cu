@@ -267,7 +267,7 @@ void cc_destroy(cc_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cc_release(c, c->orig4); cc_release(c, c->dec4); cc_release(c, c->cor4); cc_release(c, c->posA);
-    cc_release(c, c->posB); cc_release(c, c->origE); cc_release(c, c->xs);
+    cc_release(c, c->posB); cc_release(c, c->origE); cc_release(c, c->xk);
     cc_release(c, c->key); cc_release(c, c->rnk); cc_release(c, c->cell_count); cc_release(c, c->cell_start);
     cc_release(c, c->slot_of); cc_release(c, c->deg); cc_release(c, c->eidx); cc_release(c, c->rows);
     cc_release(c, c->slotE); cc_release(c, c->parent); cc_release(c, c->mingid); cc_release(c, c->gsize);

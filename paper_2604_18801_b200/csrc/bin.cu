@@ -10,7 +10,7 @@
 //  3. scatter of one full 32-byte record (x,y,z,x_hat,y_hat,z_hat,gid,i) per particle: one
 //     aligned full-sector write each, instead of re-gathering six arrays later.
 //  4. per-cell finish: each cell (~1/K particles on average) sorts its records by x in
-//     registers (crowded cells: a block bitonic) and writes the float4 records, xs and slot_of.
+//     registers (crowded cells: a block bitonic) and writes the float4 records, xk and slot_of.
 //     Consecutive threads own consecutive cells, so reads and writes stream.
 // The slot order is fully determined by the data (x ties broken by input index).
 #include <cmath>
@@ -75,10 +75,10 @@ k_bin_scatter(int64_t n, const float* __restrict__ x, const float* __restrict__ 
 }
 
 __device__ __forceinline__ void emit(const Rec& r, uint32_t s, float4* __restrict__ orig4, float4* __restrict__ dec4,
-                                     float* __restrict__ xs, uint32_t* __restrict__ slot_of) {
+                                     uint32_t* __restrict__ xk, uint32_t* __restrict__ slot_of, const Grid& g) {
     orig4[s] = make_float4(r.x, r.y, r.z, __uint_as_float(r.gid));
     dec4[s] = make_float4(r.xh, r.yh, r.zh, __uint_as_float(r.i));
-    xs[s] = r.x;
+    xk[s] = x_sort_key(r.x, g);
     slot_of[r.i] = s;
 }
 
@@ -97,7 +97,7 @@ __device__ __forceinline__ unsigned long long rec_key(const Rec& r, const Grid& 
 // per-cell finish: sort the cell's records by x and write the slot-ordered arrays
 __global__ void __launch_bounds__(BIN_THREADS)
 k_cell_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restrict__ rec, Grid g,
-              float4* __restrict__ orig4, float4* __restrict__ dec4, float* __restrict__ xs,
+              float4* __restrict__ orig4, float4* __restrict__ dec4, uint32_t* __restrict__ xk,
               uint32_t* __restrict__ slot_of, uint32_t* __restrict__ long_list, unsigned long long* __restrict__ n_long) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= ncell) return;
@@ -105,7 +105,7 @@ k_cell_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restr
     const int len = (int)(b - a);
     if (len == 0) return;
     if (len == 1) {
-        emit(load_rec(rec, a), a, orig4, dec4, xs, slot_of);
+        emit(load_rec(rec, a), a, orig4, dec4, xk, slot_of, g);
         return;
     }
     if (len > CELL_SHORT) {
@@ -126,14 +126,14 @@ k_cell_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restr
         v[j + 1] = xk;
         off[j + 1] = k;
     }
-    for (int k = 0; k < len; k++) emit(load_rec(rec, a + off[k]), a + k, orig4, dec4, xs, slot_of);
+    for (int k = 0; k < len; k++) emit(load_rec(rec, a + off[k]), a + k, orig4, dec4, xk, slot_of, g);
 }
 
 // crowded cells: one block per cell, bitonic sort of (key, local offset) in shared memory
 __global__ void __launch_bounds__(512)
 k_cell_finish_long(const uint32_t* __restrict__ long_list, const unsigned long long* __restrict__ n_long,
                    const uint32_t* __restrict__ cs, const Rec* __restrict__ rec, Grid g, float4* __restrict__ orig4,
-                   float4* __restrict__ dec4, float* __restrict__ xs, uint32_t* __restrict__ slot_of) {
+                   float4* __restrict__ dec4, uint32_t* __restrict__ xk, uint32_t* __restrict__ slot_of) {
     __shared__ unsigned long long sh[CELL_LONG_MAX];
     __shared__ unsigned short so[CELL_LONG_MAX];
     const unsigned long long nl = *n_long;
@@ -169,7 +169,7 @@ k_cell_finish_long(const uint32_t* __restrict__ long_list, const unsigned long l
                 }
             }
             for (int k = threadIdx.x; k < len; k += blockDim.x)
-                emit(load_rec(rec, a + so[k]), a + k, orig4, dec4, xs, slot_of);
+                emit(load_rec(rec, a + so[k]), a + k, orig4, dec4, xk, slot_of, g);
             __syncthreads();
         } else if (threadIdx.x == 0) {
             // pathological crowding: selection by repeated minimum (correct, slow)
@@ -185,7 +185,7 @@ k_cell_finish_long(const uint32_t* __restrict__ long_list, const unsigned long l
                         bq = q2;
                     }
                 }
-                emit(load_rec(rec, a + bq), a + k, orig4, dec4, xs, slot_of);
+                emit(load_rec(rec, a + bq), a + k, orig4, dec4, xk, slot_of, g);
                 prev = best;
             }
         }
@@ -204,7 +204,7 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
     CC_TRY(cc_ensure(c, c->cell_start, (size_t)nc + 1, "cell_start"));
     CC_TRY(cc_ensure(c, c->orig4, n1, "orig4"));
     CC_TRY(cc_ensure(c, c->dec4, n1, "dec4"));
-    CC_TRY(cc_ensure(c, c->xs, n1, "xs"));
+    CC_TRY(cc_ensure(c, c->xk, n1, "x keys"));
     CC_TRY(cc_ensure(c, c->slot_of, n1, "slot_of"));
     CC_TRY(cc_ensure(c, c->rec32, 2 * n1, "binning records"));  // 32 B per particle
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
@@ -233,9 +233,9 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
         unsigned long long* nl = reinterpret_cast<unsigned long long*>(c->scratch_u64.p);
         int t2 = cc_prof_begin(c, "K1_finish");
         CCL(c, k_cell_finish<<<(unsigned)((nc + BIN_THREADS - 1) / BIN_THREADS), BIN_THREADS, 0, c->stream>>>(
-                   nc, c->cell_start.p, rec, c->g, c->orig4.p, c->dec4.p, c->xs.p, c->slot_of.p, c->scratch_u32.p, nl));
+                   nc, c->cell_start.p, rec, c->g, c->orig4.p, c->dec4.p, c->xk.p, c->slot_of.p, c->scratch_u32.p, nl));
         CCL(c, k_cell_finish_long<<<148 * 2, 512, 0, c->stream>>>(c->scratch_u32.p, nl, c->cell_start.p, rec, c->g,
-                                                                  c->orig4.p, c->dec4.p, c->xs.p, c->slot_of.p));
+                                                                  c->orig4.p, c->dec4.p, c->xk.p, c->slot_of.p));
         cc_prof_end(c, t2);
         CC_CUDA(c, cudaGetLastError());
     }

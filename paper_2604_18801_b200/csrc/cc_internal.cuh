@@ -42,7 +42,7 @@ struct Th {
 // ny x nz rows of side >= r_max = (b + 2 sqrt3 xi)(1 + 1e-5); each row is cut along x into nx
 // bins; particles are counting-sorted by (z-row, y-row, x-bin) and sorted by x inside every bin,
 // so every row is one x-sorted slot range.  A radius-r search from a particle visits the 9
-// neighbouring rows and, in each, only the x-window [u - r, u + r] (binary search on xs[]).
+// neighbouring rows and, in each, only the x-window [u - r, u + r] (binary search on the x keys xk[]).
 // Coordinates: u = x - x0 wrapped once into [0, L) (x0 = 0 on one GPU; the slab's lower ghost
 // edge on several); all window arithmetic in fp64.
 struct Grid {
@@ -168,7 +168,7 @@ struct cc_ctx {
     cc::DBuf<uint32_t> key, rnk, cell_count, cell_start, slot_of, deg, eidx, rows, slotE, parent, mingid,
         gsize, scratch_u32;
     cc::DBuf<uint64_t> rowoff, rowptr, scratch_u64;
-    cc::DBuf<float> xs;          // original x per slot (row-sorted search key)
+    cc::DBuf<uint32_t> xk;       // x_sort_key of the original x per slot (the in-row search key)
     cc::DBuf<uint4> rec32;       // K1 binning records, 2 x uint4 = 32 B per particle
     cc::DBuf<uint32_t> parent_base;  // FoF forest of the stable links (d2 <= lo2), per build
     bool base_valid = false;
@@ -335,12 +335,34 @@ __device__ __forceinline__ uint32_t x_sort_key(float x, const Grid& g) {
 
 __device__ __forceinline__ int wrapi(int a, int n) { return a < 0 ? a + n : (a >= n ? a - n : a); }
 
-// first slot j in [j0, j1) with u(xs[j]) >= a (u non-decreasing over the range)
-__device__ __forceinline__ uint32_t lower_bound_u(const float* __restrict__ xs, uint32_t j0, uint32_t j1, double a,
-                                                  const Grid& g) {
+// in-row key bounds of a local-x window [a, b] (0 <= a, b <= L): every slot with a <= u <= b
+// has key_lo(a) <= key <= key_hi(b) (directed fp32 rounding widens, never narrows; the exact
+// distance test filters the candidates afterwards)
+__device__ __forceinline__ uint32_t key_lo(double a, const Grid& g) {
+    double x = a + g.x0;
+    uint32_t w = 0u;
+    if (x >= g.L) {
+        x -= g.L;
+        w = 0x80000000u;
+    }
+    return __float_as_uint(__fadd_rn(__double2float_rd(fmax(x, 0.0)), 0.0f)) | w;
+}
+__device__ __forceinline__ uint32_t key_hi(double b, const Grid& g) {
+    double x = b + g.x0;
+    uint32_t w = 0u;
+    if (x >= g.L) {
+        x -= g.L;
+        w = 0x80000000u;
+    }
+    return __float_as_uint(__fadd_rn(__double2float_ru(fmax(x, 0.0)), 0.0f)) | w;
+}
+
+// first slot j in [j0, j1) with xk[j] >= k (keys non-decreasing over the range)
+__device__ __forceinline__ uint32_t lower_bound_key(const uint32_t* __restrict__ xk, uint32_t j0, uint32_t j1,
+                                                    uint32_t k) {
     while (j0 < j1) {
         const uint32_t m = (j0 + j1) >> 1;
-        if (local_u((double)xs[m], g) < a) j0 = m + 1;
+        if (xk[m] < k) j0 = m + 1;
         else j1 = m;
     }
     return j0;
@@ -349,20 +371,21 @@ __device__ __forceinline__ uint32_t lower_bound_u(const float* __restrict__ xs, 
 // visit every slot j of the row starting at cell index `rowbase` with a <= u_j <= b
 template <class F>
 __device__ __forceinline__ void scan_row_window(const Grid& g, const uint32_t* __restrict__ cs,
-                                                const float* __restrict__ xs, int64_t rowbase, double a, double b,
+                                                const uint32_t* __restrict__ xk, int64_t rowbase, double a, double b,
                                                 F& f) {
     const int ca = cell_coord(a, 0.0, g.inv_wx, g.nx), cb = cell_coord(b, 0.0, g.inv_wx, g.nx);
     const uint32_t j1 = cs[rowbase + cb + 1];
-    uint32_t j = lower_bound_u(xs, cs[rowbase + ca], j1, a, g);
+    const uint32_t khi = key_hi(b, g);
+    uint32_t j = lower_bound_key(xk, cs[rowbase + ca], j1, key_lo(a, g));
     for (; j < j1; j++) {
-        if (local_u((double)xs[j], g) > b) break;
+        if (xk[j] > khi) break;
         f(j);
     }
 }
 
 // visit the x-window [u - r, u + r] (periodic in x when g.xwrap) of one row
 template <class F>
-__device__ __forceinline__ void scan_row(const Grid& g, const uint32_t* __restrict__ cs, const float* __restrict__ xs,
+__device__ __forceinline__ void scan_row(const Grid& g, const uint32_t* __restrict__ cs, const uint32_t* __restrict__ xk,
                                          int64_t rowbase, double u, double r, F& f) {
     double a = u - r, b = u + r;
     double sa[3], sb[3];
@@ -385,14 +408,14 @@ __device__ __forceinline__ void scan_row(const Grid& g, const uint32_t* __restri
     sa[ns] = a;
     sb[ns++] = b;
 #pragma unroll 1
-    for (int k = 0; k < ns; k++) scan_row_window(g, cs, xs, rowbase, sa[k], sb[k], f);
+    for (int k = 0; k < ns; k++) scan_row_window(g, cs, xk, rowbase, sa[k], sb[k], f);
 }
 
 // Radius-r candidates of a particle at local x u in row (cy, cz): the 9 neighbouring rows
 // (offsets de-duplicated when an axis has fewer than 3 rows, R1), x-window per row.  f(j).
 template <class F>
 __device__ __forceinline__ void for_each_candidate(const Grid& g, const uint32_t* __restrict__ cs,
-                                                   const float* __restrict__ xs, double u, int cy, int cz, double r,
+                                                   const uint32_t* __restrict__ xk, double u, int cy, int cz, double r,
                                                    bool periodic_yz, F&& f) {
     const int ny_off = g.ny >= 3 ? 3 : g.ny, nz_off = g.nz >= 3 ? 3 : g.nz;
     const int offs[3] = {0, 1, -1};
@@ -406,7 +429,7 @@ __device__ __forceinline__ void for_each_candidate(const Grid& g, const uint32_t
             int yy = cy + offs[ky];
             if (periodic_yz) yy = wrapi(yy, g.ny);
             else if (yy < 0 || yy >= g.ny) continue;
-            scan_row(g, cs, xs, ((int64_t)zz * g.ny + yy) * g.nx, u, r, f);
+            scan_row(g, cs, xk, ((int64_t)zz * g.ny + yy) * g.nx, u, r, f);
         }
     }
 }

@@ -31,7 +31,7 @@ __global__ void k_iota(int64_t n, uint32_t* __restrict__ par) {
 // is b (ORIG) or b + 2 sqrt3 xi (DECOMP / CORR, whose positions are within xi of the original
 // ones that built the structure), with the fp32 rounding margin.
 __global__ void __launch_bounds__(FOF_THREADS)
-k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ orig4, const float* __restrict__ xs,
+k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ orig4, const uint32_t* __restrict__ xk,
            const uint32_t* __restrict__ cs, Grid g, Th t, double r, float thr2, uint32_t* __restrict__ par) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
@@ -51,7 +51,7 @@ k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ o
         auto fwd = [&](uint32_t j) {
             if (j > (uint32_t)s) link(j);
         };
-        for_each_candidate(g, cs, xs, u, cy, cz, r, periodic_yz, fwd);
+        for_each_candidate(g, cs, xk, u, cy, cz, r, periodic_yz, fwd);
         return;
     }
     // own row: forward in slot (= x) order, plus the periodic wrap at the row's start
@@ -59,11 +59,12 @@ k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ o
         const int64_t rowbase = ((int64_t)cz * g.ny + cy) * g.nx;
         const double b = u + r;
         const uint32_t row_end = cs[rowbase + g.nx];
+        const uint32_t khi = key_hi(fmin(b, g.xwrap ? g.L : g.ext_x), g);
         for (uint32_t j = (uint32_t)s + 1; j < row_end; j++) {
-            if (local_u((double)xs[j], g) > b) break;
+            if (xk[j] > khi) break;
             link(j);
         }
-        if (g.xwrap && b >= g.L) scan_row_window(g, cs, xs, rowbase, 0.0, b - g.L, link);
+        if (g.xwrap && b >= g.L) scan_row_window(g, cs, xk, rowbase, 0.0, b - g.L, link);
     }
     const int rows_dz[4] = {0, 1, 1, 1};
     const int rows_dy[4] = {1, -1, 0, 1};
@@ -75,7 +76,7 @@ k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ o
         } else if (zz < 0 || zz >= g.nz || yy < 0 || yy >= g.ny) {
             continue;
         }
-        scan_row(g, cs, xs, ((int64_t)zz * g.ny + yy) * g.nx, u, r, link);
+        scan_row(g, cs, xk, ((int64_t)zz * g.ny + yy) * g.nx, u, r, link);
     }
 }
 
@@ -225,7 +226,7 @@ static cc_status fof_base(cc_ctx* c) {
         CCL(c, k_iota<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent_base.p));
         if (c->th.lo2 >= 0.0f) {
             const double r = std::sqrt((double)c->th.lo2) * (1.0 + 1e-5);
-            CCL(c, k_fof_link<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->orig4.p, c->orig4.p, c->xs.p, c->cell_start.p,
+            CCL(c, k_fof_link<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->orig4.p, c->orig4.p, c->xk.p, c->cell_start.p,
                                                                  c->g, c->th, r, c->th.lo2, c->parent_base.p));
         }
         CCL(c, k_flatten<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent_base.p));
@@ -285,7 +286,7 @@ cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
             }
         } else {
             CCL(c, k_iota<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p));
-            CCL(c, k_fof_link<<<nb, FOF_THREADS, 0, c->stream>>>(n, P, c->orig4.p, c->xs.p, c->cell_start.p, c->g,
+            CCL(c, k_fof_link<<<nb, FOF_THREADS, 0, c->stream>>>(n, P, c->orig4.p, c->xk.p, c->cell_start.p, c->g,
                                                                  c->th, which == CC_ORIG ? c->r_link : c->r_pair,
                                                                  c->th.b2, c->parent.p));
         }

@@ -26,7 +26,7 @@ constexpr int PAIR_THREADS = 256;
 // of owned particles get bit 31 of their deg word (multi-GPU: they become ghost editables).
 __global__ void __launch_bounds__(PAIR_THREADS)
 k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
-              const float* __restrict__ xs, const uint32_t* __restrict__ cs, Grid g, Th t, double r, uint32_t n_own,
+              const uint32_t* __restrict__ xk, const uint32_t* __restrict__ cs, Grid g, Th t, double r, uint32_t n_own,
               uint32_t* __restrict__ deg, uint32_t* __restrict__ par_base) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
@@ -51,7 +51,7 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
             uf_link(par_base, (uint32_t)s, j, rs);
         }
     };
-    for_each_candidate(g, cs, xs, u, cy, cz, r, t.periodic != 0, test);
+    for_each_candidate(g, cs, xk, u, cy, cz, r, t.periodic != 0, test);
     deg[s] = cnt;  // an owned slot never carries the ghost bit
 }
 
@@ -78,7 +78,7 @@ __global__ void k_resolve(int64_t n, const uint32_t* __restrict__ cls, ClassBase
 
 // pass 2: write the row of every owned editable slot
 __global__ void __launch_bounds__(PAIR_THREADS)
-k_pairs_fill(int64_t n, const float4* __restrict__ orig4, const float* __restrict__ xs,
+k_pairs_fill(int64_t n, const float4* __restrict__ orig4, const uint32_t* __restrict__ xk,
              const uint32_t* __restrict__ cs, Grid g, Th t, double r, const uint32_t* __restrict__ deg,
              const unsigned long long* __restrict__ rowoff, const uint32_t* __restrict__ eidx, uint32_t e_own,
              uint32_t* __restrict__ rows) {
@@ -102,7 +102,7 @@ k_pairs_fill(int64_t n, const float4* __restrict__ orig4, const float* __restric
             rows[k++] = ent;
         }
     };
-    for_each_candidate(g, cs, xs, u, cy, cz, r, t.periodic != 0, emit);
+    for_each_candidate(g, cs, xk, u, cy, cz, r, t.periodic != 0, emit);
 }
 
 // compaction: editable e -> slot, row start, original and starting position
@@ -214,7 +214,7 @@ cc_status pairs_count(cc_ctx* c) {
     if (n > 0) {
         int tok = cc_prof_begin(c, "K2_count");
         CCL(c, k_pairs_count<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
-            n, c->orig4.p, c->dec4.p, c->xs.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in, c->deg.p,
+            n, c->orig4.p, c->dec4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in, c->deg.p,
             c->parent_base.p));
         cc_prof_end(c, tok);
         CC_CUDA(c, cudaGetLastError());
@@ -254,7 +254,7 @@ cc_status pairs_fill(cc_ctx* c) {
     if (n > 0 && c->nent > 0) {
         int tok = cc_prof_begin(c, "K2_fill");
         CCL(c, k_pairs_fill<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
-            n, c->orig4.p, c->xs.p, c->cell_start.p, c->g, c->th, c->r_pair, c->deg.p,
+            n, c->orig4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, c->deg.p,
             reinterpret_cast<const unsigned long long*>(c->rowoff.p), c->eidx.p, (uint32_t)c->E, c->rows.p));
         cc_prof_end(c, tok);
         CC_CUDA(c, cudaGetLastError());

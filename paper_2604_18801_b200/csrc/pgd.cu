@@ -229,7 +229,7 @@ __device__ __forceinline__ void touch(uint32_t* __restrict__ unext, uint32_t j) 
     if (!(*((volatile uint32_t*)&unext[j >> 5]) & bit)) atomicOr(&unext[j >> 5], bit);
 }
 
-__global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
+__global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
     Ctl* ctl = a.ctl;
     if (!a.count_only && *((volatile int*)&ctl->done)) return;
     const int t = a.count_only ? 0 : ctl->t + 1;
@@ -437,19 +437,25 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
         __syncwarp();
         for (uint32_t b0 = 0; b0 < total; b0 += 32u) {
             const uint32_t k = b0 + lane;
-            int lo = 0, hi = 31;  // the word holding selected item k: largest s with pre[s] <= k
-#pragma unroll
-            for (int it = 0; it < 5; it++) {
-                const int mid = (lo + hi + 1) >> 1;
-                const uint32_t pm = __shfl_sync(0xffffffffu, pre, mid);
-                if (pm <= k) lo = mid;
-                else hi = mid - 1;
-            }
-            const uint32_t ms = __shfl_sync(0xffffffffu, mask, lo);
-            const uint32_t ps = __shfl_sync(0xffffffffu, pre, lo);
             const bool valid = k < total;
             uint32_t e = 0u;
-            if (valid) e = (r * 32u + (uint32_t)lo) * 32u + __fns(ms, 0u, (int)(k - ps) + 1);
+            int lo = (int)(b0 >> 5);
+            if (select) {
+                lo = 0;  // the word holding selected item k: largest s with pre[s] <= k
+                int hi = 31;
+#pragma unroll
+                for (int it = 0; it < 5; it++) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    const uint32_t pm = __shfl_sync(0xffffffffu, pre, mid);
+                    if (pm <= k) lo = mid;
+                    else hi = mid - 1;
+                }
+                const uint32_t ms = __shfl_sync(0xffffffffu, mask, lo);
+                const uint32_t ps = __shfl_sync(0xffffffffu, pre, lo);
+                if (valid) e = (r * 32u + (uint32_t)lo) * 32u + __fns(ms, 0u, (int)(k - ps) + 1);
+            } else if (valid) {  // every editable of the range: batch = one whole word
+                e = r * 1024u + k;
+            }
             const bool awake = process_batch(e, valid);
             if (build && awake) atomicOr(&ws.aw[lo], 1u << (e & 31));
             __syncwarp();
