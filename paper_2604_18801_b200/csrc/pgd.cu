@@ -61,6 +61,7 @@ struct PgdArgs {
     const float2* __restrict__ bc;
     Th t;
     float alpha, b1, b2, omb1, omb2, eps, vstep;
+    float lb2;  // log2(b2 (1 - 2^-24)): the slowest per-step decay of v (replay_still)
     int optimizer;
     int t_max;
     int stop_mode;
@@ -165,6 +166,22 @@ __device__ __forceinline__ float adam_reg(float x, float g, float& m, float& v, 
 // (the Adam step then shrinks by ~10% per iteration), the frontier's freeze condition
 __device__ __forceinline__ bool negligible(float step_abs, float x) { return step_abs <= fabsf(x) * 1.4901161e-8f; }
 
+// True if K zero-gradient Adam steps from state (m, v) provably leave coordinate x unchanged:
+// a rigorous upper bound of every step's magnitude (|m| never grows, bc1 never shrinks, v
+// shrinks by at most b2 (1 - 2^-24) per step, each fp32 operation adds at most a relative
+// 2^-24 plus 2^-149 absolute) is below half an ulp of x, so x - step rounds back to x and the
+// projection (x already inside the box) is the identity.
+__device__ __forceinline__ bool replay_still(float x, float m, float v, int K, float bc1a, const PgdArgs& a) {
+    const float ax = fabsf(x);
+    if (!(ax >= 1e-30f)) return false;
+    // factors 0.999 / 1.001 dominate every rounding error (including exp2f's) by far
+    const float mh = fabsf(m) / bc1a * 1.001f + 1e-44f;
+    const float vmin = v * exp2f((float)K * a.lb2) * 0.999f;
+    const float sq = vmin >= 1e-36f ? sqrtf(vmin) * 0.999f : 0.0f;
+    const float bound = a.alpha * mh / (sq + a.eps * 0.999f) * 1.001f + 1e-44f;
+    return bound < ax * 2.98023224e-8f;  // 2^-25 |x| <= half an ulp of x
+}
+
 // Adam (or vanilla) step + projection of editable e, written to dst.  `replay` zero-gradient
 // iterations missed while e was frozen (frontier) are first re-run exactly, in order.
 // Returns bit0 = moved, bit1 = freeze-eligible step (negligible on all coordinates).
@@ -178,6 +195,23 @@ __device__ __forceinline__ int update(const PgdArgs& a, uint32_t e, const float4
         const size_t E = a.E;
         float mx = M[e], my = M[E + e], mz = M[2 * E + e], vx = M[3 * E + e], vy = M[4 * E + e], vz = M[5 * E + e];
         float sx, sy, sz;
+        if (replay_from < t) {
+            const int K = t - replay_from;
+            const float bc1a = a.bc[replay_from - 1].x;
+            if (replay_still(x, mx, vx, K, bc1a, a) && replay_still(y, my, vy, K, bc1a, a) &&
+                replay_still(z, mz, vz, K, bc1a, a)) {
+                // provably no move: only the moments evolve (same expressions as adam_reg, g = 0)
+                for (int tt = replay_from; tt < t; tt++) {
+                    mx = __fadd_rn(__fmul_rn(a.b1, mx), __fmul_rn(a.omb1, 0.0f));
+                    my = __fadd_rn(__fmul_rn(a.b1, my), __fmul_rn(a.omb1, 0.0f));
+                    mz = __fadd_rn(__fmul_rn(a.b1, mz), __fmul_rn(a.omb1, 0.0f));
+                    vx = __fadd_rn(__fmul_rn(a.b2, vx), __fmul_rn(a.omb2, __fmul_rn(0.0f, 0.0f)));
+                    vy = __fadd_rn(__fmul_rn(a.b2, vy), __fmul_rn(a.omb2, __fmul_rn(0.0f, 0.0f)));
+                    vz = __fadd_rn(__fmul_rn(a.b2, vz), __fmul_rn(a.omb2, __fmul_rn(0.0f, 0.0f)));
+                }
+                replay_from = t;
+            }
+        }
         for (int tt = replay_from; tt < t; tt++) {  // frozen iterations: gradient exactly 0
             const float2 b = a.bc[tt - 1];
             const float nx = project(adam_reg(x, 0.0f, mx, vx, a, b.x, b.y, sx), o.x, a.t.xip_f);
@@ -603,6 +637,7 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.b2 = (float)c->p.beta2;
     a.omb1 = (float)(1.0 - c->p.beta1);
     a.omb2 = (float)(1.0 - c->p.beta2);
+    a.lb2 = (float)(std::log2((double)a.b2 * (1.0 - std::ldexp(1.0, -24))) * (1.0 + 1e-6));
     a.eps = (float)c->p.eps_adam;
     a.vstep = (float)c->p.vanilla_step;
     a.optimizer = c->p.optimizer;

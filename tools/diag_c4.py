@@ -42,6 +42,11 @@ print("schedule (t, items, awake, moved entries):")
 for t in sorted(set(list(range(0, 12)) + list(range(12, len(sch), max(1, len(sch) // 40))) + [len(sch) - 1])):
     if t < len(sch):
         print("  ", t + 1, *sch[t].tolist())
+gi, gj, fl = c.get_pairs()
+deg = torch.bincount(torch.cat([gi.long(), gj.long()]), minlength=w.n)
+dv, di = torch.sort(deg, descending=True)
+print("row lengths: max", int(dv[0]), "top10", dv[:10].tolist(), "rows>32:", int((deg > 32).sum()),
+      ">1000:", int((deg > 1000).sum()), ">10000:", int((deg > 10000).sum()), flush=True)
 if os.environ.get("DIAG_ONLY_K3"):
     sys.exit(0)
 m = c.mcc(cc.CC_CORR)
