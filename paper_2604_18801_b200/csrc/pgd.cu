@@ -61,7 +61,6 @@ struct PgdArgs {
     const float2* __restrict__ bc;
     Th t;
     float alpha, b1, b2, omb1, omb2, eps, vstep;
-    float lb2;  // log2(b2 (1 - 2^-24)): the slowest per-step decay of v (replay_still)
     int optimizer;
     int t_max;
     int stop_mode;
@@ -166,19 +165,19 @@ __device__ __forceinline__ float adam_reg(float x, float g, float& m, float& v, 
 // (the Adam step then shrinks by ~10% per iteration), the frontier's freeze condition
 __device__ __forceinline__ bool negligible(float step_abs, float x) { return step_abs <= fabsf(x) * 1.4901161e-8f; }
 
-// True if K zero-gradient Adam steps from state (m, v) provably leave coordinate x unchanged:
-// a rigorous upper bound of every step's magnitude (|m| never grows, bc1 never shrinks, v
-// shrinks by at most b2 (1 - 2^-24) per step, each fp32 operation adds at most a relative
-// 2^-24 plus 2^-149 absolute) is below half an ulp of x, so x - step rounds back to x and the
-// projection (x already inside the box) is the identity.
-__device__ __forceinline__ bool replay_still(float x, float m, float v, int K, float bc1a, const PgdArgs& a) {
+// True if any number of zero-gradient Adam steps from state (m, v) provably leaves coordinate x
+// unchanged.  With g = 0, step k has |m_k| <= |m| (b1 (1+d))^k, v_k >= v (b2 (1-d))^k and
+// bc1_k >= bc1a, so |step_k| <= alpha |m| b1^k / (bc1a (sqrt(v b2^k) + eps)) up to rounding
+// factors; since b1 < sqrt(b2) the bound is largest at k = 1.  If that bound is below half an
+// ulp of x, x - step rounds back to x at every step and the projection (x is already inside the
+// box) is the identity.  Factors 0.999 / 1.001 and the 1e-44 terms dominate every fp32
+// rounding (relative 2^-24, absolute 2^-149 for subnormals) and exp/sqrt error by far.
+__device__ __forceinline__ bool replay_still(float x, float m, float v, float bc1a, const PgdArgs& a) {
     const float ax = fabsf(x);
-    if (!(ax >= 1e-30f)) return false;
-    // factors 0.999 / 1.001 dominate every rounding error (including exp2f's) by far
-    const float mh = fabsf(m) / bc1a * 1.001f + 1e-44f;
-    const float vmin = v * exp2f((float)K * a.lb2) * 0.999f;
-    const float sq = vmin >= 1e-36f ? sqrtf(vmin) * 0.999f : 0.0f;
-    const float bound = a.alpha * mh / (sq + a.eps * 0.999f) * 1.001f + 1e-44f;
+    if (!(ax >= 1e-30f) || !(a.b1 < sqrtf(a.b2) * 0.999f)) return false;
+    const float mh = fabsf(m) * a.b1 / bc1a * 1.001f + 1e-44f;
+    const float den = (sqrtf(v * a.b2) * 0.999f + a.eps) * 0.999f;
+    const float bound = a.alpha * mh / den * 1.001f + 1e-44f;
     return bound < ax * 2.98023224e-8f;  // 2^-25 |x| <= half an ulp of x
 }
 
@@ -196,10 +195,9 @@ __device__ __forceinline__ int update(const PgdArgs& a, uint32_t e, const float4
         float mx = M[e], my = M[E + e], mz = M[2 * E + e], vx = M[3 * E + e], vy = M[4 * E + e], vz = M[5 * E + e];
         float sx, sy, sz;
         if (replay_from < t) {
-            const int K = t - replay_from;
             const float bc1a = a.bc[replay_from - 1].x;
-            if (replay_still(x, mx, vx, K, bc1a, a) && replay_still(y, my, vy, K, bc1a, a) &&
-                replay_still(z, mz, vz, K, bc1a, a)) {
+            if (replay_still(x, mx, vx, bc1a, a) && replay_still(y, my, vy, bc1a, a) &&
+                replay_still(z, mz, vz, bc1a, a)) {
                 // provably no move: only the moments evolve (same expressions as adam_reg, g = 0)
                 for (int tt = replay_from; tt < t; tt++) {
                     mx = __fadd_rn(__fmul_rn(a.b1, mx), __fmul_rn(a.omb1, 0.0f));
@@ -637,7 +635,6 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.b2 = (float)c->p.beta2;
     a.omb1 = (float)(1.0 - c->p.beta1);
     a.omb2 = (float)(1.0 - c->p.beta2);
-    a.lb2 = (float)(std::log2((double)a.b2 * (1.0 - std::ldexp(1.0, -24))) * (1.0 + 1e-6));
     a.eps = (float)c->p.eps_adam;
     a.vstep = (float)c->p.vanilla_step;
     a.optimizer = c->p.optimizer;
