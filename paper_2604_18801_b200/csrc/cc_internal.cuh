@@ -64,7 +64,7 @@ struct Ctl {
     unsigned int ticket;
     int sel;           // K3: this launch processes only the bitmap-selected editables (pgd.cu)
     int bld;           // K3: this launch builds the awake/touched bitmaps
-    int pad3;
+    unsigned int nsel; // K3: editables selected for the next k_pgd (k_select)
     unsigned long long active;   // L_tight-active pairs at the last check
     unsigned long long violated; // pairs whose link status differs from the original (Eq. 1)
     double loss;
@@ -179,7 +179,7 @@ struct cc_ctx {
     cc::DBuf<unsigned long long> counters;
     cc::DBuf<cc::Ctl> ctl;
     cc::DBuf<long long> trace_a, trace_v, trace_s;
-    cc::DBuf<uint32_t> frozen, fbits;  // K3 frontier: last-processed iteration, awake/touched bitmaps (pgd.cu)
+    cc::DBuf<uint32_t> frozen, fbits, slist;  // K3 frontier: last-processed iteration, awake/touched bitmaps (pgd.cu)
     cc::DBuf<unsigned long long> k3work;  // K3 work totals (editables updated, entries evaluated)
     int64_t E_cls[4] = {0, 0, 0, 0};  // editables per K3 work class (row_class), numbered class-major
     cc::DBuf<double> trace_l;

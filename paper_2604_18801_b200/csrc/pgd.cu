@@ -45,7 +45,6 @@ struct WarpSh {               // per-warp staging of K3's flattened row evaluati
     unsigned long long k0[32];
     uint32_t off[32];         // exclusive scan of the row lengths
     unsigned char seg[CH];    // owning lane of each chunk entry
-    uint32_t aw[32];          // awake bits of the current 32-word range
 };
 
 struct PgdArgs {
@@ -81,6 +80,7 @@ struct PgdArgs {
     uint32_t* abits;  // 2 bitmaps of nwords words: editables awake after an iteration
     uint32_t* ubits;  // 3 bitmaps: editables touched (a partner moved) in an iteration
     uint32_t nwords;
+    uint32_t* slist;  // editables selected for the current iteration, k_select's output
     unsigned long long* errs;
     unsigned long long* work;  // running totals: [0] editables updated, [1] row entries evaluated
 };
@@ -299,14 +299,8 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
     const bool select = front && ctl->sel;
     const bool build = front && ctl->bld;
     const uint32_t nw32 = a.nwords;
-    const uint32_t* __restrict__ acur = a.abits + (size_t)(t & 1) * nw32;
     uint32_t* __restrict__ anext = a.abits + (size_t)((t + 1) & 1) * nw32;
-    const uint32_t* __restrict__ ucur = a.ubits + (size_t)(t % 3) * nw32;
     uint32_t* __restrict__ unext = a.ubits + (size_t)((t + 1) % 3) * nw32;
-    if (front) {  // (cleared even when not building: a later build must start from zero)
-        uint32_t* uclr = a.ubits + (size_t)((t + 2) % 3) * nw32;
-        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nw32; i += gridDim.x * blockDim.x) uclr[i] = 0u;
-    }
 
     auto count = [&](const Term& tm, uint32_t ent) {  // each pair once, at its lower-gid endpoint
         if (ent & ENT_UPPER) {
@@ -442,58 +436,21 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
         return awake;
     };
 
-    // ---- work items: a warp takes a range of 32 bitmap words (1024 editables) at a time and
-    // processes its selected editables in index order, 32 per batch
+    // ---- work items: every editable (sweep) or the selected list built by k_select; a warp
+    // takes 32 consecutive items per batch
+    const uint32_t n_items = select ? ctl->nsel : a.E;
     const uint32_t gw = blockIdx.x * (PGD_THREADS / 32) + w, nwarps = gridDim.x * (PGD_THREADS / 32);
-    const uint32_t nranges = (nw32 + 31) / 32;
-    for (uint32_t r = gw; r < nranges; r += nwarps) {
-        const uint32_t wi = r * 32u + lane;
-        uint32_t mask = 0u;
-        if (wi < nw32) {
-            if (select) {
-                mask = acur[wi] | ucur[wi];
-            } else {
-                const uint32_t e0 = wi * 32u;
-                mask = (a.E - e0 >= 32u) ? 0xFFFFFFFFu : ((1u << (a.E - e0)) - 1u);
-            }
+    for (uint32_t b0 = gw * 32u; b0 < n_items; b0 += nwarps * 32u) {
+        const uint32_t k = b0 + lane;
+        const bool valid = k < n_items;
+        const uint32_t e = valid ? (select ? a.slist[k] : k) : 0xFFFFFFFFu;
+        const bool awake = process_batch(valid ? e : 0u, valid);
+        if (build) {  // awake bits for t+1, one atomic per distinct word of the batch
+            const uint32_t word = e >> 5;
+            const unsigned peers = __match_any_sync(0xffffffffu, word);
+            const uint32_t bits = __reduce_or_sync(peers, awake ? (1u << (e & 31)) : 0u);
+            if (valid && bits && lane == __ffs(peers) - 1) atomicOr(&anext[word], bits);
         }
-        const uint32_t cnt = __popc(mask);
-        uint32_t pre = cnt;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, pre, o);
-            if (lane >= o) pre += v;
-        }
-        const uint32_t total = __shfl_sync(0xffffffffu, pre, 31);
-        pre -= cnt;
-        ws.aw[lane] = 0u;
-        __syncwarp();
-        for (uint32_t b0 = 0; b0 < total; b0 += 32u) {
-            const uint32_t k = b0 + lane;
-            const bool valid = k < total;
-            uint32_t e = 0u;
-            int lo = (int)(b0 >> 5);
-            if (select) {
-                lo = 0;  // the word holding selected item k: largest s with pre[s] <= k
-                int hi = 31;
-#pragma unroll
-                for (int it = 0; it < 5; it++) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    const uint32_t pm = __shfl_sync(0xffffffffu, pre, mid);
-                    if (pm <= k) lo = mid;
-                    else hi = mid - 1;
-                }
-                const uint32_t ms = __shfl_sync(0xffffffffu, mask, lo);
-                const uint32_t ps = __shfl_sync(0xffffffffu, pre, lo);
-                if (valid) e = (r * 32u + (uint32_t)lo) * 32u + __fns(ms, 0u, (int)(k - ps) + 1);
-            } else if (valid) {  // every editable of the range: batch = one whole word
-                e = r * 1024u + k;
-            }
-            const bool awake = process_batch(e, valid);
-            if (build && awake) atomicOr(&ws.aw[lo], 1u << (e & 31));
-            __syncwarp();
-        }
-        if (build && wi < nw32) anext[wi] = ws.aw[lane];
-        __syncwarp();
     }
 
     // ---- work counters (integers: order-free), one atomic per warp
@@ -538,6 +495,7 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
     ctl->violated = tv;
     ctl->loss = td;
     ctl->ticket = 0;
+    ctl->nsel = 0u;  // consumed (k_select of the next iteration refills it)
     if (!a.count_only && a.trace_s && t >= 1 && t <= a.t_max) {
         a.trace_s[3 * (t - 1)] = (long long)tot[LFX_STATS + 2];
         a.trace_s[3 * (t - 1) + 1] = (long long)tot[LFX_STATS];
@@ -568,18 +526,70 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
     __threadfence();
 }
 
+// Frontier selection for iteration t (runs before k_pgd in every iteration): the editables
+// awake after t-1 or touched at t-1 (A[t & 1] | U[t % 3]) as a list, sorted within each block's
+// 8192-editable segment; segments are placed by one atomic per block-step.  Also clears the
+// touched bitmap U[(t+2) % 3] (written next at t+1) and, when t builds, the awake bitmap
+// A[(t+1) & 1] it will fill.
+__global__ void __launch_bounds__(PGD_THREADS) k_select(PgdArgs a) {
+    Ctl* ctl = a.ctl;
+    if (!a.frontier || *((volatile int*)&ctl->done)) return;
+    const int t = ctl->t + 1;
+    const uint32_t nw32 = a.nwords;
+    const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+    uint32_t* uclr = a.ubits + (size_t)((t + 2) % 3) * nw32;
+    for (uint32_t i = gt; i < nw32; i += gs) uclr[i] = 0u;
+    if (ctl->bld) {
+        uint32_t* anext = a.abits + (size_t)((t + 1) & 1) * nw32;
+        for (uint32_t i = gt; i < nw32; i += gs) anext[i] = 0u;
+    }
+    if (!ctl->sel) return;
+    const uint32_t* __restrict__ acur = a.abits + (size_t)(t & 1) * nw32;
+    const uint32_t* __restrict__ ucur = a.ubits + (size_t)(t % 3) * nw32;
+    __shared__ uint32_t wsum[PGD_THREADS / 32];
+    __shared__ uint32_t bbase;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (uint32_t w0 = blockIdx.x * blockDim.x; w0 < nw32; w0 += gs) {  // block-uniform loop
+        const uint32_t wi = w0 + threadIdx.x;
+        const uint32_t mask = wi < nw32 ? (acur[wi] | ucur[wi]) : 0u;
+        const uint32_t cnt = __popc(mask);
+        uint32_t pre = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += v;
+        }
+        if (lane == 31) wsum[w] = pre;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+            for (int k = 0; k < PGD_THREADS / 32; k++) {
+                const uint32_t v = wsum[k];
+                wsum[k] = tot;
+                tot += v;
+            }
+            bbase = tot ? atomicAdd(&ctl->nsel, tot) : 0u;
+        }
+        __syncthreads();
+        uint32_t pos = bbase + wsum[w] + pre - cnt;
+        for (uint32_t m = mask; m; m &= m - 1) a.slist[pos++] = wi * 32u + (uint32_t)(__ffs(m) - 1);
+        __syncthreads();
+    }
+}
+
 __global__ void k_ctl_reset(Ctl* ctl) {
     ctl->done = 0;
     ctl->t = 0;
     ctl->t_res = 0;
     ctl->converged = 0;
     ctl->ticket = 0;
+    ctl->nsel = 0u;  // consumed (k_select of the next iteration refills it)
     ctl->active = 0;
     ctl->violated = 0;
     ctl->loss = 0.0;
     for (int k = 0; k < 12; k++) ctl->acc[k] = 0ull;
     ctl->sel = 0;
     ctl->bld = 0;
+    ctl->nsel = 0u;
 }
 
 __global__ void k_reset_pos(int64_t Ea, const uint32_t* __restrict__ slotE, const float4* __restrict__ dec4,
@@ -654,6 +664,7 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.work = c->k3work.p;
     a.nwords = (uint32_t)((std::max<int64_t>(c->E, 1) + 31) / 32);
     a.abits = c->fbits.p;
+    a.slist = c->slist.p;
     a.ubits = c->fbits.p + 2 * (size_t)a.nwords;
     return a;
 }
@@ -718,6 +729,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     CC_TRY(cc_ensure(c, c->frozen, (size_t)std::max<int64_t>(E, 1), "frontier state"));
     const size_t nwords = (size_t)((std::max<int64_t>(E, 1) + 31) / 32);
     CC_TRY(cc_ensure(c, c->fbits, 5 * nwords, "frontier bitmaps"));
+    CC_TRY(cc_ensure(c, c->slist, (size_t)std::max<int64_t>(E, 1), "frontier selection"));
     CC_CUDA(c, cudaMemsetAsync(c->fbits.p, 0, 5 * nwords * sizeof(uint32_t), c->stream));
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
     CC_CUDA(c, cudaMemsetAsync(c->counters.p + 15, 0, sizeof(unsigned long long), c->stream));
@@ -799,6 +811,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
             CC_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
             for (int k = 0; k < batch; k++) {
                 if (c->p.profile) cudaEventRecordWithFlags(c->graph_ev[2 * k], c->stream, cudaEventRecordExternal);
+                CCL(c, k_select<<<nb, PGD_THREADS, 0, c->stream>>>(a));
                 CCL(c, k_pgd<<<nb, PGD_THREADS, 0, c->stream>>>(a));
                 if (c->p.profile)
                     cudaEventRecordWithFlags(c->graph_ev[2 * k + 1], c->stream, cudaEventRecordExternal);
@@ -815,7 +828,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
                     c->launches = l0;
                 }
             }
-            c->launches -= batch;  // captured, not launched
+            c->launches -= 2 * batch;  // captured, not launched
             cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
             CC_CUDA(c, ce);
             CC_CUDA(c, cudaGraphInstantiate(&c->pgd_exec, graph, 0));
@@ -825,7 +838,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
         int t_before = 0;
         for (;;) {
             CC_CUDA(c, cudaGraphLaunch(c->pgd_exec, c->stream));
-            c->launches += batch * (1 + c->launches_per_iter_tail);
+            c->launches += batch * (2 + c->launches_per_iter_tail);
             CC_CUDA(c, cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
             CC_CUDA(c, cudaStreamSynchronize(c->stream));
             const Ctl h = *c->h_ctl;
