@@ -255,11 +255,6 @@ __device__ __forceinline__ bool frontier_after(const PgdArgs& a, uint32_t e, int
     return !freeze;
 }
 
-// a moved editable marks partner j (owned) for iteration t+1 in the touched bitmap
-__device__ __forceinline__ void touch(uint32_t* __restrict__ unext, uint32_t j) {
-    const uint32_t bit = 1u << (j & 31);
-    if (!(*((volatile uint32_t*)&unext[j >> 5]) & bit)) atomicOr(&unext[j >> 5], bit);
-}
 
 __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
     Ctl* ctl = a.ctl;
@@ -414,22 +409,16 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
                 if (flags & 1) st[(LFX_STATS + 1) * PGD_THREADS] += len;
             }
         }
-        if (build) {  // a mover touches its owned partners for t+1
-            const bool moved = (flags & 1) != 0;
-            if (moved && len <= 32u)
-                for (unsigned long long k = k0; k < k0 + len; k++) {
-                    const uint32_t j = a.rows[k] & ENT_IDX;
-                    if (j < a.E) touch(unext, j);
-                }
-            unsigned lm = __ballot_sync(0xffffffffu, moved && len > 32u);
-            while (lm) {  // long rows: the whole warp
-                const int sl = __ffs(lm) - 1;
-                lm &= lm - 1;
+        if (build) {  // a mover touches its owned partners for t+1: the warp walks each mover's row
+            unsigned mv = __ballot_sync(0xffffffffu, (flags & 1) != 0);
+            while (mv) {
+                const int sl = __ffs(mv) - 1;
+                mv &= mv - 1;
                 const unsigned long long kb = __shfl_sync(0xffffffffu, k0, sl);
                 const uint32_t ln = __shfl_sync(0xffffffffu, len, sl);
                 for (uint32_t i = lane; i < ln; i += 32) {
                     const uint32_t j = a.rows[kb + i] & ENT_IDX;
-                    if (j < a.E) touch(unext, j);
+                    if (j < a.E) atomicOr(&unext[j >> 5], 1u << (j & 31));  // fire-and-forget (RED)
                 }
             }
         }
