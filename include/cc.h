@@ -149,8 +149,10 @@ cc_status cc_get_trace(cc_ctx* ctx, int64_t* active_h, double* loss_h, int64_t* 
                        int64_t* n_h);
 
 /* K3 schedule per iteration of the last cc_correct (diagnostics of the frontier):
- * sched_h[3 t + 0] = work items processed, [3 t + 1] = editables left awake, [3 t + 2] = row
- * entries of editables that moved; up to cap iterations, *n_h = iterations recorded. */
+ * sched_h[5 t + 0] = editables processed, [5 t + 1] = editables left awake, [5 t + 2] = row
+ * entries of editables that moved, [5 t + 3] = zero-gradient steps replayed in full, [5 t + 4] =
+ * zero-gradient steps replayed on the proven-still path; up to cap iterations, *n_h = iterations
+ * recorded. */
 cc_status cc_get_schedule(cc_ctx* ctx, int64_t* sched_h, int64_t cap, int64_t* n_h);
 
 /* S6 -- FoF labels (§II-B, Fig. 1) on ORIG, DECOMP or CORR positions: edge iff the

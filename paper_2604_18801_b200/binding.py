@@ -238,9 +238,10 @@ class Corrector:
         return a[: n.value], l[: n.value], v[: n.value]
 
     def schedule(self):
-        """K3 schedule per iteration: (items processed, editables left awake, moved row entries)."""
+        """K3 schedule per iteration: (editables processed, left awake, moved row entries, full
+        replay steps, proven-still replay steps)."""
         n = C.c_int64()
-        a = np.zeros((self.params.t_max + 1, 3), np.int64)
+        a = np.zeros((self.params.t_max + 1, 5), np.int64)
         self._chk(self.lib.cc_get_schedule(self.h, a.ctypes.data_as(C.POINTER(C.c_int64)), a.shape[0], C.byref(n)))
         return a[: n.value]
 

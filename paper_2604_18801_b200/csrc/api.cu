@@ -447,7 +447,7 @@ cc_status cc_get_schedule(cc_ctx* c, int64_t* sched_h, int64_t cap, int64_t* n_h
     const int64_t n = std::min<int64_t>((int64_t)c->last_iters, (int64_t)c->p.t_max);
     const int64_t k = std::min(n, cap);
     if (k > 0) {
-        CC_CUDA(c, cudaMemcpyAsync(sched_h, c->trace_s.p, (size_t)(3 * k) * sizeof(long long), cudaMemcpyDeviceToHost,
+        CC_CUDA(c, cudaMemcpyAsync(sched_h, c->trace_s.p, (size_t)(5 * k) * sizeof(long long), cudaMemcpyDeviceToHost,
                                    c->stream));
         CC_CUDA(c, cudaStreamSynchronize(c->stream));
     }

@@ -68,7 +68,7 @@ struct Ctl {
     unsigned long long active;   // L_tight-active pairs at the last check
     unsigned long long violated; // pairs whose link status differs from the original (Eq. 1)
     double loss;
-    unsigned long long acc[12];  // K3 launch statistics being summed (LFX layout + schedule counts)
+    unsigned long long acc[14];  // K3 launch statistics being summed (LFX layout + schedule counts)
 };
 
 // ---------------------------------------------------------------------------------------

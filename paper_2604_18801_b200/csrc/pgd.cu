@@ -35,7 +35,7 @@ namespace {
 
 constexpr int PGD_THREADS = 256;
 constexpr int PGD_MAX_BLOCKS = 148 * 8;
-constexpr int NSTAT = LFX_STATS + 3;
+constexpr int NSTAT = LFX_STATS + 5;
 constexpr int NB = 4;         // row entries per lane per chunk
 constexpr int CH = 32 * NB;   // flattened row entries per warp chunk
 
@@ -210,6 +210,7 @@ __device__ __forceinline__ int update(const PgdArgs& a, uint32_t e, const float4
                 replay_from = t;
             }
         }
+        if (replay_from < t) flags |= 4;  // full replay (reported in the schedule trace)
         for (int tt = replay_from; tt < t; tt++) {  // frozen iterations: gradient exactly 0
             const float2 b = a.bc[tt - 1];
             const float nx = project(adam_reg(x, 0.0f, mx, vx, a, b.x, b.y, sx), o.x, a.t.xip_f);
@@ -403,6 +404,7 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
         if (valid && !a.count_only) {
             const int replay_from = (fz != 0u && fz != FZ_NEVER) ? (int)fz + 1 : t;  // zero-gradient
             flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);               // steps missed while frozen
+            if (replay_from < t) st[(LFX_STATS + ((flags & 4) ? 3 : 4)) * PGD_THREADS] += (unsigned)(t - replay_from);
             if (a.frontier) {
                 awake = frontier_after(a, e, t, flags, any_active, fz);
                 if (awake) st[LFX_STATS * PGD_THREADS]++;
@@ -486,9 +488,12 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
     ctl->ticket = 0;
     ctl->nsel = 0u;  // consumed (k_select of the next iteration refills it)
     if (!a.count_only && a.trace_s && t >= 1 && t <= a.t_max) {
-        a.trace_s[3 * (t - 1)] = (long long)tot[LFX_STATS + 2];
-        a.trace_s[3 * (t - 1) + 1] = (long long)tot[LFX_STATS];
-        a.trace_s[3 * (t - 1) + 2] = (long long)tot[LFX_STATS + 1];
+        long long* ts = a.trace_s + 5 * (t - 1);
+        ts[0] = (long long)tot[LFX_STATS + 2];
+        ts[1] = (long long)tot[LFX_STATS];
+        ts[2] = (long long)tot[LFX_STATS + 1];
+        ts[3] = (long long)tot[LFX_STATS + 3];
+        ts[4] = (long long)tot[LFX_STATS + 4];
     }
     if (front) {
         ctl->sel = build ? 1 : 0;
@@ -575,7 +580,7 @@ __global__ void k_ctl_reset(Ctl* ctl) {
     ctl->active = 0;
     ctl->violated = 0;
     ctl->loss = 0.0;
-    for (int k = 0; k < 12; k++) ctl->acc[k] = 0ull;
+    for (int k = 0; k < 14; k++) ctl->acc[k] = 0ull;
     ctl->sel = 0;
     ctl->bld = 0;
     ctl->nsel = 0u;
@@ -709,7 +714,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     CC_TRY(cc_ensure(c, c->trace_a, (size_t)tmax + 1, "trace"));
     CC_TRY(cc_ensure(c, c->trace_l, (size_t)tmax + 1, "trace"));
     CC_TRY(cc_ensure(c, c->trace_v, (size_t)tmax + 1, "trace"));
-    CC_TRY(cc_ensure(c, c->trace_s, 3 * ((size_t)tmax + 1), "trace"));
+    CC_TRY(cc_ensure(c, c->trace_s, 5 * ((size_t)tmax + 1), "trace"));
     if (c->nranks > 1) CC_TRY(cc_ensure(c, c->red, LFX_STATS, "allreduce buffer"));
     if (!c->k3work.p) {
         CC_TRY(cc_ensure(c, c->k3work, 2, "K3 work counters"));

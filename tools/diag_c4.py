@@ -38,7 +38,7 @@ idx = sorted(set([0, 1, 2, 5, 10, 20, 50, 100, 150, 200, 300, 500, 1000, 2000, 5
 print("trace (t, active, loss, violated)", [(i, int(a[i]), float(l[i]), int(v[i])) for i in idx if i < len(a)],
       flush=True)
 sch = c.schedule()
-print("schedule (t, items, awake, moved entries):")
+print("schedule (t, processed, awake, moved entries, full replay steps, quick replay steps):")
 for t in sorted(set(list(range(0, 12)) + list(range(12, len(sch), max(1, len(sch) // 40))) + [len(sch) - 1])):
     if t < len(sch):
         print("  ", t + 1, *sch[t].tolist())
