@@ -54,7 +54,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
-            subprocess.check_call(cmd)
+            try:
+                subprocess.check_call(cmd)
+            except subprocess.CalledProcessError:
+                for f in (obj, LIB):  # never leave a stale library behind a failed build
+                    if os.path.exists(f):
+                        os.remove(f)
+                raise
         objs.append(obj)
     tmp = LIB + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, *LDFLAGS])

@@ -275,10 +275,15 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
     // schedule counts: editables left awake, row entries of editables that moved, editables
     // processed.  Per-thread counters live in shared memory (touched rarely; registers are the
     // occupancy limit of this latency-bound kernel).
-    __shared__ unsigned long long st_sh[NSTAT][PGD_THREADS];
+    // counters (u32 per thread) in LFX/schedule order without the limbs: 0 active, 1 violated,
+    // 2 awake, 3 moved entries, 4 processed, 5 full-replay steps, 6 proven-still replay steps
+    __shared__ unsigned long long lim_sh[6][PGD_THREADS];
+    __shared__ uint32_t cn_sh[NSTAT - 6][PGD_THREADS];
 #pragma unroll
-    for (int k = 0; k < NSTAT; k++) st_sh[k][threadIdx.x] = 0ull;
-    unsigned long long* st = &st_sh[0][threadIdx.x];  // st[k * PGD_THREADS] = counter k
+    for (int k = 0; k < 6; k++) lim_sh[k][threadIdx.x] = 0ull;
+#pragma unroll
+    for (int k = 0; k < NSTAT - 6; k++) cn_sh[k][threadIdx.x] = 0u;
+    uint32_t* cn = &cn_sh[0][threadIdx.x];  // cn[k * PGD_THREADS] = counter k
     __shared__ WarpSh wsh[PGD_THREADS / 32];
     unsigned long long wk_e = 0, wk_n = 0;  // work done: editables updated, row entries evaluated
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -301,10 +306,10 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
     auto count = [&](const Term& tm, uint32_t ent) {  // each pair once, at its lower-gid endpoint
         if (ent & ENT_UPPER) {
             if (tm.kind) {
-                st[0]++;
-                lfx_add<PGD_THREADS>(st + 2 * PGD_THREADS, (double)tm.ee * (double)tm.ee);
+                cn[0]++;
+                lfx_add<PGD_THREADS>(&lim_sh[0][threadIdx.x], (double)tm.ee * (double)tm.ee);
             }
-            if (tm.viol) st[PGD_THREADS]++;
+            if (tm.viol) cn[PGD_THREADS]++;
         }
     };
 
@@ -324,7 +329,7 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
             if (front) fz = a.frozen[e];
             wk_e++;
             wk_n += len;
-            st[(LFX_STATS + 2) * PGD_THREADS]++;
+            cn[4 * PGD_THREADS]++;
         }
         uint32_t off = len;  // exclusive scan of the row lengths over the warp
         for (int o = 1; o < 32; o <<= 1) {
@@ -404,11 +409,11 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
         if (valid && !a.count_only) {
             const int replay_from = (fz != 0u && fz != FZ_NEVER) ? (int)fz + 1 : t;  // zero-gradient
             flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);               // steps missed while frozen
-            if (replay_from < t) st[(LFX_STATS + ((flags & 4) ? 3 : 4)) * PGD_THREADS] += (unsigned)(t - replay_from);
+            if (replay_from < t) cn[((flags & 4) ? 5 : 6) * PGD_THREADS] += (unsigned)(t - replay_from);
             if (a.frontier) {
                 awake = frontier_after(a, e, t, flags, any_active, fz);
-                if (awake) st[LFX_STATS * PGD_THREADS]++;
-                if (flags & 1) st[(LFX_STATS + 1) * PGD_THREADS] += len;
+                if (awake) cn[2 * PGD_THREADS]++;
+                if (flags & 1) cn[3 * PGD_THREADS] += len;
             }
         }
         if (build) {  // a mover touches its owned partners for t+1: the warp walks each mover's row
@@ -459,9 +464,13 @@ __global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
     // ---- statistics: integer sums (LFX), so the order of warps, blocks and ranks is free
     __shared__ bool am_last;
     __syncthreads();
-    for (int k = w; k < NSTAT; k += PGD_THREADS / 32) {  // warp w sums counters w, w+8, ...
+    for (int k = w; k < NSTAT; k += PGD_THREADS / 32) {  // warp w sums statistics w, w+8, ...
         unsigned long long v = 0ull;
-        for (int i = lane; i < PGD_THREADS; i += 32) v += st_sh[k][i];
+        // statistic k (LFX layout): 0, 1 counters; 2..7 limbs; 8.. counters 2..
+        if (k >= 2 && k < LFX_STATS)
+            for (int i = lane; i < PGD_THREADS; i += 32) v += lim_sh[k - 2][i];
+        else
+            for (int i = lane; i < PGD_THREADS; i += 32) v += cn_sh[k < 2 ? k : k - 6][i];
         for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
         if (lane == 0 && v) atomicAdd(&ctl->acc[k], v);
     }
