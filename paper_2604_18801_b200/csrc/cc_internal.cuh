@@ -179,6 +179,7 @@ struct cc_ctx {
     cc::DBuf<unsigned long long> counters;
     cc::DBuf<cc::Ctl> ctl;
     cc::DBuf<long long> trace_a, trace_v, trace_s;
+    cc::DBuf<uint32_t> lab_s;     // FoF labels in slot order (fof.cu)
     cc::DBuf<uint32_t> frozen, fbits, slist;  // K3 frontier: last-processed iteration, awake/touched bitmaps (pgd.cu)
     cc::DBuf<unsigned long long> k3work;  // K3 work totals (editables updated, entries evaluated)
     int64_t E_cls[4] = {0, 0, 0, 0};  // editables per K3 work class (row_class), numbered class-major

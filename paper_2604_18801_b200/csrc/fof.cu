@@ -120,14 +120,18 @@ __global__ void k_mingid(int64_t n, const uint32_t* __restrict__ par, const floa
     if (threadIdx.x == 0 && cnt) atomicAdd(n_roots, (unsigned long long)cnt);
 }
 
-// labels in input order, written from slot order (one random store instead of three
-// dependent random loads per particle)
-__global__ void k_labels(int64_t n, uint32_t n_in, const float4* __restrict__ dec4, const uint32_t* __restrict__ par,
-                         const uint32_t* __restrict__ mingid, uint32_t* __restrict__ labels) {
+// labels: first in slot order (par and, for the many singletons, mingid are read in order),
+// then gathered into input order (a random 4-byte read per particle instead of a random partial
+// sector write)
+__global__ void k_labels_slot(int64_t n, const uint32_t* __restrict__ par, const uint32_t* __restrict__ mingid,
+                              uint32_t* __restrict__ lab_s) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
-    const uint32_t i = __float_as_uint(dec4[s].w);
-    if (i < n_in) labels[i] = mingid[par[s]];
+    if (s < n) lab_s[s] = mingid[par[s]];
+}
+__global__ void k_labels(int64_t n_in, const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ lab_s,
+                         uint32_t* __restrict__ labels) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n_in) labels[i] = lab_s[slot_of[i]];
 }
 
 // MCC counters over the vulnerable pairs owned here (lower-gid endpoint, R17)
@@ -295,9 +299,12 @@ cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
                                                     c->counters.p + 8));
     }
     if (c->nranks > 1) CC_TRY(dist_fof_merge(c, n_groups));  // global labels across slabs (X4)
-    if (n > 0 && labels && c->n_in > 0)
-        CCL(c, k_labels<<<nb, FOF_THREADS, 0, c->stream>>>(n, (uint32_t)c->n_in, c->dec4.p, c->parent.p, c->mingid.p,
-                                                           labels));
+    if (n > 0 && labels && c->n_in > 0) {
+        CC_TRY(cc_ensure(c, c->lab_s, n1, "slot labels"));
+        CCL(c, k_labels_slot<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p, c->mingid.p, c->lab_s.p));
+        CCL(c, k_labels<<<(unsigned)((c->n_in + FOF_THREADS - 1) / FOF_THREADS), FOF_THREADS, 0, c->stream>>>(
+                   c->n_in, c->slot_of.p, c->lab_s.p, labels));
+    }
     cc_prof_end(c, tok);
     CC_CUDA(c, cudaGetLastError());
     if (n_groups && c->nranks == 1) {
