@@ -166,17 +166,18 @@ __device__ __forceinline__ float adam_reg(float x, float g, float& m, float& v, 
 __device__ __forceinline__ bool negligible(float step_abs, float x) { return step_abs <= fabsf(x) * 1.4901161e-8f; }
 
 // True if any number of zero-gradient Adam steps from state (m, v) provably leaves coordinate x
-// unchanged.  With g = 0, step k has |m_k| <= |m| (b1 (1+d))^k, v_k >= v (b2 (1-d))^k and
-// bc1_k >= bc1a, so |step_k| <= alpha |m| b1^k / (bc1a (sqrt(v b2^k) + eps)) up to rounding
-// factors; since b1 < sqrt(b2) the bound is largest at k = 1.  If that bound is below half an
+// unchanged.  With g = 0, step k has |m_k| <= |m| (b1 (1+d))^k, v_k >= v (b2 (1-d))^k,
+// bc1_k >= bc1a and bc2_k <= bc2z (the last replayed step's), so |step_k| <= alpha |m| b1^k /
+// (bc1a (sqrt(v b2^k / bc2z) + eps)) up to rounding factors; since b1 < sqrt(b2) the bound is
+// largest at k = 1.  If that bound is below half an
 // ulp of x, x - step rounds back to x at every step and the projection (x is already inside the
 // box) is the identity.  Factors 0.999 / 1.001 and the 1e-44 terms dominate every fp32
 // rounding (relative 2^-24, absolute 2^-149 for subnormals) and exp/sqrt error by far.
-__device__ __forceinline__ bool replay_still(float x, float m, float v, float bc1a, const PgdArgs& a) {
+__device__ __forceinline__ bool replay_still(float x, float m, float v, float bc1a, float bc2z, const PgdArgs& a) {
     const float ax = fabsf(x);
     if (!(ax >= 1e-30f) || !(a.b1 < sqrtf(a.b2) * 0.999f)) return false;
     const float mh = fabsf(m) * a.b1 / bc1a * 1.001f + 1e-44f;
-    const float den = (sqrtf(v * a.b2) * 0.999f + a.eps) * 0.999f;
+    const float den = (sqrtf(v * a.b2 / bc2z) * 0.999f + a.eps) * 0.999f;
     const float bound = a.alpha * mh / den * 1.001f + 1e-44f;
     return bound < ax * 2.98023224e-8f;  // 2^-25 |x| <= half an ulp of x
 }
@@ -195,9 +196,9 @@ __device__ __forceinline__ int update(const PgdArgs& a, uint32_t e, const float4
         float mx = M[e], my = M[E + e], mz = M[2 * E + e], vx = M[3 * E + e], vy = M[4 * E + e], vz = M[5 * E + e];
         float sx, sy, sz;
         if (replay_from < t) {
-            const float bc1a = a.bc[replay_from - 1].x;
-            if (replay_still(x, mx, vx, bc1a, a) && replay_still(y, my, vy, bc1a, a) &&
-                replay_still(z, mz, vz, bc1a, a)) {
+            const float bc1a = a.bc[replay_from - 1].x, bc2z = a.bc[t - 2].y;
+            if (replay_still(x, mx, vx, bc1a, bc2z, a) && replay_still(y, my, vy, bc1a, bc2z, a) &&
+                replay_still(z, mz, vz, bc1a, bc2z, a)) {
                 // provably no move: only the moments evolve (same expressions as adam_reg, g = 0)
                 for (int tt = replay_from; tt < t; tt++) {
                     mx = __fadd_rn(__fmul_rn(a.b1, mx), __fmul_rn(a.omb1, 0.0f));
