@@ -258,7 +258,7 @@ __device__ __forceinline__ bool frontier_after(const PgdArgs& a, uint32_t e, int
 }
 
 
-__global__ void __launch_bounds__(PGD_THREADS, 3) k_pgd(PgdArgs a) {
+__global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
     Ctl* ctl = a.ctl;
     if (!a.count_only && *((volatile int*)&ctl->done)) return;
     const int t = a.count_only ? 0 : ctl->t + 1;
