@@ -30,7 +30,7 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
               uint32_t* __restrict__ deg, uint32_t* __restrict__ par_base) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    if (__float_as_uint(dec4[s].w) >= n_own) return;  // ghost: no row
+    const bool ghost = __float_as_uint(dec4[s].w) >= n_own;  // ghost: no row, stable links only
     const float4 p = orig4[s];
     double u;
     int cx, cy, cz;
@@ -43,8 +43,10 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
         const float4 q = orig4[j];
         const float d2 = dist2(p, q, t);
         if (t.lo2 < d2 && d2 <= t.hi2) {
-            cnt++;
-            if (multi && __float_as_uint(dec4[j].w) >= n_own) atomicOr(&deg[j], 0x80000000u);
+            if (!ghost) {
+                cnt++;
+                if (multi && __float_as_uint(dec4[j].w) >= n_own) atomicOr(&deg[j], 0x80000000u);
+            }
         } else if (d2 <= t.lo2 && j > (uint32_t)s) {
             // a stable FoF link (linked in original, decompressed and corrected positions alike,
             // fof.cu): united here, in the same candidate sweep, once per pair
@@ -52,7 +54,7 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
         }
     };
     for_each_candidate(g, cs, xk, u, cy, cz, r, t.periodic != 0, test);
-    deg[s] = cnt;  // an owned slot never carries the ghost bit
+    if (!ghost) deg[s] = cnt;  // an owned slot never carries the ghost bit
 }
 
 // after the scan: editable ranks and row offsets become global (class-major numbering: class
