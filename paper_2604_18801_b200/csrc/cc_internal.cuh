@@ -435,6 +435,68 @@ __device__ __forceinline__ void for_each_candidate(const Grid& g, const uint32_t
     }
 }
 
+// Every unordered pair {s, j} within radius r, visited once over all s: the half-shell of rows
+// (own row forward in slot = x order plus the periodic wrap at the row start, then rows
+// (dz=0,dy=+1) and (dz=+1,dy=-1..1)); with fewer than 3 periodic rows on an axis, all 9 rows
+// with j > s.  f(j) for each candidate j (the caller tests the distance).
+template <class F>
+__device__ __forceinline__ void for_each_pair_forward(const Grid& g, const uint32_t* __restrict__ cs,
+                                                      const uint32_t* __restrict__ xk, uint32_t s, double u, int cy,
+                                                      int cz, double r, bool periodic_yz, F&& f) {
+    const bool half = !periodic_yz || (g.ny >= 3 && g.nz >= 3);
+    if (!half) {
+        auto fwd = [&](uint32_t j) {
+            if (j > s) f(j);
+        };
+        for_each_candidate(g, cs, xk, u, cy, cz, r, periodic_yz, fwd);
+        return;
+    }
+    {
+        const int64_t rowbase = ((int64_t)cz * g.ny + cy) * g.nx;
+        const double b = u + r;
+        const uint32_t row_end = cs[rowbase + g.nx];
+        const uint32_t khi = key_hi(fmin(b, g.xwrap ? g.L : g.ext_x), g);
+        for (uint32_t j = s + 1; j < row_end; j++) {
+            if (xk[j] > khi) break;
+            f(j);
+        }
+        if (g.xwrap && b >= g.L) scan_row_window(g, cs, xk, rowbase, 0.0, b - g.L, f);
+    }
+    const int rows_dz[4] = {0, 1, 1, 1};
+    const int rows_dy[4] = {1, -1, 0, 1};
+#pragma unroll 1
+    for (int k = 0; k < 4; k++) {
+        int zz = cz + rows_dz[k], yy = cy + rows_dy[k];
+        if (periodic_yz) {
+            zz = wrapi(zz, g.nz);
+            yy = wrapi(yy, g.ny);
+        } else if (zz < 0 || zz >= g.nz || yy < 0 || yy >= g.ny) {
+            continue;
+        }
+        scan_row(g, cs, xk, ((int64_t)zz * g.ny + yy) * g.nx, u, r, f);
+    }
+}
+
+// pinned d2 without the minimum image: identical to dist2 whenever no coordinate difference
+// can exceed L/2, i.e. for particles away from the periodic faces (interior below)
+__device__ __forceinline__ float dist2_nw(const float4& a, const float4& b) {
+    const float dx = __fsub_rn(b.x, a.x), dy = __fsub_rn(b.y, a.y), dz = __fsub_rn(b.z, a.z);
+    float s = __fmul_rn(dx, dx);
+    s = __fadd_rn(s, __fmul_rn(dy, dy));
+    s = __fadd_rn(s, __fmul_rn(dz, dz));
+    return s;
+}
+
+// true if every candidate of a search around this ORIGINAL position (rows +-1 of width w >= r,
+// x-window r; positions within xi of the originals) has |difference| far below L/2 on every axis,
+// so min_image is the identity: the particle keeps >= 2.5 w from the periodic faces
+__device__ __forceinline__ bool interior(float x, float y, float z, const Grid& g, const Th& t) {
+    if (!t.periodic) return true;
+    const double m = 2.5 / g.inv_w;
+    return 4.0 * m < g.L && (double)x >= m && (double)x <= g.L - m && (double)y >= m && (double)y <= g.L - m &&
+           (double)z >= m && (double)z <= g.L - m;
+}
+
 }  // namespace cc
 
 // ---------------------------------------------------------------------------------------

@@ -46,38 +46,7 @@ k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ o
         const float4 q = P[j];
         if (dist2(p, q, t) <= thr2) uf_link(par, (uint32_t)s, j, rs);
     };
-    const bool half = !periodic_yz || (g.ny >= 3 && g.nz >= 3);
-    if (!half) {
-        auto fwd = [&](uint32_t j) {
-            if (j > (uint32_t)s) link(j);
-        };
-        for_each_candidate(g, cs, xk, u, cy, cz, r, periodic_yz, fwd);
-        return;
-    }
-    // own row: forward in slot (= x) order, plus the periodic wrap at the row's start
-    {
-        const int64_t rowbase = ((int64_t)cz * g.ny + cy) * g.nx;
-        const double b = u + r;
-        const uint32_t row_end = cs[rowbase + g.nx];
-        const uint32_t khi = key_hi(fmin(b, g.xwrap ? g.L : g.ext_x), g);
-        for (uint32_t j = (uint32_t)s + 1; j < row_end; j++) {
-            if (xk[j] > khi) break;
-            link(j);
-        }
-        if (g.xwrap && b >= g.L) scan_row_window(g, cs, xk, rowbase, 0.0, b - g.L, link);
-    }
-    const int rows_dz[4] = {0, 1, 1, 1};
-    const int rows_dy[4] = {1, -1, 0, 1};
-    for (int k = 0; k < 4; k++) {
-        int zz = cz + rows_dz[k], yy = cy + rows_dy[k];
-        if (periodic_yz) {
-            zz = wrapi(zz, g.nz);
-            yy = wrapi(yy, g.ny);
-        } else if (zz < 0 || zz >= g.nz || yy < 0 || yy >= g.ny) {
-            continue;
-        }
-        scan_row(g, cs, xk, ((int64_t)zz * g.ny + yy) * g.nx, u, r, link);
-    }
+    for_each_pair_forward(g, cs, xk, (uint32_t)s, u, cy, cz, r, periodic_yz, link);
 }
 
 // read-only root walk: the flatten pass must not path-halve, or a halving write could land

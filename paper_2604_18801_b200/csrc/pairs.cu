@@ -22,39 +22,46 @@ namespace {
 
 constexpr int PAIR_THREADS = 256;
 
-// pass 1: deg[s] = number of band partners of slot s (owned particles only); ghost partners
-// of owned particles get bit 31 of their deg word (multi-GPU: they become ghost editables).
+// pass 1 (each unordered pair once, for_each_pair_forward): deg[] = band partners per slot
+// (atomics for the far endpoint), ghost endpoints of band pairs with an owned partner get bit 31
+// of their deg word (multi-GPU: they become ghost editables); stable links (d2 <= lo2) are
+// united into the stable FoF forest in the same sweep.
 __global__ void __launch_bounds__(PAIR_THREADS)
 k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
               const uint32_t* __restrict__ xk, const uint32_t* __restrict__ cs, Grid g, Th t, double r, uint32_t n_own,
               uint32_t* __restrict__ deg, uint32_t* __restrict__ par_base) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    const bool ghost = __float_as_uint(dec4[s].w) >= n_own;  // ghost: no row, stable links only
+    const bool multi = n_own < (uint32_t)n;
+    const bool ghost = multi && __float_as_uint(dec4[s].w) >= n_own;
     const float4 p = orig4[s];
     double u;
     int cx, cy, cz;
     cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
+    const bool inner = interior(p.x, p.y, p.z, g, t);
     uint32_t cnt = 0;
     uint32_t rs = (uint32_t)s;  // cached ancestor of s in the stable forest (uf_link)
-    const bool multi = n_own < (uint32_t)n;
     auto test = [&](uint32_t j) {
-        if (j == (uint32_t)s) return;
         const float4 q = orig4[j];
-        const float d2 = dist2(p, q, t);
+        const float d2 = inner ? dist2_nw(p, q) : dist2(p, q, t);
         if (t.lo2 < d2 && d2 <= t.hi2) {
+            const bool gj = multi && __float_as_uint(dec4[j].w) >= n_own;
             if (!ghost) {
                 cnt++;
-                if (multi && __float_as_uint(dec4[j].w) >= n_own) atomicOr(&deg[j], 0x80000000u);
+                if (gj) atomicOr(&deg[j], 0x80000000u);
+                else atomicAdd(&deg[j], 1u);
+            } else if (!gj) {
+                atomicAdd(&deg[j], 1u);
+                atomicOr(&deg[s], 0x80000000u);
             }
-        } else if (d2 <= t.lo2 && j > (uint32_t)s) {
+        } else if (d2 <= t.lo2) {
             // a stable FoF link (linked in original, decompressed and corrected positions alike,
-            // fof.cu): united here, in the same candidate sweep, once per pair
+            // fof.cu): united here, in the same candidate sweep
             uf_link(par_base, (uint32_t)s, j, rs);
         }
     };
-    for_each_candidate(g, cs, xk, u, cy, cz, r, t.periodic != 0, test);
-    if (!ghost) deg[s] = cnt;  // an owned slot never carries the ghost bit
+    for_each_pair_forward(g, cs, xk, (uint32_t)s, u, cy, cz, r, t.periodic != 0, test);
+    if (cnt) atomicAdd(&deg[s], cnt);
 }
 
 // after the scan: editable ranks and row offsets become global (class-major numbering: class
@@ -78,33 +85,34 @@ __global__ void k_resolve(int64_t n, const uint32_t* __restrict__ cls, ClassBase
     }
 }
 
-// pass 2: write the row of every owned editable slot
+// pass 2 (each unordered pair once again): both entries of every band pair, placed by a
+// per-row cursor (the order inside a row is fixed afterwards by the gid sort)
 __global__ void __launch_bounds__(PAIR_THREADS)
 k_pairs_fill(int64_t n, const float4* __restrict__ orig4, const uint32_t* __restrict__ xk,
              const uint32_t* __restrict__ cs, Grid g, Th t, double r, const uint32_t* __restrict__ deg,
-             const unsigned long long* __restrict__ rowoff, const uint32_t* __restrict__ eidx, uint32_t e_own,
-             uint32_t* __restrict__ rows) {
+             const uint32_t* __restrict__ eidx, uint32_t e_own, const unsigned long long* __restrict__ rowptr,
+             uint32_t* __restrict__ cur, uint32_t* __restrict__ rows) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    if ((deg[s] & 0x7FFFFFFFu) == 0) return;
+    if (deg[s] == 0u) return;  // not editable: no band pair at all
     const float4 p = orig4[s];
     const uint32_t gp = __float_as_uint(p.w);
+    const uint32_t es = eidx[s];
     double u;
     int cx, cy, cz;
     cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
-    unsigned long long k = rowoff[s];
+    const bool inner = interior(p.x, p.y, p.z, g, t);
     auto emit = [&](uint32_t j) {
-        if (j == (uint32_t)s) return;
         const float4 q = orig4[j];
-        const float d2 = dist2(p, q, t);
+        const float d2 = inner ? dist2_nw(p, q) : dist2(p, q, t);
         if (t.lo2 < d2 && d2 <= t.hi2) {
-            uint32_t ent = eidx[j];
-            if (__float_as_uint(q.w) > gp) ent |= ENT_UPPER;
-            if (d2 <= t.b2) ent |= ENT_OLINK;
-            rows[k++] = ent;
+            const uint32_t ej = eidx[j], gq = __float_as_uint(q.w);
+            const uint32_t ol = d2 <= t.b2 ? ENT_OLINK : 0u;
+            if (es < e_own) rows[rowptr[es] + atomicAdd(&cur[es], 1u)] = ej | (gq > gp ? ENT_UPPER : 0u) | ol;
+            if (ej < e_own) rows[rowptr[ej] + atomicAdd(&cur[ej], 1u)] = es | (gp > gq ? ENT_UPPER : 0u) | ol;
         }
     };
-    for_each_candidate(g, cs, xk, u, cy, cz, r, t.periodic != 0, emit);
+    for_each_pair_forward(g, cs, xk, (uint32_t)s, u, cy, cz, r, t.periodic != 0, emit);
 }
 
 // compaction: editable e -> slot, row start, original and starting position
@@ -255,9 +263,12 @@ cc_status pairs_fill(cc_ctx* c) {
     CC_TRY(cc_ensure(c, c->rows, (size_t)std::max<int64_t>(c->nent, 1), "rows"));
     if (n > 0 && c->nent > 0) {
         int tok = cc_prof_begin(c, "K2_fill");
+        CC_TRY(cc_ensure(c, c->scratch_u32, (size_t)std::max<int64_t>(c->E, 1), "row cursors"));
+        CC_CUDA(c, cudaMemsetAsync(c->scratch_u32.p, 0, (size_t)std::max<int64_t>(c->E, 1) * sizeof(uint32_t),
+                                   c->stream));
         CCL(c, k_pairs_fill<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
-            n, c->orig4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, c->deg.p,
-            reinterpret_cast<const unsigned long long*>(c->rowoff.p), c->eidx.p, (uint32_t)c->E, c->rows.p));
+            n, c->orig4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, c->deg.p, c->eidx.p, (uint32_t)c->E,
+            reinterpret_cast<const unsigned long long*>(c->rowptr.p), c->scratch_u32.p, c->rows.p));
         cc_prof_end(c, tok);
         CC_CUDA(c, cudaGetLastError());
     }
