@@ -341,13 +341,24 @@ def main():
         "K2_fill": 16.0 * n + 4.0 * n + 8.0 * n + 4.0 * nent,
         "K4_fof": 16.0 * n + 4 * 4.0 * n,
     }
+    # ncu traffic of the dominant kernel (committed capture): dram bytes of one
+    # captured launch next to that launch's algorithmic bytes
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "r01_k3_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f)
     roof = None
     if dom:
         d_ms, d_l = cls_ms[dom]
         avg_ms = d_ms / max(d_l, 1)
         ach = alg_bytes[dom] / (avg_ms * 1e-3) / 1e9 if dom in alg_bytes else None
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": (ach / hbm) if ach is not None else None, "traffic": None,
+                "frac": (ach / hbm) if ach is not None else None,
+                "traffic": traffic["dram_bytes"] if traffic and dom == traffic["kernel"] else None,
+                "traffic_capture": ({k: traffic[k] for k in ("capture", "dram_bytes", "algorithmic_bytes",
+                                                             "traffic_over_algorithmic", "duration_ms", "source")}
+                                    if traffic and dom == traffic["kernel"] else None),
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})", "launch_ms": avg_ms, "launches": d_l}
     k3 = cls_ms.get("K3_pgd")
     k3_roof = None
