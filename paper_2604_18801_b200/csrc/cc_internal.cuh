@@ -172,6 +172,8 @@ struct cc_ctx {
     cc::DBuf<uint4> rec32;       // K1 binning records, 2 x uint4 = 32 B per particle
     cc::DBuf<uint32_t> parent_base;  // FoF forest of the stable links (d2 <= lo2), per build
     bool base_valid = false;
+    cc::DBuf<uint32_t> parent_orig;  // stable forest + original-linked band pairs = FoF(ORIG), per build
+    bool orig_valid = false;
     bool corr_base_ok = false;   // xi - xi' margin >> fp32 rounding: CORR FoF may reuse the base
     double r_pair = 0, r_link = 0;   // search radii: vulnerable band / FoF on original positions
     cc::DBuf<float> mom;         // 6 * E floats: mx, my, mz, vx, vy, vz

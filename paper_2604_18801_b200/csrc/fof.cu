@@ -215,6 +215,7 @@ cc_status fof_base_begin(cc_ctx* c) {
     const int64_t n = c->n;
     CC_TRY(cc_ensure(c, c->parent_base, (size_t)std::max<int64_t>(n, 1), "stable forest"));
     c->base_valid = false;
+    c->orig_valid = false;
     if (n > 0) CCL(c, k_iota<<<(unsigned)((n + FOF_THREADS - 1) / FOF_THREADS), FOF_THREADS, 0, c->stream>>>(
                           n, c->parent_base.p));
     CC_CUDA(c, cudaGetLastError());
@@ -247,7 +248,10 @@ cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
     const unsigned nb = (unsigned)((n + FOF_THREADS - 1) / FOF_THREADS);
     int tok = cc_prof_begin(c, "K4_fof");
     if (n > 0) {
-        if (via_base) {
+        if (via_base && which == CC_ORIG && c->orig_valid) {  // built by K2's fill sweep
+            CC_CUDA(c, cudaMemcpyAsync(c->parent.p, c->parent_orig.p, (size_t)n * sizeof(uint32_t),
+                                       cudaMemcpyDeviceToDevice, c->stream));
+        } else if (via_base) {
             CC_CUDA(c, cudaMemcpyAsync(c->parent.p, c->parent_base.p, (size_t)n * sizeof(uint32_t),
                                        cudaMemcpyDeviceToDevice, c->stream));
             if (c->E > 0) {

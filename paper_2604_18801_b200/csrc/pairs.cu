@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(PAIR_THREADS)
 k_pairs_fill(int64_t n, const float4* __restrict__ orig4, const uint32_t* __restrict__ xk,
              const uint32_t* __restrict__ cs, Grid g, Th t, double r, const uint32_t* __restrict__ deg,
              const uint32_t* __restrict__ eidx, uint32_t e_own, const unsigned long long* __restrict__ rowptr,
-             uint32_t* __restrict__ cur, uint32_t* __restrict__ rows) {
+             uint32_t* __restrict__ cur, uint32_t* __restrict__ rows, uint32_t* __restrict__ par_orig) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
     if (deg[s] == 0u) return;  // not editable: no band pair at all
@@ -102,6 +102,7 @@ k_pairs_fill(int64_t n, const float4* __restrict__ orig4, const uint32_t* __rest
     int cx, cy, cz;
     cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
     const bool inner = interior(p.x, p.y, p.z, g, t);
+    uint32_t rs = (uint32_t)s;  // cached ancestor of s in the ORIG forest (uf_link)
     auto emit = [&](uint32_t j) {
         const float4 q = orig4[j];
         const float d2 = inner ? dist2_nw(p, q) : dist2(p, q, t);
@@ -110,6 +111,9 @@ k_pairs_fill(int64_t n, const float4* __restrict__ orig4, const uint32_t* __rest
             const uint32_t ol = d2 <= t.b2 ? ENT_OLINK : 0u;
             if (es < e_own) rows[rowptr[es] + atomicAdd(&cur[es], 1u)] = ej | (gq > gp ? ENT_UPPER : 0u) | ol;
             if (ej < e_own) rows[rowptr[ej] + atomicAdd(&cur[ej], 1u)] = es | (gp > gq ? ENT_UPPER : 0u) | ol;
+            // FoF(ORIG) = the stable forest + the original-linked band pairs (an owned endpoint;
+            // ghost-ghost pairs belong to their owner rank)
+            if (ol && (es < e_own || ej < e_own)) uf_link(par_orig, (uint32_t)s, j, rs);
         }
     };
     for_each_pair_forward(g, cs, xk, (uint32_t)s, u, cy, cz, r, t.periodic != 0, emit);
@@ -260,6 +264,11 @@ cc_status rows_resolve(cc_ctx* c, const unsigned long long* totals_h) {
 
 cc_status pairs_fill(cc_ctx* c) {
     const int64_t n = c->n;
+    CC_TRY(cc_ensure(c, c->parent_orig, (size_t)std::max<int64_t>(n, 1), "ORIG forest"));
+    if (n > 0)
+        CC_CUDA(c, cudaMemcpyAsync(c->parent_orig.p, c->parent_base.p, (size_t)n * sizeof(uint32_t),
+                                   cudaMemcpyDeviceToDevice, c->stream));
+    c->orig_valid = true;
     CC_TRY(cc_ensure(c, c->rows, (size_t)std::max<int64_t>(c->nent, 1), "rows"));
     if (n > 0 && c->nent > 0) {
         int tok = cc_prof_begin(c, "K2_fill");
@@ -268,7 +277,8 @@ cc_status pairs_fill(cc_ctx* c) {
                                    c->stream));
         CCL(c, k_pairs_fill<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
             n, c->orig4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, c->deg.p, c->eidx.p, (uint32_t)c->E,
-            reinterpret_cast<const unsigned long long*>(c->rowptr.p), c->scratch_u32.p, c->rows.p));
+            reinterpret_cast<const unsigned long long*>(c->rowptr.p), c->scratch_u32.p, c->rows.p,
+            c->parent_orig.p));
         cc_prof_end(c, tok);
         CC_CUDA(c, cudaGetLastError());
     }

@@ -280,10 +280,6 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
     // 2 awake, 3 moved entries, 4 processed, 5 full-replay steps, 6 proven-still replay steps
     __shared__ unsigned long long lim_sh[6][PGD_THREADS];
     __shared__ uint32_t cn_sh[NSTAT - 6][PGD_THREADS];
-#pragma unroll
-    for (int k = 0; k < 6; k++) lim_sh[k][threadIdx.x] = 0ull;
-#pragma unroll
-    for (int k = 0; k < NSTAT - 6; k++) cn_sh[k][threadIdx.x] = 0u;
     uint32_t* cn = &cn_sh[0][threadIdx.x];  // cn[k * PGD_THREADS] = counter k
     __shared__ WarpSh wsh[PGD_THREADS / 32];
     unsigned long long wk_e = 0, wk_n = 0;  // work done: editables updated, row entries evaluated
@@ -300,6 +296,15 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
     const bool front = a.frontier && !a.count_only;
     const bool select = front && ctl->sel;
     const bool build = front && ctl->bld;
+    const uint32_t n_items = select ? ctl->nsel : a.E;
+    // a block without items (small frontier) only takes part in the final ticket
+    const bool idle = blockIdx.x * (uint32_t)PGD_THREADS >= n_items;
+    if (!idle) {
+#pragma unroll
+        for (int k = 0; k < 6; k++) lim_sh[k][threadIdx.x] = 0ull;
+#pragma unroll
+        for (int k = 0; k < NSTAT - 6; k++) cn_sh[k][threadIdx.x] = 0u;
+    }
     const uint32_t nw32 = a.nwords;
     uint32_t* __restrict__ anext = a.abits + (size_t)((t + 1) & 1) * nw32;
     uint32_t* __restrict__ unext = a.ubits + (size_t)((t + 1) % 3) * nw32;
@@ -435,7 +440,6 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
 
     // ---- work items: every editable (sweep) or the selected list built by k_select; a warp
     // takes 32 consecutive items per batch
-    const uint32_t n_items = select ? ctl->nsel : a.E;
     const uint32_t gw = blockIdx.x * (PGD_THREADS / 32) + w, nwarps = gridDim.x * (PGD_THREADS / 32);
     for (uint32_t b0 = gw * 32u; b0 < n_items; b0 += nwarps * 32u) {
         const uint32_t k = b0 + lane;
@@ -465,7 +469,7 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
     // ---- statistics: integer sums (LFX), so the order of warps, blocks and ranks is free
     __shared__ bool am_last;
     __syncthreads();
-    for (int k = w; k < NSTAT; k += PGD_THREADS / 32) {  // warp w sums statistics w, w+8, ...
+    for (int k = w; k < NSTAT && !idle; k += PGD_THREADS / 32) {  // warp w sums statistics w, w+8, ...
         unsigned long long v = 0ull;
         // statistic k (LFX layout): 0, 1 counters; 2..7 limbs; 8.. counters 2..
         if (k >= 2 && k < LFX_STATS)
@@ -507,7 +511,7 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
     }
     if (front) {
         ctl->sel = build ? 1 : 0;
-        ctl->bld = (tot[LFX_STATS] + tot[LFX_STATS + 1] <= (unsigned long long)(a.E >> 2)) ? 1 : 0;
+        ctl->bld = (tot[LFX_STATS] + tot[LFX_STATS + 1] <= (unsigned long long)a.E * 4ull) ? 1 : 0;
     }
     if (a.red) {  // multi-GPU: the decision waits for the allreduce (dist.cu k_decide)
         for (int k = 0; k < LFX_STATS; k++) a.red[k] = tot[k];
