@@ -10,7 +10,8 @@ import numpy as np
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(HERE, "libcc.so")
+# CC_LIB_PATH: load another build of libcc (development A/B measurements only)
+_LIB_PATH = os.environ.get("CC_LIB_PATH") or os.path.join(HERE, "libcc.so")
 
 CC_OK, CC_NOT_CONVERGED = 0, 2
 CC_ORIG, CC_DECOMP, CC_CORR = 0, 1, 2

@@ -69,6 +69,10 @@ struct Ctl {
     unsigned long long violated; // pairs whose link status differs from the original (Eq. 1)
     double loss;
     unsigned long long acc[14];  // K3 launch statistics being summed (LFX layout + schedule counts)
+    unsigned int tail_nn;        // k_tail: length of the list being built
+    unsigned int tail_ncur;      // k_tail: length of the list of the next iteration
+    int tail_go;                 // k_tail: 1 while the tail loop continues
+    unsigned int bar_count, bar_gen;  // k_tail's grid barrier
 };
 
 // ---------------------------------------------------------------------------------------
@@ -182,7 +186,7 @@ struct cc_ctx {
     cc::DBuf<cc::Ctl> ctl;
     cc::DBuf<long long> trace_a, trace_v, trace_s;
     cc::DBuf<uint32_t> lab_s;     // FoF labels in slot order (fof.cu)
-    cc::DBuf<uint32_t> frozen, fbits, slist;  // K3 frontier: last-processed iteration, awake/touched bitmaps (pgd.cu)
+    cc::DBuf<uint32_t> frozen, fbits, slist, tlist;  // K3 frontier: last-processed iteration, awake/touched bitmaps (pgd.cu)
     cc::DBuf<unsigned long long> k3work;  // K3 work totals (editables updated, entries evaluated)
     int64_t E_cls[4] = {0, 0, 0, 0};  // editables per K3 work class (row_class), numbered class-major
     cc::DBuf<double> trace_l;

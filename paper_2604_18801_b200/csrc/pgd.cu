@@ -21,6 +21,7 @@
 // Algorithmic bytes per launch: 104 B per editable (pos r/w 32, orig 16, m,v r/w 48, rowptr 8)
 // + 4 B per directed row entry; partner positions are gathers (L2 when local).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -38,6 +39,9 @@ constexpr int PGD_MAX_BLOCKS = 148 * 8;
 constexpr int NSTAT = LFX_STATS + 5;
 constexpr int NB = 4;         // row entries per lane per chunk
 constexpr int CH = 32 * NB;   // flattened row entries per warp chunk
+constexpr uint32_t TAIL_ENTER = 4096;  // k_tail takes over when a selected list is this small
+constexpr uint32_t TAIL_CAP = 16384;   // ... and hands back when a list would exceed this
+constexpr int TAIL_BLOCKS = 64;        // k_tail's co-resident blocks
 
 struct WarpSh {               // per-warp staging of K3's flattened row evaluation
     float4 t[CH];             // term (px, py, pz, kind bits) of each chunk entry
@@ -81,6 +85,8 @@ struct PgdArgs {
     uint32_t* ubits;  // 3 bitmaps: editables touched (a partner moved) in an iteration
     uint32_t nwords;
     uint32_t* slist;  // editables selected for the current iteration, k_select's output
+    uint32_t* tlist;  // k_tail: 2 lists of TAIL_CAP editables (ping-pong)
+    uint32_t* tbits;  // k_tail: 2 membership bitmaps of nwords words (kept all-zero outside k_tail)
     unsigned long long* errs;
     unsigned long long* work;  // running totals: [0] editables updated, [1] row entries evaluated
 };
@@ -147,7 +153,14 @@ __device__ __forceinline__ float div_rn(float a, float b) {
     return __fdiv_rn(a, b);
 }
 
-// Adam (or vanilla) step + projection of editable e, written to dst
+// per-editable state loads: plain, or through L2 only (k_tail: blocks read what other blocks
+// wrote an iteration earlier)
+template <bool CG, typename T>
+__device__ __forceinline__ T ldst(const T* p) {
+    if (CG) return __ldcg(p);
+    return *p;
+}
+
 // one coordinate's Adam step in registers (R9); returns the new coordinate, sets |step|
 __device__ __forceinline__ float adam_reg(float x, float g, float& m, float& v, const PgdArgs& a, float bc1, float bc2,
                                           float& step_abs) {
@@ -185,6 +198,7 @@ __device__ __forceinline__ bool replay_still(float x, float m, float v, float bc
 // Adam (or vanilla) step + projection of editable e, written to dst.  `replay` zero-gradient
 // iterations missed while e was frozen (frontier) are first re-run exactly, in order.
 // Returns bit0 = moved, bit1 = freeze-eligible step (negligible on all coordinates).
+template <bool CG>
 __device__ __forceinline__ int update(const PgdArgs& a, uint32_t e, const float4& p, float gx, float gy, float gz,
                                       int t, int replay_from, float4* __restrict__ dst) {
     const float4 o = a.origE[e];
@@ -193,34 +207,44 @@ __device__ __forceinline__ int update(const PgdArgs& a, uint32_t e, const float4
     if (a.optimizer == CC_OPT_ADAM) {
         float* M = a.mom;
         const size_t E = a.E;
-        float mx = M[e], my = M[E + e], mz = M[2 * E + e], vx = M[3 * E + e], vy = M[4 * E + e], vz = M[5 * E + e];
+        float mx = ldst<CG>(M + e), my = ldst<CG>(M + E + e), mz = ldst<CG>(M + 2 * E + e);
+        float vx = ldst<CG>(M + 3 * E + e), vy = ldst<CG>(M + 4 * E + e), vz = ldst<CG>(M + 5 * E + e);
         float sx, sy, sz;
+        // zero-gradient iterations missed while frozen, in order: steps that provably cannot
+        // move the coordinates only advance the moments; the others are recomputed in full and
+        // checked (a move would mean the freeze was unsafe).  k_tail retries the proof every 8
+        // full steps (the bound shrinks as the moments decay); k_pgd proves once, up front.
         if (replay_from < t) {
-            const float bc1a = a.bc[replay_from - 1].x, bc2z = a.bc[t - 2].y;
-            if (replay_still(x, mx, vx, bc1a, bc2z, a) && replay_still(y, my, vy, bc1a, bc2z, a) &&
-                replay_still(z, mz, vz, bc1a, bc2z, a)) {
-                // provably no move: only the moments evolve (same expressions as adam_reg, g = 0)
-                for (int tt = replay_from; tt < t; tt++) {
-                    mx = __fadd_rn(__fmul_rn(a.b1, mx), __fmul_rn(a.omb1, 0.0f));
-                    my = __fadd_rn(__fmul_rn(a.b1, my), __fmul_rn(a.omb1, 0.0f));
-                    mz = __fadd_rn(__fmul_rn(a.b1, mz), __fmul_rn(a.omb1, 0.0f));
-                    vx = __fadd_rn(__fmul_rn(a.b2, vx), __fmul_rn(a.omb2, __fmul_rn(0.0f, 0.0f)));
-                    vy = __fadd_rn(__fmul_rn(a.b2, vy), __fmul_rn(a.omb2, __fmul_rn(0.0f, 0.0f)));
-                    vz = __fadd_rn(__fmul_rn(a.b2, vz), __fmul_rn(a.omb2, __fmul_rn(0.0f, 0.0f)));
+            const float bc2z = a.bc[t - 2].y;
+            int tt = replay_from;
+            for (;;) {
+                const float bc1a = a.bc[tt - 1].x;
+                if (replay_still(x, mx, vx, bc1a, bc2z, a) && replay_still(y, my, vy, bc1a, bc2z, a) &&
+                    replay_still(z, mz, vz, bc1a, bc2z, a)) {
+                    for (; tt < t; tt++) {  // provably no move (same expressions as adam_reg, g = 0)
+                        mx = __fadd_rn(__fmul_rn(a.b1, mx), __fmul_rn(a.omb1, 0.0f));
+                        my = __fadd_rn(__fmul_rn(a.b1, my), __fmul_rn(a.omb1, 0.0f));
+                        mz = __fadd_rn(__fmul_rn(a.b1, mz), __fmul_rn(a.omb1, 0.0f));
+                        vx = __fadd_rn(__fmul_rn(a.b2, vx), __fmul_rn(a.omb2, __fmul_rn(0.0f, 0.0f)));
+                        vy = __fadd_rn(__fmul_rn(a.b2, vy), __fmul_rn(a.omb2, __fmul_rn(0.0f, 0.0f)));
+                        vz = __fadd_rn(__fmul_rn(a.b2, vz), __fmul_rn(a.omb2, __fmul_rn(0.0f, 0.0f)));
+                    }
+                    break;
                 }
-                replay_from = t;
+                flags |= 4;  // full replay steps (reported in the schedule trace)
+                const int t8 = CG ? min(t, tt + 8) : t;  // k_pgd: no retry (registers)
+                for (; tt < t8; tt++) {
+                    const float2 b = a.bc[tt - 1];
+                    const float nx = project(adam_reg(x, 0.0f, mx, vx, a, b.x, b.y, sx), o.x, a.t.xip_f);
+                    const float ny = project(adam_reg(y, 0.0f, my, vy, a, b.x, b.y, sy), o.y, a.t.xip_f);
+                    const float nz = project(adam_reg(z, 0.0f, mz, vz, a, b.x, b.y, sz), o.z, a.t.xip_f);
+                    if (nx != x || ny != y || nz != z) atomicAdd(a.errs, 1ull);  // freeze was unsafe
+                    x = nx;
+                    y = ny;
+                    z = nz;
+                }
+                if (tt >= t || !CG) break;
             }
-        }
-        if (replay_from < t) flags |= 4;  // full replay (reported in the schedule trace)
-        for (int tt = replay_from; tt < t; tt++) {  // frozen iterations: gradient exactly 0
-            const float2 b = a.bc[tt - 1];
-            const float nx = project(adam_reg(x, 0.0f, mx, vx, a, b.x, b.y, sx), o.x, a.t.xip_f);
-            const float ny = project(adam_reg(y, 0.0f, my, vy, a, b.x, b.y, sy), o.y, a.t.xip_f);
-            const float nz = project(adam_reg(z, 0.0f, mz, vz, a, b.x, b.y, sz), o.z, a.t.xip_f);
-            if (nx != x || ny != y || nz != z) atomicAdd(a.errs, 1ull);  // freeze was unsafe
-            x = nx;
-            y = ny;
-            z = nz;
         }
         const float2 b = a.bc[t - 1];
         const float nx = project(adam_reg(x, gx, mx, vx, a, b.x, b.y, sx), o.x, a.t.xip_f);
@@ -258,242 +282,190 @@ __device__ __forceinline__ bool frontier_after(const PgdArgs& a, uint32_t e, int
 }
 
 
-__global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
-    Ctl* ctl = a.ctl;
-    if (!a.count_only && *((volatile int*)&ctl->done)) return;
-    const int t = a.count_only ? 0 : ctl->t + 1;
-    const float4* __restrict__ src;
-    float4* __restrict__ dst;
-    if (a.count_only) {
-        src = (ctl->t_res & 1) ? a.pos1 : a.pos0;
-        dst = nullptr;
-    } else {
-        src = ((t - 1) & 1) ? a.pos1 : a.pos0;
-        dst = (t & 1) ? a.pos1 : a.pos0;
+// per-block K3 working state, shared by k_pgd (one iteration over the grid) and k_tail (one
+// block, many iterations)
+struct K3Ctx {
+    int t;
+    const float4* src;        // positions read (state t-1)
+    float4* dst;              // positions written (state t)
+    bool front, build;
+    uint32_t* unext;          // k_pgd build: touched bitmap for t+1
+    uint32_t* tbn;            // k_tail: membership bitmap of the list for t+1
+    uint32_t* tnext;          // k_tail: the list for t+1
+    uint32_t* n_next;         // k_tail: its length (shared memory)
+    uint32_t* cn;             // this thread's counters, stride PGD_THREADS
+    unsigned long long* lim;  // this thread's loss limbs, stride PGD_THREADS
+    WarpSh* ws;
+    int lane;
+    unsigned long long wk_e, wk_n;  // work done: editables updated, row entries evaluated
+};
+
+// positions: plain loads in k_pgd (measured faster than the non-coherent path for these
+// gathers); k_tail reads what other blocks wrote an iteration earlier (through L2)
+template <bool TAIL>
+__device__ __forceinline__ float4 ldpos(const float4* p) {
+    if (TAIL) return __ldcg(p);
+    return *p;
+}
+
+// k_tail: put editable j on the list for t+1 (once: the membership bitmap dedups)
+__device__ __forceinline__ void tail_push(K3Ctx& k, uint32_t j) {
+    const uint32_t bit = 1u << (j & 31);
+    if (atomicOr(&k.tbn[j >> 5], bit) & bit) return;
+    const uint32_t i = atomicAdd(k.n_next, 1u);
+    if (i < TAIL_CAP) k.tnext[i] = j;
+}
+
+// ---- one batch: up to 32 editables (one per lane, `valid`).  The concatenation of their rows
+// is evaluated flattened across the lanes: CH entries per chunk, NB independent row/partner
+// loads per lane in flight, the terms parked in shared memory; then each lane sums its own
+// row's terms in row order (the pinned order, R14) and applies Adam + the projection to its
+// editable.  Returns whether the lane's editable stays awake.
+template <bool TAIL>
+__device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const uint32_t e, const bool valid) {
+    const Th& th = a.t;
+    WarpSh& ws = *k.ws;
+    const int lane = k.lane;
+    unsigned long long k0 = 0ull;
+    uint32_t len = 0u, fz = 0u;
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid) {
+        k0 = a.rowptr[e];
+        len = (uint32_t)(a.rowptr[e + 1] - k0);
+        p = ldpos<TAIL>(k.src + e);
+        if (k.front) fz = ldst<TAIL>(a.frozen + e);
+        k.wk_e++;
+        k.wk_n += len;
+        k.cn[4 * PGD_THREADS]++;
     }
-    const Th th = a.t;
-    // statistics: active pairs, violated pairs, loss limbs (exact sums, LFX layout), then the
-    // schedule counts: editables left awake, row entries of editables that moved, editables
-    // processed.  Per-thread counters live in shared memory (touched rarely; registers are the
-    // occupancy limit of this latency-bound kernel).
-    // counters (u32 per thread) in LFX/schedule order without the limbs: 0 active, 1 violated,
-    // 2 awake, 3 moved entries, 4 processed, 5 full-replay steps, 6 proven-still replay steps
-    __shared__ unsigned long long lim_sh[6][PGD_THREADS];
-    __shared__ uint32_t cn_sh[NSTAT - 6][PGD_THREADS];
-    uint32_t* cn = &cn_sh[0][threadIdx.x];  // cn[k * PGD_THREADS] = counter k
-    __shared__ WarpSh wsh[PGD_THREADS / 32];
-    unsigned long long wk_e = 0, wk_n = 0;  // work done: editables updated, row entries evaluated
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    WarpSh& ws = wsh[w];
-
-    // frontier (exact active-set skipping): from iteration 2 on, only the editables awake after
-    // t-1 or touched (a partner moved at t-1) are processed.  Bitmaps over the E editables:
-    // awake A[t & 1] read / A[(t+1) & 1] written whole words; touched U[t % 3] read /
-    // U[(t+1) % 3] set by atomics / U[(t+2) % 3] cleared for the next launch.
-    // Building the bitmaps costs a random atomic per partner of every mover, so launch t builds
-    // them only when the previous launch saw few awake editables and movers (ctl->bld); launch
-    // t+1 selects iff launch t built (ctl->sel), else it processes every editable.
-    const bool front = a.frontier && !a.count_only;
-    const bool select = front && ctl->sel;
-    const bool build = front && ctl->bld;
-    const uint32_t n_items = select ? ctl->nsel : a.E;
-    // a block without items (small frontier) only takes part in the final ticket
-    const bool idle = blockIdx.x * (uint32_t)PGD_THREADS >= n_items;
-    if (!idle) {
-#pragma unroll
-        for (int k = 0; k < 6; k++) lim_sh[k][threadIdx.x] = 0ull;
-#pragma unroll
-        for (int k = 0; k < NSTAT - 6; k++) cn_sh[k][threadIdx.x] = 0u;
+    uint32_t off = len;  // exclusive scan of the row lengths over the warp
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, off, o);
+        if (lane >= o) off += v;
     }
-    const uint32_t nw32 = a.nwords;
-    uint32_t* __restrict__ anext = a.abits + (size_t)((t + 1) & 1) * nw32;
-    uint32_t* __restrict__ unext = a.ubits + (size_t)((t + 1) % 3) * nw32;
-
-    auto count = [&](const Term& tm, uint32_t ent) {  // each pair once, at its lower-gid endpoint
-        if (ent & ENT_UPPER) {
-            if (tm.kind) {
-                cn[0]++;
-                lfx_add<PGD_THREADS>(&lim_sh[0][threadIdx.x], (double)tm.ee * (double)tm.ee);
-            }
-            if (tm.viol) cn[PGD_THREADS]++;
-        }
-    };
-
-    // ---- one batch: up to 32 editables (one per lane, `valid`).  The concatenation of their
-    // rows is evaluated flattened across the lanes: CH entries per chunk, NB independent
-    // row/partner loads per lane in flight, the terms parked in shared memory; then each lane
-    // sums its own row's terms in row order (the pinned order, R14) and applies Adam + the
-    // projection to its editable.  Returns whether the lane's editable stays awake.
-    auto process_batch = [&](const uint32_t e, const bool valid) -> bool {
-        unsigned long long k0 = 0ull;
-        uint32_t len = 0u, fz = 0u;
-        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid) {
-            k0 = a.rowptr[e];
-            len = (uint32_t)(a.rowptr[e + 1] - k0);
-            p = src[e];
-            if (front) fz = a.frozen[e];
-            wk_e++;
-            wk_n += len;
-            cn[4 * PGD_THREADS]++;
-        }
-        uint32_t off = len;  // exclusive scan of the row lengths over the warp
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, off, o);
-            if (lane >= o) off += v;
-        }
-        const uint32_t T = __shfl_sync(0xffffffffu, off, 31);
-        off -= len;
-        ws.off[lane] = off;
-        ws.k0[lane] = k0;
-        ws.p[lane] = p;
+    const uint32_t T = __shfl_sync(0xffffffffu, off, 31);
+    off -= len;
+    ws.off[lane] = off;
+    ws.k0[lane] = k0;
+    ws.p[lane] = p;
+    __syncwarp();
+    bool any_active = false;
+    float gx = 0.0f, gy = 0.0f, gz = 0.0f;
+    for (uint32_t c = 0; c < T; c += CH) {
+        // this lane's own row inside the chunk: mark which lane owns each position (unless one
+        // row covers the whole chunk, the long-row case)
+        const uint32_t f0 = max(off, c), f1 = min(off + len, c + CH);
+        const unsigned cover = __ballot_sync(0xffffffffu, f0 == c && f1 == min(c + CH, T) && f1 > f0);
+        const int whole = cover ? __ffs(cover) - 1 : -1;
+        if (whole < 0)
+            for (uint32_t f = f0; f < f1; f++) ws.seg[f - c] = (unsigned char)lane;
         __syncwarp();
-        bool any_active = false;
-        float gx = 0.0f, gy = 0.0f, gz = 0.0f;
-        for (uint32_t c = 0; c < T; c += CH) {
-            // this lane's own row inside the chunk: mark which lane owns each position (unless one
-            // row covers the whole chunk, the long-row case)
-            const uint32_t f0 = max(off, c), f1 = min(off + len, c + CH);
-            const unsigned cover = __ballot_sync(0xffffffffu, f0 == c && f1 == min(c + CH, T) && f1 > f0);
-            const int whole = cover ? __ffs(cover) - 1 : -1;
-            if (whole < 0)
-                for (uint32_t f = f0; f < f1; f++) ws.seg[f - c] = (unsigned char)lane;
-            __syncwarp();
-            uint32_t ent[NB];
-            int sg[NB];
+        uint32_t ent[NB];
+        int sg[NB];
 #pragma unroll
-            for (int j = 0; j < NB; j++) {
-                const uint32_t f = c + lane + 32u * j;
-                sg[j] = -1;
-                ent[j] = 0u;
-                if (f < T) {
-                    const int o = whole >= 0 ? whole : ws.seg[f - c];
-                    sg[j] = o;
-                    ent[j] = a.rows[ws.k0[o] + (f - ws.off[o])];
-                }
-            }
-            float4 q[NB];
-#pragma unroll
-            for (int j = 0; j < NB; j++)
-                if (sg[j] >= 0) q[j] = src[ent[j] & ENT_IDX];
-#pragma unroll
-            for (int j = 0; j < NB; j++) {
-                if (sg[j] >= 0) {
-                    const Term tm = pair_term(ws.p[sg[j]], q[j], ent[j], th);
-                    count(tm, ent[j]);
-                    ws.t[lane + 32 * j] = make_float4(tm.px, tm.py, tm.pz, __int_as_float(tm.kind));
-                }
-            }
-            __syncwarp();
-            // own row, in row order (R14).  Branch-free: an inactive term is (+0, +0, +0) and a
-            // coincident one (+-2e, +0, +0); g + 0 == g exactly since g is never -0 (it starts at
-            // +0 and x + (-x) rounds to +0).  Loads of 4 terms are issued ahead of the sums.
-            uint32_t f = f0;
-            for (; f + 4 <= f1; f += 4) {
-                float4 u[4];
-#pragma unroll
-                for (int i = 0; i < 4; i++) u[i] = ws.t[f + i - c];
-#pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    any_active |= __float_as_int(u[i].w) != 0;
-                    gx = __fadd_rn(gx, u[i].x);
-                    gy = __fadd_rn(gy, u[i].y);
-                    gz = __fadd_rn(gz, u[i].z);
-                }
-            }
-            for (; f < f1; f++) {
-                const float4 u = ws.t[f - c];
-                any_active |= __float_as_int(u.w) != 0;
-                gx = __fadd_rn(gx, u.x);
-                gy = __fadd_rn(gy, u.y);
-                gz = __fadd_rn(gz, u.z);
-            }
-            __syncwarp();
-        }
-        int flags = 0;
-        bool awake = false;
-        if (valid && !a.count_only) {
-            const int replay_from = (fz != 0u && fz != FZ_NEVER) ? (int)fz + 1 : t;  // zero-gradient
-            flags = update(a, e, p, gx, gy, gz, t, replay_from, dst);               // steps missed while frozen
-            if (replay_from < t) cn[((flags & 4) ? 5 : 6) * PGD_THREADS] += (unsigned)(t - replay_from);
-            if (a.frontier) {
-                awake = frontier_after(a, e, t, flags, any_active, fz);
-                if (awake) cn[2 * PGD_THREADS]++;
-                if (flags & 1) cn[3 * PGD_THREADS] += len;
+        for (int j = 0; j < NB; j++) {
+            const uint32_t f = c + lane + 32u * j;
+            sg[j] = -1;
+            ent[j] = 0u;
+            if (f < T) {
+                const int o = whole >= 0 ? whole : ws.seg[f - c];
+                sg[j] = o;
+                ent[j] = a.rows[ws.k0[o] + (f - ws.off[o])];
             }
         }
-        if (build) {  // a mover touches its owned partners for t+1: the warp walks each mover's row
-            unsigned mv = __ballot_sync(0xffffffffu, (flags & 1) != 0);
-            while (mv) {
-                const int sl = __ffs(mv) - 1;
-                mv &= mv - 1;
-                const unsigned long long kb = __shfl_sync(0xffffffffu, k0, sl);
-                const uint32_t ln = __shfl_sync(0xffffffffu, len, sl);
-                for (uint32_t i = lane; i < ln; i += 32) {
-                    const uint32_t j = a.rows[kb + i] & ENT_IDX;
-                    if (j < a.E) atomicOr(&unext[j >> 5], 1u << (j & 31));  // fire-and-forget (RED)
+        float4 q[NB];
+#pragma unroll
+        for (int j = 0; j < NB; j++)
+            if (sg[j] >= 0) q[j] = ldpos<TAIL>(k.src + (ent[j] & ENT_IDX));
+#pragma unroll
+        for (int j = 0; j < NB; j++) {
+            if (sg[j] >= 0) {
+                const Term tm = pair_term(ws.p[sg[j]], q[j], ent[j], th);
+                if (ent[j] & ENT_UPPER) {  // each pair counted once, at its lower-gid endpoint
+                    if (tm.kind) {
+                        k.cn[0]++;
+                        lfx_add<PGD_THREADS>(k.lim, (double)tm.ee * (double)tm.ee);
+                    }
+                    if (tm.viol) k.cn[PGD_THREADS]++;
+                }
+                ws.t[lane + 32 * j] = make_float4(tm.px, tm.py, tm.pz, __int_as_float(tm.kind));
+            }
+        }
+        __syncwarp();
+        // own row, in row order (R14).  Branch-free: an inactive term is (+0, +0, +0) and a
+        // coincident one (+-2e, +0, +0); g + 0 == g exactly since g is never -0 (it starts at
+        // +0 and x + (-x) rounds to +0).  Loads of 4 terms are issued ahead of the sums.
+        uint32_t f = f0;
+        for (; f + 4 <= f1; f += 4) {
+            float4 u[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) u[i] = ws.t[f + i - c];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                any_active |= __float_as_int(u[i].w) != 0;
+                gx = __fadd_rn(gx, u[i].x);
+                gy = __fadd_rn(gy, u[i].y);
+                gz = __fadd_rn(gz, u[i].z);
+            }
+        }
+        for (; f < f1; f++) {
+            const float4 u = ws.t[f - c];
+            any_active |= __float_as_int(u.w) != 0;
+            gx = __fadd_rn(gx, u.x);
+            gy = __fadd_rn(gy, u.y);
+            gz = __fadd_rn(gz, u.z);
+        }
+        __syncwarp();
+    }
+    int flags = 0;
+    bool awake = false;
+    if (valid && !a.count_only) {
+        const int t = k.t;
+        const int replay_from = (fz != 0u && fz != FZ_NEVER) ? (int)fz + 1 : t;  // zero-gradient
+        flags = update<TAIL>(a, e, p, gx, gy, gz, t, replay_from, k.dst);             // steps missed while frozen
+        if (replay_from < t) k.cn[((flags & 4) ? 5 : 6) * PGD_THREADS] += (unsigned)(t - replay_from);
+        if (a.frontier) {
+            awake = frontier_after(a, e, t, flags, any_active, fz);
+            if (awake) k.cn[2 * PGD_THREADS]++;
+            if (flags & 1) k.cn[3 * PGD_THREADS] += len;
+        }
+    }
+    if (TAIL || k.build) {  // a mover touches its owned partners for t+1: the warp walks each mover's row
+        unsigned mv = __ballot_sync(0xffffffffu, (flags & 1) != 0);
+        while (mv) {
+            const int sl = __ffs(mv) - 1;
+            mv &= mv - 1;
+            const unsigned long long kb = __shfl_sync(0xffffffffu, k0, sl);
+            const uint32_t ln = __shfl_sync(0xffffffffu, len, sl);
+            for (uint32_t i = lane; i < ln; i += 32) {
+                const uint32_t j = a.rows[kb + i] & ENT_IDX;
+                if (j < a.E) {
+                    if (TAIL) tail_push(k, j);
+                    else atomicOr(&k.unext[j >> 5], 1u << (j & 31));  // fire-and-forget (RED)
                 }
             }
         }
-        return awake;
-    };
+    }
+    return awake;
+}
 
-    // ---- work items: every editable (sweep) or the selected list built by k_select; a warp
-    // takes 32 consecutive items per batch
-    const uint32_t gw = blockIdx.x * (PGD_THREADS / 32) + w, nwarps = gridDim.x * (PGD_THREADS / 32);
-    for (uint32_t b0 = gw * 32u; b0 < n_items; b0 += nwarps * 32u) {
-        const uint32_t k = b0 + lane;
-        const bool valid = k < n_items;
-        const uint32_t e = valid ? (select ? a.slist[k] : k) : 0xFFFFFFFFu;
-        const bool awake = process_batch(valid ? e : 0u, valid);
-        if (build) {  // awake bits for t+1, one atomic per distinct word of the batch
-            const uint32_t word = e >> 5;
-            const unsigned peers = __match_any_sync(0xffffffffu, word);
-            const uint32_t bits = __reduce_or_sync(peers, awake ? (1u << (e & 31)) : 0u);
-            if (valid && bits && lane == __ffs(peers) - 1) atomicOr(&anext[word], bits);
-        }
-    }
+// statistic s of the block (warp-cooperative; all lanes get it).  LFX layout: 0, 1 counters;
+// 2..7 loss limbs; 8.. schedule counters 2..
+__device__ __forceinline__ unsigned long long block_stat(int s, int lane,
+                                                         const unsigned long long (*lim_sh)[PGD_THREADS],
+                                                         const uint32_t (*cn_sh)[PGD_THREADS]) {
+    unsigned long long v = 0ull;
+    if (s >= 2 && s < LFX_STATS)
+        for (int i = lane; i < PGD_THREADS; i += 32) v += lim_sh[s - 2][i];
+    else
+        for (int i = lane; i < PGD_THREADS; i += 32) v += cn_sh[s < 2 ? s : s - 6][i];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 
-    // ---- work counters (integers: order-free), one atomic per warp
-    if (!a.count_only) {
-        for (int o = 16; o > 0; o >>= 1) {
-            wk_e += __shfl_down_sync(0xffffffffu, wk_e, o);
-            wk_n += __shfl_down_sync(0xffffffffu, wk_n, o);
-        }
-        if (lane == 0 && wk_e) {
-            atomicAdd(&a.work[0], wk_e);
-            atomicAdd(&a.work[1], wk_n);
-        }
-    }
-
-    // ---- statistics: integer sums (LFX), so the order of warps, blocks and ranks is free
-    __shared__ bool am_last;
-    __syncthreads();
-    for (int k = w; k < NSTAT && !idle; k += PGD_THREADS / 32) {  // warp w sums statistics w, w+8, ...
-        unsigned long long v = 0ull;
-        // statistic k (LFX layout): 0, 1 counters; 2..7 limbs; 8.. counters 2..
-        if (k >= 2 && k < LFX_STATS)
-            for (int i = lane; i < PGD_THREADS; i += 32) v += lim_sh[k - 2][i];
-        else
-            for (int i = lane; i < PGD_THREADS; i += 32) v += cn_sh[k < 2 ? k : k - 6][i];
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-        if (lane == 0 && v) atomicAdd(&ctl->acc[k], v);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned int tk = atomicAdd(&ctl->ticket, 1u);
-        am_last = (tk == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!am_last || threadIdx.x != 0) return;
-    // last block: every other block's sums are in ctl->acc
-    __threadfence();
-    unsigned long long tot[NSTAT];
-    for (int k = 0; k < NSTAT; k++) {
-        tot[k] = ((volatile unsigned long long*)ctl->acc)[k];
-        ctl->acc[k] = 0ull;
-    }
+// the end of iteration t (one thread): publish its statistics and apply the stop rule (R11) to
+// the state the iteration READ; if it holds, that buffer is the result
+__device__ void k3_finish(const PgdArgs& a, Ctl* ctl, int t, const unsigned long long* tot, bool build) {
     const unsigned long long tu = tot[0], tv = tot[1];
     const double td = lfx_value(tot + 2);
     ctl->active = tu;
@@ -509,7 +481,7 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
         ts[3] = (long long)tot[LFX_STATS + 3];
         ts[4] = (long long)tot[LFX_STATS + 4];
     }
-    if (front) {
+    if (a.frontier && !a.count_only) {
         ctl->sel = build ? 1 : 0;
         ctl->bld = (tot[LFX_STATS] + tot[LFX_STATS + 1] <= (unsigned long long)a.E * 4ull) ? 1 : 0;
     }
@@ -531,7 +503,247 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
         }
         ctl->t = t;
     }
+}
+
+__global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
+    Ctl* ctl = a.ctl;
+    if (!a.count_only && *((volatile int*)&ctl->done)) return;
+    const int t = a.count_only ? 0 : ctl->t + 1;
+    // statistics: active pairs, violated pairs, loss limbs (exact sums, LFX layout), then the
+    // schedule counts.  Per-thread counters live in shared memory (touched rarely; registers are
+    // the occupancy limit of this latency-bound kernel): 0 active, 1 violated, 2 awake, 3 moved
+    // entries, 4 processed, 5 full-replay steps, 6 proven-still replay steps
+    __shared__ unsigned long long lim_sh[6][PGD_THREADS];
+    __shared__ uint32_t cn_sh[NSTAT - 6][PGD_THREADS];
+    __shared__ WarpSh wsh[PGD_THREADS / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    K3Ctx k;
+    k.t = t;
+    if (a.count_only) {
+        k.src = (ctl->t_res & 1) ? a.pos1 : a.pos0;
+        k.dst = nullptr;
+    } else {
+        k.src = ((t - 1) & 1) ? a.pos1 : a.pos0;
+        k.dst = (t & 1) ? a.pos1 : a.pos0;
+    }
+    // frontier (exact active-set skipping): from iteration 2 on, only the editables awake after
+    // t-1 or touched (a partner moved at t-1) are processed.  Bitmaps over the E editables:
+    // awake A[t & 1] read / A[(t+1) & 1] written whole words; touched U[t % 3] read /
+    // U[(t+1) % 3] set by atomics / U[(t+2) % 3] cleared for the next launch.
+    // Building the bitmaps costs a random atomic per partner of every mover, so launch t builds
+    // them only when the previous launch saw few awake editables and movers (ctl->bld); launch
+    // t+1 selects iff launch t built (ctl->sel), else it processes every editable.
+    k.front = a.frontier && !a.count_only;
+    const bool select = k.front && ctl->sel;
+    k.build = k.front && ctl->bld;
+    const uint32_t nw32 = a.nwords;
+    k.unext = a.ubits + (size_t)((t + 1) % 3) * nw32;
+    k.tbn = k.tnext = k.n_next = nullptr;
+    k.cn = &cn_sh[0][threadIdx.x];  // cn[s * PGD_THREADS] = counter s
+    k.lim = &lim_sh[0][threadIdx.x];
+    k.ws = &wsh[w];
+    k.lane = lane;
+    k.wk_e = k.wk_n = 0ull;
+    const uint32_t n_items = select ? ctl->nsel : a.E;
+    // a block without items (small frontier) only takes part in the final ticket
+    const bool idle = blockIdx.x * (uint32_t)PGD_THREADS >= n_items;
+    if (!idle) {
+#pragma unroll
+        for (int s = 0; s < 6; s++) lim_sh[s][threadIdx.x] = 0ull;
+#pragma unroll
+        for (int s = 0; s < NSTAT - 6; s++) cn_sh[s][threadIdx.x] = 0u;
+    }
+    uint32_t* __restrict__ anext = a.abits + (size_t)((t + 1) & 1) * nw32;
+
+    // ---- work items: every editable (sweep) or the selected list built by k_select; a warp
+    // takes 32 consecutive items per batch
+    const uint32_t gw = blockIdx.x * (PGD_THREADS / 32) + w, nwarps = gridDim.x * (PGD_THREADS / 32);
+    for (uint32_t b0 = gw * 32u; b0 < n_items; b0 += nwarps * 32u) {
+        const uint32_t kk = b0 + lane;
+        const bool valid = kk < n_items;
+        const uint32_t e = valid ? (select ? a.slist[kk] : kk) : 0xFFFFFFFFu;
+        const bool awake = process_batch<false>(a, k, valid ? e : 0u, valid);
+        if (k.build) {  // awake bits for t+1, one atomic per distinct word of the batch
+            const uint32_t word = e >> 5;
+            const unsigned peers = __match_any_sync(0xffffffffu, word);
+            const uint32_t bits = __reduce_or_sync(peers, awake ? (1u << (e & 31)) : 0u);
+            if (valid && bits && lane == __ffs(peers) - 1) atomicOr(&anext[word], bits);
+        }
+    }
+
+    // ---- work counters (integers: order-free), one atomic per warp
+    if (!a.count_only) {
+        for (int o = 16; o > 0; o >>= 1) {
+            k.wk_e += __shfl_down_sync(0xffffffffu, k.wk_e, o);
+            k.wk_n += __shfl_down_sync(0xffffffffu, k.wk_n, o);
+        }
+        if (lane == 0 && k.wk_e) {
+            atomicAdd(&a.work[0], k.wk_e);
+            atomicAdd(&a.work[1], k.wk_n);
+        }
+    }
+
+    // ---- statistics: integer sums (LFX), so the order of warps, blocks and ranks is free
+    __shared__ bool am_last;
+    __syncthreads();
+    for (int s = w; s < NSTAT && !idle; s += PGD_THREADS / 32) {  // warp w sums statistics w, w+8, ...
+        const unsigned long long v = block_stat(s, lane, lim_sh, cn_sh);
+        if (lane == 0 && v) atomicAdd(&ctl->acc[s], v);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int tk = atomicAdd(&ctl->ticket, 1u);
+        am_last = (tk == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!am_last || threadIdx.x != 0) return;
+    // last block: every other block's sums are in ctl->acc
     __threadfence();
+    unsigned long long tot[NSTAT];
+    for (int s = 0; s < NSTAT; s++) {
+        tot[s] = ((volatile unsigned long long*)ctl->acc)[s];
+        ctl->acc[s] = 0ull;
+    }
+    k3_finish(a, ctl, t, tot, k.build);
+    __threadfence();
+}
+
+// k_tail's grid barrier.  The TAIL_BLOCKS blocks are co-resident (one per SM at most, nothing
+// else runs on the stream); acquire loads + fences make the other blocks' writes visible.
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void tail_grid_sync(Ctl* ctl) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = ld_acquire(&ctl->bar_gen);
+        __threadfence();
+        if (atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1) {
+            ctl->bar_count = 0u;  // nobody arrives at the next barrier before the generation moves
+            __threadfence();
+            atomicAdd(&ctl->bar_gen, 1u);
+        } else {
+            while (ld_acquire(&ctl->bar_gen) == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// K3 tail: once the frontier is small (the long convergence tail: a few hundred
+// editables per iteration for ~1,200 iterations on C4), TAIL_BLOCKS co-resident blocks run the
+// remaining iterations back to back in one launch, separated by grid barriers -- the same
+// per-editable work as k_pgd, with lists instead of bitmaps, and the list spread over all warps
+// (a short list gets one editable per warp, so rows are evaluated with all lanes).  It takes
+// over after k_select of a selected iteration whose list has at most TAIL_ENTER editables, and
+// runs until the stop rule or T_max ends the loop, or hands back to the grid kernels (the next
+// iteration a full sweep, exact) when a list would exceed TAIL_CAP.  The list for t+1 holds the
+// editables left awake at t and the partners of those that moved at t (deduplicated by a
+// membership bitmap): k_select's set.  Per iteration: process, block statistics -> ctl->acc,
+// barrier, block 0 applies the stop rule (k3_finish), barrier.
+__global__ void __launch_bounds__(PGD_THREADS, 1) k_tail(PgdArgs a) {
+    Ctl* ctl = a.ctl;
+    // every block reads the same entry state: nothing changes it before the first barrier
+    if (!a.frontier || a.red || a.count_only || !a.tlist) return;
+    if (*((volatile int*)&ctl->done) || !ctl->sel || ctl->nsel > TAIL_ENTER) return;
+    __shared__ unsigned long long lim_sh[6][PGD_THREADS];
+    __shared__ uint32_t cn_sh[NSTAT - 6][PGD_THREADS];
+    __shared__ WarpSh wsh[PGD_THREADS / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    K3Ctx k;
+    k.front = true;
+    k.build = false;
+    k.unext = nullptr;
+    k.n_next = &ctl->tail_nn;
+    k.cn = &cn_sh[0][threadIdx.x];
+    k.lim = &lim_sh[0][threadIdx.x];
+    k.ws = &wsh[w];
+    k.lane = lane;
+    k.wk_e = k.wk_n = 0ull;
+    const uint32_t* cur = a.slist;
+    uint32_t n_cur = ctl->nsel;
+    int t = ctl->t + 1;
+    const uint32_t nwarps = gridDim.x * (PGD_THREADS / 32), gw = blockIdx.x * (PGD_THREADS / 32) + w;
+    const uint32_t gt = blockIdx.x * PGD_THREADS + threadIdx.x, gs = gridDim.x * PGD_THREADS;
+    for (;;) {
+        uint32_t* nxt = a.tlist + (size_t)(t & 1) * TAIL_CAP;
+        k.t = t;
+        k.src = ((t - 1) & 1) ? a.pos1 : a.pos0;
+        k.dst = (t & 1) ? a.pos1 : a.pos0;
+        k.tbn = a.tbits + (size_t)(t & 1) * a.nwords;
+        k.tnext = nxt;
+#pragma unroll
+        for (int s = 0; s < 6; s++) lim_sh[s][threadIdx.x] = 0ull;
+#pragma unroll
+        for (int s = 0; s < NSTAT - 6; s++) cn_sh[s][threadIdx.x] = 0u;
+        __syncthreads();
+        // gi editables per warp batch, so that the list covers all warps once
+        const uint32_t gi = min(32u, max(1u, (n_cur + nwarps - 1) / nwarps));
+        const uint32_t nbatch = (n_cur + gi - 1) / gi;
+        for (uint32_t bt = gw; bt < nbatch; bt += nwarps) {
+            const uint32_t kk = bt * gi + lane;
+            const bool valid = lane < (int)gi && kk < n_cur;
+            const uint32_t e = valid ? __ldcg(cur + kk) : 0u;
+            const bool awake = process_batch<true>(a, k, e, valid);
+            if (valid && awake) tail_push(k, e);
+        }
+        __syncthreads();
+        for (int s = w; s < NSTAT; s += PGD_THREADS / 32) {
+            const unsigned long long v = block_stat(s, lane, lim_sh, cn_sh);
+            if (lane == 0 && v) atomicAdd(&ctl->acc[s], v);
+        }
+        // the current list's members leave its membership bitmap (clean for the list of t+2)
+        if (cur != a.slist) {
+            uint32_t* tbc = a.tbits + (size_t)((t - 1) & 1) * a.nwords;
+            for (uint32_t i = gt; i < n_cur; i += gs) tbc[__ldcg(cur + i) >> 5] = 0u;
+        }
+        tail_grid_sync(ctl);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            unsigned long long tot[NSTAT];
+            for (int s = 0; s < NSTAT; s++) {
+                tot[s] = ((volatile unsigned long long*)ctl->acc)[s];
+                ctl->acc[s] = 0ull;
+            }
+            k3_finish(a, ctl, t, tot, false);
+            const uint32_t nn = *((volatile unsigned*)&ctl->tail_nn);
+            int go = !ctl->done;
+            if (go && nn > TAIL_CAP) {  // hand back: the next iteration sweeps every editable
+                ctl->sel = 0;
+                ctl->bld = 0;
+                go = 0;
+            }
+            ctl->tail_go = go;
+            ctl->tail_ncur = nn;
+            ctl->tail_nn = 0u;
+            __threadfence();
+        }
+        tail_grid_sync(ctl);
+        const int go = *((volatile int*)&ctl->tail_go);
+        const uint32_t nn = *((volatile unsigned*)&ctl->tail_ncur);
+        if (!go) {  // leave the membership bitmap of the list for t+1 clean
+            uint32_t* tbn = k.tbn;
+            if (nn > TAIL_CAP)
+                for (uint32_t i = gt; i < a.nwords; i += gs) tbn[i] = 0u;
+            else
+                for (uint32_t i = gt; i < nn; i += gs) tbn[__ldcg(nxt + i) >> 5] = 0u;
+            break;
+        }
+        cur = nxt;
+        n_cur = nn;
+        t++;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        k.wk_e += __shfl_down_sync(0xffffffffu, k.wk_e, o);
+        k.wk_n += __shfl_down_sync(0xffffffffu, k.wk_n, o);
+    }
+    if (lane == 0 && k.wk_e) {
+        atomicAdd(&a.work[0], k.wk_e);
+        atomicAdd(&a.work[1], k.wk_n);
+    }
 }
 
 // Frontier selection for iteration t (runs before k_pgd in every iteration): the editables
@@ -598,6 +810,11 @@ __global__ void k_ctl_reset(Ctl* ctl) {
     ctl->sel = 0;
     ctl->bld = 0;
     ctl->nsel = 0u;
+    ctl->tail_nn = 0u;
+    ctl->tail_ncur = 0u;
+    ctl->tail_go = 0;
+    ctl->bar_count = 0u;
+    ctl->bar_gen = 0u;
 }
 
 __global__ void k_reset_pos(int64_t Ea, const uint32_t* __restrict__ slotE, const float4* __restrict__ dec4,
@@ -674,6 +891,8 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.abits = c->fbits.p;
     a.slist = c->slist.p;
     a.ubits = c->fbits.p + 2 * (size_t)a.nwords;
+    a.tbits = c->fbits.p + 5 * (size_t)a.nwords;
+    a.tlist = c->tlist.p;
     return a;
 }
 
@@ -736,9 +955,10 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     }
     CC_TRY(cc_ensure(c, c->frozen, (size_t)std::max<int64_t>(E, 1), "frontier state"));
     const size_t nwords = (size_t)((std::max<int64_t>(E, 1) + 31) / 32);
-    CC_TRY(cc_ensure(c, c->fbits, 5 * nwords, "frontier bitmaps"));
+    CC_TRY(cc_ensure(c, c->fbits, 7 * nwords, "frontier bitmaps"));
     CC_TRY(cc_ensure(c, c->slist, (size_t)std::max<int64_t>(E, 1), "frontier selection"));
-    CC_CUDA(c, cudaMemsetAsync(c->fbits.p, 0, 5 * nwords * sizeof(uint32_t), c->stream));
+    CC_TRY(cc_ensure(c, c->tlist, 2 * (size_t)TAIL_CAP, "frontier tail lists"));
+    CC_CUDA(c, cudaMemsetAsync(c->fbits.p, 0, 7 * nwords * sizeof(uint32_t), c->stream));
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
     CC_CUDA(c, cudaMemsetAsync(c->counters.p + 15, 0, sizeof(unsigned long long), c->stream));
     if (E > 0)
@@ -767,6 +987,15 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     CCL(c, k_ctl_reset<<<1, 1, 0, c->stream>>>(c->ctl.p));
     const int nb = pgd_blocks(E);
     const int batch = c->p.graph_batch > 0 ? c->p.graph_batch : 16;
+    // k_tail (single GPU; CC_NO_TAIL=1 disables it, a diagnostic)
+    const bool use_tail = c->nranks == 1 && !(std::getenv("CC_NO_TAIL") && std::getenv("CC_NO_TAIL")[0] == '1');
+    const int k3_per_iter = use_tail ? 3 : 2;  // k_select (+ k_tail) + k_pgd
+    int tail_blocks = TAIL_BLOCKS;  // co-resident: at most one per SM
+    {
+        int sms = 0;
+        CC_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+        if (sms > 0 && sms < tail_blocks) tail_blocks = sms;
+    }
     PgdArgs a = make_args(c, 0);
     // initial statistics of P_hat^(0) for the report
     PgdArgs a0 = make_args(c, 1);
@@ -794,6 +1023,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
         put(&a, sizeof(a));
         put(&nb, sizeof(nb));
         put(&batch, sizeof(batch));
+        put(&use_tail, sizeof(use_tail));
         if (c->nranks > 1) {
             for (int d = 0; d < 2; d++) {
                 const void* ptrs[4] = {c->send_e[d].p, c->recv_e[d].p, c->rsb[d].p, c->rrb[d].p};
@@ -820,6 +1050,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
             for (int k = 0; k < batch; k++) {
                 if (c->p.profile) cudaEventRecordWithFlags(c->graph_ev[2 * k], c->stream, cudaEventRecordExternal);
                 CCL(c, k_select<<<nb, PGD_THREADS, 0, c->stream>>>(a));
+                if (use_tail) CCL(c, k_tail<<<tail_blocks, PGD_THREADS, 0, c->stream>>>(a));
                 CCL(c, k_pgd<<<nb, PGD_THREADS, 0, c->stream>>>(a));
                 if (c->p.profile)
                     cudaEventRecordWithFlags(c->graph_ev[2 * k + 1], c->stream, cudaEventRecordExternal);
@@ -836,7 +1067,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
                     c->launches = l0;
                 }
             }
-            c->launches -= 2 * batch;  // captured, not launched
+            c->launches -= k3_per_iter * batch;  // captured, not launched
             cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
             CC_CUDA(c, ce);
             CC_CUDA(c, cudaGraphInstantiate(&c->pgd_exec, graph, 0));
@@ -846,7 +1077,7 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
         int t_before = 0;
         for (;;) {
             CC_CUDA(c, cudaGraphLaunch(c->pgd_exec, c->stream));
-            c->launches += batch * (2 + c->launches_per_iter_tail);
+            c->launches += batch * (k3_per_iter + c->launches_per_iter_tail);
             CC_CUDA(c, cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
             CC_CUDA(c, cudaStreamSynchronize(c->stream));
             const Ctl h = *c->h_ctl;
