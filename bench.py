@@ -29,6 +29,9 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+# NCCL's version banner goes to stderr: stdout carries exactly one JSON line
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
 import synth  # noqa: E402
 
 METRIC = "corrected Mparticles/s (device-timed, 1/2/4/8 B200) and % HBM roofline; MCC=1"

@@ -48,6 +48,7 @@ struct WarpSh {               // per-warp staging of K3's flattened row evaluati
     float4 p[32];             // positions of the warp's 32 editables
     unsigned long long k0[32];
     uint32_t off[32];         // exclusive scan of the row lengths
+    uint32_t ent[CH];         // partner editable of each chunk entry (the movers' touches)
     unsigned char seg[CH];    // owning lane of each chunk entry
 };
 
@@ -351,12 +352,14 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
     __syncwarp();
     bool any_active = false;
     float gx = 0.0f, gy = 0.0f, gz = 0.0f;
+    int whole_last = -1;  // the last chunk's single owner (-1: owners in ws.seg)
     for (uint32_t c = 0; c < T; c += CH) {
         // this lane's own row inside the chunk: mark which lane owns each position (unless one
         // row covers the whole chunk, the long-row case)
         const uint32_t f0 = max(off, c), f1 = min(off + len, c + CH);
         const unsigned cover = __ballot_sync(0xffffffffu, f0 == c && f1 == min(c + CH, T) && f1 > f0);
         const int whole = cover ? __ffs(cover) - 1 : -1;
+        whole_last = whole;
         if (whole < 0)
             for (uint32_t f = f0; f < f1; f++) ws.seg[f - c] = (unsigned char)lane;
         __syncwarp();
@@ -380,6 +383,7 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
 #pragma unroll
         for (int j = 0; j < NB; j++) {
             if (sg[j] >= 0) {
+                ws.ent[lane + 32 * j] = ent[j] & ENT_IDX;
                 const Term tm = pair_term(ws.p[sg[j]], q[j], ent[j], th);
                 if (ent[j] & ENT_UPPER) {  // each pair counted once, at its lower-gid endpoint
                     if (tm.kind) {
@@ -430,9 +434,22 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
             if (flags & 1) k.cn[3 * PGD_THREADS] += len;
         }
     }
-    if (TAIL || k.build) {  // a mover touches its owned partners for t+1: the warp walks each mover's row
+    if (TAIL || k.build) {  // a mover touches its owned partners for t+1
         unsigned mv = __ballot_sync(0xffffffffu, (flags & 1) != 0);
-        while (mv) {
+        if (mv && T <= CH) {  // the batch's entries are still staged: each lane touches its own
+            for (uint32_t f = lane; f < T; f += 32u) {
+                {
+                    const int o = whole_last >= 0 ? whole_last : ws.seg[f];
+                    const uint32_t jj = ws.ent[f];
+                    if (((mv >> o) & 1u) && jj < a.E) {
+                        if (TAIL) tail_push(k, jj);
+                        else atomicOr(&k.unext[jj >> 5], 1u << (jj & 31));  // fire-and-forget (RED)
+                    }
+                }
+            }
+            mv = 0u;
+        }
+        while (mv) {  // longer batches: the warp walks each mover's row
             const int sl = __ffs(mv) - 1;
             mv &= mv - 1;
             const unsigned long long kb = __shfl_sync(0xffffffffu, k0, sl);
@@ -441,7 +458,7 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
                 const uint32_t j = a.rows[kb + i] & ENT_IDX;
                 if (j < a.E) {
                     if (TAIL) tail_push(k, j);
-                    else atomicOr(&k.unext[j >> 5], 1u << (j & 31));  // fire-and-forget (RED)
+                    else atomicOr(&k.unext[j >> 5], 1u << (j & 31));
                 }
             }
         }
