@@ -86,18 +86,21 @@ __global__ void k_resolve(int64_t n, const uint32_t* __restrict__ cls, ClassBase
 }
 
 // pass 2 (each unordered pair once again): both entries of every band pair, placed by a
-// per-row cursor (the order inside a row is fixed afterwards by the gid sort)
+// per-row cursor (the order inside a row is fixed afterwards by the gid sort).  One thread per
+// EDITABLE particle (slotE; a band pair has two editable endpoints, so the forward search from
+// editables alone finds every pair): all lanes busy, and the class-major numbering gives a
+// warp neighbours of similar row length.
 __global__ void __launch_bounds__(PAIR_THREADS)
-k_pairs_fill(int64_t n, const float4* __restrict__ orig4, const uint32_t* __restrict__ xk,
-             const uint32_t* __restrict__ cs, Grid g, Th t, double r, const uint32_t* __restrict__ deg,
+k_pairs_fill(uint32_t e_all, const uint32_t* __restrict__ slotE, const float4* __restrict__ orig4,
+             const uint32_t* __restrict__ xk, const uint32_t* __restrict__ cs, Grid g, Th t, double r,
              const uint32_t* __restrict__ eidx, uint32_t e_own, const unsigned long long* __restrict__ rowptr,
              uint32_t* __restrict__ cur, uint32_t* __restrict__ rows, uint32_t* __restrict__ par_orig) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
-    if (deg[s] == 0u) return;  // not editable: no band pair at all
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= e_all) return;
+    const uint32_t s = slotE[e];
     const float4 p = orig4[s];
     const uint32_t gp = __float_as_uint(p.w);
-    const uint32_t es = eidx[s];
+    const uint32_t es = e;
     double u;
     int cx, cy, cz;
     cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
@@ -275,8 +278,10 @@ cc_status pairs_fill(cc_ctx* c) {
         CC_TRY(cc_ensure(c, c->scratch_u32, (size_t)std::max<int64_t>(c->E, 1), "row cursors"));
         CC_CUDA(c, cudaMemsetAsync(c->scratch_u32.p, 0, (size_t)std::max<int64_t>(c->E, 1) * sizeof(uint32_t),
                                    c->stream));
-        CCL(c, k_pairs_fill<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
-            n, c->orig4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, c->deg.p, c->eidx.p, (uint32_t)c->E,
+        CCL(c, k_pairs_fill<<<(unsigned)((c->E_all + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0,
+                              c->stream>>>(
+            (uint32_t)c->E_all, c->slotE.p, c->orig4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, c->eidx.p,
+            (uint32_t)c->E,
             reinterpret_cast<const unsigned long long*>(c->rowptr.p), c->scratch_u32.p, c->rows.p,
             c->parent_orig.p));
         cc_prof_end(c, tok);
