@@ -22,6 +22,7 @@ namespace {
 
 constexpr int BIN_THREADS = 256;
 constexpr int CELL_SHORT = 16;
+constexpr int CELL_MID = 64;    // 17..64: one warp per cell (k_cell_finish_mid)
 constexpr int CELL_LONG_MAX = 4096;
 
 struct __align__(16) Rec {
@@ -57,10 +58,11 @@ __global__ void __launch_bounds__(BIN_THREADS)
 k_bin_scatter(int64_t n, const float* __restrict__ x, const float* __restrict__ y, const float* __restrict__ z,
               const float* __restrict__ xh, const float* __restrict__ yh, const float* __restrict__ zh,
               const uint32_t* __restrict__ gid, const uint32_t* __restrict__ key, const uint32_t* __restrict__ rnk,
-              const uint32_t* __restrict__ cell_start, Rec* __restrict__ rec) {
+              const uint32_t* __restrict__ cell_start, Rec* __restrict__ rec, uint32_t* __restrict__ slot_of) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t s = cell_start[key[i]] + rnk[i];
+    slot_of[i] = s;  // provisional: k_cell_finish* rewrite only the records the in-cell sort moves
     Rec r;
     r.x = x[i];
     r.y = y[i];
@@ -70,16 +72,21 @@ k_bin_scatter(int64_t n, const float* __restrict__ x, const float* __restrict__ 
     r.zh = zh[i];
     r.gid = gid ? gid[i] : (uint32_t)i;
     r.i = (uint32_t)i;
-    reinterpret_cast<uint4*>(rec)[2 * s] = *reinterpret_cast<const uint4*>(&r.x);
-    reinterpret_cast<uint4*>(rec)[2 * s + 1] = *reinterpret_cast<const uint4*>(&r.yh);
+    // one full-sector 256-bit store (two 16-byte stores would be partial-sector writes)
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(rec + s), "r"(__float_as_uint(r.x)),
+                 "r"(__float_as_uint(r.y)), "r"(__float_as_uint(r.z)), "r"(__float_as_uint(r.xh)),
+                 "r"(__float_as_uint(r.yh)), "r"(__float_as_uint(r.zh)), "r"(r.gid), "r"(r.i)
+                 : "memory");
 }
 
-__device__ __forceinline__ void emit(const Rec& r, uint32_t s, float4* __restrict__ orig4, float4* __restrict__ dec4,
-                                     uint32_t* __restrict__ xk, uint32_t* __restrict__ slot_of, const Grid& g) {
+// record r (scattered to slot s0) goes to slot s; slot_of[r.i] already holds s0 (k_bin_scatter)
+__device__ __forceinline__ void emit(const Rec& r, uint32_t s, uint32_t s0, float4* __restrict__ orig4,
+                                     float4* __restrict__ dec4, uint32_t* __restrict__ xk,
+                                     uint32_t* __restrict__ slot_of, const Grid& g) {
     orig4[s] = make_float4(r.x, r.y, r.z, __uint_as_float(r.gid));
     dec4[s] = make_float4(r.xh, r.yh, r.zh, __uint_as_float(r.i));
     xk[s] = x_sort_key(r.x, g);
-    slot_of[r.i] = s;
+    if (s != s0) slot_of[r.i] = s;
 }
 
 __device__ __forceinline__ Rec load_rec(const Rec* __restrict__ rec, uint32_t s) {
@@ -98,19 +105,20 @@ __device__ __forceinline__ unsigned long long rec_key(const Rec& r, const Grid& 
 __global__ void __launch_bounds__(BIN_THREADS)
 k_cell_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restrict__ rec, Grid g,
               float4* __restrict__ orig4, float4* __restrict__ dec4, uint32_t* __restrict__ xk,
-              uint32_t* __restrict__ slot_of, uint32_t* __restrict__ long_list, unsigned long long* __restrict__ n_long) {
+              uint32_t* __restrict__ slot_of, uint32_t* __restrict__ long_list, uint64_t cap,
+              unsigned long long* __restrict__ n_long) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= ncell) return;
     const uint32_t a = cs[c], b = cs[c + 1];
     const int len = (int)(b - a);
     if (len == 0) return;
     if (len == 1) {
-        emit(load_rec(rec, a), a, orig4, dec4, xk, slot_of, g);
+        emit(load_rec(rec, a), a, a, orig4, dec4, xk, slot_of, g);
         return;
     }
-    if (len > CELL_SHORT) {
-        const unsigned long long q = atomicAdd(n_long, 1ull);
-        long_list[q] = (uint32_t)c;
+    if (len > CELL_SHORT) {  // mid cells from the front of the list, long ones from the back
+        if (len <= CELL_MID) long_list[atomicAdd(n_long, 1ull)] = (uint32_t)c;
+        else long_list[cap - 1 - atomicAdd(n_long + 1, 1ull)] = (uint32_t)c;
         return;
     }
     unsigned long long v[CELL_SHORT];  // (x key << 32 | input index): unique, data-determined order
@@ -126,19 +134,74 @@ k_cell_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restr
         v[j + 1] = xk;
         off[j + 1] = k;
     }
-    for (int k = 0; k < len; k++) emit(load_rec(rec, a + off[k]), a + k, orig4, dec4, xk, slot_of, g);
+    for (int k = 0; k < len; k++) emit(load_rec(rec, a + off[k]), a + k, a + off[k], orig4, dec4, xk, slot_of, g);
+}
+
+
+// mid cells (CELL_SHORT < len <= CELL_MID): one warp per cell, bitonic sort of the 64-slot
+// padded key array held two per lane (element lane and lane + 32)
+__global__ void __launch_bounds__(BIN_THREADS)
+k_cell_finish_mid(const uint32_t* __restrict__ long_list, const unsigned long long* __restrict__ n_long,
+                  const uint32_t* __restrict__ cs, const Rec* __restrict__ rec, Grid g, float4* __restrict__ orig4,
+                  float4* __restrict__ dec4, uint32_t* __restrict__ xk, uint32_t* __restrict__ slot_of) {
+    const unsigned long long nm = n_long[0];
+    const int lane = threadIdx.x & 31;
+    const unsigned long long w0 = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned long long nw = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    for (unsigned long long q = w0; q < nm; q += nw) {
+        const uint32_t c = long_list[q];
+        const uint32_t a = cs[c], b = cs[c + 1];
+        const int len = (int)(b - a);
+        // (key, local offset) pairs; keys are unique (input index), padding sorts last
+        unsigned long long k0 = lane < len ? rec_key(load_rec(rec, a + lane), g) : ~0ull;
+        unsigned long long k1 = lane + 32 < len ? rec_key(load_rec(rec, a + lane + 32), g) : ~0ull;
+        int o0 = lane, o1 = lane + 32;
+        for (int k = 2; k <= 64; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                if (j == 32) {  // partners in the same lane: elements lane and lane + 32
+                    const bool up = (lane & k) == 0;  // k == 64: always ascending
+                    if ((k0 > k1) == up) {
+                        const unsigned long long tk = k0;
+                        k0 = k1;
+                        k1 = tk;
+                        const int to = o0;
+                        o0 = o1;
+                        o1 = to;
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        unsigned long long& kk = h ? k1 : k0;
+                        int& oo = h ? o1 : o0;
+                        const int idx = lane + 32 * h;
+                        const unsigned long long pk = __shfl_xor_sync(0xffffffffu, kk, j);
+                        const int po = __shfl_xor_sync(0xffffffffu, oo, j);
+                        const bool up = (idx & k) == 0;
+                        const bool lower = (lane & j) == 0;  // idx < idx ^ j
+                        const bool take = lower ? ((kk > pk) == up) : ((kk < pk) == up);
+                        if (take) {
+                            kk = pk;
+                            oo = po;
+                        }
+                    }
+                }
+            }
+        }
+        if (lane < len) emit(load_rec(rec, a + o0), a + lane, a + o0, orig4, dec4, xk, slot_of, g);
+        if (lane + 32 < len) emit(load_rec(rec, a + o1), a + lane + 32, a + o1, orig4, dec4, xk, slot_of, g);
+    }
 }
 
 // crowded cells: one block per cell, bitonic sort of (key, local offset) in shared memory
 __global__ void __launch_bounds__(512)
-k_cell_finish_long(const uint32_t* __restrict__ long_list, const unsigned long long* __restrict__ n_long,
+k_cell_finish_long(const uint32_t* __restrict__ long_list, uint64_t cap, const unsigned long long* __restrict__ n_long,
                    const uint32_t* __restrict__ cs, const Rec* __restrict__ rec, Grid g, float4* __restrict__ orig4,
                    float4* __restrict__ dec4, uint32_t* __restrict__ xk, uint32_t* __restrict__ slot_of) {
     __shared__ unsigned long long sh[CELL_LONG_MAX];
     __shared__ unsigned short so[CELL_LONG_MAX];
-    const unsigned long long nl = *n_long;
+    const unsigned long long nl = n_long[1];
     for (unsigned long long q = blockIdx.x; q < nl; q += gridDim.x) {
-        const uint32_t c = long_list[q];
+        const uint32_t c = long_list[cap - 1 - q];
         const uint32_t a = cs[c], b = cs[c + 1];
         const int len = (int)(b - a);
         if (len <= CELL_LONG_MAX) {
@@ -169,7 +232,7 @@ k_cell_finish_long(const uint32_t* __restrict__ long_list, const unsigned long l
                 }
             }
             for (int k = threadIdx.x; k < len; k += blockDim.x)
-                emit(load_rec(rec, a + so[k]), a + k, orig4, dec4, xk, slot_of, g);
+                emit(load_rec(rec, a + so[k]), a + k, a + so[k], orig4, dec4, xk, slot_of, g);
             __syncthreads();
         } else if (threadIdx.x == 0) {
             // pathological crowding: selection by repeated minimum (correct, slow)
@@ -185,7 +248,7 @@ k_cell_finish_long(const uint32_t* __restrict__ long_list, const unsigned long l
                         bq = q2;
                     }
                 }
-                emit(load_rec(rec, a + bq), a + k, orig4, dec4, xk, slot_of, g);
+                emit(load_rec(rec, a + bq), a + k, a + bq, orig4, dec4, xk, slot_of, g);
                 prev = best;
             }
         }
@@ -211,7 +274,7 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
     CC_TRY(cc_ensure(c, c->scratch_u64, 2, "long count"));
     CC_CUDA(c, cudaMemsetAsync(c->cell_count.p, 0, (size_t)nc * sizeof(uint32_t), c->stream));
     CC_CUDA(c, cudaMemsetAsync(c->counters.p, 0, 16 * sizeof(unsigned long long), c->stream));
-    CC_CUDA(c, cudaMemsetAsync(c->scratch_u64.p, 0, sizeof(uint64_t), c->stream));
+    CC_CUDA(c, cudaMemsetAsync(c->scratch_u64.p, 0, 2 * sizeof(uint64_t), c->stream));
     Rec* rec = reinterpret_cast<Rec*>(c->rec32.p);
     const unsigned nb = (unsigned)((n + BIN_THREADS - 1) / BIN_THREADS);
     if (n > 0) {
@@ -225,17 +288,22 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
     CC_TRY(scan_u32_to_u32(c, c->cell_count.p, c->cell_start.p, nc,
                            reinterpret_cast<uint64_t*>(c->cell_start.p + nc)));
     if (n > 0) {
-        CC_TRY(cc_ensure(c, c->scratch_u32, (size_t)std::max<int64_t>(std::min<int64_t>(nc, n), 1), "crowded cells"));
+        const uint64_t cap = (uint64_t)std::max<int64_t>(std::min<int64_t>(nc, n), 1);  // >= crowded cells
+        CC_TRY(cc_ensure(c, c->scratch_u32, (size_t)cap, "crowded cells"));
         int tok = cc_prof_begin(c, "K1_scatter");
         CCL(c, k_bin_scatter<<<nb, BIN_THREADS, 0, c->stream>>>(n, x, y, z, xh, yh, zh, gid, c->key.p, c->rnk.p,
-                                                                 c->cell_start.p, rec));
+                                                                 c->cell_start.p, rec, c->slot_of.p));
         cc_prof_end(c, tok);
         unsigned long long* nl = reinterpret_cast<unsigned long long*>(c->scratch_u64.p);
         int t2 = cc_prof_begin(c, "K1_finish");
         CCL(c, k_cell_finish<<<(unsigned)((nc + BIN_THREADS - 1) / BIN_THREADS), BIN_THREADS, 0, c->stream>>>(
-                   nc, c->cell_start.p, rec, c->g, c->orig4.p, c->dec4.p, c->xk.p, c->slot_of.p, c->scratch_u32.p, nl));
-        CCL(c, k_cell_finish_long<<<148 * 2, 512, 0, c->stream>>>(c->scratch_u32.p, nl, c->cell_start.p, rec, c->g,
-                                                                  c->orig4.p, c->dec4.p, c->xk.p, c->slot_of.p));
+                   nc, c->cell_start.p, rec, c->g, c->orig4.p, c->dec4.p, c->xk.p, c->slot_of.p, c->scratch_u32.p, cap,
+                   nl));
+        CCL(c, k_cell_finish_mid<<<148 * 8, BIN_THREADS, 0, c->stream>>>(c->scratch_u32.p, nl, c->cell_start.p, rec,
+                                                                          c->g, c->orig4.p, c->dec4.p, c->xk.p,
+                                                                          c->slot_of.p));
+        CCL(c, k_cell_finish_long<<<148 * 2, 512, 0, c->stream>>>(c->scratch_u32.p, cap, nl, c->cell_start.p, rec,
+                                                                  c->g, c->orig4.p, c->dec4.p, c->xk.p, c->slot_of.p));
         cc_prof_end(c, t2);
         CC_CUDA(c, cudaGetLastError());
     }
