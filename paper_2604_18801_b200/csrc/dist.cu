@@ -427,13 +427,14 @@ cc_status dist_iter_tail(cc_ctx* c, const float4* p0, const float4* p1) {
         CC_NCCL(c, ncclRecv(c->rrb[1].p, (size_t)(4 * c->n_ref_recv[1]), ncclFloat32, c->right, comm(c), c->stream));
     if (c->n_ref_recv[0] > 0)
         CC_NCCL(c, ncclRecv(c->rrb[0].p, (size_t)(4 * c->n_ref_recv[0]), ncclFloat32, c->left, comm(c), c->stream));
+    // the stop statistics travel in the same NCCL group as the ghost refresh (one launch)
+    CC_NCCL(c, ncclAllReduce(c->red.p, c->red.p, LFX_STATS, ncclUint64, ncclSum, comm(c), c->stream));
     CC_NCCL(c, ncclGroupEnd());
     for (int d = 0; d < 2; d++)
         if (c->n_ref_recv[d] > 0)
             CCL(c, k_refresh_unpack<<<(unsigned)((c->n_ref_recv[d] + DT - 1) / DT), DT, 0, c->stream>>>(
                        c->n_ref_recv[d], c->recv_e[d].p, c->ctl.p, const_cast<float4*>(p0), const_cast<float4*>(p1),
                        c->rrb[d].p));
-    CC_NCCL(c, ncclAllReduce(c->red.p, c->red.p, LFX_STATS, ncclUint64, ncclSum, comm(c), c->stream));
     CCL(c, k_decide<<<1, 1, 0, c->stream>>>(c->ctl.p, c->red.p, c->p.stop_mode, c->p.eps_loss, c->p.t_max,
                                             c->trace_a.p, c->trace_l.p, c->trace_v.p));
     return CC_OK;
