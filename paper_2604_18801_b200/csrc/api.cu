@@ -283,7 +283,7 @@ void cc_destroy(cc_ctx* c) {
         cc_release(c, c->send_e[d]); cc_release(c, c->lsb[d]); cc_release(c, c->lrb[d]); cc_release(c, c->rsb[d]);
         cc_release(c, c->rrb[d]);
     }
-    cc_release(c, c->stage); cc_release(c, c->gath); cc_release(c, c->dcnt); cc_release(c, c->red);
+    cc_release(c, c->stage); cc_release(c, c->gath); cc_release(c, c->dcnt); cc_release(c, c->red); cc_release(c, c->red_sum);
     cc_release(c, c->bnd);
     cudaStreamSynchronize(c->stream);
     // the PGD graph holds NCCL work (multi-GPU): release it before the communicator

@@ -73,6 +73,7 @@ struct Ctl {
     unsigned int tail_ncur;      // k_tail: length of the list of the next iteration
     int tail_go;                 // k_tail: 1 while the tail loop continues
     unsigned int bar_count, bar_gen;  // k_tail's grid barrier
+    unsigned int ep_base;        // multi-GPU peer exchange: epoch of iteration t is ep_base + t
 };
 
 // ---------------------------------------------------------------------------------------
@@ -206,6 +207,18 @@ struct cc_ctx {
     int64_t n_shell[2] = {0, 0}, n_from_left = 0, n_from_right = 0, stage_cap = 0;
     int64_t n_ref_send[2] = {0, 0}, n_ref_recv[2] = {0, 0};
     int64_t launches_per_iter_tail = 0;
+    // per-iteration exchange over NVLink peer memory (dist.cu): one cudaMalloc'd block per rank
+    // (flags, stop statistics, two parities of the two ghost-refresh receive areas), mapped by
+    // every peer through CUDA IPC
+    void* pm_local = nullptr;
+    size_t pm_bytes = 0;
+    int64_t pm_cap[2] = {0, 0};
+    void* pm_peer[8] = {};
+    unsigned char pm_handle[8][64] = {};
+    int64_t pm_peer_cap[8][2] = {};
+    bool pm_ok = false;
+    unsigned int epoch_base = 0;
+    cc::DBuf<unsigned long long> red_sum;
     unsigned long long* h_red = nullptr;
     unsigned long long final_active = 0;
     double final_loss = 0.0;

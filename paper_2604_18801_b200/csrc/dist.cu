@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <unordered_map>
 #include <vector>
@@ -146,6 +147,96 @@ __global__ void k_refresh_unpack(int64_t m, const uint32_t* __restrict__ recv_e,
     dst[recv_e[k]] = buf[k];
 }
 
+
+// ---- per-iteration exchange over NVLink peer memory (X3, replaces NCCL send/recv + allreduce)
+// Block layout (bytes): [0, 64) flags u32[16] (rank r's epoch at index r); [64, 1088) stop
+// statistics u64 [2 parities][8 ranks][LFX_STATS]; [1088, 1092) local ticket; [1280, ...) the two
+// receive areas (0: from the left rank, 1: from the right rank), each 2 parities x cap float4.
+constexpr size_t PM_STATS = 64, PM_TICKET = 1088, PM_AREAS = 1280;
+__host__ __device__ inline size_t pm_area_off(int d, const int64_t cap[2]) {
+    return PM_AREAS + (d ? 2 * (size_t)cap[0] * sizeof(float4) : 0);
+}
+
+struct PeerArgs {
+    Ctl* ctl;
+    const float4* p0;
+    const float4* p1;
+    const uint32_t* send_e[2];
+    int64_t ns[2];
+    float4* dst[2];       // send dir 0 -> the left rank's area 1, dir 1 -> the right rank's area 0
+    int64_t dstride[2];   // their capacity per parity
+    const unsigned long long* red;  // this rank's statistics (k_pgd's last block)
+    unsigned long long* red_sum;    // the global sums (k_decide's input)
+    unsigned char* blk[8];          // every rank's block (mine included), mapped here
+    int rank, nranks;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// push the updated owned positions the neighbours hold as ghosts straight into their receive
+// areas (P2P stores over NVLink), then the last block publishes this rank's statistics and epoch
+// flag in every rank's block, waits for every rank's flag and sums the statistics (integer sums:
+// the same value on every rank, in any order)
+__global__ void __launch_bounds__(256) k_peer_exchange(PeerArgs a) {
+    Ctl* ctl = a.ctl;
+    if (ctl->done) return;
+    const int t = ctl->t + 1;  // the iteration whose update was just written
+    const int par = t & 1;
+    const float4* src = par ? a.p1 : a.p0;
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+    for (int d = 0; d < 2; d++) {
+        float4* dst = a.dst[d] + (size_t)par * a.dstride[d];
+        for (int64_t k = gt; k < a.ns[d]; k += gs) dst[k] = src[a.send_e[d][k]];
+    }
+    __threadfence_system();
+    __syncthreads();
+    __shared__ bool last;
+    unsigned* ticket = reinterpret_cast<unsigned*>(a.blk[a.rank] + PM_TICKET);
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    *ticket = 0u;
+    __threadfence_system();
+    const unsigned epoch = ctl->ep_base + (unsigned)t;
+    for (int r = 0; r < a.nranks; r++) {
+        unsigned long long* st = reinterpret_cast<unsigned long long*>(a.blk[r] + PM_STATS) +
+                                 ((size_t)par * 8 + a.rank) * LFX_STATS;
+        for (int w = 0; w < LFX_STATS; w++) st[w] = a.red[w];
+    }
+    __threadfence_system();
+    for (int r = 0; r < a.nranks; r++) st_release_sys(reinterpret_cast<unsigned*>(a.blk[r]) + a.rank, epoch);
+    const unsigned* fl = reinterpret_cast<const unsigned*>(a.blk[a.rank]);
+    for (int r = 0; r < a.nranks; r++)
+        while ((int)(ld_acquire_sys(fl + r) - epoch) < 0) __nanosleep(64);
+    const volatile unsigned long long* mine =
+        reinterpret_cast<const volatile unsigned long long*>(a.blk[a.rank] + PM_STATS) + (size_t)par * 8 * LFX_STATS;
+    for (int w = 0; w < LFX_STATS; w++) {
+        unsigned long long v = 0ull;
+        for (int r = 0; r < a.nranks; r++) v += mine[(size_t)r * LFX_STATS + w];
+        a.red_sum[w] = v;
+    }
+    __threadfence();
+}
+
+// unpack this iteration's parity of a receive area into the ghost slots
+__global__ void k_peer_unpack(int64_t m, const uint32_t* __restrict__ recv_e, const Ctl* __restrict__ ctl,
+                              float4* __restrict__ p0, float4* __restrict__ p1, const float4* __restrict__ area,
+                              int64_t cap) {
+    if (ctl->done) return;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const int t = ctl->t + 1;
+    float4* dst = (t & 1) ? p1 : p0;
+    dst[recv_e[k]] = __ldcv(area + (size_t)(t & 1) * cap + k);
+}
+
 // global stop decision after the allreduce of (active, loss)
 __global__ void k_decide(Ctl* ctl, const unsigned long long* __restrict__ red, int stop_mode, double eps_loss,
                          int t_max, long long* trace_a, double* trace_l, long long* trace_v) {
@@ -254,6 +345,11 @@ cc_status dist_init(cc_ctx* c, const cc_dist* d) {
 }
 
 void dist_destroy(cc_ctx* c) {
+    for (int r = 0; r < 8; r++)
+        if (c->pm_peer[r] && c->pm_peer[r] != c->pm_local) cudaIpcCloseMemHandle(c->pm_peer[r]);
+    if (c->pm_local) cudaFree(c->pm_local);
+    c->pm_local = nullptr;
+    for (int r = 0; r < 8; r++) c->pm_peer[r] = nullptr;
     if (c->nranks > 1 && c->nccl_comm) ncclCommDestroy(comm(c));
     c->nccl_comm = nullptr;
 }
@@ -350,6 +446,65 @@ cc_status dist_exchange_ghosts(cc_ctx* c, int64_t n, const float* x, const float
 }
 
 // refresh lists of ghost editables (X2), after the rows exist
+
+// map every rank's peer block (X3 over NVLink): (re)allocate mine if the receive areas grew,
+// exchange IPC handles with an allgather, open the peers' blocks that changed
+static cc_status dist_setup_peer(cc_ctx* c) {
+    c->pm_ok = false;
+    const char* env = std::getenv("CC_PEER");
+    if ((env && env[0] == '0') || c->nranks > 8) return CC_OK;  // NCCL path
+    const int64_t need0 = std::max<int64_t>(c->n_ref_recv[0], 1), need1 = std::max<int64_t>(c->n_ref_recv[1], 1);
+    if (!c->pm_local || need0 > c->pm_cap[0] || need1 > c->pm_cap[1]) {
+        if (c->pm_local) cudaFree(c->pm_local);
+        c->pm_local = nullptr;
+        c->pm_cap[0] = need0 + need0 / 4 + 64;
+        c->pm_cap[1] = need1 + need1 / 4 + 64;
+        c->pm_bytes = pm_area_off(1, c->pm_cap) + 2 * (size_t)c->pm_cap[1] * sizeof(float4);
+        CC_CUDA(c, cudaMalloc(&c->pm_local, c->pm_bytes));
+        CC_CUDA(c, cudaMemsetAsync(c->pm_local, 0, c->pm_bytes, c->stream));
+    }
+    struct Rec {
+        cudaIpcMemHandle_t h;
+        int64_t cap[2];
+        unsigned char pad[128 - sizeof(cudaIpcMemHandle_t) - 16];
+    };
+    static_assert(sizeof(Rec) == 128, "");
+    Rec mine;
+    std::memset(&mine, 0, sizeof(mine));
+    CC_CUDA(c, cudaIpcGetMemHandle(&mine.h, c->pm_local));
+    mine.cap[0] = c->pm_cap[0];
+    mine.cap[1] = c->pm_cap[1];
+    unsigned char* dbuf = nullptr;
+    CC_CUDA(c, cudaMalloc(&dbuf, 128 * (size_t)(c->nranks + 1)));
+    CC_CUDA(c, cudaMemcpyAsync(dbuf, &mine, 128, cudaMemcpyHostToDevice, c->stream));
+    CC_NCCL(c, ncclAllGather(dbuf, dbuf + 128, 128, ncclUint8, comm(c), c->stream));
+    std::vector<Rec> all((size_t)c->nranks);
+    CC_CUDA(c, cudaMemcpyAsync(all.data(), dbuf + 128, 128 * (size_t)c->nranks, cudaMemcpyDeviceToHost, c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    cudaFree(dbuf);
+    for (int r = 0; r < c->nranks; r++) {
+        c->pm_peer_cap[r][0] = all[(size_t)r].cap[0];
+        c->pm_peer_cap[r][1] = all[(size_t)r].cap[1];
+        if (r == c->rank) {
+            c->pm_peer[r] = c->pm_local;
+            continue;
+        }
+        if (c->pm_peer[r] && std::memcmp(c->pm_handle[r], &all[(size_t)r].h, 64) == 0) continue;
+        if (c->pm_peer[r]) cudaIpcCloseMemHandle(c->pm_peer[r]);
+        c->pm_peer[r] = nullptr;
+        void* ptr = nullptr;
+        if (cudaIpcOpenMemHandle(&ptr, all[(size_t)r].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            return CC_OK;  // no peer mapping: the NCCL path stays in use
+        }
+        c->pm_peer[r] = ptr;
+        std::memcpy(c->pm_handle[r], &all[(size_t)r].h, 64);
+    }
+    CC_TRY(cc_ensure(c, c->red_sum, LFX_STATS, "peer statistics"));
+    c->pm_ok = true;
+    return CC_OK;
+}
+
 cc_status dist_setup_refresh(cc_ctx* c) {
     const int64_t n = c->n;
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
@@ -409,11 +564,49 @@ cc_status dist_setup_refresh(cc_ctx* c) {
     CC_CUDA(c, cudaStreamSynchronize(c->stream));
     if (c->h_counters[14] & 8ull) return cc_fail(c, CC_E_DATA, "ghost editable is not editable on its owner");
     CC_TRY(cc_ensure(c, c->red, LFX_STATS, "allreduce buffer"));
-    return CC_OK;
+    return dist_setup_peer(c);
 }
 
 // per-iteration tail (X3): refresh ghosts, allreduce the stop statistics, decide
 cc_status dist_iter_tail(cc_ctx* c, const float4* p0, const float4* p1) {
+    if (c->pm_ok) {
+        PeerArgs a;
+        std::memset(&a, 0, sizeof(a));
+        a.ctl = c->ctl.p;
+        a.p0 = p0;
+        a.p1 = p1;
+        for (int d = 0; d < 2; d++) {
+            a.send_e[d] = c->send_e[d].p;
+            a.ns[d] = c->n_ref_send[d];
+        }
+        // my dir-0 sends land in the left rank's area 1 (its "from the right"), dir 1 in the
+        // right rank's area 0
+        a.dst[0] = reinterpret_cast<float4*>(static_cast<unsigned char*>(c->pm_peer[c->left]) +
+                                             pm_area_off(1, c->pm_peer_cap[c->left]));
+        a.dstride[0] = c->pm_peer_cap[c->left][1];
+        a.dst[1] = reinterpret_cast<float4*>(static_cast<unsigned char*>(c->pm_peer[c->right]) +
+                                             pm_area_off(0, c->pm_peer_cap[c->right]));
+        a.dstride[1] = c->pm_peer_cap[c->right][0];
+        a.red = c->red.p;
+        a.red_sum = c->red_sum.p;
+        for (int r = 0; r < c->nranks; r++) a.blk[r] = static_cast<unsigned char*>(c->pm_peer[r]);
+        a.rank = c->rank;
+        a.nranks = c->nranks;
+        const int64_t ns = std::max(c->n_ref_send[0], c->n_ref_send[1]);
+        const unsigned nb = (unsigned)std::min<int64_t>(std::max<int64_t>((ns + 255) / 256, 1), 148);
+        CCL(c, k_peer_exchange<<<nb, 256, 0, c->stream>>>(a));
+        for (int d = 0; d < 2; d++)
+            if (c->n_ref_recv[d] > 0)
+                CCL(c, k_peer_unpack<<<(unsigned)((c->n_ref_recv[d] + DT - 1) / DT), DT, 0, c->stream>>>(
+                           c->n_ref_recv[d], c->recv_e[d].p, c->ctl.p, const_cast<float4*>(p0),
+                           const_cast<float4*>(p1),
+                           reinterpret_cast<const float4*>(static_cast<unsigned char*>(c->pm_local) +
+                                                           pm_area_off(d, c->pm_cap)),
+                           c->pm_cap[d]));
+        CCL(c, k_decide<<<1, 1, 0, c->stream>>>(c->ctl.p, c->red_sum.p, c->p.stop_mode, c->p.eps_loss, c->p.t_max,
+                                                c->trace_a.p, c->trace_l.p, c->trace_v.p));
+        return CC_OK;
+    }
     for (int d = 0; d < 2; d++)
         if (c->n_ref_send[d] > 0)
             CCL(c, k_refresh_pack<<<(unsigned)((c->n_ref_send[d] + DT - 1) / DT), DT, 0, c->stream>>>(

@@ -1026,6 +1026,11 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
         info->violated0 = (int64_t)al[2];
     }
     CCL(c, k_ctl_reset<<<1, 1, 0, c->stream>>>(c->ctl.p));
+    // multi-GPU peer exchange: a fresh epoch range per run (identical on every rank)
+    c->epoch_base += (unsigned)tmax + 2u;
+    CC_CUDA(c, cudaMemcpyAsync(&c->ctl.p->ep_base, &c->epoch_base, sizeof(unsigned), cudaMemcpyHostToDevice,
+                               c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));  // the source is a host field
 
     int iters = 0;
     if (tmax > 0) {
@@ -1050,6 +1055,12 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
             }
             const void* r = c->red.p;
             put(&r, sizeof(r));
+            put(&c->pm_ok, sizeof(c->pm_ok));
+            put(c->pm_peer, sizeof(c->pm_peer));
+            put(c->pm_peer_cap, sizeof(c->pm_peer_cap));
+            put(c->pm_cap, sizeof(c->pm_cap));
+            const void* rs = c->red_sum.p;
+            put(&rs, sizeof(rs));
         }
         const bool same = c->pgd_exec && sig == c->pgd_sig;
         if (!same) {
