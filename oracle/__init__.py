@@ -86,6 +86,10 @@ def lib():
         L.oc_tight_f64.restype = C.c_double
         L.oc_correct.argtypes = [C.c_int64, f32p, f32p, f32p, f32p, f32p, f32p, u32p, C.c_int64, i64p, i64p,
                                  u8p, P(Cfg), f32p, f32p, f32p, P(CorrInfo), i64p, f64p, i64p]
+        L.oc_edit_encode.argtypes = [C.c_int64, f32p, f32p, f32p, f32p, f32p, f32p, P(Cfg), u8p, i64p,
+                                     C.c_int64, i64p]
+        L.oc_edit_decode.argtypes = [C.c_int64, f32p, f32p, f32p, u8p, i64p, C.c_int64, P(Cfg),
+                                     f32p, f32p, f32p]
         _lib = L
     return _lib
 
@@ -295,6 +299,43 @@ def hmf(sizes, vol: float, n_bins: int = 50, lo: float | None = None, hi: float 
 def iteration_budget(xi: float, n_tight: int, eps_loss: float) -> int:
     """T <= ceil(12 xi^2 |V_tight| / eps_L)  (§III-E)."""
     return int(math.ceil(12.0 * xi * xi * n_tight / eps_loss))
+
+
+def edit_step(c: Cfg) -> float:
+    """Quantiser lattice step s = xi_f 2^(1-m) (R25)."""
+    return math.ldexp(float(np.float32(c.xi)), 1 - c.m)
+
+
+def edit_encode(xh0, yh0, zh0, xc, yc, zc, c: Cfg):
+    """Alg. 1 lines 11-13, §III-B P:446 (R24, R25): returns (flags u8[ceil(3n/8)],
+    q int64[n_edits]) for Delta = corrected - decompressed."""
+    h = [_f32(a) for a in (xh0, yh0, zh0)]
+    p = [_f32(a) for a in (xc, yc, zc)]
+    n = h[0].size
+    flags = np.zeros((3 * n + 7) // 8, np.uint8)
+    cap = 3 * n
+    q = np.zeros(max(cap, 1), np.int64)
+    ne = C.c_int64(0)
+    st = lib().oc_edit_encode(n, *[_ptr(a, C.c_float) for a in h + p], C.byref(c), _ptr(flags, C.c_uint8),
+                              _ptr(q, C.c_int64), cap, C.byref(ne))
+    if st:
+        raise ValueError(f"oc_edit_encode status {st}")
+    return flags, q[:ne.value].copy()
+
+
+def edit_decode(xh0, yh0, zh0, flags, q, c: Cfg):
+    """Reconstruction, §III-B P:456 (R26): x_hat0 + scatter(dequantise(q), flags)."""
+    h = [_f32(a) for a in (xh0, yh0, zh0)]
+    n = h[0].size
+    flags = np.ascontiguousarray(flags, np.uint8)
+    q = np.ascontiguousarray(q, np.int64)
+    qq = q if q.size else np.zeros(1, np.int64)
+    out = [np.empty(n, np.float32) for _ in range(3)]
+    st = lib().oc_edit_decode(n, *[_ptr(a, C.c_float) for a in h], _ptr(flags, C.c_uint8),
+                              _ptr(qq, C.c_int64), q.size, C.byref(c), *[_ptr(a, C.c_float) for a in out])
+    if st:
+        raise ValueError(f"oc_edit_decode status {st}")
+    return tuple(out)
 
 
 @dataclass

@@ -718,3 +718,72 @@ done:
     free(P); free(Q); free(eidx); free(deg); free(emap); free(rp); free(rows); free(mom); free(box);
     return st;
 }
+
+/* ---------------------------------------------------------------------------------------------
+ * f1 -- edit log: compaction + m-bit quantisation (Alg. 1 lines 11-13; §III-B
+ * "Compaction, quantization, and lossless compression") and reconstruction (§III-B
+ * "Reconstruction of the edited decompressed data").  Readings R24-R26:
+ *   R24  coordinate k = 3 i + a (particle i in input order, axis a = x,y,z); flags bit k is bit
+ *        (k mod 8) of byte k/8 (LSB first); ceil(3n/8) bytes; bit set iff fl32 corrected !=
+ *        fl32 decompressed (Delta != 0, "bitmask of non-zero entries in Delta").
+ *   R25  Delta_k = (double)corrected - (double)decompressed (exact in fp64); uniform quantiser
+ *        on the lattice s = xi_f 2^(1-m) (2^(m+1)+1 levels over [-2 xi, 2 xi], "uniform
+ *        quantization into 2^m intervals" per xi of half-width): q = rint(Delta / s) in fp64
+ *        (round half to even), |Delta| <= 2 xi_f required (else 66, CC_E_BOUND).  Max
+ *        reconstruction error s/2 = xi 2^-m = xi - xi' < eps_q.
+ *   R26  reconstruction: x_rec = fl32((double)x_hat0 + (double)q * s) for a flagged coordinate,
+ *        x_hat0 unchanged otherwise ("element-wise addition ... to the initial output").
+ * The Huffman+ZSTD stage is a lossless host stage, not part of this oracle.
+ * ------------------------------------------------------------------------------------------- */
+static double oc_edit_step(const oc_cfg* c) {
+    return ldexp((double)(float)c->xi, 1 - c->m);
+}
+
+/* Returns 0, 64 (arguments), 66 (|Delta| > 2 xi_f) or 67 (more edits than cap; *n_edits set). */
+int oc_edit_encode(int64_t n, const float* xh0, const float* yh0, const float* zh0,
+                   const float* xc, const float* yc, const float* zc, const oc_cfg* c,
+                   uint8_t* flags, int64_t* q, int64_t cap, int64_t* n_edits) {
+    if (n < 0 || !c || !n_edits || c->m < 2 || c->m > 40 || !(c->xi > 0)) return 64;
+    const double s = oc_edit_step(c), lim = 2.0 * (double)(float)c->xi;
+    const float* h[3] = {xh0, yh0, zh0};
+    const float* p[3] = {xc, yc, zc};
+    memset(flags, 0, (size_t)((3 * n + 7) / 8));
+    int64_t ne = 0;
+    for (int64_t i = 0; i < n; i++) {
+        for (int a = 0; a < 3; a++) {
+            int64_t k = 3 * i + a;
+            if (p[a][i] == h[a][i]) continue;                 /* Delta = 0: no flag */
+            double delta = (double)p[a][i] - (double)h[a][i];  /* exact (R25) */
+            if (fabs(delta) > lim) return 66;
+            flags[k / 8] |= (uint8_t)(1u << (k % 8));
+            if (ne < cap) q[ne] = (int64_t)rint(delta / s);
+            ne++;
+        }
+    }
+    *n_edits = ne;
+    return ne > cap ? 67 : 0;
+}
+
+/* x_rec (R26).  Returns 0, 64 (arguments) or 65 (popcount(flags) != n_edits). */
+int oc_edit_decode(int64_t n, const float* xh0, const float* yh0, const float* zh0,
+                   const uint8_t* flags, const int64_t* q, int64_t n_edits, const oc_cfg* c,
+                   float* xr, float* yr, float* zr) {
+    if (n < 0 || !c || c->m < 2 || c->m > 40 || !(c->xi > 0)) return 64;
+    const double s = oc_edit_step(c);
+    const float* h[3] = {xh0, yh0, zh0};
+    float* r[3] = {xr, yr, zr};
+    int64_t e = 0;
+    for (int64_t i = 0; i < n; i++) {
+        for (int a = 0; a < 3; a++) {
+            int64_t k = 3 * i + a;
+            if (flags[k / 8] >> (k % 8) & 1u) {
+                if (e >= n_edits) return 65;
+                r[a][i] = (float)((double)h[a][i] + (double)q[e] * s);
+                e++;
+            } else {
+                r[a][i] = h[a][i];
+            }
+        }
+    }
+    return e == n_edits ? 0 : 65;
+}
