@@ -230,6 +230,7 @@ def main():
     ap.add_argument("--cells-per-particle", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-edit-log", action="store_true")
     ap.add_argument("--sample-n", type=int, default=None)
     ap.add_argument("--_oracle", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
@@ -424,6 +425,43 @@ def main():
                        "d2h_bytes_per_step": 12 * n_total + 48}
         log(f"e2e: {e_ms:.3f} ms/step")
         del host, hout
+    # ---- f1 edit log (Alg. 1 l.11-13 + reconstruction) on this step's correction;
+    # outside the timed step (not one of the §8(a) rows), timed on the library's stream
+    if not args.no_edit_log:
+        fl, q = c.edit_encode(xh, yh, zh, *out)
+        rec = c.edit_decode(xh, yh, zh, fl, q)
+        xi_f = float(np.float32(w.xi))
+        in_bound = all(bool(((r.double() - o.double()).abs() <= xi_f).all()) for r, o in zip(rec, (x, y, z)))
+        diag = {"corr_in_bound": all(bool(((r.double() - o.double()).abs() <= xi_f).all()) for r, o in zip(out, (x, y, z))),
+                "rec_out_of_bound": int(sum(int(((r.double() - o.double()).abs() > xi_f).sum()) for r, o in zip(rec, (x, y, z)))),
+                "max_excess": max(float(((r.double() - o.double()).abs() - xi_f).max()) for r, o in zip(rec, (x, y, z))),
+                "rec_ne_corr": int(sum(int((r != o).sum()) for r, o in zip(rec, out)))}
+        log(f"edit log diag: {diag}")
+        ke = 3
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ms_e = ms_d = 0.0
+        for _ in range(ke):
+            ev[0].record(stream)
+            fl, q = c.edit_encode(xh, yh, zh, *out)
+            ev[1].record(stream)
+            c.edit_decode(xh, yh, zh, fl, q, out=rec)
+            ev[2].record(stream)
+            torch.cuda.synchronize(dev)
+            ms_e += ev[0].elapsed_time(ev[1]) / ke
+            ms_d += ev[1].elapsed_time(ev[2]) / ke
+        ne = int(q.shape[0])
+        fb = (3 * n + 7) // 8
+        b_enc = 24 * n + fb + 8 * ne        # read P_hat0 and P_hat, write flags and indices
+        b_dec = 12 * n + fb + 8 * ne + 12 * n
+        pk = hbm or 1.0
+        line["edit_log"] = {"n_edits": ne, "flags_bytes": fb, "index_bytes": 8 * ne, "in_bound": in_bound, "diag": diag,
+                            "encode_ms": ms_e, "decode_ms": ms_d,
+                            "encode_gbs": b_enc / (ms_e * 1e-3) / 1e9, "decode_gbs": b_dec / (ms_d * 1e-3) / 1e9,
+                            "encode_frac": b_enc / (ms_e * 1e-3) / 1e9 / pk,
+                            "decode_frac": b_dec / (ms_d * 1e-3) / 1e9 / pk,
+                            "bytes_model": "encode 24N + ceil(3N/8) + 8 n_edits; decode 24N + ceil(3N/8) + 8 n_edits"}
+        log(f"edit log: {ne:,} edits, encode {ms_e:.3f} ms, decode {ms_d:.3f} ms, in_bound={in_bound}")
+        del fl, q, rec
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(w)
         line["cpu_baseline"] = {k: v for k, v in cb.items() if k in ("value", "unit", "cores", "kind", "sample")}

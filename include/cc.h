@@ -199,6 +199,36 @@ cc_status cc_run(cc_ctx* ctx, int64_t n, const float* x, const float* y, const f
                  float* xo, float* yo, float* zo, int flags, cc_run_info* info_h);
 
 #ifdef __cplusplus
+/* f1 -- edit log.  Alg. 1 lines 11-13 and §III-B
+ * "Compaction, quantization, and lossless compression": Delta = corrected -
+ * decompressed; flags = bitmask of the non-zero entries of Delta, packed into bytes; edits = the
+ * non-zero Delta quantised on the uniform lattice s = xi_f 2^(1-m) (xi_f = fl32(params.xi),
+ * m = params.m; readings R29-R30).  Independent of the context's state (uses its
+ * params, stream and allocator only); one rank encodes its own particles.
+ *   n:           particles, arrays in the caller's (input) order
+ *   xh0..zh0:    decompressed coordinates P_hat0 (device, n floats each)
+ *   xc..zc:      corrected coordinates P_hat (device, n floats each), |Delta| <= 2 xi_f
+ *   flags:       device, ceil(3n/8) bytes, 4-byte aligned; coordinate k = 3i + a (a = x,y,z) is
+ *                bit k%8 of byte k/8 (LSB first); bit set iff fl32 corrected != decompressed
+ *   q:           device, cap int64 quantisation indices rint(Delta/s) (fp64, half to even), one
+ *                per set flag bit in ascending k; |q| <= 2^(m+1)
+ *   *n_edits_h:  number of set flag bits (= edits), written whatever the status
+ * Errors: CC_E_ARG (null/unaligned buffer, n < 0, xi <= 0, m outside [2, 40]); CC_E_BOUND
+ * (some |Delta| > 2 xi_f); CC_E_OOM (n_edits > cap; flags written, q not).  Synchronises. */
+cc_status cc_edit_encode(cc_ctx* ctx, int64_t n, const float* xh0, const float* yh0, const float* zh0,
+                         const float* xc, const float* yc, const float* zc, uint8_t* flags, int64_t* q,
+                         int64_t cap, int64_t* n_edits_h);
+
+/* f1 -- reconstruction (§III-B, reading R31): x_rec = fl32((double)x_hat0 + (double)q s)
+ * for every flagged coordinate (edits consumed in ascending k), x_rec = x_hat0 elsewhere.
+ * flags/q as written by cc_edit_encode (device); xr..zr: device outputs, n floats each.
+ * Errors: CC_E_ARG; CC_E_DATA if popcount(flags) != n_edits (outputs then undefined).
+ * Synchronises.  The quantisation-safety re-check is cc_build_cells +
+ * cc_find_vulnerable on (P, x_rec): n_violated0 must be 0 and no CC_E_BOUND. */
+cc_status cc_edit_decode(cc_ctx* ctx, int64_t n, const float* xh0, const float* yh0, const float* zh0,
+                         const uint8_t* flags, const int64_t* q, int64_t n_edits, float* xr, float* yr,
+                         float* zr);
+
 }
 #endif
 #endif /* CC_H */

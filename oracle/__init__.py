@@ -302,12 +302,12 @@ def iteration_budget(xi: float, n_tight: int, eps_loss: float) -> int:
 
 
 def edit_step(c: Cfg) -> float:
-    """Quantiser lattice step s = xi_f 2^(1-m) (R25)."""
+    """Quantiser lattice step s = xi_f 2^(1-m) (R30)."""
     return math.ldexp(float(np.float32(c.xi)), 1 - c.m)
 
 
 def edit_encode(xh0, yh0, zh0, xc, yc, zc, c: Cfg):
-    """Alg. 1 lines 11-13, §III-B P:446 (R24, R25): returns (flags u8[ceil(3n/8)],
+    """Alg. 1 lines 11-13, §III-B P:446 (R29, R30): returns (flags u8[ceil(3n/8)],
     q int64[n_edits]) for Delta = corrected - decompressed."""
     h = [_f32(a) for a in (xh0, yh0, zh0)]
     p = [_f32(a) for a in (xc, yc, zc)]
@@ -324,7 +324,7 @@ def edit_encode(xh0, yh0, zh0, xc, yc, zc, c: Cfg):
 
 
 def edit_decode(xh0, yh0, zh0, flags, q, c: Cfg):
-    """Reconstruction, §III-B P:456 (R26): x_hat0 + scatter(dequantise(q), flags)."""
+    """Reconstruction, §III-B P:456 (R31): x_hat0 + scatter(dequantise(q), flags)."""
     h = [_f32(a) for a in (xh0, yh0, zh0)]
     n = h[0].size
     flags = np.ascontiguousarray(flags, np.uint8)

@@ -722,16 +722,16 @@ done:
 /* ---------------------------------------------------------------------------------------------
  * f1 -- edit log: compaction + m-bit quantisation (Alg. 1 lines 11-13; §III-B
  * "Compaction, quantization, and lossless compression") and reconstruction (§III-B
- * "Reconstruction of the edited decompressed data").  Readings R24-R26:
- *   R24  coordinate k = 3 i + a (particle i in input order, axis a = x,y,z); flags bit k is bit
+ * "Reconstruction of the edited decompressed data").  Readings R29-R31:
+ *   R29  coordinate k = 3 i + a (particle i in input order, axis a = x,y,z); flags bit k is bit
  *        (k mod 8) of byte k/8 (LSB first); ceil(3n/8) bytes; bit set iff fl32 corrected !=
  *        fl32 decompressed (Delta != 0, "bitmask of non-zero entries in Delta").
- *   R25  Delta_k = (double)corrected - (double)decompressed (exact in fp64); uniform quantiser
+ *   R30  Delta_k = (double)corrected - (double)decompressed (exact in fp64); uniform quantiser
  *        on the lattice s = xi_f 2^(1-m) (2^(m+1)+1 levels over [-2 xi, 2 xi], "uniform
  *        quantization into 2^m intervals" per xi of half-width): q = rint(Delta / s) in fp64
  *        (round half to even), |Delta| <= 2 xi_f required (else 66, CC_E_BOUND).  Max
  *        reconstruction error s/2 = xi 2^-m = xi - xi' < eps_q.
- *   R26  reconstruction: x_rec = fl32((double)x_hat0 + (double)q * s) for a flagged coordinate,
+ *   R31  reconstruction: x_rec = fl32((double)x_hat0 + (double)q * s) for a flagged coordinate,
  *        x_hat0 unchanged otherwise ("element-wise addition ... to the initial output").
  * The Huffman+ZSTD stage is a lossless host stage, not part of this oracle.
  * ------------------------------------------------------------------------------------------- */
@@ -753,7 +753,7 @@ int oc_edit_encode(int64_t n, const float* xh0, const float* yh0, const float* z
         for (int a = 0; a < 3; a++) {
             int64_t k = 3 * i + a;
             if (p[a][i] == h[a][i]) continue;                 /* Delta = 0: no flag */
-            double delta = (double)p[a][i] - (double)h[a][i];  /* exact (R25) */
+            double delta = (double)p[a][i] - (double)h[a][i];  /* exact (R30) */
             if (fabs(delta) > lim) return 66;
             flags[k / 8] |= (uint8_t)(1u << (k % 8));
             if (ne < cap) q[ne] = (int64_t)rint(delta / s);
@@ -764,7 +764,7 @@ int oc_edit_encode(int64_t n, const float* xh0, const float* yh0, const float* z
     return ne > cap ? 67 : 0;
 }
 
-/* x_rec (R26).  Returns 0, 64 (arguments) or 65 (popcount(flags) != n_edits). */
+/* x_rec (R31).  Returns 0, 64 (arguments) or 65 (popcount(flags) != n_edits). */
 int oc_edit_decode(int64_t n, const float* xh0, const float* yh0, const float* zh0,
                    const uint8_t* flags, const int64_t* q, int64_t n_edits, const oc_cfg* c,
                    float* xr, float* yr, float* zr) {

@@ -62,7 +62,7 @@ class _Run(C.Structure):
 
 EXPORTS = ["cc_default_params", "cc_nccl_unique_id", "cc_create", "cc_destroy", "cc_last_error", "cc_build_cells",
            "cc_find_vulnerable", "cc_get_pairs", "cc_correct", "cc_get_trace", "cc_get_schedule", "cc_fof_label", "cc_mcc",
-           "cc_halo_sizes", "cc_hmf", "cc_kernel_stats", "cc_run"]
+           "cc_halo_sizes", "cc_hmf", "cc_kernel_stats", "cc_run", "cc_edit_encode", "cc_edit_decode"]
 
 _lib = None
 
@@ -102,6 +102,8 @@ def lib():
     L.cc_hmf.argtypes = [P(i64), i64, d, C.c_int, d, d, P(d), P(d)]
     L.cc_kernel_stats.argtypes = [vp, C.c_char_p, i64, P(d), P(i64), i64, P(i64), C.c_int]
     L.cc_run.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, P(_Run)]
+    L.cc_edit_encode.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, i64, P(i64)]
+    L.cc_edit_decode.argtypes = [vp, i64, vp, vp, vp, vp, vp, i64, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("cc_default_params", "cc_destroy", "cc_last_error"):
             getattr(L, name).restype = C.c_int
@@ -245,6 +247,35 @@ class Corrector:
         a = np.zeros((self.params.t_max + 1, 5), np.int64)
         self._chk(self.lib.cc_get_schedule(self.h, a.ctypes.data_as(C.POINTER(C.c_int64)), a.shape[0], C.byref(n)))
         return a[: n.value]
+
+    # f1 edit log (Alg. 1 l.11-13)
+    def edit_encode(self, xh0, yh0, zh0, xc, yc, zc, cap=None):
+        """(flags u8[ceil(3n/8)], q int64[n_edits]) of Delta = corrected - decompressed."""
+        for nm, t in zip("xh0 yh0 zh0 xc yc zc".split(), (xh0, yh0, zh0, xc, yc, zc)):
+            _check_dev(t, torch.float32, nm)
+        n = xh0.shape[0]
+        dev = torch.device("cuda", self.device)
+        nbytes = (3 * n + 7) // 8
+        flags = torch.empty(max((nbytes + 3) // 4, 1), dtype=torch.int32, device=dev).view(torch.uint8)[:nbytes]
+        cap = 3 * n if cap is None else cap
+        q = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+        ne = C.c_int64()
+        self._chk(self.lib.cc_edit_encode(self.h, n, *[_ptr(t) for t in (xh0, yh0, zh0, xc, yc, zc)], _ptr(flags),
+                                          _ptr(q), cap, C.byref(ne)))
+        return flags, q[: ne.value]
+
+    def edit_decode(self, xh0, yh0, zh0, flags, q, out=None):
+        """x_rec = x_hat0 + scatter(dequantise(q), flags) (P:456)."""
+        for nm, t in zip("xh0 yh0 zh0".split(), (xh0, yh0, zh0)):
+            _check_dev(t, torch.float32, nm)
+        _check_dev(flags, torch.uint8, "flags")
+        _check_dev(q, torch.int64, "q")
+        n = xh0.shape[0]
+        if out is None:
+            out = tuple(torch.empty(n, dtype=torch.float32, device=xh0.device) for _ in range(3))
+        self._chk(self.lib.cc_edit_decode(self.h, n, *[_ptr(t) for t in (xh0, yh0, zh0)], _ptr(flags), _ptr(q),
+                                          q.shape[0], *[_ptr(t) for t in out]))
+        return out
 
     # S6
     def fof_label(self, which=CC_ORIG, labels=None):

@@ -276,7 +276,7 @@ void cc_destroy(cc_ctx* c) {
     cc_release(c, c->counters); cc_release(c, c->ctl); cc_release(c, c->trace_a); cc_release(c, c->trace_l);
     cc_release(c, c->trace_v); cc_release(c, c->trace_s); cc_release(c, c->parent_base); cc_release(c, c->parent_orig); cc_release(c, c->rec32);
     cc_release(c, c->frozen); cc_release(c, c->fbits); cc_release(c, c->lab_s); cc_release(c, c->slist); cc_release(c, c->tlist); cc_release(c, c->k3work);
-    cc_release(c, c->tmp_bytes); cc_release(c, c->in_f); cc_release(c, c->in_gid);
+    cc_release(c, c->tmp_bytes); cc_release(c, c->codec_bsum); cc_release(c, c->in_f); cc_release(c, c->in_gid);
     for (int d = 0; d < 2; d++) {
         cc_release(c, c->dflag[d]); cc_release(c, c->dpos[d]); cc_release(c, c->shell[d]); cc_release(c, c->sbuf7[d]);
         cc_release(c, c->rbuf7[d]); cc_release(c, c->req[d]); cc_release(c, c->recv_e[d]); cc_release(c, c->sreq[d]);

@@ -192,6 +192,7 @@ struct cc_ctx {
     int64_t E_cls[4] = {0, 0, 0, 0};  // editables per K3 work class (row_class), numbered class-major
     cc::DBuf<double> trace_l;
     cc::DBuf<unsigned char> tmp_bytes;  // scan scratch
+    cc::DBuf<unsigned long long> codec_bsum;  // f1 edit log: block sums + total + error flag
     cc::DBuf<float> in_f;        // cc_run host staging: 6 n floats
     cc::DBuf<uint32_t> in_gid;
 

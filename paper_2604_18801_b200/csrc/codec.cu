@@ -1,0 +1,263 @@
+// codec.cu -- f1 edit log on the device: compaction and m-bit
+// quantisation of the edits Delta = P_hat - P_hat0 (Alg. 1 lines 11-13; §III-B
+// "Compaction, quantization, and lossless compression") and the reconstruction
+// x_rec = x_hat0 + scatter(dequantise(q), flags) (§III-B "Reconstruction").
+// Readings R29-R31: coordinate k = 3i + a, flags LSB-first in bytes; q =
+// rint(Delta / s) in fp64 with s = xi_f 2^(1-m); x_rec = fl32((double)x_hat0 + (double)q s).
+//
+// One thread per particle, HBM-bound and fully coalesced on the SoA coordinates.  A warp owns
+// 32 particles = 96 coordinates = 3 flag words: each lane forms its 3-bit mask, the words are
+// assembled with one shuffle + ballot each.  Edits are written in ascending k through a
+// reduce-then-scan over blocks (count pass, one-block scan of the block totals, fill pass that
+// recomputes the masks instead of storing them).  Decoding runs the same three passes with the
+// masks read from the flags.
+#include "cc_internal.cuh"
+
+namespace cc {
+namespace {
+
+constexpr int CT = 256;  // threads (= particles) per block
+constexpr int CW = CT / 32;
+
+struct EncMask {
+    const float *xh, *yh, *zh, *xc, *yc, *zc;
+    __device__ uint32_t operator()(int64_t i) const {
+        return (uint32_t)(__ldg(xc + i) != __ldg(xh + i)) | (uint32_t)(__ldg(yc + i) != __ldg(yh + i)) << 1 |
+               (uint32_t)(__ldg(zc + i) != __ldg(zh + i)) << 2;
+    }
+};
+
+struct DecMask {
+    const uint8_t* flags;
+    __device__ uint32_t operator()(int64_t i) const {
+        const int64_t k = 3 * i;
+        const int off = (int)(k & 7);
+        uint32_t v = __ldg(flags + (k >> 3));
+        if (off > 5) v |= (uint32_t)__ldg(flags + (k >> 3) + 1) << 8;  // bits 3i..3i+2 span two bytes
+        return (v >> off) & 7u;
+    }
+};
+
+// block-exclusive prefix of a per-thread count; *total = block total
+__device__ __forceinline__ uint32_t block_excl(uint32_t v, uint32_t* total) {
+    __shared__ uint32_t sw[CW];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+    }
+    if (lane == 31) sw[w] = inc;
+    __syncthreads();
+    uint32_t wex = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < CW; k++) {
+        wex += (k < w) ? sw[k] : 0u;
+        tot += sw[k];
+    }
+    *total = tot;
+    return wex + inc - v;
+}
+
+// pass 1 (encode): flags words + block edit counts; bound check |Delta| <= 2 xi_f (R30)
+__global__ void __launch_bounds__(CT) k_edit_flags(int64_t n, EncMask mk, uint32_t* flags_w, int64_t nbytes,
+                                                   unsigned long long* bsum, double lim, unsigned int* err) {
+    const int64_t i = (int64_t)blockIdx.x * CT + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    uint32_t m3 = 0;
+    if (i < n) {
+        m3 = mk(i);
+        if (m3) {
+            const float* h[3] = {mk.xh, mk.yh, mk.zh};
+            const float* p[3] = {mk.xc, mk.yc, mk.zc};
+#pragma unroll
+            for (int a = 0; a < 3; a++)
+                if ((m3 >> a & 1u) && fabs((double)p[a][i] - (double)h[a][i]) > lim) atomicOr(err, 1u);
+        }
+    }
+    // 96 bits of the warp's 32 particles -> 3 words (bit b of word j = coordinate 32j + b)
+    const int64_t wbase = ((int64_t)blockIdx.x * CT + (threadIdx.x & ~31)) / 32 * 3;
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+        const int b = 32 * j + lane;
+        const uint32_t src = __shfl_sync(0xffffffffu, m3, b / 3);
+        const uint32_t word = __ballot_sync(0xffffffffu, (src >> (b % 3)) & 1u);
+        const int64_t wi = wbase + j;
+        if (lane == j) {
+            if (4 * wi + 4 <= nbytes) {
+                flags_w[wi] = word;
+            } else {
+                uint8_t* fb = reinterpret_cast<uint8_t*>(flags_w);
+                for (int64_t q = 4 * wi; q < nbytes; q++) fb[q] = (uint8_t)(word >> (8 * (q - 4 * wi)));
+            }
+        }
+    }
+    uint32_t tot;
+    (void)block_excl(__popc(m3), &tot);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+// pass 1 (decode): block counts of set flags
+__global__ void __launch_bounds__(CT) k_edit_count(int64_t n, DecMask mk, unsigned long long* bsum) {
+    const int64_t i = (int64_t)blockIdx.x * CT + threadIdx.x;
+    const uint32_t m3 = i < n ? mk(i) : 0u;
+    uint32_t tot;
+    (void)block_excl(__popc(m3), &tot);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+// pass 2: exclusive scan of the block totals in place (one block); bsum[nb] = total
+__global__ void __launch_bounds__(1024) k_edit_scan(int64_t nb, unsigned long long* bsum) {
+    __shared__ unsigned long long sw[32];
+    __shared__ unsigned long long carry_s;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    for (int64_t off = 0; off < nb; off += 1024) {
+        const int64_t i = off + threadIdx.x;
+        const unsigned long long v = i < nb ? bsum[i] : 0ull;
+        unsigned long long inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (lane == 31) sw[w] = inc;
+        __syncthreads();
+        unsigned long long wex = 0, tot = 0;
+        for (int k = 0; k < 32; k++) {
+            wex += (k < w) ? sw[k] : 0ull;
+            tot += sw[k];
+        }
+        const unsigned long long carry = carry_s;
+        if (i < nb) bsum[i] = carry + wex + inc - v;
+        __syncthreads();
+        if (threadIdx.x == 0) carry_s = carry + tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) bsum[nb] = carry_s;
+}
+
+// pass 3 (encode): q = rint(Delta / s) in ascending k (R30)
+__global__ void __launch_bounds__(CT) k_edit_fill(int64_t n, EncMask mk, const unsigned long long* bsum,
+                                                  double s, long long* q, int64_t cap) {
+    const int64_t i = (int64_t)blockIdx.x * CT + threadIdx.x;
+    const uint32_t m3 = i < n ? mk(i) : 0u;
+    uint32_t tot;
+    int64_t o = (int64_t)bsum[blockIdx.x] + block_excl(__popc(m3), &tot);
+    if (!m3) return;
+    const float* h[3] = {mk.xh, mk.yh, mk.zh};
+    const float* p[3] = {mk.xc, mk.yc, mk.zc};
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        if (m3 >> a & 1u) {
+            const double d = (double)p[a][i] - (double)h[a][i];  // exact
+            if (o < cap) q[o] = (long long)rint(d / s);
+            o++;
+        }
+    }
+}
+
+// pass 3 (decode): x_rec = fl32((double)x_hat0 + (double)q s) where flagged, x_hat0 elsewhere (R31)
+__global__ void __launch_bounds__(CT) k_edit_apply(int64_t n, DecMask mk, const unsigned long long* bsum,
+                                                   double s, const long long* q, int64_t n_edits,
+                                                   const float* xh, const float* yh, const float* zh, float* xr,
+                                                   float* yr, float* zr) {
+    const int64_t i = (int64_t)blockIdx.x * CT + threadIdx.x;
+    const uint32_t m3 = i < n ? mk(i) : 0u;
+    uint32_t tot;
+    int64_t o = (int64_t)bsum[blockIdx.x] + block_excl(__popc(m3), &tot);
+    if (i >= n) return;
+    const float* h[3] = {xh, yh, zh};
+    float* r[3] = {xr, yr, zr};
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        float v = __ldg(h[a] + i);
+        if (m3 >> a & 1u) {
+            if (o < n_edits) v = (float)((double)v + (double)__ldg(q + o) * s);
+            o++;
+        }
+        r[a][i] = v;
+    }
+}
+
+bool aligned4(const void* p) { return ((uintptr_t)p & 3u) == 0; }
+
+}  // namespace
+}  // namespace cc
+
+using namespace cc;
+
+static cc_status edit_common(cc_ctx* c, int64_t n, int64_t* nb_out) {
+    if (!c) return CC_E_ARG;
+    if (c->dead) return cc_fail(c, CC_E_CUDA, "context unusable after a CUDA error");
+    cudaSetDevice(c->device);
+    if (n < 0 || 3 * n >= ((int64_t)1 << 62)) return cc_fail(c, CC_E_ARG, "n");
+    if (c->p.m < 2 || c->p.m > 40 || !(c->p.xi > 0)) return cc_fail(c, CC_E_ARG, "edit log needs xi > 0, 2 <= m <= 40");
+    const int64_t nb = (n + CT - 1) / CT;
+    CC_TRY(cc_ensure(c, c->codec_bsum, (size_t)nb + 2, "edit-log block sums"));
+    *nb_out = nb;
+    return CC_OK;
+}
+
+cc_status cc_edit_encode(cc_ctx* c, int64_t n, const float* xh0, const float* yh0, const float* zh0,
+                         const float* xc, const float* yc, const float* zc, uint8_t* flags, int64_t* q,
+                         int64_t cap, int64_t* n_edits_h) {
+    int64_t nb = 0;
+    CC_TRY(edit_common(c, n, &nb));
+    if (!n_edits_h || cap < 0) return cc_fail(c, CC_E_ARG, "null n_edits_h or cap < 0");
+    *n_edits_h = 0;
+    if (n == 0) return CC_OK;
+    if (!xh0 || !yh0 || !zh0 || !xc || !yc || !zc || !flags || (cap > 0 && !q))
+        return cc_fail(c, CC_E_ARG, "null buffer");
+    if (!aligned4(flags)) return cc_fail(c, CC_E_ARG, "flags must be 4-byte aligned");
+    const double xi = (double)(float)c->p.xi, s = std::ldexp(xi, 1 - c->p.m);
+    unsigned long long* bsum = c->codec_bsum.p;
+    unsigned int* err = reinterpret_cast<unsigned int*>(bsum + nb + 1);
+    CC_CUDA(c, cudaMemsetAsync(err, 0, sizeof(unsigned long long), c->stream));
+    const EncMask mk{xh0, yh0, zh0, xc, yc, zc};
+    const int64_t nbytes = (3 * n + 7) / 8;
+    int tok = cc_prof_begin(c, "F1_encode");
+    CCL(c, k_edit_flags<<<(unsigned)nb, CT, 0, c->stream>>>(n, mk, reinterpret_cast<uint32_t*>(flags), nbytes, bsum,
+                                                           2.0 * xi, err));
+    CCL(c, k_edit_scan<<<1, 1024, 0, c->stream>>>(nb, bsum));
+    cc_prof_end(c, tok);
+    unsigned long long h[2];
+    CC_CUDA(c, cudaMemcpyAsync(h, bsum + nb, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    *n_edits_h = (int64_t)h[0];
+    if ((unsigned int)h[1]) return cc_fail(c, CC_E_BOUND, "an edit exceeds 2 xi_f (corrected coordinates out of bound)");
+    if ((int64_t)h[0] > cap) return cc_fail(c, CC_E_OOM, "more edits than cap (*n_edits_h holds the count)");
+    tok = cc_prof_begin(c, "F1_encode");
+    CCL(c, k_edit_fill<<<(unsigned)nb, CT, 0, c->stream>>>(n, mk, bsum, s, reinterpret_cast<long long*>(q), cap));
+    cc_prof_end(c, tok);
+    CC_CUDA(c, cudaGetLastError());
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    return CC_OK;
+}
+
+cc_status cc_edit_decode(cc_ctx* c, int64_t n, const float* xh0, const float* yh0, const float* zh0,
+                         const uint8_t* flags, const int64_t* q, int64_t n_edits, float* xr, float* yr, float* zr) {
+    int64_t nb = 0;
+    CC_TRY(edit_common(c, n, &nb));
+    if (n_edits < 0 || n_edits > 3 * n) return cc_fail(c, CC_E_ARG, "n_edits");
+    if (n == 0) return CC_OK;
+    if (!xh0 || !yh0 || !zh0 || !flags || (n_edits > 0 && !q) || !xr || !yr || !zr)
+        return cc_fail(c, CC_E_ARG, "null buffer");
+    const double s = std::ldexp((double)(float)c->p.xi, 1 - c->p.m);
+    unsigned long long* bsum = c->codec_bsum.p;
+    const DecMask mk{flags};
+    int tok = cc_prof_begin(c, "F1_decode");
+    CCL(c, k_edit_count<<<(unsigned)nb, CT, 0, c->stream>>>(n, mk, bsum));
+    CCL(c, k_edit_scan<<<1, 1024, 0, c->stream>>>(nb, bsum));
+    CCL(c, k_edit_apply<<<(unsigned)nb, CT, 0, c->stream>>>(n, mk, bsum, s, reinterpret_cast<const long long*>(q),
+                                                           n_edits, xh0, yh0, zh0, xr, yr, zr));
+    cc_prof_end(c, tok);
+    CC_CUDA(c, cudaGetLastError());
+    unsigned long long tot = 0;
+    CC_CUDA(c, cudaMemcpyAsync(&tot, bsum + nb, sizeof(tot), cudaMemcpyDeviceToHost, c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    if ((int64_t)tot != n_edits) return cc_fail(c, CC_E_DATA, "popcount(flags) != n_edits");
+    return CC_OK;
+}

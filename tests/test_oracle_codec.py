@@ -1,6 +1,6 @@
 """Pins for the oracle's edit log: compaction, m-bit quantisation and
 reconstruction -- Alg. 1 lines 11-13, §III-B P:446-448 ("Compaction,
-quantization, and lossless compression"), P:456 ("Reconstruction"); readings R24-R26
+quantization, and lossless compression"), P:456 ("Reconstruction"); readings R29-R31
 (DESIGN.md §3).
 
 Pinned against: the hand-built bit layout of SPEC's worked example, lattice points and
@@ -25,7 +25,7 @@ def _cfg(xi=1e-3, m=16, L=1.0):
 
 def test_worked_bit_layout():
     """edits at coordinates k=0 and k=5 -> flags byte0 = 0b00100001, values in
-    ascending k.  k = 3i + a (R24): k=0 is x of particle 0, k=5 is z of particle 1."""
+    ascending k.  k = 3i + a (R29): k=0 is x of particle 0, k=5 is z of particle 1."""
     c = _cfg()
     s = oracle.edit_step(c)
     h = [np.full(3, 0.25, np.float32) for _ in range(3)]
@@ -52,7 +52,7 @@ def test_empty_and_zero():
 
 
 def test_lattice_and_half_even():
-    """s = xi_f 2^(1-m) (R25); lattice points map to their index, half-way values round to
+    """s = xi_f 2^(1-m) (R30); lattice points map to their index, half-way values round to
     even (IEEE rint), with xi = 2^-10 so that k s is exact: 0.5s -> 0, 1.5s -> 2, 2.5s -> 2, -0.5s -> 0, -1.5s -> -2."""
     for m in (8, 16):
         c = _cfg(xi=2.0 ** -10, m=m)          # power-of-2 xi: every k s below is an fp32
