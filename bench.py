@@ -428,7 +428,7 @@ def main():
     # ---- f1 edit log (Alg. 1 l.11-13 + reconstruction) on this step's correction;
     # outside the timed step (not one of the §8(a) rows), timed on the library's stream
     if not args.no_edit_log:
-        fl, q = c.edit_encode(xh, yh, zh, *out)
+        fl, q = c.edit_encode(x, y, z, xh, yh, zh, *out)
         rec = c.edit_decode(xh, yh, zh, fl, q)
         xi_f = float(np.float32(w.xi))
         in_bound = all(bool(((r.double() - o.double()).abs() <= xi_f).all()) for r, o in zip(rec, (x, y, z)))
@@ -442,19 +442,23 @@ def main():
         ms_e = ms_d = 0.0
         for _ in range(ke):
             ev[0].record(stream)
-            fl, q = c.edit_encode(xh, yh, zh, *out)
+            fl, q = c.edit_encode(x, y, z, xh, yh, zh, *out)
             ev[1].record(stream)
             c.edit_decode(xh, yh, zh, fl, q, out=rec)
             ev[2].record(stream)
             torch.cuda.synchronize(dev)
             ms_e += ev[0].elapsed_time(ev[1]) / ke
             ms_d += ev[1].elapsed_time(ev[2]) / ke
+        # quantisation-safety re-check (R31): S1 + S2 on (P, x_rec) -> violated pairs
+        c.build_cells(x, y, z, *rec, gid=gid)
+        recheck = c.find_vulnerable()
         ne = int(q.shape[0])
         fb = (3 * n + 7) // 8
         b_enc = 24 * n + fb + 8 * ne        # read P_hat0 and P_hat, write flags and indices
         b_dec = 12 * n + fb + 8 * ne + 12 * n
         pk = hbm or 1.0
         line["edit_log"] = {"n_edits": ne, "flags_bytes": fb, "index_bytes": 8 * ne, "in_bound": in_bound, "diag": diag,
+                            "recheck_pairs": recheck["n_pairs"], "recheck_violated": recheck["n_violated0"],
                             "encode_ms": ms_e, "decode_ms": ms_d,
                             "encode_gbs": b_enc / (ms_e * 1e-3) / 1e9, "decode_gbs": b_dec / (ms_d * 1e-3) / 1e9,
                             "encode_frac": b_enc / (ms_e * 1e-3) / 1e9 / pk,

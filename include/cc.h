@@ -203,9 +203,11 @@ cc_status cc_run(cc_ctx* ctx, int64_t n, const float* x, const float* y, const f
  * "Compaction, quantization, and lossless compression": Delta = corrected -
  * decompressed; flags = bitmask of the non-zero entries of Delta, packed into bytes; edits = the
  * non-zero Delta quantised on the uniform lattice s = xi_f 2^(1-m) (xi_f = fl32(params.xi),
- * m = params.m; readings R29-R30).  Independent of the context's state (uses its
+ * m = params.m; readings R29-R30, R32).  Independent of the context's state (uses its
  * params, stream and allocator only); one rank encodes its own particles.
  *   n:           particles, arrays in the caller's (input) order
+ *   x..z:        original coordinates P (device; Alg. 1 REQUIRE): each index is stepped toward
+ *                x while the decoder's fp32 x_rec would leave |x_rec - x| <= xi_f (R32)
  *   xh0..zh0:    decompressed coordinates P_hat0 (device, n floats each)
  *   xc..zc:      corrected coordinates P_hat (device, n floats each), |Delta| <= 2 xi_f
  *   flags:       device, ceil(3n/8) bytes, 4-byte aligned; coordinate k = 3i + a (a = x,y,z) is
@@ -214,8 +216,9 @@ cc_status cc_run(cc_ctx* ctx, int64_t n, const float* x, const float* y, const f
  *                per set flag bit in ascending k; |q| <= 2^(m+1)
  *   *n_edits_h:  number of set flag bits (= edits), written whatever the status
  * Errors: CC_E_ARG (null/unaligned buffer, n < 0, xi <= 0, m outside [2, 40]); CC_E_BOUND
- * (some |Delta| > 2 xi_f); CC_E_OOM (n_edits > cap; flags written, q not).  Synchronises. */
-cc_status cc_edit_encode(cc_ctx* ctx, int64_t n, const float* xh0, const float* yh0, const float* zh0,
+ * (some |Delta| > 2 xi_f, or no index within 8 steps reconstructs in bound); CC_E_OOM (n_edits > cap; flags written, q not).  Synchronises. */
+cc_status cc_edit_encode(cc_ctx* ctx, int64_t n, const float* x, const float* y, const float* z,
+                         const float* xh0, const float* yh0, const float* zh0,
                          const float* xc, const float* yc, const float* zc, uint8_t* flags, int64_t* q,
                          int64_t cap, int64_t* n_edits_h);
 

@@ -86,7 +86,7 @@ def lib():
         L.oc_tight_f64.restype = C.c_double
         L.oc_correct.argtypes = [C.c_int64, f32p, f32p, f32p, f32p, f32p, f32p, u32p, C.c_int64, i64p, i64p,
                                  u8p, P(Cfg), f32p, f32p, f32p, P(CorrInfo), i64p, f64p, i64p]
-        L.oc_edit_encode.argtypes = [C.c_int64, f32p, f32p, f32p, f32p, f32p, f32p, P(Cfg), u8p, i64p,
+        L.oc_edit_encode.argtypes = [C.c_int64, f32p, f32p, f32p, f32p, f32p, f32p, f32p, f32p, f32p, P(Cfg), u8p, i64p,
                                      C.c_int64, i64p]
         L.oc_edit_decode.argtypes = [C.c_int64, f32p, f32p, f32p, u8p, i64p, C.c_int64, P(Cfg),
                                      f32p, f32p, f32p]
@@ -306,9 +306,10 @@ def edit_step(c: Cfg) -> float:
     return math.ldexp(float(np.float32(c.xi)), 1 - c.m)
 
 
-def edit_encode(xh0, yh0, zh0, xc, yc, zc, c: Cfg):
-    """Alg. 1 lines 11-13, §III-B P:446 (R29, R30): returns (flags u8[ceil(3n/8)],
-    q int64[n_edits]) for Delta = corrected - decompressed."""
+def edit_encode(x, y, z, xh0, yh0, zh0, xc, yc, zc, c: Cfg):
+    """Alg. 1 lines 11-13, §III-B P:446 (R29, R30, R32): returns (flags
+    u8[ceil(3n/8)], q int64[n_edits]) for Delta = corrected - decompressed; x, y, z = P."""
+    o = [_f32(a) for a in (x, y, z)]
     h = [_f32(a) for a in (xh0, yh0, zh0)]
     p = [_f32(a) for a in (xc, yc, zc)]
     n = h[0].size
@@ -316,7 +317,7 @@ def edit_encode(xh0, yh0, zh0, xc, yc, zc, c: Cfg):
     cap = 3 * n
     q = np.zeros(max(cap, 1), np.int64)
     ne = C.c_int64(0)
-    st = lib().oc_edit_encode(n, *[_ptr(a, C.c_float) for a in h + p], C.byref(c), _ptr(flags, C.c_uint8),
+    st = lib().oc_edit_encode(n, *[_ptr(a, C.c_float) for a in o + h + p], C.byref(c), _ptr(flags, C.c_uint8),
                               _ptr(q, C.c_int64), cap, C.byref(ne))
     if st:
         raise ValueError(f"oc_edit_encode status {st}")

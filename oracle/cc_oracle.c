@@ -733,6 +733,10 @@ done:
  *        reconstruction error s/2 = xi 2^-m = xi - xi' < eps_q.
  *   R31  reconstruction: x_rec = fl32((double)x_hat0 + (double)q * s) for a flagged coordinate,
  *        x_hat0 unchanged otherwise ("element-wise addition ... to the initial output").
+ *   R32  bound-safe index: xi' + s/2 = xi leaves no room for the fp32 rounding of x_rec where
+ *        ulp(x) < s, so the encoder (which holds P, Alg. 1 REQUIRE) checks the decoder's value
+ *        and, while |x_rec - x| > xi_f, moves q one lattice step toward x (at most 8 steps,
+ *        else 66).  |x_rec - x| <= xi_f then holds exactly (Eq. 2).
  * The Huffman+ZSTD stage is a lossless host stage, not part of this oracle.
  * ------------------------------------------------------------------------------------------- */
 static double oc_edit_step(const oc_cfg* c) {
@@ -740,11 +744,13 @@ static double oc_edit_step(const oc_cfg* c) {
 }
 
 /* Returns 0, 64 (arguments), 66 (|Delta| > 2 xi_f) or 67 (more edits than cap; *n_edits set). */
-int oc_edit_encode(int64_t n, const float* xh0, const float* yh0, const float* zh0,
+int oc_edit_encode(int64_t n, const float* x, const float* y, const float* z,
+                   const float* xh0, const float* yh0, const float* zh0,
                    const float* xc, const float* yc, const float* zc, const oc_cfg* c,
                    uint8_t* flags, int64_t* q, int64_t cap, int64_t* n_edits) {
     if (n < 0 || !c || !n_edits || c->m < 2 || c->m > 40 || !(c->xi > 0)) return 64;
-    const double s = oc_edit_step(c), lim = 2.0 * (double)(float)c->xi;
+    const double s = oc_edit_step(c), xi_f = (double)(float)c->xi, lim = 2.0 * xi_f;
+    const float* o[3] = {x, y, z};
     const float* h[3] = {xh0, yh0, zh0};
     const float* p[3] = {xc, yc, zc};
     memset(flags, 0, (size_t)((3 * n + 7) / 8));
@@ -756,7 +762,15 @@ int oc_edit_encode(int64_t n, const float* xh0, const float* yh0, const float* z
             double delta = (double)p[a][i] - (double)h[a][i];  /* exact (R30) */
             if (fabs(delta) > lim) return 66;
             flags[k / 8] |= (uint8_t)(1u << (k % 8));
-            if (ne < cap) q[ne] = (int64_t)rint(delta / s);
+            int64_t qi = (int64_t)rint(delta / s);
+            for (int step = 0;; step++) {                       /* R32 */
+                float r = (float)((double)h[a][i] + (double)qi * s);
+                double dev = (double)r - (double)o[a][i];
+                if (fabs(dev) <= xi_f) break;
+                if (step == 8) return 66;
+                qi += dev > 0 ? -1 : 1;
+            }
+            if (ne < cap) q[ne] = qi;
             ne++;
         }
     }

@@ -102,7 +102,7 @@ def lib():
     L.cc_hmf.argtypes = [P(i64), i64, d, C.c_int, d, d, P(d), P(d)]
     L.cc_kernel_stats.argtypes = [vp, C.c_char_p, i64, P(d), P(i64), i64, P(i64), C.c_int]
     L.cc_run.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, P(_Run)]
-    L.cc_edit_encode.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, i64, P(i64)]
+    L.cc_edit_encode.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, P(i64)]
     L.cc_edit_decode.argtypes = [vp, i64, vp, vp, vp, vp, vp, i64, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("cc_default_params", "cc_destroy", "cc_last_error"):
@@ -249,9 +249,10 @@ class Corrector:
         return a[: n.value]
 
     # f1 edit log (Alg. 1 l.11-13)
-    def edit_encode(self, xh0, yh0, zh0, xc, yc, zc, cap=None):
-        """(flags u8[ceil(3n/8)], q int64[n_edits]) of Delta = corrected - decompressed."""
-        for nm, t in zip("xh0 yh0 zh0 xc yc zc".split(), (xh0, yh0, zh0, xc, yc, zc)):
+    def edit_encode(self, x, y, z, xh0, yh0, zh0, xc, yc, zc, cap=None):
+        """(flags u8[ceil(3n/8)], q int64[n_edits]) of Delta = corrected - decompressed;
+        x, y, z = the original positions (bound-safe indices, R32)."""
+        for nm, t in zip("x y z xh0 yh0 zh0 xc yc zc".split(), (x, y, z, xh0, yh0, zh0, xc, yc, zc)):
             _check_dev(t, torch.float32, nm)
         n = xh0.shape[0]
         dev = torch.device("cuda", self.device)
@@ -260,7 +261,7 @@ class Corrector:
         cap = 3 * n if cap is None else cap
         q = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
         ne = C.c_int64()
-        self._chk(self.lib.cc_edit_encode(self.h, n, *[_ptr(t) for t in (xh0, yh0, zh0, xc, yc, zc)], _ptr(flags),
+        self._chk(self.lib.cc_edit_encode(self.h, n, *[_ptr(t) for t in (x, y, z, xh0, yh0, zh0, xc, yc, zc)], _ptr(flags),
                                           _ptr(q), cap, C.byref(ne)))
         return flags, q[: ne.value]
 

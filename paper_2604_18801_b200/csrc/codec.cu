@@ -2,8 +2,9 @@
 // quantisation of the edits Delta = P_hat - P_hat0 (Alg. 1 lines 11-13; §III-B
 // "Compaction, quantization, and lossless compression") and the reconstruction
 // x_rec = x_hat0 + scatter(dequantise(q), flags) (§III-B "Reconstruction").
-// Readings R29-R31: coordinate k = 3i + a, flags LSB-first in bytes; q =
-// rint(Delta / s) in fp64 with s = xi_f 2^(1-m); x_rec = fl32((double)x_hat0 + (double)q s).
+// Readings R29-R32: coordinate k = 3i + a, flags LSB-first in bytes; q =
+// rint(Delta / s) in fp64 with s = xi_f 2^(1-m), then stepped toward x while the decoder's
+// x_rec = fl32((double)x_hat0 + (double)q s) would leave |x_rec - x| <= xi_f (R32).
 //
 // One thread per particle, HBM-bound and fully coalesced on the SoA coordinates.  A warp owns
 // 32 particles = 96 coordinates = 3 flag words: each lane forms its 3-bit mask, the words are
@@ -139,9 +140,11 @@ __global__ void __launch_bounds__(1024) k_edit_scan(int64_t nb, unsigned long lo
     if (threadIdx.x == 0) bsum[nb] = carry_s;
 }
 
-// pass 3 (encode): q = rint(Delta / s) in ascending k (R30)
-__global__ void __launch_bounds__(CT) k_edit_fill(int64_t n, EncMask mk, const unsigned long long* bsum,
-                                                  double s, long long* q, int64_t cap) {
+// pass 3 (encode): q = rint(Delta / s) in ascending k (R30), bound-safe against the decoder's
+// fp32 rounding (R32; err bit 2 if 8 steps do not suffice)
+__global__ void __launch_bounds__(CT) k_edit_fill(int64_t n, EncMask mk, const float* x, const float* y,
+                                                  const float* z, const unsigned long long* bsum, double s,
+                                                  double xi_f, long long* q, int64_t cap, unsigned int* err) {
     const int64_t i = (int64_t)blockIdx.x * CT + threadIdx.x;
     const uint32_t m3 = i < n ? mk(i) : 0u;
     uint32_t tot;
@@ -149,11 +152,24 @@ __global__ void __launch_bounds__(CT) k_edit_fill(int64_t n, EncMask mk, const u
     if (!m3) return;
     const float* h[3] = {mk.xh, mk.yh, mk.zh};
     const float* p[3] = {mk.xc, mk.yc, mk.zc};
+    const float* org[3] = {x, y, z};
 #pragma unroll
     for (int a = 0; a < 3; a++) {
         if (m3 >> a & 1u) {
-            const double d = (double)p[a][i] - (double)h[a][i];  // exact
-            if (o < cap) q[o] = (long long)rint(d / s);
+            const double hv = (double)h[a][i];
+            const double d = (double)p[a][i] - hv;  // exact
+            long long qi = (long long)rint(d / s);
+            const double xo = (double)__ldg(org[a] + i);
+            for (int step = 0;; step++) {
+                const double dev = (double)(float)(hv + (double)qi * s) - xo;
+                if (fabs(dev) <= xi_f) break;
+                if (step == 8) {
+                    atomicOr(err, 2u);
+                    break;
+                }
+                qi += dev > 0 ? -1 : 1;
+            }
+            if (o < cap) q[o] = qi;
             o++;
         }
     }
@@ -201,7 +217,8 @@ static cc_status edit_common(cc_ctx* c, int64_t n, int64_t* nb_out) {
     return CC_OK;
 }
 
-cc_status cc_edit_encode(cc_ctx* c, int64_t n, const float* xh0, const float* yh0, const float* zh0,
+cc_status cc_edit_encode(cc_ctx* c, int64_t n, const float* x, const float* y, const float* z,
+                         const float* xh0, const float* yh0, const float* zh0,
                          const float* xc, const float* yc, const float* zc, uint8_t* flags, int64_t* q,
                          int64_t cap, int64_t* n_edits_h) {
     int64_t nb = 0;
@@ -209,7 +226,7 @@ cc_status cc_edit_encode(cc_ctx* c, int64_t n, const float* xh0, const float* yh
     if (!n_edits_h || cap < 0) return cc_fail(c, CC_E_ARG, "null n_edits_h or cap < 0");
     *n_edits_h = 0;
     if (n == 0) return CC_OK;
-    if (!xh0 || !yh0 || !zh0 || !xc || !yc || !zc || !flags || (cap > 0 && !q))
+    if (!x || !y || !z || !xh0 || !yh0 || !zh0 || !xc || !yc || !zc || !flags || (cap > 0 && !q))
         return cc_fail(c, CC_E_ARG, "null buffer");
     if (!aligned4(flags)) return cc_fail(c, CC_E_ARG, "flags must be 4-byte aligned");
     const double xi = (double)(float)c->p.xi, s = std::ldexp(xi, 1 - c->p.m);
@@ -230,10 +247,14 @@ cc_status cc_edit_encode(cc_ctx* c, int64_t n, const float* xh0, const float* yh
     if ((unsigned int)h[1]) return cc_fail(c, CC_E_BOUND, "an edit exceeds 2 xi_f (corrected coordinates out of bound)");
     if ((int64_t)h[0] > cap) return cc_fail(c, CC_E_OOM, "more edits than cap (*n_edits_h holds the count)");
     tok = cc_prof_begin(c, "F1_encode");
-    CCL(c, k_edit_fill<<<(unsigned)nb, CT, 0, c->stream>>>(n, mk, bsum, s, reinterpret_cast<long long*>(q), cap));
+    CCL(c, k_edit_fill<<<(unsigned)nb, CT, 0, c->stream>>>(n, mk, x, y, z, bsum, s, xi,
+                                                          reinterpret_cast<long long*>(q), cap, err));
     cc_prof_end(c, tok);
     CC_CUDA(c, cudaGetLastError());
+    unsigned int e2 = 0;
+    CC_CUDA(c, cudaMemcpyAsync(&e2, err, sizeof(e2), cudaMemcpyDeviceToHost, c->stream));
     CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (e2) return cc_fail(c, CC_E_BOUND, "no lattice index reconstructs within xi_f (R32)");
     return CC_OK;
 }
 

@@ -1,6 +1,6 @@
 """GPU parity of the f1 edit log (cc_edit_encode / cc_edit_decode through the C ABI) against
 the oracle's oc_edit_encode / oc_edit_decode: Alg. 1 lines 11-13, §III-B
-and P:456, readings R29-R31.  Flags bytes, quantisation indices and reconstructed coordinates
+and P:456, readings R29-R32.  Flags bytes, quantisation indices and reconstructed coordinates
 are bit-exact (integer/byte work; the fp64 quantiser and the single fp32 rounding of the
 reconstruction are the same IEEE operations on both sides).  Inputs: seeded synthetic edit sets
 (sparse, ragged sizes, several magnitudes and bit depths) and the C1 correction of each side;
@@ -43,9 +43,9 @@ def _check(h, p, L, xi, m):
     params = cc.Params(box=L, b=0.01 * L, xi=xi, m=m)
     ctx = cc.Corrector(params, device=0)
     hd, pd = [_dev(a) for a in h], [_dev(a) for a in p]
-    flags, q = ctx.edit_encode(*hd, *pd)
+    flags, q = ctx.edit_encode(*pd, *hd, *pd)
     oc = oracle.cfg(L=L, b=0.01 * L, xi=xi, m=m)
-    of, oq = oracle.edit_encode(*h, *p, oc)
+    of, oq = oracle.edit_encode(*p, *h, *p, oc)
     assert np.array_equal(flags.cpu().numpy(), of)
     assert np.array_equal(q.cpu().numpy(), oq)
     rec = ctx.edit_decode(*hd, flags, q)
@@ -82,17 +82,17 @@ def test_errors():
     p = [t.clone() for t in h]
     p[1][7] = 2.5e-3                                         # |Delta| > 2 xi_f
     with pytest.raises(cc.CCError, match="CC_E_BOUND"):
-        ctx.edit_encode(*h, *p)
+        ctx.edit_encode(*p, *h, *p)
     p[1][7] = 1e-3
     p[2][9] = -1e-3
     with pytest.raises(cc.CCError, match="CC_E_OOM"):
-        ctx.edit_encode(*h, *p, cap=1)
-    flags, q = ctx.edit_encode(*h, *p)
+        ctx.edit_encode(*p, *h, *p, cap=1)
+    flags, q = ctx.edit_encode(*p, *h, *p)
     assert q.shape[0] == 2
     with pytest.raises(cc.CCError, match="CC_E_DATA"):
         ctx.edit_decode(*h, flags, q[:1])
     e = [torch.zeros(0, dtype=torch.float32, device=DEV) for _ in range(3)]
-    f0, q0 = ctx.edit_encode(*e, *e)
+    f0, q0 = ctx.edit_encode(*e, *e, *e)
     assert f0.numel() == 0 and q0.numel() == 0
     ctx.close()
 
@@ -112,13 +112,13 @@ def test_c1_correction_edit_log_and_recheck(xi_rel):
     ctx.find_vulnerable()
     out, info = ctx.correct()
     assert info["converged"]
-    flags, q = ctx.edit_encode(*ts[3:], *out)
+    flags, q = ctx.edit_encode(*ts, *out)
     rec = ctx.edit_decode(*ts[3:], flags, q)
     ctx.close()
 
     c = oracle_cfg(params, len(arrs[0]))
     r = oracle.pipeline(*arrs, c)
-    of, oq = oracle.edit_encode(*arrs[3:], r.xo, r.yo, r.zo, c)
+    of, oq = oracle.edit_encode(*arrs, r.xo, r.yo, r.zo, c)
     assert np.array_equal(flags.cpu().numpy(), of)
     assert np.array_equal(q.cpu().numpy(), oq)
 
@@ -132,3 +132,29 @@ def test_c1_correction_edit_log_and_recheck(xi_rel):
     ld, _ = chk.fof_label(cc.CC_DECOMP)
     assert np.array_equal(lo, ld.cpu().numpy())
     chk.close()
+
+
+def test_bound_safe_index_near_origin():
+    """R32 on the GPU: box-saturated corrections near the origin (ulp(x) < s), where the plain
+    nearest index can reconstruct up to half an ulp outside xi_f; bit-exact vs the oracle and
+    every reconstruction within xi_f of the original."""
+    rng = np.random.default_rng(12)
+    n, xi = 300_001, 1e-3
+    oc = oracle.cfg(L=1.0, b=0.01, xi=xi)
+    th = oracle.thresholds(oc)
+    x = rng.uniform(0.0, 0.3, n).astype(np.float32)
+    sign = np.where(rng.random(n) < 0.5, -1.0, 1.0)
+    h = (x.astype(np.float64) - sign * rng.uniform(0, th["xi_f"], n)).astype(np.float32)
+    p = (x.astype(np.float64) + sign * float(th["xip_f"])).astype(np.float32)
+    ok = (np.abs(p.astype(np.float64) - x) <= float(th["xip_f"])) & (np.abs(h.astype(np.float64) - x) <= th["xi_f"])
+    x, h, p = x[ok], h[ok], p[ok]
+    y = np.full_like(x, 0.5)
+    ctx = cc.Corrector(cc.Params(box=1.0, b=0.01, xi=xi), device=0)
+    d = [_dev(a) for a in (x, y, y, h, y, y, p, y, y)]
+    flags, q = ctx.edit_encode(*d)
+    of, oq = oracle.edit_encode(x, y, y, h, y, y, p, y, y, oc)
+    assert np.array_equal(flags.cpu().numpy(), of) and np.array_equal(q.cpu().numpy(), oq)
+    xr, _, _ = ctx.edit_decode(d[3], d[4], d[5], flags, q)
+    xr = xr.cpu().numpy()
+    assert np.all(np.abs(xr.astype(np.float64) - x) <= th["xi_f"])
+    ctx.close()

@@ -32,7 +32,7 @@ def test_worked_bit_layout():
     p = [a.copy() for a in h]
     p[0][0] = np.float32(0.25 + 3 * s)     # k = 0, q = +3
     p[2][1] = np.float32(0.25 - 7 * s)     # k = 5, q = -7
-    flags, q = oracle.edit_encode(*h, *p, c)
+    flags, q = oracle.edit_encode(*p, *h, *p, c)
     assert flags.tolist() == [0b00100001, 0]          # ceil(9/8) = 2 bytes
     assert q.tolist() == [3, -7]
     r = oracle.edit_decode(*h, flags, q, c)
@@ -43,11 +43,11 @@ def test_worked_bit_layout():
 def test_empty_and_zero():
     c = _cfg()
     h = [np.arange(5, dtype=np.float32) / 7 for _ in range(3)]
-    flags, q = oracle.edit_encode(*h, *h, c)
+    flags, q = oracle.edit_encode(*h, *h, *h, c)
     assert flags.tolist() == [0, 0] and q.size == 0
     r = oracle.edit_decode(*h, flags, q, c)
     assert all(np.array_equal(r[a], h[a]) for a in range(3))
-    f0, q0 = oracle.edit_encode(*[np.zeros(0, np.float32)] * 6, c)
+    f0, q0 = oracle.edit_encode(*[np.zeros(0, np.float32)] * 9, c)
     assert f0.size == 0 and q0.size == 0
 
 
@@ -64,7 +64,7 @@ def test_lattice_and_half_even():
         p = [np.zeros(len(ks), np.float32) for _ in range(3)]
         p[1][:] = np.array([k * s for k in ks], np.float32)     # exact in fp32 (power-of-2 scale)
         assert all(Fraction(float(v)) == Fraction(k) * Fraction(s) for v, k in zip(p[1], ks))
-        flags, q = oracle.edit_encode(*h, *p, c)
+        flags, q = oracle.edit_encode(*p, *h, *p, c)
         assert q.tolist() == want
 
 
@@ -84,7 +84,7 @@ def test_quantisation_error_bound_exact():
             d = p[a].astype(np.float64) - h[a]
             bad = np.abs(d) > 2 * xi_f
             p[a][bad] = h[a][bad]
-        flags, q = oracle.edit_encode(*h, *p, c)
+        flags, q = oracle.edit_encode(*p, *h, *p, c)
         bits = np.unpackbits(flags, bitorder="little")[: 3 * n].reshape(n, 3)
         want_bits = np.stack([p[a] != h[a] for a in range(3)], 1)
         assert np.array_equal(bits.astype(bool), want_bits)
@@ -112,7 +112,7 @@ def test_bound_violation_rejected():
     p = [a.copy() for a in h]
     p[0][1] = np.float32(2.01e-3)
     with pytest.raises(ValueError, match="66"):
-        oracle.edit_encode(*h, *p, c)
+        oracle.edit_encode(*h, *h, *p, c)
 
 
 @pytest.mark.parametrize("xi_rel", [1e-3, 1e-4])
@@ -127,7 +127,7 @@ def test_no_violation_reintroduced(xi_rel):
     c = oracle.cfg(L=1.0, b=w.linking_length, xi=w.xi)
     r = oracle.pipeline(x, y, z, xh, yh, zh, c)
     assert r.info["converged"]
-    flags, q = oracle.edit_encode(xh, yh, zh, r.xo, r.yo, r.zo, c)
+    flags, q = oracle.edit_encode(x, y, z, xh, yh, zh, r.xo, r.yo, r.zo, c)
     xr, yr, zr = oracle.edit_decode(xh, yh, zh, flags, q, c)
     ol = (r.pairs[2] & 1).astype(bool)
     assert np.array_equal(oracle.pair_links(r.pairs[0], r.pairs[1], xr, yr, zr, c), ol)
@@ -142,3 +142,38 @@ def test_no_violation_reintroduced(xi_rel):
     # at most 3|E| edits
     ed = np.zeros(len(x), bool); ed[r.pairs[0]] = True; ed[r.pairs[1]] = True
     assert q.size <= 3 * int(ed.sum())
+
+
+def test_bound_safe_index_near_origin():
+    """R32: where ulp(x) < s the fp32 rounding of x_hat0 + q s can leave the box by up to half an
+    ulp when the correction sits on the projection box (xi' + s/2 = xi).  Brute force over
+    box-saturated corrections near the origin: every reconstruction lies within xi_f of the
+    original (exact fp64 test of fp32 values), each index is within one lattice step of the
+    nearest one (exact rationals), and the plain nearest index would have failed on some."""
+    rng = np.random.default_rng(11)
+    n, xi = 20000, 1e-3
+    c = _cfg(xi=xi)
+    s = Fraction(oracle.edit_step(c))
+    th = oracle.thresholds(c)
+    xi_f, xip = th["xi_f"], th["xip_f"]
+    x = rng.uniform(0.0, 0.3, n).astype(np.float32)
+    sign = np.where(rng.random(n) < 0.5, -1.0, 1.0)
+    h = (x.astype(np.float64) - sign * rng.uniform(0, xi_f, n)).astype(np.float32)
+    p = (x.astype(np.float64) + sign * float(xip)).astype(np.float32)     # on the B(xi') box
+    ok = np.abs(p.astype(np.float64) - x) <= float(xip)
+    ok &= np.abs(h.astype(np.float64) - x) <= xi_f
+    x, h, p = x[ok], h[ok], p[ok]
+    z = np.zeros_like(x)
+    flags, q = oracle.edit_encode(x, z, z, h, z, z, p, z, z, c)
+    assert q.size == int((p != h).sum())
+    xr, _, _ = oracle.edit_decode(h, z, z, flags, q, c)
+    assert np.all(np.abs(xr.astype(np.float64) - x) <= xi_f)
+    moved = np.nonzero(p != h)[0]
+    plain_bad = 0
+    for k, i in enumerate(moved):
+        d = Fraction(float(p[i])) - Fraction(float(h[i]))
+        q0 = round(d / s)                                   # nearest lattice index (half even)
+        assert abs(int(q[k]) - q0) <= 1
+        r0 = np.float32(float(Fraction(float(h[i])) + q0 * s))
+        plain_bad += abs(Fraction(float(r0)) - Fraction(float(x[i]))) > Fraction(xi_f)
+    assert plain_bad > 0
