@@ -6,7 +6,8 @@
 // rint(Delta / s) in fp64 with s = xi_f 2^(1-m), then stepped toward x while the decoder's
 // x_rec = fl32((double)x_hat0 + (double)q s) would leave |x_rec - x| <= xi_f (R32).
 //
-// One thread per particle, HBM-bound and fully coalesced on the SoA coordinates.  A warp owns
+// One thread per particle (a block walks SUB sub-tiles of CT particles), HBM-bound and fully
+// coalesced on the SoA coordinates.  A warp owns
 // 32 particles = 96 coordinates = 3 flag words: each lane forms its 3-bit mask, the words are
 // assembled with one shuffle + ballot each.  Edits are written in ascending k through a
 // reduce-then-scan over blocks (count pass, one-block scan of the block totals, fill pass that
@@ -17,8 +18,11 @@
 namespace cc {
 namespace {
 
-constexpr int CT = 256;  // threads (= particles) per block
+constexpr int CT = 256;         // threads per block; one particle per thread per sub-tile
 constexpr int CW = CT / 32;
+constexpr int SUB = 8;          // sub-tiles per block: a block owns CT * SUB consecutive particles
+constexpr int TILE = CT * SUB;  // (keeps the block-sum scan short: N / 2048 entries)
+constexpr int SCAN_ITEMS = 8;   // block sums per thread per k_edit_scan iteration
 
 struct EncMask {
     const float *xh, *yh, *zh, *xc, *yc, *zc;
@@ -43,6 +47,7 @@ struct DecMask {
 __device__ __forceinline__ uint32_t block_excl(uint32_t v, uint32_t* total) {
     __shared__ uint32_t sw[CW];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();  // sw may still be read by the previous call
     uint32_t inc = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -64,60 +69,76 @@ __device__ __forceinline__ uint32_t block_excl(uint32_t v, uint32_t* total) {
 // pass 1 (encode): flags words + block edit counts; bound check |Delta| <= 2 xi_f (R30)
 __global__ void __launch_bounds__(CT) k_edit_flags(int64_t n, EncMask mk, uint32_t* flags_w, int64_t nbytes,
                                                    unsigned long long* bsum, double lim, unsigned int* err) {
-    const int64_t i = (int64_t)blockIdx.x * CT + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    uint32_t m3 = 0;
-    if (i < n) {
-        m3 = mk(i);
-        if (m3) {
-            const float* h[3] = {mk.xh, mk.yh, mk.zh};
-            const float* p[3] = {mk.xc, mk.yc, mk.zc};
+    uint32_t cnt = 0;
+    for (int t = 0; t < SUB; t++) {
+        const int64_t i0 = (int64_t)blockIdx.x * TILE + t * CT;
+        if (i0 >= n) break;  // uniform over the block
+        const int64_t i = i0 + threadIdx.x;
+        uint32_t m3 = 0;
+        if (i < n) {
+            m3 = mk(i);
+            if (m3) {
+                const float* h[3] = {mk.xh, mk.yh, mk.zh};
+                const float* p[3] = {mk.xc, mk.yc, mk.zc};
 #pragma unroll
-            for (int a = 0; a < 3; a++)
-                if ((m3 >> a & 1u) && fabs((double)p[a][i] - (double)h[a][i]) > lim) atomicOr(err, 1u);
+                for (int a = 0; a < 3; a++)
+                    if ((m3 >> a & 1u) && fabs((double)p[a][i] - (double)h[a][i]) > lim) atomicOr(err, 1u);
+            }
         }
-    }
-    // 96 bits of the warp's 32 particles -> 3 words (bit b of word j = coordinate 32j + b)
-    const int64_t wbase = ((int64_t)blockIdx.x * CT + (threadIdx.x & ~31)) / 32 * 3;
+        cnt += __popc(m3);
+        // 96 bits of the warp's 32 particles -> 3 words (bit b of word j = coordinate 32j + b)
+        const int64_t wbase = (i0 + (threadIdx.x & ~31)) / 32 * 3;
 #pragma unroll
-    for (int j = 0; j < 3; j++) {
-        const int b = 32 * j + lane;
-        const uint32_t src = __shfl_sync(0xffffffffu, m3, b / 3);
-        const uint32_t word = __ballot_sync(0xffffffffu, (src >> (b % 3)) & 1u);
-        const int64_t wi = wbase + j;
-        if (lane == j) {
-            if (4 * wi + 4 <= nbytes) {
-                flags_w[wi] = word;
-            } else {
-                uint8_t* fb = reinterpret_cast<uint8_t*>(flags_w);
-                for (int64_t q = 4 * wi; q < nbytes; q++) fb[q] = (uint8_t)(word >> (8 * (q - 4 * wi)));
+        for (int j = 0; j < 3; j++) {
+            const int b = 32 * j + lane;
+            const uint32_t src = __shfl_sync(0xffffffffu, m3, b / 3);
+            const uint32_t word = __ballot_sync(0xffffffffu, (src >> (b % 3)) & 1u);
+            const int64_t wi = wbase + j;
+            if (lane == j) {
+                if (4 * wi + 4 <= nbytes) {
+                    flags_w[wi] = word;
+                } else {
+                    uint8_t* fb = reinterpret_cast<uint8_t*>(flags_w);
+                    for (int64_t q = 4 * wi; q < nbytes; q++) fb[q] = (uint8_t)(word >> (8 * (q - 4 * wi)));
+                }
             }
         }
     }
     uint32_t tot;
-    (void)block_excl(__popc(m3), &tot);
+    (void)block_excl(cnt, &tot);
     if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
 }
 
 // pass 1 (decode): block counts of set flags
 __global__ void __launch_bounds__(CT) k_edit_count(int64_t n, DecMask mk, unsigned long long* bsum) {
-    const int64_t i = (int64_t)blockIdx.x * CT + threadIdx.x;
-    const uint32_t m3 = i < n ? mk(i) : 0u;
+    uint32_t cnt = 0;
+    for (int t = 0; t < SUB; t++) {
+        const int64_t i = (int64_t)blockIdx.x * TILE + t * CT + threadIdx.x;
+        if (i < n) cnt += __popc(mk(i));
+    }
     uint32_t tot;
-    (void)block_excl(__popc(m3), &tot);
+    (void)block_excl(cnt, &tot);
     if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
 }
 
-// pass 2: exclusive scan of the block totals in place (one block); bsum[nb] = total
+// pass 2: exclusive scan of the block totals in place (one block, SCAN_ITEMS per thread per
+// iteration); bsum[nb] = total
 __global__ void __launch_bounds__(1024) k_edit_scan(int64_t nb, unsigned long long* bsum) {
     __shared__ unsigned long long sw[32];
     __shared__ unsigned long long carry_s;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (threadIdx.x == 0) carry_s = 0;
     __syncthreads();
-    for (int64_t off = 0; off < nb; off += 1024) {
-        const int64_t i = off + threadIdx.x;
-        const unsigned long long v = i < nb ? bsum[i] : 0ull;
+    for (int64_t off = 0; off < nb; off += 1024 * SCAN_ITEMS) {
+        const int64_t i0 = off + (int64_t)threadIdx.x * SCAN_ITEMS;
+        unsigned long long item[SCAN_ITEMS];
+        unsigned long long v = 0;
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; k++) {
+            item[k] = i0 + k < nb ? bsum[i0 + k] : 0ull;
+            v += item[k];
+        }
         unsigned long long inc = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -131,10 +152,14 @@ __global__ void __launch_bounds__(1024) k_edit_scan(int64_t nb, unsigned long lo
             wex += (k < w) ? sw[k] : 0ull;
             tot += sw[k];
         }
-        const unsigned long long carry = carry_s;
-        if (i < nb) bsum[i] = carry + wex + inc - v;
+        unsigned long long run = carry_s + wex + inc - v;
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; k++) {
+            if (i0 + k < nb) bsum[i0 + k] = run;
+            run += item[k];
+        }
         __syncthreads();
-        if (threadIdx.x == 0) carry_s = carry + tot;
+        if (threadIdx.x == 0) carry_s += tot;
         __syncthreads();
     }
     if (threadIdx.x == 0) bsum[nb] = carry_s;
@@ -145,32 +170,38 @@ __global__ void __launch_bounds__(1024) k_edit_scan(int64_t nb, unsigned long lo
 __global__ void __launch_bounds__(CT) k_edit_fill(int64_t n, EncMask mk, const float* x, const float* y,
                                                   const float* z, const unsigned long long* bsum, double s,
                                                   double xi_f, long long* q, int64_t cap, unsigned int* err) {
-    const int64_t i = (int64_t)blockIdx.x * CT + threadIdx.x;
-    const uint32_t m3 = i < n ? mk(i) : 0u;
-    uint32_t tot;
-    int64_t o = (int64_t)bsum[blockIdx.x] + block_excl(__popc(m3), &tot);
-    if (!m3) return;
+    int64_t base = (int64_t)bsum[blockIdx.x];
     const float* h[3] = {mk.xh, mk.yh, mk.zh};
     const float* p[3] = {mk.xc, mk.yc, mk.zc};
     const float* org[3] = {x, y, z};
+    for (int t = 0; t < SUB; t++) {
+        const int64_t i0 = (int64_t)blockIdx.x * TILE + t * CT;
+        if (i0 >= n) break;  // uniform over the block
+        const int64_t i = i0 + threadIdx.x;
+        const uint32_t m3 = i < n ? mk(i) : 0u;
+        uint32_t tot;
+        int64_t o = base + block_excl(__popc(m3), &tot);
+        base += tot;
+        if (!m3) continue;
 #pragma unroll
-    for (int a = 0; a < 3; a++) {
-        if (m3 >> a & 1u) {
-            const double hv = (double)h[a][i];
-            const double d = (double)p[a][i] - hv;  // exact
-            long long qi = (long long)rint(d / s);
-            const double xo = (double)__ldg(org[a] + i);
-            for (int step = 0;; step++) {
-                const double dev = (double)(float)(hv + (double)qi * s) - xo;
-                if (fabs(dev) <= xi_f) break;
-                if (step == 8) {
-                    atomicOr(err, 2u);
-                    break;
+        for (int a = 0; a < 3; a++) {
+            if (m3 >> a & 1u) {
+                const double hv = (double)h[a][i];
+                const double d = (double)p[a][i] - hv;  // exact
+                long long qi = (long long)rint(d / s);
+                const double xo = (double)__ldg(org[a] + i);
+                for (int step = 0;; step++) {
+                    const double dev = (double)(float)(hv + (double)qi * s) - xo;
+                    if (fabs(dev) <= xi_f) break;
+                    if (step == 8) {
+                        atomicOr(err, 2u);
+                        break;
+                    }
+                    qi += dev > 0 ? -1 : 1;
                 }
-                qi += dev > 0 ? -1 : 1;
+                if (o < cap) q[o] = qi;
+                o++;
             }
-            if (o < cap) q[o] = qi;
-            o++;
         }
     }
 }
@@ -180,21 +211,27 @@ __global__ void __launch_bounds__(CT) k_edit_apply(int64_t n, DecMask mk, const 
                                                    double s, const long long* q, int64_t n_edits,
                                                    const float* xh, const float* yh, const float* zh, float* xr,
                                                    float* yr, float* zr) {
-    const int64_t i = (int64_t)blockIdx.x * CT + threadIdx.x;
-    const uint32_t m3 = i < n ? mk(i) : 0u;
-    uint32_t tot;
-    int64_t o = (int64_t)bsum[blockIdx.x] + block_excl(__popc(m3), &tot);
-    if (i >= n) return;
+    int64_t base = (int64_t)bsum[blockIdx.x];
     const float* h[3] = {xh, yh, zh};
     float* r[3] = {xr, yr, zr};
+    for (int t = 0; t < SUB; t++) {
+        const int64_t i0 = (int64_t)blockIdx.x * TILE + t * CT;
+        if (i0 >= n) break;  // uniform over the block
+        const int64_t i = i0 + threadIdx.x;
+        const uint32_t m3 = i < n ? mk(i) : 0u;
+        uint32_t tot;
+        int64_t o = base + block_excl(__popc(m3), &tot);
+        base += tot;
+        if (i >= n) continue;
 #pragma unroll
-    for (int a = 0; a < 3; a++) {
-        float v = __ldg(h[a] + i);
-        if (m3 >> a & 1u) {
-            if (o < n_edits) v = (float)((double)v + (double)__ldg(q + o) * s);
-            o++;
+        for (int a = 0; a < 3; a++) {
+            float v = __ldg(h[a] + i);
+            if (m3 >> a & 1u) {
+                if (o < n_edits) v = (float)((double)v + (double)__ldg(q + o) * s);
+                o++;
+            }
+            r[a][i] = v;
         }
-        r[a][i] = v;
     }
 }
 
@@ -211,7 +248,7 @@ static cc_status edit_common(cc_ctx* c, int64_t n, int64_t* nb_out) {
     cudaSetDevice(c->device);
     if (n < 0 || 3 * n >= ((int64_t)1 << 62)) return cc_fail(c, CC_E_ARG, "n");
     if (c->p.m < 2 || c->p.m > 40 || !(c->p.xi > 0)) return cc_fail(c, CC_E_ARG, "edit log needs xi > 0, 2 <= m <= 40");
-    const int64_t nb = (n + CT - 1) / CT;
+    const int64_t nb = (n + TILE - 1) / TILE;
     CC_TRY(cc_ensure(c, c->codec_bsum, (size_t)nb + 2, "edit-log block sums"));
     *nb_out = nb;
     return CC_OK;
