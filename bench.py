@@ -195,7 +195,8 @@ def reference_arm(args, w, rank):
     for k in range(args.warmup + args.steps):
         r = run_oracle(ws, timeout=300)
         if r is None:
-            print(json.dumps({"impl": "reference", "unavailable": f"oracle sample N={n_s} exceeded 300 s"}))
+            print(json.dumps({"impl": "reference", "unavailable": f"oracle sample N={n_s} exceeded 300 s"}), file=_OUT,
+                  flush=True)
             return 0
         if k >= args.warmup:
             times.append(r[0])
@@ -211,8 +212,11 @@ def reference_arm(args, w, rank):
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=_OUT, flush=True)
     return 0
+
+
+_OUT = sys.stdout
 
 
 def main():
@@ -236,6 +240,12 @@ def main():
     args = ap.parse_args()
     if args._oracle:
         return _oracle_child(args._oracle)
+    # stdout carries exactly one JSON line: everything else written to fd 1 (NCCL's version
+    # banner from inside the libraries included) goes to stderr
+    global _OUT
+    _OUT = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
 
     rank, world, local = dist_env()
     w = _workload(args)
@@ -470,7 +480,7 @@ def main():
         cb = cpu_baseline(w)
         line["cpu_baseline"] = {k: v for k, v in cb.items() if k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=_OUT, flush=True)
     c.close()
     if world > 1:
         torch.distributed.destroy_process_group()
