@@ -158,3 +158,31 @@ def test_bound_safe_index_near_origin():
     xr = xr.cpu().numpy()
     assert np.all(np.abs(xr.astype(np.float64) - x) <= th["xi_f"])
     ctx.close()
+
+
+@pytest.mark.parametrize("path", ["vector", "scalar_env", "misaligned"])
+def test_vector_and_scalar_paths(path, monkeypatch):
+    """the float4 kernels (16-byte aligned buffers) and the scalar ones (CC_CODEC_SCALAR=1, or
+    views that start one float in) give the oracle's bytes"""
+    n = 100_003
+    h, p = _edits(n + 1, 1.0, 1e-3, seed=5, frac=0.4)
+    if path == "scalar_env":
+        monkeypatch.setenv("CC_CODEC_SCALAR", "1")
+    off = 1 if path == "misaligned" else 0
+    h = [a[off:off + n] for a in h]
+    p = [a[off:off + n] for a in p]
+    params = cc.Params(box=1.0, b=0.01, xi=1e-3)
+    ctx = cc.Corrector(params, device=0)
+    hd = [_dev(np.concatenate([np.zeros(off, np.float32), a]))[off:] for a in h]
+    pd = [_dev(np.concatenate([np.zeros(off, np.float32), a]))[off:] for a in p]
+    assert all((t.data_ptr() % 16 == 0) == (off == 0) for t in hd + pd)
+    flags, q = ctx.edit_encode(*pd, *hd, *pd)
+    oc = oracle.cfg(L=1.0, b=0.01, xi=1e-3)
+    of, oq = oracle.edit_encode(*p, *h, *p, oc)
+    assert np.array_equal(flags.cpu().numpy(), of) and np.array_equal(q.cpu().numpy(), oq)
+    out = [torch.empty(n + off, dtype=torch.float32, device=DEV)[off:] for _ in range(3)]
+    rec = ctx.edit_decode(*hd, flags, q, out=tuple(out))
+    orec = oracle.edit_decode(*h, of, oq, oc)
+    for a in range(3):
+        assert np.array_equal(rec[a].cpu().numpy().view(np.uint32), orec[a].view(np.uint32))
+    ctx.close()
