@@ -60,7 +60,7 @@ typedef struct {
     int64_t active_final;    /* L_tight-active pairs at the returned positions */
     int64_t violated0;       /* pairs whose link status differs at P_hat^(0) (Eq. 1 support) */
     int64_t violated_final;
-    double loss0, loss_final;/* L_tight, fp64 sum of fp32 terms */
+    double loss0, loss_final;/* L_tight: the exact sum of the fp32 terms e^2, rounded (R16) */
     int64_t n_editable;
     int converged;           /* active_final == 0 (stop_mode 0/2) or loss_final <= eps_loss (1) */
     int pad;
@@ -453,18 +453,54 @@ static int cmp_rent(const void* a, const void* b) {
     return x < y ? -1 : (x > y ? 1 : 0);
 }
 
-/* evaluate L_tight (active count, fp64 loss, violated count) over the pair list in order */
+/* Exact sum of doubles (R16, R28): the real number L_tight = sum of e^2 (each e^2 exact in fp64,
+ * e being fp32) is held as a nonoverlapping expansion -- Shewchuk's "grow-expansion", the
+ * partials of Python's math.fsum -- so the stop test L_tight <= eps_L (Alg. 1 line 6)
+ * is decided on the exact value, not on a rounded running sum.  Components are nonoverlapping
+ * and increase in magnitude; at most ~40 are non-zero for doubles. */
+typedef struct { int n; double p[96]; } xsum_t;
+
+static void xsum_add(xsum_t* s, double x) {
+    int i = 0;
+    for (int k = 0; k < s->n; k++) {
+        double y = s->p[k];
+        if (fabs(x) < fabs(y)) { double tmp = x; x = y; y = tmp; }
+        double hi = x + y, lo = y - (hi - x);
+        if (lo != 0.0) s->p[i++] = lo;
+        x = hi;
+    }
+    s->p[i++] = x;
+    s->n = i;
+}
+
+/* sign of (exact sum - v): the sign of the largest non-zero component of the expansion */
+static int xsum_cmp(const xsum_t* s, double v) {
+    xsum_t t = *s;
+    xsum_add(&t, -v);
+    for (int k = t.n - 1; k >= 0; k--)
+        if (t.p[k] != 0.0) return t.p[k] > 0.0 ? 1 : -1;
+    return 0;
+}
+
+/* the exact sum rounded (largest component first; reporting only) */
+static double xsum_value(const xsum_t* s) {
+    double r = 0.0;
+    for (int k = s->n - 1; k >= 0; k--) r += s->p[k];
+    return r;
+}
+
+/* evaluate L_tight (active count, exact loss, violated count) over the pair list in order */
 static void eval_pairs(const float* P, int64_t np, const int64_t* pi, const int64_t* pj,
                        const uint8_t* pf, const oc_th* t, int periodic, int64_t* active,
-                       double* loss, int64_t* violated) {
+                       xsum_t* loss, int64_t* violated) {
     int64_t a = 0, v = 0;
-    double l = 0.0;
+    loss->n = 0;
     for (int64_t k = 0; k < np; k++) {
         float r[3], dh, e;
         int ol = pf[k] & 1;
         if (tight_pair(P, pi[k], pj[k], ol, t, periodic, r, &dh, &e)) {
             a++;
-            l += (double)e * (double)e;
+            xsum_add(loss, (double)e * (double)e);
         }
         float s = r[0] * r[0];
         s = s + r[1] * r[1];
@@ -472,7 +508,6 @@ static void eval_pairs(const float* P, int64_t np, const int64_t* pi, const int6
         if ((s <= t->b2) != (ol != 0)) v++;
     }
     *active = a;
-    *loss = l;
     *violated = v;
 }
 
@@ -488,7 +523,9 @@ int oc_tight_eval_f32(int64_t n, const float* xh, const float* yh, const float* 
     if (!P) return 67;
     for (int64_t i = 0; i < n; i++) { P[3 * i] = xh[i]; P[3 * i + 1] = yh[i]; P[3 * i + 2] = zh[i]; }
     int64_t viol;
-    eval_pairs(P, np, pi, pj, pf, &t, c->periodic, active, loss, &viol);
+    xsum_t xs;
+    eval_pairs(P, np, pi, pj, pf, &t, c->periodic, active, &xs, &viol);
+    *loss = xsum_value(&xs);
     if (grad) {
         memset(grad, 0, (size_t)n * 3 * sizeof(float));
         for (int64_t k = 0; k < np; k++) {
@@ -653,18 +690,20 @@ int oc_correct(int64_t n, const float* x, const float* y, const float* z, const 
         const float vstep = (float)c->vanilla_step;
         double p1 = 1.0, p2 = 1.0;
         int64_t act, viol;
-        double loss;
+        xsum_t loss;
         eval_pairs(P, np, pi, pj, pf, &t, per, &act, &loss, &viol);
-        info->active0 = act; info->loss0 = loss; info->violated0 = viol;
+        info->active0 = act; info->loss0 = xsum_value(&loss); info->violated0 = viol;
         int64_t t_it;
         for (t_it = 1; t_it <= c->t_max; t_it++) {
             if (t_it > 1) eval_pairs(P, np, pi, pj, pf, &t, per, &act, &loss, &viol);
             if (trace_active) trace_active[t_it - 1] = act;
-            if (trace_loss) trace_loss[t_it - 1] = loss;
+            if (trace_loss) trace_loss[t_it - 1] = xsum_value(&loss);
             if (trace_violated) trace_violated[t_it - 1] = viol;
+            /* Alg. 1 line 6 on the exact L_tight (R11, R16) */
+            const int loss_le = xsum_cmp(&loss, c->eps_loss) <= 0;
             if (c->stop_mode == 0 && act == 0) break;
-            if (c->stop_mode == 1 && loss <= c->eps_loss) break;
-            if (c->stop_mode == 3 && viol == 0 && loss <= c->eps_loss) break;
+            if (c->stop_mode == 1 && loss_le) break;
+            if (c->stop_mode == 3 && viol == 0 && loss_le) break;
             p1 = p1 * c->beta1;
             p2 = p2 * c->beta2;
             const float bc1 = (float)(1.0 - p1), bc2 = (float)(1.0 - p2);
@@ -704,13 +743,14 @@ int oc_correct(int64_t n, const float* x, const float* y, const float* z, const 
         }
         eval_pairs(P, np, pi, pj, pf, &t, per, &act, &loss, &viol);
         if (trace_active) trace_active[info->iterations] = act;
-        if (trace_loss) trace_loss[info->iterations] = loss;
+        if (trace_loss) trace_loss[info->iterations] = xsum_value(&loss);
         if (trace_violated) trace_violated[info->iterations] = viol;
         info->active_final = act;
-        info->loss_final = loss;
+        info->loss_final = xsum_value(&loss);
         info->violated_final = viol;
-        if (c->stop_mode == 1) info->converged = loss <= c->eps_loss;
-        else if (c->stop_mode == 3) info->converged = viol == 0 && loss <= c->eps_loss;
+        const int loss_le = xsum_cmp(&loss, c->eps_loss) <= 0;
+        if (c->stop_mode == 1) info->converged = loss_le;
+        else if (c->stop_mode == 3) info->converged = viol == 0 && loss_le;
         else info->converged = act == 0;
     }
     for (int64_t i = 0; i < n; i++) { xo[i] = P[3 * i]; yo[i] = P[3 * i + 1]; zo[i] = P[3 * i + 2]; }

@@ -51,10 +51,12 @@ def test_fof_spec_examples():
     c = oracle.cfg(L=1.0, b=b, xi=0.0)
     h2 = np.full(2, 0.5, np.float32)
     # d = b -> one component; d = next float above -> two
-    lab, ng = oracle.fof(np.array([0.25, 0.375], np.float32), h2, h2, c)
-    assert ng == 1 and list(lab) == [0, 0]
-    lab, ng = oracle.fof(np.array([0.25, np.nextafter(np.float32(0.375), np.float32(1))], np.float32), h2, h2, c)
-    assert ng == 2 and list(lab) == [0, 1]
+    for brute in (False, True):
+        lab, ng = oracle.fof(np.array([0.25, 0.375], np.float32), h2, h2, c, brute=brute)
+        assert ng == 1 and list(lab) == [0, 0]
+        lab, ng = oracle.fof(np.array([0.25, np.nextafter(np.float32(0.375), np.float32(1))], np.float32), h2, h2, c,
+                             brute=brute)
+        assert ng == 2 and list(lab) == [0, 1]
     # chain p0-p1-p2 each link <= b, d(p0,p2) > b -> one component of size 3
     h3 = np.full(3, 0.5, np.float32)
     lab, ng = oracle.fof(np.array([0.25, 0.375, 0.5], np.float32), h3, h3, c)

@@ -15,11 +15,15 @@ import synth  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
 w = synth.CONFIGS[cfg]
+if len(sys.argv) > 2:  # xi_rel override
+    w = synth.Workload(w.name, w.kind, w.n, w.L, float(sys.argv[2]), eta=w.eta, b=w.b, seed=w.seed, extra=w.extra)
+    cfg = f"{cfg}_{sys.argv[2]}"
+REPS = int(os.environ.get("SCHED_REPS", "2"))
 dev = torch.device("cuda", 0)
 arrs = synth.make(w, device=dev)
 p = cc.Params(box=w.L, b=w.linking_length, xi=w.xi, t_max=10000, stop_mode=cc.STOP_RESTORED, profile=1)
 c = cc.Corrector(p)
-for rep in range(2):
+for rep in range(REPS):
     c.build_cells(*arrs)
     vp = c.find_vulnerable()
     c.kernel_stats(reset=True)
