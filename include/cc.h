@@ -80,13 +80,24 @@ void cc_default_params(cc_params* p);
 
 /* Multi-GPU (§III-D): x-slab decomposition, rank r owns original x in
  * [r L/R, (r+1) L/R).  nccl_id = 128-byte ncclUniqueId identical on all ranks (from
- * cc_nccl_unique_id() on rank 0, broadcast by the caller).  dist == NULL means one GPU. */
+ * cc_nccl_unique_id() on rank 0, broadcast by the caller).  dist == NULL means one GPU.
+ * vgroup != NULL (from cc_vgroup_create): the R ranks are contexts of ONE process on one GPU,
+ * each driven by its own host thread; collectives become device copies and reduction kernels
+ * ordered by events (comm.cu) -- a correctness mode that runs the multi-rank protocol on a
+ * single GPU (results bit-identical to NCCL ranks and to one rank); nccl_id_h is then unused. */
 typedef struct {
     int rank, nranks;
     const void* nccl_id_h;
+    void* vgroup;
 } cc_dist;
 
 cc_status cc_nccl_unique_id(void* id_h /* 128 bytes */);
+
+/* An in-process group of nranks (1..8) virtual ranks (see cc_dist.vgroup).  Destroy it after
+ * every context of the group was destroyed.  Every rank of the group must make the same
+ * sequence of calls (each collective blocks until all ranks reach it). */
+cc_status cc_vgroup_create(int nranks, void** group_h);
+void cc_vgroup_destroy(void* group);
 
 /* Create a context on `device` enqueuing on `stream` (a cudaStream_t; NULL = legacy
  * default stream).  *ctx is NULL on failure. */
@@ -149,10 +160,11 @@ cc_status cc_get_trace(cc_ctx* ctx, int64_t* active_h, double* loss_h, int64_t* 
                        int64_t* n_h);
 
 /* K3 schedule per iteration of the last cc_correct (diagnostics of the frontier):
- * sched_h[5 t + 0] = editables processed, [5 t + 1] = editables left awake, [5 t + 2] = row
- * entries of editables that moved, [5 t + 3] = zero-gradient steps replayed in full, [5 t + 4] =
- * zero-gradient steps replayed on the proven-still path; up to cap iterations, *n_h = iterations
- * recorded. */
+ * sched_h[6 t + 0] = editables processed, [6 t + 1] = editables left awake, [6 t + 2] = row
+ * entries of editables that moved, [6 t + 3] = zero-gradient steps replayed in full, [6 t + 4] =
+ * zero-gradient steps replayed on the proven-still path, [6 t + 5] = device %globaltimer (ns)
+ * when the iteration's statistics were final; up to cap iterations (cap rows of 6), *n_h =
+ * iterations recorded. */
 cc_status cc_get_schedule(cc_ctx* ctx, int64_t* sched_h, int64_t cap, int64_t* n_h);
 
 /* S6 -- FoF labels (§II-B, Fig. 1) on ORIG, DECOMP or CORR positions: edge iff the
@@ -198,7 +210,6 @@ cc_status cc_run(cc_ctx* ctx, int64_t n, const float* x, const float* y, const f
                  const float* xh, const float* yh, const float* zh, const uint32_t* gid,
                  float* xo, float* yo, float* zo, int flags, cc_run_info* info_h);
 
-#ifdef __cplusplus
 /* f1 -- edit log.  Alg. 1 lines 11-13 and §III-B
  * "Compaction, quantization, and lossless compression": Delta = corrected -
  * decompressed; flags = bitmask of the non-zero entries of Delta, packed into bytes; edits = the
@@ -232,6 +243,22 @@ cc_status cc_edit_decode(cc_ctx* ctx, int64_t n, const float* xh0, const float* 
                          const uint8_t* flags, const int64_t* q, int64_t n_edits, float* xr, float* yr,
                          float* zr);
 
+/* S0 thresholds actually used (after cc_build_cells; near_pairs after cc_find_vulnerable), for
+ * the boundary tests: every fp32 value is the single rounding of the paper's formula (Alg. 1
+ * l.1-3 P:419-421, Eq. 3; readings R2-R8 of DESIGN.md §3).  lo2s/hi2s: the
+ * proven-link shells: original d2 <= lo2s => linked under any positions within
+ * xi_f of the originals, d2 > hi2s => never linked (_i interior pairs, _w pairs whose minimum
+ * image wraps).  r_search: ghost width / pair-search radius; r_link: FoF(ORIG) search radius. */
+typedef struct {
+    float xi_f, xip_f, b2, lo2, hi2, c_b, c_f, Lf, hLf;
+    float lo2s_i, hi2s_i, lo2s_w, hi2s_w;
+    int pad;
+    double b, eps_q, mu, r_search, r_link;
+    int64_t near_pairs;    /* pairs in (lo2s, lo2] U (hi2, hi2s] found by cc_find_vulnerable */
+} cc_thresholds;
+cc_status cc_get_thresholds(cc_ctx* ctx, cc_thresholds* out_h);
+
+#ifdef __cplusplus
 }
 #endif
 #endif /* CC_H */

@@ -448,6 +448,10 @@ static void grad_add(float g[3], const float r[3], float dh, float e, int i_is_l
 }
 
 typedef struct { int64_t j; uint32_t gj; int olink; } rent_t;
+
+/* gradient summation order (R14): chunks of GC terms, trees over groups of GG chunk sums */
+#define GC 16
+#define GG 32
 static int cmp_rent(const void* a, const void* b) {
     uint32_t x = ((const rent_t*)a)->gj, y = ((const rent_t*)b)->gj;
     return x < y ? -1 : (x > y ? 1 : 0);
@@ -711,11 +715,26 @@ int oc_correct(int64_t n, const float* x, const float* y, const float* z, const 
             for (int64_t e = 0; e < ne; e++) {
                 int64_t i = emap[e];
                 uint32_t gi = gid ? gid[i] : (uint32_t)i;
+                /* R14: the row's terms in ascending partner gid (an inactive pair's term is 0);
+                 * chunks of GC consecutive terms summed left to right from +0; the chunk sums
+                 * of each group of GG chunks combined by the adjacent-pairwise tree (zero
+                 * padded); group results summed left to right from +0. */
                 float g[3] = {0.0f, 0.0f, 0.0f};
-                for (int64_t k = rp[e]; k < rp[e + 1]; k++) {
-                    float r[3], dh, ee;
-                    if (tight_pair(P, i, rows[k].j, rows[k].olink, &t, per, r, &dh, &ee))
-                        grad_add(g, r, dh, ee, gi < rows[k].gj);
+                for (int64_t g0 = rp[e]; g0 < rp[e + 1]; g0 += GC * GG) {
+                    float cs[GG][3];
+                    memset(cs, 0, sizeof(cs));
+                    for (int j = 0; j < GG; j++)
+                        for (int q = 0; q < GC; q++) {
+                            const int64_t k = g0 + (int64_t)GC * j + q;
+                            if (k >= rp[e + 1]) break;
+                            float r[3], dh, ee;
+                            if (tight_pair(P, i, rows[k].j, rows[k].olink, &t, per, r, &dh, &ee))
+                                grad_add(cs[j], r, dh, ee, gi < rows[k].gj);
+                        }
+                    for (int off = 1; off < GG; off *= 2)
+                        for (int l = 0; l < GG; l += 2 * off)
+                            for (int q = 0; q < 3; q++) cs[l][q] = cs[l][q] + cs[l + off][q];
+                    for (int q = 0; q < 3; q++) g[q] = g[q] + cs[0][q];
                 }
                 for (int q = 0; q < 3; q++) {
                     float xq = P[3 * i + q];

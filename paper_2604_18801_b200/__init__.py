@@ -5,8 +5,8 @@ provides device memory, streams and process groups.  There is no CPU fallback: i
 works without a GPU (for building and ABI checks) but every compute call needs the CUDA
 extension and a device, and raises otherwise.
 """
-from .binding import (CC_CORR, CC_DECOMP, CC_ORIG, CCError, Corrector, Params, STOP_ACTIVE, STOP_EPS,
+from .binding import (CC_CORR, CC_DECOMP, CC_ORIG, CCError, Corrector, Params, STOP_ACTIVE, STOP_EPS, VGroup,
                       STOP_NONE, STOP_RESTORED, hmf, lib, lib_path, nccl_unique_id, shell_masks, slab_of)
 
-__all__ = ["Corrector", "Params", "CCError", "hmf", "lib", "lib_path", "nccl_unique_id", "slab_of", "CC_ORIG",
+__all__ = ["Corrector", "Params", "VGroup", "CCError", "hmf", "lib", "lib_path", "nccl_unique_id", "slab_of", "CC_ORIG",
            "CC_DECOMP", "CC_CORR", "STOP_ACTIVE", "STOP_EPS", "STOP_NONE", "STOP_RESTORED"]

@@ -37,7 +37,7 @@ class _Params(C.Structure):
 
 
 class _Dist(C.Structure):
-    _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("nccl_id_h", C.c_void_p)]
+    _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("nccl_id_h", C.c_void_p), ("vgroup", C.c_void_p)]
 
 
 class _VP(C.Structure):
@@ -56,13 +56,21 @@ class _Mcc(C.Structure):
     _fields_ = [("tp", C.c_uint64), ("tn", C.c_uint64), ("fp", C.c_uint64), ("fn", C.c_uint64), ("mcc", C.c_double)]
 
 
+class _Th(C.Structure):
+    _fields_ = [(k, C.c_float) for k in ("xi_f", "xip_f", "b2", "lo2", "hi2", "c_b", "c_f", "Lf", "hLf", "lo2s_i",
+                                         "hi2s_i", "lo2s_w", "hi2s_w")] + \
+               [("pad", C.c_int)] + [(k, C.c_double) for k in ("b", "eps_q", "mu", "r_search", "r_link")] + \
+               [("near_pairs", C.c_int64)]
+
+
 class _Run(C.Structure):
     _fields_ = [("vp", _VP), ("corr", _Corr)]
 
 
 EXPORTS = ["cc_default_params", "cc_nccl_unique_id", "cc_create", "cc_destroy", "cc_last_error", "cc_build_cells",
            "cc_find_vulnerable", "cc_get_pairs", "cc_correct", "cc_get_trace", "cc_get_schedule", "cc_fof_label", "cc_mcc",
-           "cc_halo_sizes", "cc_hmf", "cc_kernel_stats", "cc_run", "cc_edit_encode", "cc_edit_decode"]
+           "cc_halo_sizes", "cc_hmf", "cc_kernel_stats", "cc_run", "cc_edit_encode", "cc_edit_decode",
+           "cc_get_thresholds", "cc_vgroup_create", "cc_vgroup_destroy"]
 
 _lib = None
 
@@ -104,8 +112,12 @@ def lib():
     L.cc_run.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, P(_Run)]
     L.cc_edit_encode.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, P(i64)]
     L.cc_edit_decode.argtypes = [vp, i64, vp, vp, vp, vp, vp, i64, vp, vp, vp]
+    L.cc_get_thresholds.argtypes = [vp, P(_Th)]
+    L.cc_vgroup_create.argtypes = [C.c_int, P(vp)]
+    L.cc_vgroup_destroy.argtypes = [vp]
+    L.cc_vgroup_destroy.restype = None
     for name in EXPORTS:
-        if name not in ("cc_default_params", "cc_destroy", "cc_last_error"):
+        if name not in ("cc_default_params", "cc_destroy", "cc_last_error", "cc_vgroup_destroy"):
             getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -163,9 +175,12 @@ class Corrector:
         self._p = params.to_c()
         self._d = None
         if dist is not None:
-            rank, nranks, uid = dist
-            self._uid = C.create_string_buffer(bytes(uid), 128)
-            self._d = _Dist(rank, nranks, C.cast(self._uid, C.c_void_p))
+            # (rank, nranks, nccl unique id) for NCCL ranks, or (rank, nranks, None, VGroup)
+            rank, nranks, uid = dist[:3]
+            vg = dist[3] if len(dist) > 3 else None
+            self._uid = C.create_string_buffer(bytes(uid), 128) if uid is not None else None
+            self._d = _Dist(rank, nranks, C.cast(self._uid, C.c_void_p) if uid is not None else None,
+                            vg.h if vg is not None else None)
         h = C.c_void_p()
         st = self.lib.cc_create(C.byref(h), self.device, C.c_void_p(self.stream.cuda_stream), C.byref(self._p),
                                 None if self._d is None else C.byref(self._d))
@@ -200,6 +215,12 @@ class Corrector:
         self._inputs = (x, y, z, xh, yh, zh, gid)  # keep alive until the stream is done
         self._chk(self.lib.cc_build_cells(self.h, n, *[_ptr(t) for t in (x, y, z, xh, yh, zh)], _ptr(gid)))
         self.n = n
+
+    def thresholds(self) -> dict:
+        """S0 values in use (cc_get_thresholds)."""
+        t = _Th()
+        self._chk(self.lib.cc_get_thresholds(self.h, C.byref(t)))
+        return {k: getattr(t, k) for k, _ in _Th._fields_ if k != "pad"}
 
     # S2 + S3
     def find_vulnerable(self) -> dict:
@@ -242,9 +263,9 @@ class Corrector:
 
     def schedule(self):
         """K3 schedule per iteration: (editables processed, left awake, moved row entries, full
-        replay steps, proven-still replay steps)."""
+        replay steps, proven-still replay steps, device time in ns at the iteration's end)."""
         n = C.c_int64()
-        a = np.zeros((self.params.t_max + 1, 5), np.int64)
+        a = np.zeros((self.params.t_max + 1, 6), np.int64)
         self._chk(self.lib.cc_get_schedule(self.h, a.ctypes.data_as(C.POINTER(C.c_int64)), a.shape[0], C.byref(n)))
         return a[: n.value]
 
@@ -258,12 +279,14 @@ class Corrector:
         dev = torch.device("cuda", self.device)
         nbytes = (3 * n + 7) // 8
         flags = torch.empty(max((nbytes + 3) // 4, 1), dtype=torch.int32, device=dev).view(torch.uint8)[:nbytes]
-        cap = 3 * n if cap is None else cap
-        q = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
         ne = C.c_int64()
-        self._chk(self.lib.cc_edit_encode(self.h, n, *[_ptr(t) for t in (x, y, z, xh0, yh0, zh0, xc, yc, zc)], _ptr(flags),
-                                          _ptr(q), cap, C.byref(ne)))
-        return flags, q[: ne.value]
+        args = [_ptr(t) for t in (x, y, z, xh0, yh0, zh0, xc, yc, zc)]
+        if cap is None:  # count first (CC_E_OOM with cap 0 reports n_edits), then an exact-size q
+            self._chk(self.lib.cc_edit_encode(self.h, n, *args, _ptr(flags), None, 0, C.byref(ne)), ok=(0, 67))
+            cap = ne.value
+        q = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+        self._chk(self.lib.cc_edit_encode(self.h, n, *args, _ptr(flags), _ptr(q), cap, C.byref(ne)))
+        return flags, (q if ne.value == q.shape[0] else q[: ne.value].clone())
 
     def edit_decode(self, xh0, yh0, zh0, flags, q, out=None):
         """x_rec = x_hat0 + scatter(dequantise(q), flags) (P:456)."""
@@ -272,8 +295,21 @@ class Corrector:
         _check_dev(flags, torch.uint8, "flags")
         _check_dev(q, torch.int64, "q")
         n = xh0.shape[0]
+        dev = torch.device("cuda", self.device)
+        for nm, t in (("yh0", yh0), ("zh0", zh0)):
+            if t.shape[0] != n:
+                raise ValueError(f"{nm}: length {t.shape[0]} != {n}")
+        if flags.numel() < (3 * n + 7) // 8:
+            raise ValueError(f"flags: {flags.numel()} bytes < ceil(3n/8) = {(3 * n + 7) // 8}")
+        for nm, t in (("xh0", xh0), ("flags", flags), ("q", q)):
+            if t.device != dev:
+                raise ValueError(f"{nm}: on {t.device}, the context is on {dev}")
         if out is None:
-            out = tuple(torch.empty(n, dtype=torch.float32, device=xh0.device) for _ in range(3))
+            out = tuple(torch.empty(n, dtype=torch.float32, device=dev) for _ in range(3))
+        for k, t in enumerate(out):
+            _check_dev(t, torch.float32, f"out[{k}]")
+            if t.numel() < n or t.device != dev:
+                raise ValueError(f"out[{k}]: needs {n} floats on {dev}")
         self._chk(self.lib.cc_edit_decode(self.h, n, *[_ptr(t) for t in (xh0, yh0, zh0)], _ptr(flags), _ptr(q),
                                           q.shape[0], *[_ptr(t) for t in out]))
         return out
@@ -320,6 +356,24 @@ class Corrector:
         vp = {k: getattr(info.vp, k) for k, _ in _VP._fields_}
         co = {k: getattr(info.corr, k) for k, _ in _Corr._fields_ if k != "pad"}
         return {"vp": vp, "corr": co, "status": st}
+
+
+class VGroup:
+    """cc_vgroup_create: an in-process group of virtual ranks sharing one GPU (cc_dist.vgroup).
+    Each rank's Corrector must be driven by its own thread; close every Corrector first."""
+
+    def __init__(self, nranks: int):
+        h = C.c_void_p()
+        st = lib().cc_vgroup_create(nranks, C.byref(h))
+        if st != 0:
+            raise CCError(st, "cc_vgroup_create")
+        self.h = h
+        self.nranks = nranks
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().cc_vgroup_destroy(self.h)
+            self.h = None
 
 
 def nccl_unique_id() -> bytes:

@@ -67,6 +67,14 @@ CC_INST(unsigned char)
 CC_INST(uint2)
 CC_INST(uint4)
 
+unsigned long long* cc::work_counters(cc_ctx* c) {
+    if (!c->k3work.p) {
+        if (cc_ensure(c, c->k3work, 8, "work counters") != CC_OK) return nullptr;
+        if (cudaMemsetAsync(c->k3work.p, 0, 8 * sizeof(unsigned long long), c->stream) != cudaSuccess) return nullptr;
+    }
+    return c->k3work.p;
+}
+
 // ------------------------------------------------------------------------------------------
 // profiling
 int cc_prof_begin(cc_ctx* c, const char* cls) {
@@ -115,11 +123,23 @@ static void prof_drain(cc_ctx* c) {
 
 // ------------------------------------------------------------------------------------------
 // S0 -- parameters (Alg. 1 lines 1-3 P:419-421; §III-B; readings R2-R8).
-// Directed fp32 rounding of an exact double sum (via the error term of TwoSum).
-static float rd32_sum(double a, double b) {
-    double s = a + b, bb = s - a, err = (a - (s - bb)) + (b - bb);
-    float f = (float)s;
-    if ((double)f > s || ((double)f == s && err < 0)) f = std::nextafter(f, -INFINITY);
+// Evaluated in x87 extended precision (64-bit significand) and rounded once to fp32; the
+// -m "not gpu" / -m gpu tests compare every threshold with the paper's formulas evaluated in
+// 60-digit decimals (tests/paper_s0.py), so this code is pinned independently of the oracle.
+typedef long double ld;
+
+static float f32_nearest(ld v) { return (float)v; }  // one rounding from the 64-bit significand
+
+// largest fp32 <= v
+static float f32_down(ld v) {
+    float f = (float)v;
+    while ((ld)f > v) f = std::nextafter(f, -INFINITY);
+    return f;
+}
+// smallest fp32 >= v
+static float f32_up(ld v) {
+    float f = (float)v;
+    while ((ld)f < v) f = std::nextafter(f, INFINITY);
     return f;
 }
 
@@ -132,29 +152,57 @@ static cc_status derive_params(cc_ctx* c, int64_t n_total) {
     }
     c->b = b;
     cc::Th& t = c->th;
-    t.xi_f = (float)p.xi;
-    const double xi = (double)t.xi_f;
-    c->xi_d = xi;
-    t.xip_f = rd32_sum(xi * (1.0 - std::ldexp(1.0, -p.m)), 0.0);  // xi' = xi (1 - 2^-m)
-    c->eps_q = 2.0 * xi / (std::ldexp(1.0, p.m) - 1.0);            // eps_q = 2 xi / (2^m - 1)
-    c->mu = 2.0 * std::sqrt(3.0) * c->eps_q;
-    t.c_b = (float)(b - c->mu);
-    t.c_f = (float)(b + c->mu);
-    const double s = 2.0 * std::sqrt(3.0) * xi;
-    const double lo = b - s, hi = b + s;
-    t.lo2 = lo > 0 ? (float)(lo * lo) : -1.0f;
-    t.hi2 = (float)(hi * hi);
-    t.b2 = (float)(b * b);
+    const ld sqrt3 = std::sqrt((ld)3);
+    const ld B = (ld)b;
+    t.xi_f = (float)p.xi;                                         // R6: the bound is fl32(xi)
+    const ld X = (ld)t.xi_f;
+    c->xi_d = (double)X;
+    const ld two_m = std::ldexp((ld)1, p.m);
+    t.xip_f = f32_down(X - X / two_m);                            // Alg. 1 l.2: xi' = xi (1 - 2^-m), rounded down (R8)
+    const ld eps_q = (ld)2 * X / (two_m - (ld)1);                 // Alg. 1 l.1: eps_q = 2 xi / (2^m - 1)
+    c->eps_q = (double)eps_q;
+    const ld mu = (ld)2 * sqrt3 * eps_q;                          // Eq. 3 margin 2 sqrt3 eps_q
+    c->mu = (double)mu;
+    t.c_b = f32_nearest(B - mu);
+    t.c_f = f32_nearest(B + mu);
+    const ld half = (ld)2 * sqrt3 * X;                            // Alg. 1 l.3: band half-width 2 sqrt3 xi
+    const ld edge_lo = B - half, edge_hi = B + half;
+    t.lo2 = edge_lo > 0 ? f32_nearest(edge_lo * edge_lo) : -1.0f; // R2: (b - 2 sqrt3 xi, b + 2 sqrt3 xi]
+    t.hi2 = f32_nearest(edge_hi * edge_hi);
+    t.b2 = f32_nearest(B * B);                                    // R3: d <= b
     t.Lf = (float)p.box;
-    t.hLf = (float)(0.5 * p.box);
+    t.hLf = f32_nearest((ld)p.box / 2);
     t.periodic = p.periodic ? 1 : 0;
-    // ghost / cell width: delta = b + 2 sqrt3 xi, never below the fp32 sqrt(hi2)
-    c->delta = std::max(hi, std::sqrt((double)t.hi2));
-    c->r_pair = c->delta * (1.0 + 1e-5);  // search radius / ghost width (margin for fp32 rounding)
-    c->r_link = std::max(b, std::sqrt((double)t.b2)) * (1.0 + 1e-5);
-    // corrected positions lie within xi' < xi_f of the original: a stable link (d2 <= lo2) keeps
-    // d_hat <= b - 2 sqrt3 (xi_f - xi'), safely below b when that margin >> fp32 rounding of d
-    c->corr_base_ok = 2.0 * std::sqrt(3.0) * ((double)t.xi_f - (double)t.xip_f) > 1e-6 * b;
+
+    // Proven-link shells (cc_internal.cuh Th): every pinned fp32 d2 lies within the relative
+    // factors (1 -/+ u)^k of the exact squared distance of its fp32 operands (u = 2^-24; 5
+    // roundings interior; 3 + an absolute u (L + 2 xi) per component where the minimum image
+    // wrapped), and any position within xi_f of the original moves a distance by <= 2 sqrt3 xi_f.
+    const ld u = std::ldexp((ld)1, -24), sl = (ld)1 - (ld)1e-9;   // sl: slack for the ld arithmetic
+    const ld b2 = (ld)t.b2, w = sqrt3 * u * ((ld)p.box + (ld)2 * X), dx = (ld)2 * sqrt3 * X;
+    const ld up5 = std::pow((ld)1 + u, (ld)5), dn5 = std::pow((ld)1 - u, (ld)5);
+    const ld up3 = std::pow((ld)1 + u, (ld)3), dn3 = std::pow((ld)1 - u, (ld)3);
+    {
+        const ld xi_ = std::sqrt(b2 / up5) - dx;                  // interior, stable
+        t.lo2s_i = xi_ > 0 ? f32_down(dn5 * xi_ * xi_ * sl) : -1.0f;
+        const ld yi_ = std::sqrt(b2 / dn5) + dx;                  // interior, never linked
+        t.hi2s_i = f32_up(up5 * yi_ * yi_ / sl);
+        const ld xw = ((ld)1 - u) * ((std::sqrt(b2 / up3) - w) / ((ld)1 + u) - dx) - w;
+        t.lo2s_w = xw > 0 ? f32_down(dn3 * xw * xw * sl) : -1.0f;
+        const ld yw = ((ld)1 + u) * ((std::sqrt(b2 / dn3) + w) / ((ld)1 - u) + dx) + w;
+        t.hi2s_w = f32_up(up3 * yw * yw / sl);
+        t.lo2s_i = std::min(t.lo2s_i, t.lo2);
+        t.lo2s_w = std::min(t.lo2s_w, t.lo2);
+        t.hi2s_i = std::max(t.hi2s_i, t.hi2);
+        t.hi2s_w = std::max(t.hi2s_w, t.hi2);
+    }
+    // ghost / search radius: the largest exact original distance of a pair whose pinned d2 can
+    // be <= hi2s_w (vulnerable, near shell, or linked in any position set within xi_f):
+    // |A| <= (sqrt(d2 / (1-u)^3) + w) / (1-u); never below b + 2 sqrt3 xi
+    c->delta = (double)std::max(edge_hi, (std::sqrt((ld)t.hi2s_w / dn3) + w) / ((ld)1 - u));
+    c->r_pair = c->delta * (1.0 + 1e-9);
+    // FoF on the original positions: d2 <= b2
+    c->r_link = (double)((std::sqrt(b2 / dn3) + w) / ((ld)1 - u)) * (1.0 + 1e-9);
     if (p.periodic && c->delta >= 0.5 * p.box)
         return cc_fail(c, CC_E_ARG, "b + 2 sqrt3 xi must be < box/2 for minimum-image distances");
     return CC_OK;
@@ -284,7 +332,7 @@ void cc_destroy(cc_ctx* c) {
         cc_release(c, c->rrb[d]);
     }
     cc_release(c, c->stage); cc_release(c, c->gath); cc_release(c, c->dcnt); cc_release(c, c->red); cc_release(c, c->red_sum);
-    cc_release(c, c->bnd);
+    cc_release(c, c->bnd); cc_release(c, c->near); cc_release(c, c->near_n);
     cudaStreamSynchronize(c->stream);
     // the PGD graph holds NCCL work (multi-GPU): release it before the communicator
     if (c->pgd_exec) cudaGraphExecDestroy(c->pgd_exec);
@@ -382,7 +430,10 @@ cc_status cc_find_vulnerable(cc_ctx* c, cc_vp_info* info) {
     CC_TRY(cc::scan_deg(c, c->deg.p, c->rowoff.p, c->eidx.p, c->key.p, n, tot));
     CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 2, tot, 7 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                c->stream));
+    CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 11, c->near_n.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               c->stream));
     CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->near_count = (int64_t)c->h_counters[11];
     unsigned long long totals[7];
     std::memcpy(totals, c->h_counters + 2, sizeof(totals));
     CC_TRY(cc::rows_resolve(c, totals));
@@ -440,6 +491,20 @@ cc_status cc_correct(cc_ctx* c, float* xo, float* yo, float* zo, cc_corr_info* i
     return local.converged ? CC_OK : CC_NOT_CONVERGED;
 }
 
+cc_status cc_get_thresholds(cc_ctx* c, cc_thresholds* out) {
+    CC_GUARD(c);
+    if (!out) return cc_fail(c, CC_E_ARG, "null output");
+    if (c->state < 1) return cc_fail(c, CC_E_STATE, "cc_build_cells first");
+    const cc::Th& t = c->th;
+    std::memset(out, 0, sizeof(*out));
+    out->xi_f = t.xi_f; out->xip_f = t.xip_f; out->b2 = t.b2; out->lo2 = t.lo2; out->hi2 = t.hi2;
+    out->c_b = t.c_b; out->c_f = t.c_f; out->Lf = t.Lf; out->hLf = t.hLf;
+    out->lo2s_i = t.lo2s_i; out->hi2s_i = t.hi2s_i; out->lo2s_w = t.lo2s_w; out->hi2s_w = t.hi2s_w;
+    out->b = c->b; out->eps_q = c->eps_q; out->mu = c->mu; out->r_search = c->r_pair; out->r_link = c->r_link;
+    out->near_pairs = c->state >= 2 ? c->near_count : 0;
+    return CC_OK;
+}
+
 cc_status cc_get_schedule(cc_ctx* c, int64_t* sched_h, int64_t cap, int64_t* n_h) {
     CC_GUARD(c);
     if (c->state < 3) return cc_fail(c, CC_E_STATE, "cc_correct first");
@@ -447,7 +512,7 @@ cc_status cc_get_schedule(cc_ctx* c, int64_t* sched_h, int64_t cap, int64_t* n_h
     const int64_t n = std::min<int64_t>((int64_t)c->last_iters, (int64_t)c->p.t_max);
     const int64_t k = std::min(n, cap);
     if (k > 0) {
-        CC_CUDA(c, cudaMemcpyAsync(sched_h, c->trace_s.p, (size_t)(5 * k) * sizeof(long long), cudaMemcpyDeviceToHost,
+        CC_CUDA(c, cudaMemcpyAsync(sched_h, c->trace_s.p, (size_t)(6 * k) * sizeof(long long), cudaMemcpyDeviceToHost,
                                    c->stream));
         CC_CUDA(c, cudaStreamSynchronize(c->stream));
     }
@@ -592,14 +657,15 @@ cc_status cc_kernel_stats(cc_ctx* c, char* names, int64_t names_cap, double* ms,
     all += "total_launches\n";
     k++;
     // pseudo-classes: K3 work actually done (the frontier skips frozen particles)
-    unsigned long long wk[2] = {0, 0};
+    unsigned long long wk[5] = {0, 0, 0, 0, 0};
     if (c->k3work.p) {
         CC_CUDA(c, cudaMemcpyAsync(wk, c->k3work.p, sizeof(wk), cudaMemcpyDeviceToHost, c->stream));
         CC_CUDA(c, cudaStreamSynchronize(c->stream));
         if (reset) CC_CUDA(c, cudaMemsetAsync(c->k3work.p, 0, sizeof(wk), c->stream));
     }
-    const char* wn[2] = {"K3_work_editables\n", "K3_work_entries\n"};
-    for (int q = 0; q < 2; q++) {
+    const char* wn[5] = {"K3_work_editables\n", "K3_work_entries\n", "K2_count_tests\n", "K2_fill_tests\n",
+                         "K4_link_tests\n"};
+    for (int q = 0; q < 5; q++) {
         if (k < cap) {
             if (ms) ms[k] = 0.0;
             if (launches) launches[k] = (int64_t)wk[q];

@@ -14,6 +14,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 #include <string>
 #include <vector>
@@ -36,6 +37,13 @@ struct Th {
     float lo2, hi2;    // fl32((b -/+ 2 sqrt3 xi)^2); lo2 = -1 if b - 2 sqrt3 xi <= 0
     float c_b, c_f;    // fl32(b -/+ 2 sqrt3 eps_q)
     int periodic;
+    // Proven link status under ANY positions within xi_f of the originals (DESIGN.md §5,
+    // "stable and near shells"): original d2 <= lo2s  =>  linked in every such position set;
+    // d2 > hi2s  =>  unlinked in every one -- rigorous bounds through the fp32 rounding of the
+    // pinned expression.  _i: interior pairs (no minimum-image wrap; relative rounding only),
+    // _w: pairs near a periodic face (the wrap adds an absolute error u (L + 2 xi)).  Pairs in
+    // (lo2s, lo2] or (hi2, hi2s] form the near-shell list re-tested on the positions.
+    float lo2s_i, hi2s_i, lo2s_w, hi2s_w;
 };
 
 // Search structure on ORIGINAL positions ("x-sorted rows"): the (y,z) plane is cut into
@@ -64,10 +72,12 @@ struct Ctl {
     unsigned int ticket;
     int sel;           // K3: this launch processes only the bitmap-selected editables (pgd.cu)
     int bld;           // K3: this launch builds the awake/touched bitmaps
-    unsigned int nsel; // K3: editables selected for the next k_pgd (k_select)
+    unsigned int nsel; // K3: short-row editables selected for the next k_pgd (k_select)
+    unsigned int nsel_l;  // K3: long-row editables selected (stored from slist[e_short])
     unsigned long long active;   // L_tight-active pairs at the last check
     unsigned long long violated; // pairs whose link status differs from the original (Eq. 1)
     double loss;
+    int loss_le;                 // L_tight <= eps_L at the last check, decided exactly (lfx_le)
     unsigned long long acc[14];  // K3 launch statistics being summed (LFX layout + schedule counts)
     unsigned int tail_nn;        // k_tail: length of the list being built
     unsigned int tail_ncur;      // k_tail: length of the list of the next iteration
@@ -124,6 +134,44 @@ __host__ __device__ inline double lfx_value(const unsigned long long* l) {
     return r * s70 * s70;
 }
 
+// Exact stop test of Alg. 1 line 6: sum(limbs) <= v, decided on the exact integer
+// digits (never on the rounded lfx_value).  Every L_tight term e^2 is a multiple of
+// (ulp(c)/2)^2 (e = fl(d_hat - c) is a multiple of ulp(c)/2 for c = c_b or c_f), so for
+// c >= 2^-46 the truncation to 2^-LFX_UNIT in lfx_add drops nothing and the limbs hold the
+// real number L_tight exactly; the sum is then a multiple of 2^-LFX_UNIT and
+// sum <= v  <=>  sum <= floor(v 2^LFX_UNIT) 2^-LFX_UNIT.
+__host__ __device__ inline bool lfx_le(const unsigned long long* l, double v) {
+    if (!(v >= 0.0)) return false;  // the sum is >= 0; NaN never holds
+    unsigned long long sd[7], vd[7] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull}, carry = 0ull;
+    for (int k = 0; k < 6; k++) {
+        const unsigned long long x = l[k] + carry;
+        sd[k] = x & 0xFFFFFFFFull;
+        carry = x >> 32;
+    }
+    sd[6] = carry;
+    const double two52 = 4503599627370496.0;
+    if (v >= two52) return true;  // beyond the limbs' range [2^-140, 2^52)
+    // v = mant 2^(ex - 1075), digits of floor(v 2^LFX_UNIT)
+    unsigned long long bits;
+    memcpy(&bits, &v, sizeof(bits));
+    const int ex = (int)((bits >> 52) & 0x7FF);
+    unsigned long long m = (bits & 0xFFFFFFFFFFFFFull) | (ex ? (1ull << 52) : 0ull);
+    int s = (ex ? ex : 1) - 1075 + LFX_UNIT;
+    if (s < 0) {
+        m = s <= -64 ? 0ull : (m >> -s);
+        s = 0;
+    }
+    const int k0 = s >> 5, off = s & 31;
+    for (int k = 0; k < 7; k++) {
+        if (k == k0) vd[k] = (m << off) & 0xFFFFFFFFull;
+        else if (k == k0 + 1) vd[k] = (m >> (32 - off)) & 0xFFFFFFFFull;
+        else if (k == k0 + 2 && off) vd[k] = (m >> (64 - off)) & 0xFFFFFFFFull;
+    }
+    for (int k = 6; k >= 0; k--)
+        if (sd[k] != vd[k]) return sd[k] < vd[k];
+    return true;
+}
+
 template <typename T>
 struct DBuf {
     T* p = nullptr;
@@ -149,6 +197,8 @@ struct cc_ctx {
     cc_params p{};
     int rank = 0, nranks = 1;
     void* nccl_comm = nullptr;
+    void* vgroup = nullptr;  // in-process virtual ranks (comm.cu) instead of NCCL
+    int comm_depth = 0;      // open comm groups (virtual ranks)
     std::string err;
     int state = 0;  // 0 created, 1 cells, 2 pairs, 3 corrected
     bool dead = false;
@@ -179,7 +229,9 @@ struct cc_ctx {
     bool base_valid = false;
     cc::DBuf<uint32_t> parent_orig;  // stable forest + original-linked band pairs = FoF(ORIG), per build
     bool orig_valid = false;
-    bool corr_base_ok = false;   // xi - xi' margin >> fp32 rounding: CORR FoF may reuse the base
+    cc::DBuf<uint2> near;        // near-shell pairs (slot, slot | bit 31 = linked in the original), K2 count
+    cc::DBuf<unsigned long long> near_n;  // their count (may exceed near.cap: then FoF searches directly)
+    int64_t near_count = 0;      // host copy after cc_find_vulnerable
     double r_pair = 0, r_link = 0;   // search radii: vulnerable band / FoF on original positions
     cc::DBuf<float> mom;         // 6 * E floats: mx, my, mz, vx, vy, vz
     cc::DBuf<float2> bc;         // Adam bias corrections per iteration
@@ -188,7 +240,7 @@ struct cc_ctx {
     cc::DBuf<long long> trace_a, trace_v, trace_s;
     cc::DBuf<uint32_t> lab_s;     // FoF labels in slot order (fof.cu)
     cc::DBuf<uint32_t> frozen, fbits, slist, tlist;  // K3 frontier: last-processed iteration, awake/touched bitmaps (pgd.cu)
-    cc::DBuf<unsigned long long> k3work;  // K3 work totals (editables updated, entries evaluated)
+    cc::DBuf<unsigned long long> k3work;  // work totals: K3 editables updated, entries evaluated; K2 count / fill and K4 pair tests
     int64_t E_cls[4] = {0, 0, 0, 0};  // editables per K3 work class (row_class), numbered class-major
     cc::DBuf<double> trace_l;
     cc::DBuf<unsigned char> tmp_bytes;  // scan scratch
@@ -252,11 +304,12 @@ __host__ __device__ inline int row_class(uint32_t len) { return len <= 4u ? 0 : 
 
 // Alg. 1 line 6 stop test per stop mode (R11): ACTIVE: no L_tight-active pair;
 // EPS: L_tight <= eps_L; RESTORED: L_tight <= eps_L and every link status restored (MCC = 1)
-__host__ __device__ inline bool stop_rule(int mode, unsigned long long active, double loss,
-                                          unsigned long long violated, double eps_loss) {
+// loss_le: L_tight <= eps_L decided exactly (lfx_le)
+__host__ __device__ inline bool stop_rule(int mode, unsigned long long active, bool loss_le,
+                                          unsigned long long violated) {
     if (mode == CC_STOP_ACTIVE) return active == 0ull;
-    if (mode == CC_STOP_EPS) return loss <= eps_loss;
-    if (mode == CC_STOP_RESTORED) return violated == 0ull && loss <= eps_loss;
+    if (mode == CC_STOP_EPS) return loss_le;
+    if (mode == CC_STOP_RESTORED) return violated == 0ull && loss_le;
     return false;
 }
 
@@ -497,6 +550,13 @@ __device__ __forceinline__ void for_each_pair_forward(const Grid& g, const uint3
     }
 }
 
+// per-warp sum of a per-thread counter into a global total (one atomic per warp)
+__device__ __forceinline__ void warp_count(unsigned long long* dst, unsigned v) {
+    unsigned long long x = v;
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd(dst, x);
+}
+
 // pinned d2 without the minimum image: identical to dist2 whenever no coordinate difference
 // can exceed L/2, i.e. for particles away from the periodic faces (interior below)
 __device__ __forceinline__ float dist2_nw(const float4& a, const float4& b) {
@@ -570,6 +630,19 @@ cc_status halo_sizes_run(cc_ctx* c, int64_t min_size, int64_t* sizes_h, int64_t 
 const float4* pgd_result(cc_ctx* c);
 cc_status fof_base_begin(cc_ctx* c);
 cc_status fof_base_end(cc_ctx* c);
+cc_status union_near(cc_ctx* c, const float4* P, uint32_t* par);
+unsigned long long* work_counters(cc_ctx* c);  // k3work, allocated and zeroed on first use
+// comm.cu: the exchange layer (NCCL or in-process virtual ranks)
+enum { CT_U8, CT_I32, CT_U32, CT_I64, CT_U64, CT_F32, CT_F64 };
+enum { CO_SUM, CO_MIN };
+cc_status comm_init(cc_ctx* c, const cc_dist* d);
+void comm_destroy(cc_ctx* c);
+cc_status comm_group_start(cc_ctx* c);
+cc_status comm_group_end(cc_ctx* c);
+cc_status comm_send(cc_ctx* c, const void* buf, size_t count, int type, int peer);
+cc_status comm_recv(cc_ctx* c, void* buf, size_t count, int type, int peer);
+cc_status comm_allreduce(cc_ctx* c, void* buf, size_t count, int type, int op);
+cc_status comm_allgather(cc_ctx* c, const void* send, void* recv, size_t count, int type);
 // dist.cu
 cc_status dist_init(cc_ctx* c, const cc_dist* d);
 void dist_destroy(cc_ctx* c);

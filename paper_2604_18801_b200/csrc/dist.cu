@@ -253,7 +253,7 @@ __global__ void k_decide(Ctl* ctl, const unsigned long long* __restrict__ red, i
         trace_l[t - 1] = td;
         trace_v[t - 1] = (long long)tv;
     }
-    if (stop_rule(stop_mode, tu, td, tv, eps_loss)) {
+    if (stop_rule(stop_mode, tu, lfx_le(red + 2, eps_loss), tv)) {
         ctl->done = 1;
         ctl->t_res = t - 1;
         ctl->converged = 1;
@@ -331,12 +331,8 @@ cc_status dist_init(cc_ctx* c, const cc_dist* d) {
     c->rank = d->rank;
     c->nranks = d->nranks;
     if (d->nranks <= 1) return CC_OK;
-    if (!d->nccl_id_h || d->rank < 0 || d->rank >= d->nranks) return cc_fail(c, CC_E_ARG, "bad cc_dist");
-    ncclUniqueId id;
-    std::memcpy(&id, d->nccl_id_h, sizeof(id));
-    ncclComm_t cm;
-    CC_NCCL(c, ncclCommInitRank(&cm, d->nranks, id, d->rank));
-    c->nccl_comm = cm;
+    if ((!d->nccl_id_h && !d->vgroup) || d->rank < 0 || d->rank >= d->nranks) return cc_fail(c, CC_E_ARG, "bad cc_dist");
+    CC_TRY(comm_init(c, d));
     c->left = (d->rank + d->nranks - 1) % d->nranks;
     c->right = (d->rank + 1) % d->nranks;
     c->slab_lo = c->p.box * (double)d->rank / d->nranks;
@@ -350,19 +346,18 @@ void dist_destroy(cc_ctx* c) {
     if (c->pm_local) cudaFree(c->pm_local);
     c->pm_local = nullptr;
     for (int r = 0; r < 8; r++) c->pm_peer[r] = nullptr;
-    if (c->nranks > 1 && c->nccl_comm) ncclCommDestroy(comm(c));
-    c->nccl_comm = nullptr;
+    if (c->nranks > 1) comm_destroy(c);
 }
 
 // in-place global sums of small device arrays (synchronising)
 cc_status dist_allreduce_u64(cc_ctx* c, unsigned long long* dev, size_t count) {
     if (c->nranks <= 1) return CC_OK;
-    CC_NCCL(c, ncclAllReduce(dev, dev, count, ncclUint64, ncclSum, comm(c), c->stream));
+    CC_TRY(comm_allreduce(c, dev, count, CT_U64, CO_SUM));
     return CC_OK;
 }
 cc_status dist_allreduce_f64(cc_ctx* c, double* dev, size_t count) {
     if (c->nranks <= 1) return CC_OK;
-    CC_NCCL(c, ncclAllReduce(dev, dev, count, ncclFloat64, ncclSum, comm(c), c->stream));
+    CC_TRY(comm_allreduce(c, dev, count, CT_F64, CO_SUM));
     return CC_OK;
 }
 
@@ -400,12 +395,12 @@ cc_status dist_exchange_ghosts(cc_ctx* c, int64_t n, const float* x, const float
     {
         long long h[4] = {ns[0], ns[1], 0, 0};
         CC_CUDA(c, cudaMemcpyAsync(c->dcnt.p, h, 2 * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
-        CC_NCCL(c, ncclGroupStart());
-        CC_NCCL(c, ncclSend(c->dcnt.p + 0, 1, ncclInt64, c->left, comm(c), c->stream));
-        CC_NCCL(c, ncclSend(c->dcnt.p + 1, 1, ncclInt64, c->right, comm(c), c->stream));
-        CC_NCCL(c, ncclRecv(c->dcnt.p + 2, 1, ncclInt64, c->right, comm(c), c->stream));
-        CC_NCCL(c, ncclRecv(c->dcnt.p + 3, 1, ncclInt64, c->left, comm(c), c->stream));
-        CC_NCCL(c, ncclGroupEnd());
+        CC_TRY(comm_group_start(c));
+        CC_TRY(comm_send(c, c->dcnt.p + 0, 1, CT_I64, c->left));
+        CC_TRY(comm_send(c, c->dcnt.p + 1, 1, CT_I64, c->right));
+        CC_TRY(comm_recv(c, c->dcnt.p + 2, 1, CT_I64, c->right));
+        CC_TRY(comm_recv(c, c->dcnt.p + 3, 1, CT_I64, c->left));
+        CC_TRY(comm_group_end(c));
         CC_CUDA(c, cudaMemcpyAsync(h, c->dcnt.p, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CC_CUDA(c, cudaStreamSynchronize(c->stream));
         c->n_from_right = h[2];
@@ -425,14 +420,14 @@ cc_status dist_exchange_ghosts(cc_ctx* c, int64_t n, const float* x, const float
         if (ns[d] > 0)
             CCL(c, k_pack7<<<(unsigned)((ns[d] + DT - 1) / DT), DT, 0, c->stream>>>(ns[d], c->shell[d].p, x, y, z, xh, yh,
                                                                                   zh, gid, c->sbuf7[d].p));
-    CC_NCCL(c, ncclGroupStart());
-    if (ns[0] > 0) CC_NCCL(c, ncclSend(c->sbuf7[0].p, (size_t)(7 * ns[0]), ncclUint32, c->left, comm(c), c->stream));
-    if (ns[1] > 0) CC_NCCL(c, ncclSend(c->sbuf7[1].p, (size_t)(7 * ns[1]), ncclUint32, c->right, comm(c), c->stream));
+    CC_TRY(comm_group_start(c));
+    if (ns[0] > 0) CC_TRY(comm_send(c, c->sbuf7[0].p, (size_t)(7 * ns[0]), CT_U32, c->left));
+    if (ns[1] > 0) CC_TRY(comm_send(c, c->sbuf7[1].p, (size_t)(7 * ns[1]), CT_U32, c->right));
     if (c->n_from_right > 0)
-        CC_NCCL(c, ncclRecv(c->rbuf7[1].p, (size_t)(7 * c->n_from_right), ncclUint32, c->right, comm(c), c->stream));
+        CC_TRY(comm_recv(c, c->rbuf7[1].p, (size_t)(7 * c->n_from_right), CT_U32, c->right));
     if (c->n_from_left > 0)
-        CC_NCCL(c, ncclRecv(c->rbuf7[0].p, (size_t)(7 * c->n_from_left), ncclUint32, c->left, comm(c), c->stream));
-    CC_NCCL(c, ncclGroupEnd());
+        CC_TRY(comm_recv(c, c->rbuf7[0].p, (size_t)(7 * c->n_from_left), CT_U32, c->left));
+    CC_TRY(comm_group_end(c));
     if (c->n_from_left > 0)
         CCL(c, k_unstage<<<(unsigned)((c->n_from_left + DT - 1) / DT), DT, 0, c->stream>>>(c->n_from_left, cap, n,
                                                                                           c->rbuf7[0].p, c->stage.p));
@@ -450,39 +445,50 @@ cc_status dist_exchange_ghosts(cc_ctx* c, int64_t n, const float* x, const float
 // map every rank's peer block (X3 over NVLink): (re)allocate mine if the receive areas grew,
 // exchange IPC handles with an allgather, open the peers' blocks that changed
 static cc_status dist_setup_peer(cc_ctx* c) {
+    // Every rank takes part in the same collectives whatever its environment says; the peer
+    // path is used only if EVERY rank wants it and mapped every peer (one allgather of the
+    // wishes + handles, one MIN allreduce of the outcome) -- a rank falling back alone to the
+    // NCCL path while the others spin on epoch flags would hang.
     c->pm_ok = false;
+    if (c->vgroup) return CC_OK;  // virtual ranks share one GPU: the copy transport, no peer mapping
     const char* env = std::getenv("CC_PEER");
-    if ((env && env[0] == '0') || c->nranks > 8) return CC_OK;  // NCCL path
-    const int64_t need0 = std::max<int64_t>(c->n_ref_recv[0], 1), need1 = std::max<int64_t>(c->n_ref_recv[1], 1);
-    if (!c->pm_local || need0 > c->pm_cap[0] || need1 > c->pm_cap[1]) {
-        if (c->pm_local) cudaFree(c->pm_local);
-        c->pm_local = nullptr;
-        c->pm_cap[0] = need0 + need0 / 4 + 64;
-        c->pm_cap[1] = need1 + need1 / 4 + 64;
-        c->pm_bytes = pm_area_off(1, c->pm_cap) + 2 * (size_t)c->pm_cap[1] * sizeof(float4);
-        CC_CUDA(c, cudaMalloc(&c->pm_local, c->pm_bytes));
-        CC_CUDA(c, cudaMemsetAsync(c->pm_local, 0, c->pm_bytes, c->stream));
+    const int want = !((env && env[0] == '0') || c->nranks > 8);
+    if (want) {
+        const int64_t need0 = std::max<int64_t>(c->n_ref_recv[0], 1), need1 = std::max<int64_t>(c->n_ref_recv[1], 1);
+        if (!c->pm_local || need0 > c->pm_cap[0] || need1 > c->pm_cap[1]) {
+            if (c->pm_local) cudaFree(c->pm_local);
+            c->pm_local = nullptr;
+            c->pm_cap[0] = need0 + need0 / 4 + 64;
+            c->pm_cap[1] = need1 + need1 / 4 + 64;
+            c->pm_bytes = pm_area_off(1, c->pm_cap) + 2 * (size_t)c->pm_cap[1] * sizeof(float4);
+            CC_CUDA(c, cudaMalloc(&c->pm_local, c->pm_bytes));
+            CC_CUDA(c, cudaMemsetAsync(c->pm_local, 0, c->pm_bytes, c->stream));
+        }
     }
     struct Rec {
         cudaIpcMemHandle_t h;
         int64_t cap[2];
-        unsigned char pad[128 - sizeof(cudaIpcMemHandle_t) - 16];
+        int32_t want;
+        unsigned char pad[128 - sizeof(cudaIpcMemHandle_t) - 20];
     };
     static_assert(sizeof(Rec) == 128, "");
     Rec mine;
     std::memset(&mine, 0, sizeof(mine));
-    CC_CUDA(c, cudaIpcGetMemHandle(&mine.h, c->pm_local));
+    if (want) CC_CUDA(c, cudaIpcGetMemHandle(&mine.h, c->pm_local));
     mine.cap[0] = c->pm_cap[0];
     mine.cap[1] = c->pm_cap[1];
+    mine.want = want;
     unsigned char* dbuf = nullptr;
     CC_CUDA(c, cudaMalloc(&dbuf, 128 * (size_t)(c->nranks + 1)));
     CC_CUDA(c, cudaMemcpyAsync(dbuf, &mine, 128, cudaMemcpyHostToDevice, c->stream));
-    CC_NCCL(c, ncclAllGather(dbuf, dbuf + 128, 128, ncclUint8, comm(c), c->stream));
+    CC_TRY(comm_allgather(c, dbuf, dbuf + 128, 128, CT_U8));
     std::vector<Rec> all((size_t)c->nranks);
     CC_CUDA(c, cudaMemcpyAsync(all.data(), dbuf + 128, 128 * (size_t)c->nranks, cudaMemcpyDeviceToHost, c->stream));
     CC_CUDA(c, cudaStreamSynchronize(c->stream));
-    cudaFree(dbuf);
-    for (int r = 0; r < c->nranks; r++) {
+    bool all_want = true;
+    for (int r = 0; r < c->nranks; r++) all_want = all_want && all[(size_t)r].want != 0;
+    int ok = all_want ? 1 : 0;
+    for (int r = 0; r < c->nranks && ok; r++) {
         c->pm_peer_cap[r][0] = all[(size_t)r].cap[0];
         c->pm_peer_cap[r][1] = all[(size_t)r].cap[1];
         if (r == c->rank) {
@@ -495,11 +501,21 @@ static cc_status dist_setup_peer(cc_ctx* c) {
         void* ptr = nullptr;
         if (cudaIpcOpenMemHandle(&ptr, all[(size_t)r].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
             cudaGetLastError();
-            return CC_OK;  // no peer mapping: the NCCL path stays in use
+            ok = 0;  // no peer mapping here: every rank must stay on the NCCL path
+            break;
         }
         c->pm_peer[r] = ptr;
         std::memcpy(c->pm_handle[r], &all[(size_t)r].h, 64);
     }
+    // agreement: the peer path only if every rank succeeded
+    int* dok = reinterpret_cast<int*>(dbuf);
+    CC_CUDA(c, cudaMemcpyAsync(dok, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CC_TRY(comm_allreduce(c, dok, 1, CT_I32, CO_MIN));
+    int all_ok = 0;
+    CC_CUDA(c, cudaMemcpyAsync(&all_ok, dok, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    cudaFree(dbuf);
+    if (!all_ok) return CC_OK;
     CC_TRY(cc_ensure(c, c->red_sum, LFX_STATS, "peer statistics"));
     c->pm_ok = true;
     return CC_OK;
@@ -526,12 +542,12 @@ cc_status dist_setup_refresh(cc_ctx* c) {
     {
         long long h[4] = {nreq[0], nreq[1], 0, 0};
         CC_CUDA(c, cudaMemcpyAsync(c->dcnt.p, h, 2 * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
-        CC_NCCL(c, ncclGroupStart());
-        CC_NCCL(c, ncclSend(c->dcnt.p + 0, 1, ncclInt64, c->left, comm(c), c->stream));
-        CC_NCCL(c, ncclSend(c->dcnt.p + 1, 1, ncclInt64, c->right, comm(c), c->stream));
-        CC_NCCL(c, ncclRecv(c->dcnt.p + 2, 1, ncclInt64, c->right, comm(c), c->stream));
-        CC_NCCL(c, ncclRecv(c->dcnt.p + 3, 1, ncclInt64, c->left, comm(c), c->stream));
-        CC_NCCL(c, ncclGroupEnd());
+        CC_TRY(comm_group_start(c));
+        CC_TRY(comm_send(c, c->dcnt.p + 0, 1, CT_I64, c->left));
+        CC_TRY(comm_send(c, c->dcnt.p + 1, 1, CT_I64, c->right));
+        CC_TRY(comm_recv(c, c->dcnt.p + 2, 1, CT_I64, c->right));
+        CC_TRY(comm_recv(c, c->dcnt.p + 3, 1, CT_I64, c->left));
+        CC_TRY(comm_group_end(c));
         CC_CUDA(c, cudaMemcpyAsync(h, c->dcnt.p, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CC_CUDA(c, cudaStreamSynchronize(c->stream));
         // from the right: requests about my dir-1 shell (sent to the right); from the left: dir-0
@@ -546,14 +562,14 @@ cc_status dist_setup_refresh(cc_ctx* c) {
         CC_TRY(cc_ensure(c, c->rsb[d], (size_t)std::max<int64_t>(c->n_ref_send[d], 1), "refresh send buffer"));
         CC_TRY(cc_ensure(c, c->rrb[d], (size_t)std::max<int64_t>(c->n_ref_recv[d], 1), "refresh recv buffer"));
     }
-    CC_NCCL(c, ncclGroupStart());
-    if (nreq[0] > 0) CC_NCCL(c, ncclSend(c->req[0].p, (size_t)nreq[0], ncclUint32, c->left, comm(c), c->stream));
-    if (nreq[1] > 0) CC_NCCL(c, ncclSend(c->req[1].p, (size_t)nreq[1], ncclUint32, c->right, comm(c), c->stream));
+    CC_TRY(comm_group_start(c));
+    if (nreq[0] > 0) CC_TRY(comm_send(c, c->req[0].p, (size_t)nreq[0], CT_U32, c->left));
+    if (nreq[1] > 0) CC_TRY(comm_send(c, c->req[1].p, (size_t)nreq[1], CT_U32, c->right));
     if (c->n_ref_send[1] > 0)
-        CC_NCCL(c, ncclRecv(c->sreq[1].p, (size_t)c->n_ref_send[1], ncclUint32, c->right, comm(c), c->stream));
+        CC_TRY(comm_recv(c, c->sreq[1].p, (size_t)c->n_ref_send[1], CT_U32, c->right));
     if (c->n_ref_send[0] > 0)
-        CC_NCCL(c, ncclRecv(c->sreq[0].p, (size_t)c->n_ref_send[0], ncclUint32, c->left, comm(c), c->stream));
-    CC_NCCL(c, ncclGroupEnd());
+        CC_TRY(comm_recv(c, c->sreq[0].p, (size_t)c->n_ref_send[0], CT_U32, c->left));
+    CC_TRY(comm_group_end(c));
     for (int d = 0; d < 2; d++)
         if (c->n_ref_send[d] > 0)
             CCL(c, k_map_requests<<<(unsigned)((c->n_ref_send[d] + DT - 1) / DT), DT, 0, c->stream>>>(
@@ -611,18 +627,18 @@ cc_status dist_iter_tail(cc_ctx* c, const float4* p0, const float4* p1) {
         if (c->n_ref_send[d] > 0)
             CCL(c, k_refresh_pack<<<(unsigned)((c->n_ref_send[d] + DT - 1) / DT), DT, 0, c->stream>>>(
                        c->n_ref_send[d], c->send_e[d].p, c->ctl.p, p0, p1, c->rsb[d].p));
-    CC_NCCL(c, ncclGroupStart());
+    CC_TRY(comm_group_start(c));
     if (c->n_ref_send[0] > 0)
-        CC_NCCL(c, ncclSend(c->rsb[0].p, (size_t)(4 * c->n_ref_send[0]), ncclFloat32, c->left, comm(c), c->stream));
+        CC_TRY(comm_send(c, c->rsb[0].p, (size_t)(4 * c->n_ref_send[0]), CT_F32, c->left));
     if (c->n_ref_send[1] > 0)
-        CC_NCCL(c, ncclSend(c->rsb[1].p, (size_t)(4 * c->n_ref_send[1]), ncclFloat32, c->right, comm(c), c->stream));
+        CC_TRY(comm_send(c, c->rsb[1].p, (size_t)(4 * c->n_ref_send[1]), CT_F32, c->right));
     if (c->n_ref_recv[1] > 0)
-        CC_NCCL(c, ncclRecv(c->rrb[1].p, (size_t)(4 * c->n_ref_recv[1]), ncclFloat32, c->right, comm(c), c->stream));
+        CC_TRY(comm_recv(c, c->rrb[1].p, (size_t)(4 * c->n_ref_recv[1]), CT_F32, c->right));
     if (c->n_ref_recv[0] > 0)
-        CC_NCCL(c, ncclRecv(c->rrb[0].p, (size_t)(4 * c->n_ref_recv[0]), ncclFloat32, c->left, comm(c), c->stream));
+        CC_TRY(comm_recv(c, c->rrb[0].p, (size_t)(4 * c->n_ref_recv[0]), CT_F32, c->left));
     // the stop statistics travel in the same NCCL group as the ghost refresh (one launch)
-    CC_NCCL(c, ncclAllReduce(c->red.p, c->red.p, LFX_STATS, ncclUint64, ncclSum, comm(c), c->stream));
-    CC_NCCL(c, ncclGroupEnd());
+    CC_TRY(comm_allreduce(c, c->red.p, LFX_STATS, CT_U64, CO_SUM));
+    CC_TRY(comm_group_end(c));
     for (int d = 0; d < 2; d++)
         if (c->n_ref_recv[d] > 0)
             CCL(c, k_refresh_unpack<<<(unsigned)((c->n_ref_recv[d] + DT - 1) / DT), DT, 0, c->stream>>>(
@@ -653,12 +669,12 @@ cc_status dist_fof_merge(cc_ctx* c, int64_t* n_groups) {
             CCL(c, k_label_pack<<<(unsigned)((ns1 + DT - 1) / DT), DT, 0, c->stream>>>(ns1, c->shell[1].p, c->slot_of.p,
                                                                                      c->parent.p, c->mingid.p,
                                                                                      c->lsb[1].p));
-        CC_NCCL(c, ncclGroupStart());
-        if (ns0 > 0) CC_NCCL(c, ncclSend(c->lsb[0].p, (size_t)ns0, ncclUint32, c->left, comm(c), c->stream));
-        if (ns1 > 0) CC_NCCL(c, ncclSend(c->lsb[1].p, (size_t)ns1, ncclUint32, c->right, comm(c), c->stream));
-        if (nfr > 0) CC_NCCL(c, ncclRecv(c->lrb[1].p, (size_t)nfr, ncclUint32, c->right, comm(c), c->stream));
-        if (nfl > 0) CC_NCCL(c, ncclRecv(c->lrb[0].p, (size_t)nfl, ncclUint32, c->left, comm(c), c->stream));
-        CC_NCCL(c, ncclGroupEnd());
+        CC_TRY(comm_group_start(c));
+        if (ns0 > 0) CC_TRY(comm_send(c, c->lsb[0].p, (size_t)ns0, CT_U32, c->left));
+        if (ns1 > 0) CC_TRY(comm_send(c, c->lsb[1].p, (size_t)ns1, CT_U32, c->right));
+        if (nfr > 0) CC_TRY(comm_recv(c, c->lrb[1].p, (size_t)nfr, CT_U32, c->right));
+        if (nfl > 0) CC_TRY(comm_recv(c, c->lrb[0].p, (size_t)nfl, CT_U32, c->left));
+        CC_TRY(comm_group_end(c));
         if (nfl > 0)
             CCL(c, k_label_merge<<<(unsigned)((nfl + DT - 1) / DT), DT, 0, c->stream>>>(
                        nfl, (uint32_t)c->n_in, c->slot_of.p, c->parent.p, c->mingid.p, c->lrb[0].p,
@@ -720,7 +736,7 @@ cc_status dist_halo_sizes(cc_ctx* c, int64_t min_size, std::vector<uint32_t>& ou
     long long mine[2] = {ni, nbnd};
     CC_CUDA(c, cudaMemcpyAsync(c->dcnt.p + 4 + 2 * c->rank, mine, 2 * sizeof(long long), cudaMemcpyHostToDevice,
                                c->stream));
-    CC_NCCL(c, ncclAllGather(c->dcnt.p + 4 + 2 * c->rank, c->dcnt.p + 4, 2, ncclInt64, comm(c), c->stream));
+    CC_TRY(comm_allgather(c, c->dcnt.p + 4 + 2 * c->rank, c->dcnt.p + 4, 2, CT_I64));
     std::vector<long long> all((size_t)2 * c->nranks);
     CC_CUDA(c, cudaMemcpyAsync(all.data(), c->dcnt.p + 4, all.size() * sizeof(long long), cudaMemcpyDeviceToHost,
                                c->stream));
@@ -741,7 +757,7 @@ cc_status dist_halo_sizes(cc_ctx* c, int64_t min_size, std::vector<uint32_t>& ou
     if (nbnd > 0)
         CC_CUDA(c, cudaMemcpyAsync(mineb + mi, c->bnd.p, (size_t)nbnd * sizeof(uint2), cudaMemcpyDeviceToDevice,
                                    c->stream));
-    if (per > 0) CC_NCCL(c, ncclAllGather(mineb, c->gath.p, per, ncclUint32, comm(c), c->stream));
+    if (per > 0) CC_TRY(comm_allgather(c, mineb, c->gath.p, per, CT_U32));
     std::vector<uint32_t> h(per * (size_t)c->nranks);
     if (!h.empty())
         CC_CUDA(c, cudaMemcpyAsync(h.data(), c->gath.p, h.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost,

@@ -32,9 +32,12 @@ __global__ void k_iota(int64_t n, uint32_t* __restrict__ par) {
 // ones that built the structure), with the fp32 rounding margin.
 __global__ void __launch_bounds__(FOF_THREADS)
 k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ orig4, const uint32_t* __restrict__ xk,
-           const uint32_t* __restrict__ cs, Grid g, Th t, double r, float thr2, uint32_t* __restrict__ par) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
+           const uint32_t* __restrict__ cs, Grid g, Th t, double r, float thr2, uint32_t* __restrict__ par,
+           unsigned long long* __restrict__ tests) {
+    const int64_t s0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = s0 < n;
+    const int64_t s = live ? s0 : n - 1;
+    unsigned ntest = 0;
     const float4 o = orig4[s];
     const float4 p = P[s];
     double u;
@@ -43,10 +46,13 @@ k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ o
     const bool periodic_yz = t.periodic != 0;
     uint32_t rs = (uint32_t)s;  // cached ancestor of s (uf_link)
     auto link = [&](uint32_t j) {
+        if (!live) return;
+        ntest++;
         const float4 q = P[j];
         if (dist2(p, q, t) <= thr2) uf_link(par, (uint32_t)s, j, rs);
     };
     for_each_pair_forward(g, cs, xk, (uint32_t)s, u, cy, cz, r, periodic_yz, link);
+    warp_count(tests, ntest);
 }
 
 // read-only root walk: the flatten pass must not path-halve, or a halving write could land
@@ -186,30 +192,35 @@ k_union_rows(uint32_t E, const unsigned long long* __restrict__ rowptr, const ui
     }
 }
 
-// The stable forest: links with original d2 <= lo2 (d <= b - 2 sqrt3 xi) exist in the original,
-// decompressed and corrected positions alike (R1/DESIGN.md §5), so they are searched ONCE; each
-// FoF labelling then adds only the vulnerable pairs from the CSR rows.
-static cc_status fof_base(cc_ctx* c) {
-    const int64_t n = c->n;
-    const size_t n1 = (size_t)std::max<int64_t>(n, 1);
-    CC_TRY(cc_ensure(c, c->parent_base, n1, "stable forest"));
-    const unsigned nb = (unsigned)((n + FOF_THREADS - 1) / FOF_THREADS);
-    int tok = cc_prof_begin(c, "K4_fof_base");
-    if (n > 0) {
-        CCL(c, k_iota<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent_base.p));
-        if (c->th.lo2 >= 0.0f) {
-            const double r = std::sqrt((double)c->th.lo2) * (1.0 + 1e-5);
-            CCL(c, k_fof_link<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->orig4.p, c->orig4.p, c->xk.p, c->cell_start.p,
-                                                                 c->g, c->th, r, c->th.lo2, c->parent_base.p));
+// near-shell pairs (K2 count, Th::lo2s/hi2s): linked in the original iff bit 31 (P == nullptr),
+// else iff the pinned d2 <= b2 on the slot-order positions P
+__global__ void __launch_bounds__(256)
+k_union_near(unsigned long long m, const uint2* __restrict__ near, const float4* __restrict__ P, Th t,
+             uint32_t* __restrict__ par) {
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const uint2 e = near[i];
+        const uint32_t s = e.x, j = e.y & 0x7FFFFFFFu;
+        const bool lk = P ? dist2(P[s], P[j], t) <= t.b2 : (e.y >> 31) != 0u;
+        if (lk) {
+            uint32_t rs = s;
+            uf_link(par, s, j, rs);
         }
-        CCL(c, k_flatten<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent_base.p));
     }
-    cc_prof_end(c, tok);
+}
+
+cc_status union_near(cc_ctx* c, const float4* P, uint32_t* par) {
+    const unsigned long long m = (unsigned long long)std::min<int64_t>(c->near_count, (int64_t)c->near.cap);
+    if (m == 0) return CC_OK;
+    const unsigned nb = (unsigned)std::min<unsigned long long>((m + 255) / 256, 148 * 8);
+    CCL(c, k_union_near<<<nb, 256, 0, c->stream>>>(m, c->near.p, P, c->th, par));
     CC_CUDA(c, cudaGetLastError());
-    c->base_valid = true;
     return CC_OK;
 }
 
+// The stable forest: links with original d2 <= lo2s (provably linked in the original,
+// decompressed and corrected positions alike, Th) are united ONCE per build, inside K2's count
+// sweep (pairs.cu); each FoF labelling then adds the near shell and the vulnerable rows.
 // the count sweep of K2 (pairs.cu) unites the stable links it meets; these bracket it
 cc_status fof_base_begin(cc_ctx* c) {
     const int64_t n = c->n;
@@ -239,9 +250,10 @@ cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
     CC_TRY(cc_ensure(c, c->gsize, n1, "gsize"));
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
     const float4* P = which == CC_ORIG ? c->orig4.p : (which == CC_DECOMP ? c->dec4.p : c->cor4.p);
-    // ORIG always, CORR when the xi - xi' margin dominates fp32 rounding: stable forest + rows
-    const bool via_base = c->state >= 2 && (which == CC_ORIG || (which == CC_CORR && c->corr_base_ok));
-    if (via_base && !c->base_valid) CC_TRY(fof_base(c));
+    // ORIG and CORR: the stable forest (provably linked in both, Th::lo2s) + the near shell
+    // re-tested + the vulnerable rows (the near list overflowing its buffer: direct search)
+    const bool near_ok = c->near_count <= (int64_t)c->near.cap;
+    const bool via_base = c->state >= 2 && c->base_valid && near_ok && (which == CC_ORIG || which == CC_CORR);
     CC_CUDA(c, cudaMemsetAsync(c->mingid.p, 0xFF, n1 * sizeof(uint32_t), c->stream));
     CC_CUDA(c, cudaMemsetAsync(c->gsize.p, 0, n1 * sizeof(uint32_t), c->stream));
     CC_CUDA(c, cudaMemsetAsync(c->counters.p + 8, 0, sizeof(unsigned long long), c->stream));
@@ -261,11 +273,12 @@ cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
                            c->slotE.p, which == CC_ORIG ? nullptr : pgd_result(c), which == CC_ORIG ? 1 : 0, c->th,
                            c->parent.p));
             }
+            CC_TRY(union_near(c, which == CC_ORIG ? nullptr : c->cor4.p, c->parent.p));
         } else {
             CCL(c, k_iota<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p));
             CCL(c, k_fof_link<<<nb, FOF_THREADS, 0, c->stream>>>(n, P, c->orig4.p, c->xk.p, c->cell_start.p, c->g,
                                                                  c->th, which == CC_ORIG ? c->r_link : c->r_pair,
-                                                                 c->th.b2, c->parent.p));
+                                                                 c->th.b2, c->parent.p, work_counters(c) + 4));
         }
         CCL(c, k_flatten<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p));
         CCL(c, k_mingid<<<nb, FOF_THREADS, 0, c->stream>>>(n, c->parent.p, c->orig4.p, c->mingid.p, c->gsize.p,

@@ -13,6 +13,7 @@
 // entries (partner editable index | partner-gid-above bit | original-link bit).  Rows are then
 // sorted by partner gid so the PGD gradient sum has one defined order on any grid / rank (R14).
 // Each unordered pair is tested from both endpoints: both see the identical pinned fp32 d2.
+#include <algorithm>
 #include <cstring>
 
 #include "cc_internal.cuh"
@@ -29,9 +30,12 @@ constexpr int PAIR_THREADS = 256;
 __global__ void __launch_bounds__(PAIR_THREADS)
 k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
               const uint32_t* __restrict__ xk, const uint32_t* __restrict__ cs, Grid g, Th t, double r, uint32_t n_own,
-              uint32_t* __restrict__ deg, uint32_t* __restrict__ par_base) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
+              uint32_t* __restrict__ deg, uint32_t* __restrict__ par_base, uint2* __restrict__ near,
+              unsigned long long* __restrict__ near_n, unsigned long long near_cap, unsigned long long* __restrict__ tests) {
+    const int64_t s0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned ntest = 0;  // pair tests (candidates evaluated), reported as tests/s
+    const int64_t s = s0 < n ? s0 : n - 1;  // a tail thread repeats the last particle's search without effects
+    const bool live = s0 < n;
     const bool multi = n_own < (uint32_t)n;
     const bool ghost = multi && __float_as_uint(dec4[s].w) >= n_own;
     const float4 p = orig4[s];
@@ -39,9 +43,12 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
     int cx, cy, cz;
     cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
     const bool inner = interior(p.x, p.y, p.z, g, t);
+    const float lo2s = inner ? t.lo2s_i : t.lo2s_w, hi2s = inner ? t.hi2s_i : t.hi2s_w;
     uint32_t cnt = 0;
     uint32_t rs = (uint32_t)s;  // cached ancestor of s in the stable forest (uf_link)
     auto test = [&](uint32_t j) {
+        if (!live) return;
+        ntest++;
         const float4 q = orig4[j];
         const float d2 = inner ? dist2_nw(p, q) : dist2(p, q, t);
         if (t.lo2 < d2 && d2 <= t.hi2) {
@@ -54,14 +61,20 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
                 atomicAdd(&deg[j], 1u);
                 atomicOr(&deg[s], 0x80000000u);
             }
-        } else if (d2 <= t.lo2) {
-            // a stable FoF link (linked in original, decompressed and corrected positions alike,
-            // fof.cu): united here, in the same candidate sweep
+        } else if (d2 <= lo2s) {
+            // a stable FoF link: provably linked in the original, decompressed and corrected
+            // positions alike (Th::lo2s, fof.cu), united here in the same candidate sweep
             uf_link(par_base, (uint32_t)s, j, rs);
+        } else if (d2 <= hi2s) {
+            // near shell (lo2s, lo2] or (hi2, hi2s]: not vulnerable, but fp32 rounding could flip
+            // its link in other positions -- listed, re-tested by every FoF labelling
+            const unsigned long long q = atomicAdd(near_n, 1ull);
+            if (q < near_cap) near[q] = make_uint2((uint32_t)s, j | (d2 <= t.b2 ? 0x80000000u : 0u));
         }
     };
     for_each_pair_forward(g, cs, xk, (uint32_t)s, u, cy, cz, r, t.periodic != 0, test);
     if (cnt) atomicAdd(&deg[s], cnt);
+    warp_count(tests, ntest);
 }
 
 // after the scan: editable ranks and row offsets become global (class-major numbering: class
@@ -94,9 +107,12 @@ __global__ void __launch_bounds__(PAIR_THREADS)
 k_pairs_fill(uint32_t e_all, const uint32_t* __restrict__ slotE, const float4* __restrict__ orig4,
              const uint32_t* __restrict__ xk, const uint32_t* __restrict__ cs, Grid g, Th t, double r,
              const uint32_t* __restrict__ eidx, uint32_t e_own, const unsigned long long* __restrict__ rowptr,
-             uint32_t* __restrict__ cur, uint32_t* __restrict__ rows, uint32_t* __restrict__ par_orig) {
-    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= e_all) return;
+             uint32_t* __restrict__ cur, uint32_t* __restrict__ rows, uint32_t* __restrict__ par_orig,
+             unsigned long long* __restrict__ tests) {
+    const uint32_t e0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = e0 < e_all;
+    const uint32_t e = live ? e0 : e_all - 1;
+    unsigned ntest = 0;
     const uint32_t s = slotE[e];
     const float4 p = orig4[s];
     const uint32_t gp = __float_as_uint(p.w);
@@ -107,6 +123,8 @@ k_pairs_fill(uint32_t e_all, const uint32_t* __restrict__ slotE, const float4* _
     const bool inner = interior(p.x, p.y, p.z, g, t);
     uint32_t rs = (uint32_t)s;  // cached ancestor of s in the ORIG forest (uf_link)
     auto emit = [&](uint32_t j) {
+        if (!live) return;
+        ntest++;
         const float4 q = orig4[j];
         const float d2 = inner ? dist2_nw(p, q) : dist2(p, q, t);
         if (t.lo2 < d2 && d2 <= t.hi2) {
@@ -120,6 +138,7 @@ k_pairs_fill(uint32_t e_all, const uint32_t* __restrict__ slotE, const float4* _
         }
     };
     for_each_pair_forward(g, cs, xk, (uint32_t)s, u, cy, cz, r, t.periodic != 0, emit);
+    warp_count(tests, ntest);
 }
 
 // compaction: editable e -> slot, row start, original and starting position
@@ -228,11 +247,15 @@ cc_status pairs_count(cc_ctx* c) {
     CC_TRY(cc_ensure(c, c->deg, (size_t)std::max<int64_t>(n, 1), "deg"));
     CC_CUDA(c, cudaMemsetAsync(c->deg.p, 0, (size_t)std::max<int64_t>(n, 1) * sizeof(uint32_t), c->stream));
     CC_TRY(fof_base_begin(c));  // the stable FoF forest is built inside the count sweep
+    const int64_t near_cap = std::max<int64_t>(4096, n / 128);
+    CC_TRY(cc_ensure(c, c->near, (size_t)near_cap, "near-shell pairs"));
+    CC_TRY(cc_ensure(c, c->near_n, 1, "near-shell count"));
+    CC_CUDA(c, cudaMemsetAsync(c->near_n.p, 0, sizeof(unsigned long long), c->stream));
     if (n > 0) {
         int tok = cc_prof_begin(c, "K2_count");
         CCL(c, k_pairs_count<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
             n, c->orig4.p, c->dec4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in, c->deg.p,
-            c->parent_base.p));
+            c->parent_base.p, c->near.p, c->near_n.p, (unsigned long long)c->near.cap, work_counters(c) + 2));
         cc_prof_end(c, tok);
         CC_CUDA(c, cudaGetLastError());
     }
@@ -283,11 +306,11 @@ cc_status pairs_fill(cc_ctx* c) {
             (uint32_t)c->E_all, c->slotE.p, c->orig4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, c->eidx.p,
             (uint32_t)c->E,
             reinterpret_cast<const unsigned long long*>(c->rowptr.p), c->scratch_u32.p, c->rows.p,
-            c->parent_orig.p));
+            c->parent_orig.p, work_counters(c) + 3));
         cc_prof_end(c, tok);
         CC_CUDA(c, cudaGetLastError());
     }
-    return CC_OK;
+    return union_near(c, nullptr, c->parent_orig.p);  // + the near shell's original links
 }
 
 cc_status rows_finish(cc_ctx* c) {

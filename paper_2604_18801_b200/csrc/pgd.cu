@@ -58,7 +58,7 @@ struct PgdArgs {
     const uint32_t* __restrict__ rows;
     const float4* __restrict__ origE;
     uint32_t e_short;  // editables are numbered class-major by row length (pairs.cu): [0, e_short)
-                       // have <= 32 entries (thread path), [e_short, E) more (warp path)
+                       // have <= 16 entries (k_pgd<0>), [e_short, E) more (k_pgd<1>)
     float4* pos0;
     float4* pos1;
     float* __restrict__ mom;  // 6 x E SoA
@@ -213,8 +213,9 @@ __device__ __forceinline__ int update(const PgdArgs& a, uint32_t e, const float4
         float sx, sy, sz;
         // zero-gradient iterations missed while frozen, in order: steps that provably cannot
         // move the coordinates only advance the moments; the others are recomputed in full and
-        // checked (a move would mean the freeze was unsafe).  k_tail retries the proof every 8
-        // full steps (the bound shrinks as the moments decay); k_pgd proves once, up front.
+        // checked (a move would mean the freeze was unsafe).  The proof is retried every 8 full
+        // steps (the bound shrinks as the moments decay), so a particle frozen for thousands of
+        // iterations replays a few dozen steps in full, not all of them.
         if (replay_from < t) {
             const float bc2z = a.bc[t - 2].y;
             int tt = replay_from;
@@ -233,7 +234,7 @@ __device__ __forceinline__ int update(const PgdArgs& a, uint32_t e, const float4
                     break;
                 }
                 flags |= 4;  // full replay steps (reported in the schedule trace)
-                const int t8 = CG ? min(t, tt + 8) : t;  // k_pgd: no retry (registers)
+                const int t8 = min(t, tt + 8);  // retry the proof every 8 full steps (the bound decays)
                 for (; tt < t8; tt++) {
                     const float2 b = a.bc[tt - 1];
                     const float nx = project(adam_reg(x, 0.0f, mx, vx, a, b.x, b.y, sx), o.x, a.t.xip_f);
@@ -244,7 +245,7 @@ __device__ __forceinline__ int update(const PgdArgs& a, uint32_t e, const float4
                     y = ny;
                     z = nz;
                 }
-                if (tt >= t || !CG) break;
+                if (tt >= t) break;
             }
         }
         const float2 b = a.bc[t - 1];
@@ -317,12 +318,38 @@ __device__ __forceinline__ void tail_push(K3Ctx& k, uint32_t j) {
     if (i < TAIL_CAP) k.tnext[i] = j;
 }
 
-// ---- one batch: up to 32 editables (one per lane, `valid`).  The concatenation of their rows
-// is evaluated flattened across the lanes: CH entries per chunk, NB independent row/partner
-// loads per lane in flight, the terms parked in shared memory; then each lane sums its own
-// row's terms in row order (the pinned order, R14) and applies Adam + the projection to its
-// editable.  Returns whether the lane's editable stays awake.
+// ---- one batch: up to 32 editables (one per lane, `valid`).
+// Gradient summation order (R14): the row's terms in ascending partner gid (inactive = +0), in
+// chunks of GC = 16 consecutive terms summed left to right; the chunk sums of each group of 32
+// chunks (512 terms) combined by the adjacent-pairwise tree; the group results summed left to
+// right.  A row of <= GC entries (classes 0-1, most rows) is one chunk: a plain left-to-right sum.
+// Short rows: the concatenation of the batch's short rows is evaluated flattened across the
+// lanes (CH entries per chunk, NB independent row/partner loads per lane in flight, terms parked
+// in shared memory), then every lane sums its own row from shared memory.  Longer rows: every
+// lane walks its own row (below).
+// Returns whether the lane's editable stays awake.
+constexpr int GC = 16;            // terms per chunk of the summation order (R14)
+constexpr uint32_t SHORT = GC;    // rows of one chunk take the flattened path (classes 0-1)
+
 template <bool TAIL>
+__device__ __forceinline__ void add_term(const Term& tm, uint32_t ent, K3Ctx& k, float& cx, float& cy, float& cz,
+                                         bool& act) {
+    if (ent & ENT_UPPER) {  // each pair counted once, at its lower-gid endpoint
+        if (tm.kind) {
+            k.cn[0]++;
+            lfx_add<PGD_THREADS>(k.lim, (double)tm.ee * (double)tm.ee);
+        }
+        if (tm.viol) k.cn[PGD_THREADS]++;
+    }
+    act |= tm.kind != 0;
+    cx = __fadd_rn(cx, tm.px);
+    cy = __fadd_rn(cy, tm.py);
+    cz = __fadd_rn(cz, tm.pz);
+}
+
+// KIND: 0 = every item has a short row (k_pgd<0>), 1 = every item a long row (k_pgd<1>), 2 = mixed
+// (k_tail) -- the two grid kernels keep their own register budgets
+template <bool TAIL, int KIND>
 __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const uint32_t e, const bool valid) {
     const Th& th = a.t;
     WarpSh& ws = *k.ws;
@@ -339,29 +366,26 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
         k.wk_n += len;
         k.cn[4 * PGD_THREADS]++;
     }
-    uint32_t off = len;  // exclusive scan of the row lengths over the warp
+    const bool lng = KIND == 1 ? true : (KIND == 0 ? false : len > SHORT);
+    const unsigned lmask = __ballot_sync(0xffffffffu, lng);
+    const uint32_t slen = lng ? 0u : len;
+    uint32_t off = slen;  // exclusive scan of the short row lengths over the warp
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t v = __shfl_up_sync(0xffffffffu, off, o);
         if (lane >= o) off += v;
     }
     const uint32_t T = __shfl_sync(0xffffffffu, off, 31);
-    off -= len;
+    off -= slen;
     ws.off[lane] = off;
     ws.k0[lane] = k0;
     ws.p[lane] = p;
     __syncwarp();
     bool any_active = false;
     float gx = 0.0f, gy = 0.0f, gz = 0.0f;
-    int whole_last = -1;  // the last chunk's single owner (-1: owners in ws.seg)
-    for (uint32_t c = 0; c < T; c += CH) {
-        // this lane's own row inside the chunk: mark which lane owns each position (unless one
-        // row covers the whole chunk, the long-row case)
-        const uint32_t f0 = max(off, c), f1 = min(off + len, c + CH);
-        const unsigned cover = __ballot_sync(0xffffffffu, f0 == c && f1 == min(c + CH, T) && f1 > f0);
-        const int whole = cover ? __ffs(cover) - 1 : -1;
-        whole_last = whole;
-        if (whole < 0)
-            for (uint32_t f = f0; f < f1; f++) ws.seg[f - c] = (unsigned char)lane;
+    for (uint32_t c = 0; c < (KIND == 1 ? 0u : T); c += CH) {
+        // which lane owns each position of this chunk
+        const uint32_t f0 = max(off, c), f1 = min(off + slen, c + CH);
+        for (uint32_t f = f0; f < f1; f++) ws.seg[f - c] = (unsigned char)lane;
         __syncwarp();
         uint32_t ent[NB];
         int sg[NB];
@@ -371,7 +395,7 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
             sg[j] = -1;
             ent[j] = 0u;
             if (f < T) {
-                const int o = whole >= 0 ? whole : ws.seg[f - c];
+                const int o = ws.seg[f - c];
                 sg[j] = o;
                 ent[j] = a.rows[ws.k0[o] + (f - ws.off[o])];
             }
@@ -396,9 +420,9 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
             }
         }
         __syncwarp();
-        // own row, in row order (R14).  Branch-free: an inactive term is (+0, +0, +0) and a
-        // coincident one (+-2e, +0, +0); g + 0 == g exactly since g is never -0 (it starts at
-        // +0 and x + (-x) rounds to +0).  Loads of 4 terms are issued ahead of the sums.
+        // own row, in row order (R14; a short row is one chunk).  Branch-free: an inactive term
+        // is (+0, +0, +0) and a coincident one (+-2e, +0, +0); g + 0 == g exactly since g is
+        // never -0.  Loads of 4 terms are issued ahead of the sums.
         uint32_t f = f0;
         for (; f + 4 <= f1; f += 4) {
             float4 u[4];
@@ -421,6 +445,84 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
         }
         __syncwarp();
     }
+
+    // long rows (> SHORT entries, halo cores): every lane walks its OWN row (a class-3 batch has
+    // 32 rows of similar length), 4 row/partner loads in flight, terms accumulated in registers:
+    // chunk sums of GC terms, the adjacent-pairwise tree over each group of 32 chunk sums kept
+    // as a binary counter (pending left operands by level), group results summed in order.
+    if (KIND != 0 && lng) {
+        float Gx = 0.0f, Gy = 0.0f, Gz = 0.0f;
+        float px[5], py[5], pz[5];  // pending left operands of the tree, by level
+        bool act = false;
+        for (uint32_t g0 = 0; g0 < len; g0 += 32u * GC) {
+            const uint32_t g1 = min(len, g0 + 32u * GC);
+            uint32_t m = 0;  // chunks of this group completed
+            for (uint32_t c0 = g0; c0 < g1; c0 += GC, m++) {
+                const uint32_t c1 = min(c0 + GC, g1);
+                float cx = 0.0f, cy = 0.0f, cz = 0.0f;
+                uint32_t f = c0;
+                for (; f + 4 <= c1; f += 4) {
+                    uint32_t en[4];
+                    float4 q[4];
+#pragma unroll
+                    for (int j = 0; j < 4; j++) en[j] = a.rows[k0 + f + j];
+#pragma unroll
+                    for (int j = 0; j < 4; j++) q[j] = ldpos<TAIL>(k.src + (en[j] & ENT_IDX));
+#pragma unroll
+                    for (int j = 0; j < 4; j++) add_term<TAIL>(pair_term(p, q[j], en[j], th), en[j], k, cx, cy, cz, act);
+                }
+                for (; f < c1; f++) {
+                    const uint32_t en = a.rows[k0 + f];
+                    add_term<TAIL>(pair_term(p, ldpos<TAIL>(k.src + (en & ENT_IDX)), en, th), en, k, cx, cy, cz, act);
+                }
+                // chunk m completes: right child at each level whose bit of m is set
+#pragma unroll
+                for (int L = 0; L < 5; L++) {
+                    if ((m >> L) & 1u) {
+                        cx = __fadd_rn(px[L], cx);
+                        cy = __fadd_rn(py[L], cy);
+                        cz = __fadd_rn(pz[L], cz);
+                    } else {
+                        px[L] = cx;
+                        py[L] = cy;
+                        pz[L] = cz;
+                        break;
+                    }
+                }
+                if (m == 31u) {  // a full group: the tree's root is (cx, cy, cz)
+                    Gx = __fadd_rn(Gx, cx);
+                    Gy = __fadd_rn(Gy, cy);
+                    Gz = __fadd_rn(Gz, cz);
+                }
+            }
+            if (m < 32u) {  // partial group: pending left operands, lowest level first (zero padding)
+                bool have = false;
+                float ax = 0.0f, ay = 0.0f, az = 0.0f;
+#pragma unroll
+                for (int L = 0; L < 5; L++) {
+                    if ((m >> L) & 1u) {
+                        if (have) {
+                            ax = __fadd_rn(px[L], ax);
+                            ay = __fadd_rn(py[L], ay);
+                            az = __fadd_rn(pz[L], az);
+                        } else {
+                            ax = px[L];
+                            ay = py[L];
+                            az = pz[L];
+                            have = true;
+                        }
+                    }
+                }
+                Gx = __fadd_rn(Gx, ax);
+                Gy = __fadd_rn(Gy, ay);
+                Gz = __fadd_rn(Gz, az);
+            }
+        }
+        gx = Gx;
+        gy = Gy;
+        gz = Gz;
+        any_active = act;
+    }
     int flags = 0;
     bool awake = false;
     if (valid && !a.count_only) {
@@ -435,21 +537,23 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
         }
     }
     if (TAIL || k.build) {  // a mover touches its owned partners for t+1
-        unsigned mv = __ballot_sync(0xffffffffu, (flags & 1) != 0);
-        if (mv && T <= CH) {  // the batch's entries are still staged: each lane touches its own
-            for (uint32_t f = lane; f < T; f += 32u) {
-                {
-                    const int o = whole_last >= 0 ? whole_last : ws.seg[f];
+        const unsigned mv_all = __ballot_sync(0xffffffffu, (flags & 1) != 0);
+        unsigned mv = mv_all & lmask;  // long rows: the warp walks the row
+        if (KIND != 1 && (mv_all & ~lmask)) {
+            if (T <= CH) {  // the short rows' entries are still staged: each lane touches its own
+                for (uint32_t f = lane; f < T; f += 32u) {
+                    const int o = ws.seg[f];
                     const uint32_t jj = ws.ent[f];
-                    if (((mv >> o) & 1u) && jj < a.E) {
+                    if (((mv_all >> o) & 1u) && jj < a.E) {
                         if (TAIL) tail_push(k, jj);
                         else atomicOr(&k.unext[jj >> 5], 1u << (jj & 31));  // fire-and-forget (RED)
                     }
                 }
+            } else {
+                mv |= mv_all & ~lmask;
             }
-            mv = 0u;
         }
-        while (mv) {  // longer batches: the warp walks each mover's row
+        while (mv) {
             const int sl = __ffs(mv) - 1;
             mv &= mv - 1;
             const unsigned long long kb = __shfl_sync(0xffffffffu, k0, sl);
@@ -488,15 +592,20 @@ __device__ void k3_finish(const PgdArgs& a, Ctl* ctl, int t, const unsigned long
     ctl->active = tu;
     ctl->violated = tv;
     ctl->loss = td;
+    ctl->loss_le = lfx_le(tot + 2, a.eps_loss) ? 1 : 0;
     ctl->ticket = 0;
     ctl->nsel = 0u;  // consumed (k_select of the next iteration refills it)
+    ctl->nsel_l = 0u;
     if (!a.count_only && a.trace_s && t >= 1 && t <= a.t_max) {
-        long long* ts = a.trace_s + 5 * (t - 1);
+        long long* ts = a.trace_s + 6 * (t - 1);
         ts[0] = (long long)tot[LFX_STATS + 2];
         ts[1] = (long long)tot[LFX_STATS];
         ts[2] = (long long)tot[LFX_STATS + 1];
         ts[3] = (long long)tot[LFX_STATS + 3];
         ts[4] = (long long)tot[LFX_STATS + 4];
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        ts[5] = (long long)gt;  // device time (ns) at the end of iteration t
     }
     if (a.frontier && !a.count_only) {
         ctl->sel = build ? 1 : 0;
@@ -510,7 +619,7 @@ __device__ void k3_finish(const PgdArgs& a, Ctl* ctl, int t, const unsigned long
             a.trace_l[t - 1] = td;
             a.trace_v[t - 1] = (long long)tv;
         }
-        if (stop_rule(a.stop_mode, tu, td, tv, a.eps_loss)) {
+        if (stop_rule(a.stop_mode, tu, ctl->loss_le != 0, tv)) {
             ctl->done = 1;
             ctl->t_res = t - 1;  // the state this launch read
             ctl->converged = 1;
@@ -522,7 +631,11 @@ __device__ void k3_finish(const PgdArgs& a, Ctl* ctl, int t, const unsigned long
     }
 }
 
-__global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
+// One PGD iteration over the editables of one row class: MODE 0 the short rows (<= SHORT entries,
+// editables [0, e_short)), MODE 1 the long rows ([e_short, E)); the two launches run back to back
+// in each iteration and MODE 1's last block applies the stop rule to both launches' statistics.
+template <int MODE>
+__global__ void __launch_bounds__(PGD_THREADS, MODE == 0 ? 4 : 3) k_pgd(PgdArgs a) {
     Ctl* ctl = a.ctl;
     if (!a.count_only && *((volatile int*)&ctl->done)) return;
     const int t = a.count_only ? 0 : ctl->t + 1;
@@ -561,7 +674,10 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
     k.ws = &wsh[w];
     k.lane = lane;
     k.wk_e = k.wk_n = 0ull;
-    const uint32_t n_items = select ? ctl->nsel : a.E;
+    // items: dense sweep = the class's editable range; selected = its segment of the list built
+    // by k_select (short rows from slist[0], long rows from slist[e_short])
+    const uint32_t base = MODE == 0 ? 0u : a.e_short;
+    const uint32_t n_items = select ? (MODE == 0 ? ctl->nsel : ctl->nsel_l) : (MODE == 0 ? a.e_short : a.E - a.e_short);
     // a block without items (small frontier) only takes part in the final ticket
     const bool idle = blockIdx.x * (uint32_t)PGD_THREADS >= n_items;
     if (!idle) {
@@ -578,8 +694,8 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
     for (uint32_t b0 = gw * 32u; b0 < n_items; b0 += nwarps * 32u) {
         const uint32_t kk = b0 + lane;
         const bool valid = kk < n_items;
-        const uint32_t e = valid ? (select ? a.slist[kk] : kk) : 0xFFFFFFFFu;
-        const bool awake = process_batch<false>(a, k, valid ? e : 0u, valid);
+        const uint32_t e = valid ? (select ? a.slist[base + kk] : base + kk) : 0xFFFFFFFFu;
+        const bool awake = process_batch<false, MODE>(a, k, valid ? e : 0u, valid);
         if (k.build) {  // awake bits for t+1, one atomic per distinct word of the batch
             const uint32_t word = e >> 5;
             const unsigned peers = __match_any_sync(0xffffffffu, word);
@@ -607,6 +723,7 @@ __global__ void __launch_bounds__(PGD_THREADS, 4) k_pgd(PgdArgs a) {
         const unsigned long long v = block_stat(s, lane, lim_sh, cn_sh);
         if (lane == 0 && v) atomicAdd(&ctl->acc[s], v);
     }
+    if (MODE == 0) return;  // the long-row launch that follows finishes the iteration
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -666,7 +783,8 @@ __global__ void __launch_bounds__(PGD_THREADS, 1) k_tail(PgdArgs a) {
     Ctl* ctl = a.ctl;
     // every block reads the same entry state: nothing changes it before the first barrier
     if (!a.frontier || a.red || a.count_only || !a.tlist) return;
-    if (*((volatile int*)&ctl->done) || !ctl->sel || ctl->nsel > TAIL_ENTER) return;
+    if (*((volatile int*)&ctl->done) || !ctl->sel || ctl->nsel + ctl->nsel_l > TAIL_ENTER) return;
+    const uint32_t ns0 = ctl->nsel;  // k_select's list: short rows at slist[0], long at slist[e_short]
     __shared__ unsigned long long lim_sh[6][PGD_THREADS];
     __shared__ uint32_t cn_sh[NSTAT - 6][PGD_THREADS];
     __shared__ WarpSh wsh[PGD_THREADS / 32];
@@ -682,7 +800,7 @@ __global__ void __launch_bounds__(PGD_THREADS, 1) k_tail(PgdArgs a) {
     k.lane = lane;
     k.wk_e = k.wk_n = 0ull;
     const uint32_t* cur = a.slist;
-    uint32_t n_cur = ctl->nsel;
+    uint32_t n_cur = ctl->nsel + ctl->nsel_l;
     int t = ctl->t + 1;
     const uint32_t nwarps = gridDim.x * (PGD_THREADS / 32), gw = blockIdx.x * (PGD_THREADS / 32) + w;
     const uint32_t gt = blockIdx.x * PGD_THREADS + threadIdx.x, gs = gridDim.x * PGD_THREADS;
@@ -704,8 +822,10 @@ __global__ void __launch_bounds__(PGD_THREADS, 1) k_tail(PgdArgs a) {
         for (uint32_t bt = gw; bt < nbatch; bt += nwarps) {
             const uint32_t kk = bt * gi + lane;
             const bool valid = lane < (int)gi && kk < n_cur;
-            const uint32_t e = valid ? __ldcg(cur + kk) : 0u;
-            const bool awake = process_batch<true>(a, k, e, valid);
+            const uint32_t e = !valid ? 0u
+                               : (cur != a.slist ? __ldcg(cur + kk)
+                                                 : (kk < ns0 ? __ldcg(cur + kk) : __ldcg(cur + a.e_short + (kk - ns0))));
+            const bool awake = process_batch<true, 2>(a, k, e, valid);
             if (valid && awake) tail_push(k, e);
         }
         __syncthreads();
@@ -783,13 +903,20 @@ __global__ void __launch_bounds__(PGD_THREADS) k_select(PgdArgs a) {
     if (!ctl->sel) return;
     const uint32_t* __restrict__ acur = a.abits + (size_t)(t & 1) * nw32;
     const uint32_t* __restrict__ ucur = a.ubits + (size_t)(t % 3) * nw32;
+    // short-row editables (index < e_short) go to slist[0 ..), long-row ones to slist[e_short ..):
+    // the two k_pgd launches each read their own segment.  Per-thread counts are packed as
+    // short | long << 16 (a block-step holds at most 8192 editables) and scanned together.
     __shared__ uint32_t wsum[PGD_THREADS / 32];
-    __shared__ uint32_t bbase;
+    __shared__ uint32_t bbase_s, bbase_l;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (uint32_t w0 = blockIdx.x * blockDim.x; w0 < nw32; w0 += gs) {  // block-uniform loop
         const uint32_t wi = w0 + threadIdx.x;
         const uint32_t mask = wi < nw32 ? (acur[wi] | ucur[wi]) : 0u;
-        const uint32_t cnt = __popc(mask);
+        const uint32_t lo = wi * 32u;
+        const uint32_t smask = lo + 32u <= a.e_short ? mask
+                               : (lo >= a.e_short ? 0u : mask & ((1u << (a.e_short - lo)) - 1u));
+        const uint32_t lmask = mask & ~smask;
+        const uint32_t cnt = (uint32_t)__popc(smask) | ((uint32_t)__popc(lmask) << 16);
         uint32_t pre = cnt;
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t v = __shfl_up_sync(0xffffffffu, pre, o);
@@ -804,11 +931,14 @@ __global__ void __launch_bounds__(PGD_THREADS) k_select(PgdArgs a) {
                 wsum[k] = tot;
                 tot += v;
             }
-            bbase = tot ? atomicAdd(&ctl->nsel, tot) : 0u;
+            bbase_s = (tot & 0xFFFFu) ? atomicAdd(&ctl->nsel, tot & 0xFFFFu) : 0u;
+            bbase_l = (tot >> 16) ? atomicAdd(&ctl->nsel_l, tot >> 16) : 0u;
         }
         __syncthreads();
-        uint32_t pos = bbase + wsum[w] + pre - cnt;
-        for (uint32_t m = mask; m; m &= m - 1) a.slist[pos++] = wi * 32u + (uint32_t)(__ffs(m) - 1);
+        const uint32_t ex = wsum[w] + pre - cnt;
+        uint32_t ps = bbase_s + (ex & 0xFFFFu), pl = a.e_short + bbase_l + (ex >> 16);
+        for (uint32_t m = smask; m; m &= m - 1) a.slist[ps++] = lo + (uint32_t)(__ffs(m) - 1);
+        for (uint32_t m = lmask; m; m &= m - 1) a.slist[pl++] = lo + (uint32_t)(__ffs(m) - 1);
         __syncthreads();
     }
 }
@@ -827,6 +957,7 @@ __global__ void k_ctl_reset(Ctl* ctl) {
     ctl->sel = 0;
     ctl->bld = 0;
     ctl->nsel = 0u;
+    ctl->nsel_l = 0u;
     ctl->tail_nn = 0u;
     ctl->tail_ncur = 0u;
     ctl->tail_go = 0;
@@ -876,7 +1007,7 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.rowptr = reinterpret_cast<const unsigned long long*>(c->rowptr.p);
     a.rows = c->rows.p;
     a.origE = c->origE.p;
-    a.e_short = (uint32_t)(c->E_cls[0] + c->E_cls[1] + c->E_cls[2]);
+    a.e_short = (uint32_t)(c->E_cls[0] + c->E_cls[1]);  // rows <= 16 entries (one chunk)
     a.pos0 = c->posA.p;
     a.pos1 = c->posB.p;
     a.mom = c->mom.p;
@@ -935,8 +1066,9 @@ int pgd_blocks(int64_t E) {
 
 const float4* pgd_result(cc_ctx* c) { return (c->last_iters & 1) ? c->posB.p : c->posA.p; }
 
-// (active, loss, violated) of the count-only pass just enqueued, summed over ranks (synchronising)
-static cc_status global_check(cc_ctx* c, double* al) {
+// (active, loss, violated) of the count-only pass just enqueued, summed over ranks
+// (synchronising); *loss_le = L_tight <= eps_L decided exactly on the integer limbs
+static cc_status global_check(cc_ctx* c, double* al, bool* loss_le = nullptr) {
     if (c->nranks > 1) {
         CC_TRY(dist_allreduce_u64(c, c->red.p, LFX_STATS));
         CC_CUDA(c, cudaMemcpyAsync(c->h_red, c->red.p, LFX_STATS * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -945,12 +1077,14 @@ static cc_status global_check(cc_ctx* c, double* al) {
         al[0] = (double)c->h_red[0];
         al[1] = lfx_value(c->h_red + 2);
         al[2] = (double)c->h_red[1];
+        if (loss_le) *loss_le = lfx_le(c->h_red + 2, c->p.eps_loss);
     } else {
         CC_CUDA(c, cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
         CC_CUDA(c, cudaStreamSynchronize(c->stream));
         al[0] = (double)c->h_ctl->active;
         al[1] = c->h_ctl->loss;
         al[2] = (double)c->h_ctl->violated;
+        if (loss_le) *loss_le = c->h_ctl->loss_le != 0;
     }
     return CC_OK;
 }
@@ -964,12 +1098,9 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     CC_TRY(cc_ensure(c, c->trace_a, (size_t)tmax + 1, "trace"));
     CC_TRY(cc_ensure(c, c->trace_l, (size_t)tmax + 1, "trace"));
     CC_TRY(cc_ensure(c, c->trace_v, (size_t)tmax + 1, "trace"));
-    CC_TRY(cc_ensure(c, c->trace_s, 5 * ((size_t)tmax + 1), "trace"));
+    CC_TRY(cc_ensure(c, c->trace_s, 6 * ((size_t)tmax + 1), "trace"));
     if (c->nranks > 1) CC_TRY(cc_ensure(c, c->red, LFX_STATS, "allreduce buffer"));
-    if (!c->k3work.p) {
-        CC_TRY(cc_ensure(c, c->k3work, 2, "K3 work counters"));
-        CC_CUDA(c, cudaMemsetAsync(c->k3work.p, 0, 2 * sizeof(unsigned long long), c->stream));
-    }
+    if (!work_counters(c)) return cc_fail(c, CC_E_OOM, "work counters");
     CC_TRY(cc_ensure(c, c->frozen, (size_t)std::max<int64_t>(E, 1), "frontier state"));
     const size_t nwords = (size_t)((std::max<int64_t>(E, 1) + 31) / 32);
     CC_TRY(cc_ensure(c, c->fbits, 7 * nwords, "frontier bitmaps"));
@@ -1003,20 +1134,29 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     }
     CCL(c, k_ctl_reset<<<1, 1, 0, c->stream>>>(c->ctl.p));
     const int nb = pgd_blocks(E);
+    const int64_t e_short = c->E_cls[0] + c->E_cls[1];
+    const int nb0 = pgd_blocks(e_short), nb1 = pgd_blocks(E - e_short);  // short / long-row launches
     const int batch = c->p.graph_batch > 0 ? c->p.graph_batch : 16;
     // k_tail (single GPU; CC_NO_TAIL=1 disables it, a diagnostic)
     const bool use_tail = c->nranks == 1 && !(std::getenv("CC_NO_TAIL") && std::getenv("CC_NO_TAIL")[0] == '1');
-    const int k3_per_iter = use_tail ? 3 : 2;  // k_select (+ k_tail) + k_pgd
-    int tail_blocks = TAIL_BLOCKS;  // co-resident: at most one per SM
+    
+    // k_tail's blocks wait on each other (grid barrier): it is a COOPERATIVE launch, so the
+    // driver guarantees co-residency or rejects it; the count is clamped to what the occupancy
+    // calculator says fits
+    int tail_blocks = TAIL_BLOCKS;
     {
-        int sms = 0;
+        int sms = 0, per_sm = 0;
         CC_CUDA(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-        if (sms > 0 && sms < tail_blocks) tail_blocks = sms;
+        CC_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail, PGD_THREADS, 0));
+        tail_blocks = std::min<int>(tail_blocks, std::max(sms, 1) * std::max(per_sm, 0));
     }
+    const bool tail_on = use_tail && tail_blocks > 0;
+    const int k3_per_iter = tail_on ? 4 : 3;  // k_select (+ k_tail) + k_pgd<0> + k_pgd<1>
     PgdArgs a = make_args(c, 0);
     // initial statistics of P_hat^(0) for the report
     PgdArgs a0 = make_args(c, 1);
-    CCL(c, k_pgd<<<nb, PGD_THREADS, 0, c->stream>>>(a0));
+    CCL(c, k_pgd<0><<<nb0, PGD_THREADS, 0, c->stream>>>(a0));
+    CCL(c, k_pgd<1><<<nb1, PGD_THREADS, 0, c->stream>>>(a0));
     CC_CUDA(c, cudaGetLastError());
     {
         double al[3];
@@ -1033,7 +1173,23 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     CC_CUDA(c, cudaStreamSynchronize(c->stream));  // the source is a host field
 
     int iters = 0;
-    if (tmax > 0) {
+    if (tmax > 0 && c->vgroup) {
+        // virtual ranks (comm.cu): the exchange is host-matched across the group's threads, so
+        // no graph -- every iteration is launched directly and the global stop is read back
+        for (;;) {
+            CCL(c, k_select<<<nb, PGD_THREADS, 0, c->stream>>>(a));
+            CCL(c, k_pgd<0><<<nb0, PGD_THREADS, 0, c->stream>>>(a));
+            CCL(c, k_pgd<1><<<nb1, PGD_THREADS, 0, c->stream>>>(a));
+            CC_TRY(dist_iter_tail(c, c->posA.p, c->posB.p));
+            CC_CUDA(c, cudaGetLastError());
+            CC_CUDA(c, cudaMemcpyAsync(c->h_ctl, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
+            CC_CUDA(c, cudaStreamSynchronize(c->stream));
+            if (c->h_ctl->done) {
+                iters = c->h_ctl->t_res;
+                break;
+            }
+        }
+    } else if (tmax > 0) {
         // (re)capture a graph of `batch` iterations, each bracketed by event records
         // the graph bakes in every argument of k_pgd: re-capture when any of them changed
         // signature: every byte k_pgd and the multi-GPU tail bake in
@@ -1044,8 +1200,10 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
         };
         put(&a, sizeof(a));
         put(&nb, sizeof(nb));
+        put(&nb0, sizeof(nb0));
+        put(&nb1, sizeof(nb1));
         put(&batch, sizeof(batch));
-        put(&use_tail, sizeof(use_tail));
+        put(&tail_on, sizeof(tail_on));
         if (c->nranks > 1) {
             for (int d = 0; d < 2; d++) {
                 const void* ptrs[4] = {c->send_e[d].p, c->recv_e[d].p, c->rsb[d].p, c->rrb[d].p};
@@ -1078,8 +1236,27 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
             for (int k = 0; k < batch; k++) {
                 if (c->p.profile) cudaEventRecordWithFlags(c->graph_ev[2 * k], c->stream, cudaEventRecordExternal);
                 CCL(c, k_select<<<nb, PGD_THREADS, 0, c->stream>>>(a));
-                if (use_tail) CCL(c, k_tail<<<tail_blocks, PGD_THREADS, 0, c->stream>>>(a));
-                CCL(c, k_pgd<<<nb, PGD_THREADS, 0, c->stream>>>(a));
+                if (tail_on) {
+                    cudaLaunchConfig_t cfg = {};
+                    cfg.gridDim = dim3((unsigned)tail_blocks);
+                    cfg.blockDim = dim3(PGD_THREADS);
+                    cfg.stream = c->stream;
+                    cudaLaunchAttribute attr[1];
+                    attr[0].id = cudaLaunchAttributeCooperative;
+                    attr[0].val.cooperative = 1;
+                    cfg.attrs = attr;
+                    cfg.numAttrs = 1;
+                    const cudaError_t le = cudaLaunchKernelEx(&cfg, k_tail, a);
+                    if (le != cudaSuccess) {
+                        cudaGraph_t g2 = nullptr;
+                        cudaStreamEndCapture(c->stream, &g2);
+                        if (g2) cudaGraphDestroy(g2);
+                        return cc_cuda_check(c, le, "cooperative k_tail launch");
+                    }
+                    c->launches++;
+                }
+                CCL(c, k_pgd<0><<<nb0, PGD_THREADS, 0, c->stream>>>(a));
+                CCL(c, k_pgd<1><<<nb1, PGD_THREADS, 0, c->stream>>>(a));
                 if (c->p.profile)
                     cudaEventRecordWithFlags(c->graph_ev[2 * k + 1], c->stream, cudaEventRecordExternal);
                 if (c->nranks > 1) {
@@ -1139,17 +1316,18 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     CC_CUDA(c, cudaMemcpyAsync(&c->ctl.p->t_res, &c->h_ctl->t_res, sizeof(int), cudaMemcpyHostToDevice, c->stream));
     PgdArgs af = make_args(c, 1);
     int tok = cc_prof_begin(c, "K3_final_check");
-    CCL(c, k_pgd<<<nb, PGD_THREADS, 0, c->stream>>>(af));
+    CCL(c, k_pgd<0><<<nb0, PGD_THREADS, 0, c->stream>>>(af));
+    CCL(c, k_pgd<1><<<nb1, PGD_THREADS, 0, c->stream>>>(af));
     cc_prof_end(c, tok);
     CC_CUDA(c, cudaGetLastError());
     double al[3];
-    CC_TRY(global_check(c, al));
+    bool le = false;
+    CC_TRY(global_check(c, al, &le));
     info->iterations = iters;
     info->active_final = (int64_t)al[0];
     info->loss_final = al[1];
     info->violated_final = (int64_t)al[2];
-    info->converged = stop_rule(c->p.stop_mode, (unsigned long long)al[0], al[1], (unsigned long long)al[2],
-                                c->p.eps_loss) ||
+    info->converged = stop_rule(c->p.stop_mode, (unsigned long long)al[0], le, (unsigned long long)al[2]) ||
                       (c->p.stop_mode == CC_STOP_NONE && al[0] == 0.0);
     c->final_active = (unsigned long long)al[0];
     c->final_loss = al[1];

@@ -21,7 +21,7 @@ if len(sys.argv) > 2:  # xi_rel override
 REPS = int(os.environ.get("SCHED_REPS", "2"))
 dev = torch.device("cuda", 0)
 arrs = synth.make(w, device=dev)
-p = cc.Params(box=w.L, b=w.linking_length, xi=w.xi, t_max=10000, stop_mode=cc.STOP_RESTORED, profile=1)
+p = cc.Params(box=w.L, b=w.linking_length, xi=w.xi, t_max=int(os.environ.get("CC_TMAX", "10000")), stop_mode=cc.STOP_RESTORED, profile=1)
 c = cc.Corrector(p)
 for rep in range(REPS):
     c.build_cells(*arrs)
