@@ -149,24 +149,44 @@ def _oracle_child(spec: str) -> int:
     return 0
 
 
-def cpu_baseline(w: synth.Workload, target_s: float = 15.0, n_sample=None):
-    """Oracle on the host cores (1 thread), a sample sized to ~target_s of CPU work."""
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
+
+
+def calibrated_sample(w: synth.Workload, target_s: float = 12.0, n_sample=None):
+    """The bounded oracle sample of a workload, shared by cpu_baseline and --impl reference (the
+    same N in both): start at 50,000 particles of the same recipe and
+    density, then scale N so the oracle's S1-S5 takes ~target_s (at most 4M particles).
+    Returns (sample workload, its first timing) or (sample, None) on timeout."""
     n0 = n_sample or 50_000
     ws = oracle_sample(w, n0)
-    r = run_oracle(ws, timeout=4 * target_s)
-    if r is None:
-        return {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle",
-                "sample": f"{w.name} recipe at N={n0}: oracle did not finish within {4 * target_s:.0f} s"}
-    if n_sample is None and r[0] < target_s / 3:
+    r = run_oracle(ws, timeout=6 * target_s)
+    if n_sample is None and r is not None and r[0] < target_s / 3:
         n1 = int(min(n0 * target_s / max(r[0], 1e-3), 4_000_000))
         ws1 = oracle_sample(w, n1)
-        r1 = run_oracle(ws1, timeout=4 * target_s)
+        r1 = run_oracle(ws1, timeout=6 * target_s)
         if r1 is not None:
             ws, r = ws1, r1
+    return ws, r
+
+
+def cpu_baseline(w: synth.Workload, target_s: float = 12.0, n_sample=None):
+    """Oracle on the host cores (1 thread) on the calibrated sample."""
+    ws, r = calibrated_sample(w, target_s, n_sample)
+    if r is None:
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": f"{w.name} recipe at N={ws.n}: oracle did not finish within {6 * target_s:.0f} s"}
     dt, iters, npairs = r
     return {"value": ws.n / dt / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{w.name} recipe at N={ws.n} (box {ws.L:.3f}, same density, b, xi): oracle S1-S5 to the stop "
-                      f"{dt:.2f} s (the metric's t; the S6-S7 check excluded), {iters} iterations, |V|={npairs}",
+                      f"{dt:.2f} s (the metric's t; the S6-S7 check excluded), {iters} iterations, |V|={npairs}; "
+                      f"1 thread of {os.cpu_count()} on {cpu_model()}",
             "seconds": dt, "n": ws.n, "iterations": iters}
 
 
@@ -196,8 +216,8 @@ def reference_arm(args, w, rank):
     """--impl reference: the CPU oracle as it stands, a bounded sample of the workload per step."""
     if rank != 0:
         return 0
-    n_s = args.sample_n or 30_000
-    ws = oracle_sample(w, n_s)
+    ws, _ = calibrated_sample(w, n_sample=args.sample_n)  # the same sample N as cpu_baseline
+    n_s = ws.n
     times, last = [], None
     for k in range(args.warmup + args.steps):
         r = run_oracle(ws, timeout=300)
@@ -211,7 +231,8 @@ def reference_arm(args, w, rank):
     dt = statistics.mean(times)
     v = ws.n / dt / 1e6
     sample = (f"{w.name} recipe at N={ws.n} (box {ws.L:.3f}, same density, b, xi), single-threaded C oracle, "
-              f"S1-S5 to the stop timed (the metric's t; S6-S7 check excluded), {last[1]} iterations, |V|={last[2]}")
+              f"S1-S5 to the stop timed (the metric's t; S6-S7 check excluded), {last[1]} iterations, |V|={last[2]}; "
+              f"1 thread of {os.cpu_count()} on {cpu_model()}")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -355,6 +376,7 @@ def main():
     launches = stats.pop("total_launches", (0.0, 0))[1]
     k3_we = stats.pop("K3_work_editables", (0.0, 0))[1]   # editables updated (frontier skips the rest)
     k3_wn = stats.pop("K3_work_entries", (0.0, 0))[1]     # row entries evaluated
+    tests = {k: stats.pop(k, (0.0, 0))[1] for k in ("K2_count_tests", "K2_fill_tests", "K4_link_tests")}
     E, nent = vp["n_editable"], 2 * vp["n_pairs"]
     if world > 1:  # this rank's share for the per-launch byte count
         E, nent = E / world, nent / world
@@ -398,6 +420,19 @@ def main():
                    "launches": k3[1], "editables_updated_per_launch": k3_we / k3[1],
                    "entries_per_launch": k3_wn / k3[1], "editables_total": E}
 
+    # pair tests per second of K2 (count + fill sweeps) and K4 (FoF link searches) against the
+    # fp32 issue ceiling: 148 SMs x 128 lanes x clock / ~20 instructions per pinned d2 test
+    # (the pair kernels are ALU / latency bound, not HBM bound)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    ceiling = sms * 128 * sm_max * 1e6 / 20.0
+    pair_tests = {}
+    for nm, kcls in (("K2_count", "K2_count"), ("K2_fill", "K2_fill"), ("K4_link", "K4_fof")):
+        nt = tests.get(nm + "_tests", 0)
+        ms = cls_ms.get(kcls, (0.0, 0))[0]
+        if nt and ms > 0:
+            tps = nt / (ms * 1e-3)
+            pair_tests[nm] = {"tests_per_step": nt / args.steps, "tests_per_s": tps, "ceiling_tests_per_s": ceiling,
+                              "frac": tps / ceiling, "kernel_ms_per_step": ms / args.steps}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
@@ -414,6 +449,7 @@ def main():
                    "fof_groups_orig": ng_o, "fof_groups_corr": ng_c, "halos_equal": bool(np.array_equal(h_o, h_c))},
         "roofline": roof, "k3_roofline": k3_roof,
         "kernels_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in cls_ms.items()},
+        "pair_tests": pair_tests,
         "incl_check": {"value": value_incl, "unit": UNIT, "ms_per_step": ms_incl,
                        "what": "S1-S7: + FoF labels on original and corrected positions, halo catalogues, MCC"},
         "gpu_launches": int(launches),

@@ -243,6 +243,18 @@ cc_status cc_edit_decode(cc_ctx* ctx, int64_t n, const float* xh0, const float* 
                          const uint8_t* flags, const int64_t* q, int64_t n_edits, float* xr, float* yr,
                          float* zr);
 
+/* f1 -- m-bit packing of the quantised edits (Alg. 1 line 13 P:433 "quantized to m bits"; reading
+ * R33).  |q| <= 2^m, so every index is an (m+2)-bit two's-complement field; field e
+ * occupies bits [e (m+2), (e+1)(m+2)) of an LSB-first stream of 32-bit words (bit b = bit b % 32 of
+ * word b / 32): ceil(n_edits (m+2) / 32) words, (m+2)/8 bytes per edit.  m = params.m.
+ *   cc_edit_pack:   q (device, n_edits int64) -> words (device, cap_words u32); *n_words_h = words
+ *                   needed (written whatever the status).  CC_E_OOM if cap_words is too small;
+ *                   CC_E_DATA if some |q| > 2^m.  Synchronises.
+ *   cc_edit_unpack: words (device) -> q (device, n_edits int64), sign-extended.  Synchronises. */
+cc_status cc_edit_pack(cc_ctx* ctx, const int64_t* q, int64_t n_edits, uint32_t* words, int64_t cap_words,
+                       int64_t* n_words_h);
+cc_status cc_edit_unpack(cc_ctx* ctx, const uint32_t* words, int64_t n_edits, int64_t* q);
+
 /* S0 thresholds actually used (after cc_build_cells; near_pairs after cc_find_vulnerable), for
  * the boundary tests: every fp32 value is the single rounding of the paper's formula (Alg. 1
  * l.1-3 P:419-421, Eq. 3; readings R2-R8 of DESIGN.md §3).  lo2s/hi2s: the

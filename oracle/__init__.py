@@ -90,6 +90,10 @@ def lib():
                                      C.c_int64, i64p]
         L.oc_edit_decode.argtypes = [C.c_int64, f32p, f32p, f32p, u8p, i64p, C.c_int64, P(Cfg),
                                      f32p, f32p, f32p]
+        L.oc_edit_packed_words.argtypes = [C.c_int64, C.c_int]
+        L.oc_edit_packed_words.restype = C.c_int64
+        L.oc_edit_pack.argtypes = [i64p, C.c_int64, C.c_int, u32p]
+        L.oc_edit_unpack.argtypes = [u32p, C.c_int64, C.c_int, i64p]
         _lib = L
     return _lib
 
@@ -337,6 +341,28 @@ def edit_decode(xh0, yh0, zh0, flags, q, c: Cfg):
     if st:
         raise ValueError(f"oc_edit_decode status {st}")
     return tuple(out)
+
+
+def edit_pack(q, m: int) -> np.ndarray:
+    """(m+2)-bit two's-complement fields, LSB-first in 32-bit words (Alg. 1 l.13, R33)."""
+    q = np.ascontiguousarray(q, np.int64)
+    nw = lib().oc_edit_packed_words(q.size, m)
+    w = np.zeros(max(nw, 1), np.uint32)
+    qq = q if q.size else np.zeros(1, np.int64)
+    st = lib().oc_edit_pack(_ptr(qq, C.c_int64), q.size, m, _ptr(w, C.c_uint32))
+    if st:
+        raise ValueError(f"oc_edit_pack status {st}")
+    return w[:nw]
+
+
+def edit_unpack(words, n_edits: int, m: int) -> np.ndarray:
+    w = np.ascontiguousarray(words, np.uint32)
+    ww = w if w.size else np.zeros(1, np.uint32)
+    q = np.zeros(max(n_edits, 1), np.int64)
+    st = lib().oc_edit_unpack(_ptr(ww, C.c_uint32), n_edits, m, _ptr(q, C.c_int64))
+    if st:
+        raise ValueError(f"oc_edit_unpack status {st}")
+    return q[:n_edits]
 
 
 @dataclass

@@ -860,3 +860,47 @@ int oc_edit_decode(int64_t n, const float* xh0, const float* yh0, const float* z
     }
     return e == n_edits ? 0 : 65;
 }
+
+/* ---------------------------------------------------------------------------------------------
+ * f1 -- m-bit packing of the quantised edits (Alg. 1 line 13, "edits <- non-zero values of
+ * Delta, quantized to m bits"; reading R33).  An edit index q satisfies
+ * |q| <= 2^m (|Delta| <= 2 xi_f on the lattice s = xi_f 2^(1-m), R30), so it is stored as an
+ * (m+2)-bit two's-complement field; field e occupies bits [e (m+2), (e+1)(m+2)) of a stream of
+ * 32-bit words, bit b of the stream = bit (b mod 32) of word b / 32 (LSB first).  Written bit by
+ * bit on purpose (plain and obviously correct).  Returns 0, or 64 for |q| > 2^m / bad m.
+ * ------------------------------------------------------------------------------------------- */
+int64_t oc_edit_packed_words(int64_t n_edits, int m) {
+    return (n_edits * (int64_t)(m + 2) + 31) / 32;
+}
+
+int oc_edit_pack(const int64_t* q, int64_t n_edits, int m, uint32_t* words) {
+    if (m < 2 || m > 40 || n_edits < 0) return 64;
+    const int w = m + 2;
+    const int64_t nw = oc_edit_packed_words(n_edits, m);
+    for (int64_t k = 0; k < nw; k++) words[k] = 0u;
+    const int64_t lim = (int64_t)1 << m;
+    for (int64_t e = 0; e < n_edits; e++) {
+        if (q[e] > lim || q[e] < -lim) return 64;
+        const uint64_t u = (uint64_t)q[e];  /* two's complement, low w bits kept */
+        for (int b = 0; b < w; b++) {
+            const int64_t bit = e * w + b;
+            if ((u >> b) & 1u) words[bit / 32] |= 1u << (bit % 32);
+        }
+    }
+    return 0;
+}
+
+int oc_edit_unpack(const uint32_t* words, int64_t n_edits, int m, int64_t* q) {
+    if (m < 2 || m > 40 || n_edits < 0) return 64;
+    const int w = m + 2;
+    for (int64_t e = 0; e < n_edits; e++) {
+        uint64_t u = 0;
+        for (int b = 0; b < w; b++) {
+            const int64_t bit = e * w + b;
+            u |= (uint64_t)((words[bit / 32] >> (bit % 32)) & 1u) << b;
+        }
+        if ((u >> (w - 1)) & 1u) u |= ~(uint64_t)0 << w;  /* sign extension */
+        q[e] = (int64_t)u;
+    }
+    return 0;
+}

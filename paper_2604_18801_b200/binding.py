@@ -70,7 +70,7 @@ class _Run(C.Structure):
 EXPORTS = ["cc_default_params", "cc_nccl_unique_id", "cc_create", "cc_destroy", "cc_last_error", "cc_build_cells",
            "cc_find_vulnerable", "cc_get_pairs", "cc_correct", "cc_get_trace", "cc_get_schedule", "cc_fof_label", "cc_mcc",
            "cc_halo_sizes", "cc_hmf", "cc_kernel_stats", "cc_run", "cc_edit_encode", "cc_edit_decode",
-           "cc_get_thresholds", "cc_vgroup_create", "cc_vgroup_destroy"]
+           "cc_get_thresholds", "cc_vgroup_create", "cc_vgroup_destroy", "cc_edit_pack", "cc_edit_unpack"]
 
 _lib = None
 
@@ -114,6 +114,8 @@ def lib():
     L.cc_edit_decode.argtypes = [vp, i64, vp, vp, vp, vp, vp, i64, vp, vp, vp]
     L.cc_get_thresholds.argtypes = [vp, P(_Th)]
     L.cc_vgroup_create.argtypes = [C.c_int, P(vp)]
+    L.cc_edit_pack.argtypes = [vp, vp, i64, vp, i64, P(i64)]
+    L.cc_edit_unpack.argtypes = [vp, vp, i64, vp]
     L.cc_vgroup_destroy.argtypes = [vp]
     L.cc_vgroup_destroy.restype = None
     for name in EXPORTS:
@@ -313,6 +315,22 @@ class Corrector:
         self._chk(self.lib.cc_edit_decode(self.h, n, *[_ptr(t) for t in (xh0, yh0, zh0)], _ptr(flags), _ptr(q),
                                           q.shape[0], *[_ptr(t) for t in out]))
         return out
+
+    def edit_pack(self, q):
+        """(m+2)-bit packing of the edit indices (Alg. 1 l.13, R33) -> int32 view of the u32 words."""
+        _check_dev(q, torch.int64, "q")
+        n = q.shape[0]
+        nw = C.c_int64()
+        self._chk(self.lib.cc_edit_pack(self.h, _ptr(q), n, None, 0, C.byref(nw)), ok=(0, 67))
+        words = torch.empty(max(nw.value, 1), dtype=torch.int32, device=q.device)
+        self._chk(self.lib.cc_edit_pack(self.h, _ptr(q), n, _ptr(words), nw.value, C.byref(nw)))
+        return words[: nw.value]
+
+    def edit_unpack(self, words, n_edits: int):
+        _check_dev(words, torch.int32, "words (int32 view of u32)")
+        q = torch.empty(max(n_edits, 1), dtype=torch.int64, device=words.device)
+        self._chk(self.lib.cc_edit_unpack(self.h, _ptr(words), n_edits, _ptr(q)))
+        return q[:n_edits]
 
     # S6
     def fof_label(self, which=CC_ORIG, labels=None):

@@ -226,6 +226,7 @@ static void choose_grid(cc_ctx* c, int64_t n_local, double x_extent, double x0, 
     c->g.ny = c->g.nz = (int)nyz;
     c->g.nx = (int)nx;
     c->g.inv_w = (double)nyz / L;
+    c->g.margin = 2.5 / c->g.inv_w;
     c->g.inv_wx = (double)nx / x_extent;
     c->g.x0 = x0;
     c->g.L = L;

@@ -56,6 +56,7 @@ struct Th {
 struct Grid {
     int nx, ny, nz;
     double inv_w;      // rows per unit length in y and z
+    double margin;     // 2.5 row widths: interior() (host-computed: no fp64 division in kernels)
     double inv_wx;     // x-bins per unit length
     double x0;         // lower x edge of the local grid
     double L;          // box
@@ -508,6 +509,58 @@ __device__ __forceinline__ void for_each_candidate(const Grid& g, const uint32_t
     }
 }
 
+// x-window of one search (identical for every row it visits): at most two segments of local x
+// (the periodic seam splits it on one GPU), each as (first x-bin, last x-bin, key bounds).  The
+// window math (fp64 floor, directed key rounding) is done once per particle, not once per row.
+struct XWin {
+    int n;            // segments (1 or 2)
+    bool up;          // segment 1 is the part above the seam, [0, u + r - L]
+    int ca[2], cb[2]; // first / last x-bin of each segment
+    uint32_t klo[2], khi[2];
+};
+
+__device__ __forceinline__ XWin make_xwin(const Grid& g, double u, double r) {
+    XWin w;
+    double a = u - r, b = u + r, a1 = 0.0, b1 = -1.0;
+    w.up = false;
+    if (g.xwrap) {
+        if (a < 0.0) {
+            a1 = a + g.L;
+            b1 = g.L;
+            a = 0.0;
+        } else if (b >= g.L) {
+            a1 = 0.0;
+            b1 = b - g.L;
+            b = g.L;
+            w.up = true;
+        }
+    } else {
+        if (a < 0.0) a = 0.0;
+        if (b > g.ext_x) b = g.ext_x;
+    }
+    w.n = b1 >= a1 ? 2 : 1;
+    w.ca[0] = cell_coord(a, 0.0, g.inv_wx, g.nx);
+    w.cb[0] = cell_coord(b, 0.0, g.inv_wx, g.nx);
+    w.klo[0] = key_lo(a, g);
+    w.khi[0] = key_hi(b, g);
+    w.ca[1] = cell_coord(a1, 0.0, g.inv_wx, g.nx);
+    w.cb[1] = cell_coord(fmax(b1, a1), 0.0, g.inv_wx, g.nx);
+    w.klo[1] = key_lo(a1, g);
+    w.khi[1] = key_hi(fmax(b1, a1), g);
+    return w;
+}
+
+// visit the slots of one row inside window segment k (j0/j1 = the bin range's slots)
+template <class F>
+__device__ __forceinline__ void scan_seg(const uint32_t* __restrict__ xk, uint32_t j0, uint32_t j1, uint32_t klo,
+                                         uint32_t khi, F& f) {
+    uint32_t j = lower_bound_key(xk, j0, j1, klo);
+    for (; j < j1; j++) {
+        if (xk[j] > khi) break;
+        f(j);
+    }
+}
+
 // Every unordered pair {s, j} within radius r, visited once over all s: the half-shell of rows
 // (own row forward in slot = x order plus the periodic wrap at the row start, then rows
 // (dz=0,dy=+1) and (dz=+1,dy=-1..1)); with fewer than 3 periodic rows on an axis, all 9 rows
@@ -550,11 +603,12 @@ __device__ __forceinline__ void for_each_pair_forward(const Grid& g, const uint3
     }
 }
 
-// per-warp sum of a per-thread counter into a global total (one atomic per warp)
+// per-warp sum of a per-thread counter into a global total (one atomic per warp; callable after
+// an early return of some lanes)
 __device__ __forceinline__ void warp_count(unsigned long long* dst, unsigned v) {
-    unsigned long long x = v;
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if ((threadIdx.x & 31) == 0 && x) atomicAdd(dst, x);
+    const unsigned m = __activemask();
+    const unsigned x = __reduce_add_sync(m, v);
+    if ((threadIdx.x & 31) == (unsigned)(__ffs(m) - 1) && x) atomicAdd(dst, (unsigned long long)x);
 }
 
 // pinned d2 without the minimum image: identical to dist2 whenever no coordinate difference
@@ -572,7 +626,7 @@ __device__ __forceinline__ float dist2_nw(const float4& a, const float4& b) {
 // so min_image is the identity: the particle keeps >= 2.5 w from the periodic faces
 __device__ __forceinline__ bool interior(float x, float y, float z, const Grid& g, const Th& t) {
     if (!t.periodic) return true;
-    const double m = 2.5 / g.inv_w;
+    const double m = g.margin;
     return 4.0 * m < g.L && (double)x >= m && (double)x <= g.L - m && (double)y >= m && (double)y <= g.L - m &&
            (double)z >= m && (double)z <= g.L - m;
 }

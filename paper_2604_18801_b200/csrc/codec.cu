@@ -301,6 +301,43 @@ __global__ void __launch_bounds__(CT) k_edit_apply4(int64_t n, const uint8_t* __
     }
 }
 
+// m-bit packing (R33): field e = bits [e w, (e+1) w) of the LSB-first word stream, w = m + 2,
+// two's complement.  Pack: one thread per output WORD gathers the fields overlapping it (no
+// atomics, coalesced stores); unpack: one thread per edit reads the 2-3 words of its field.
+__global__ void __launch_bounds__(CT) k_edit_pack(int64_t n_edits, int w, long long lim, const long long* __restrict__ q,
+                                                  uint32_t* __restrict__ words, int64_t nw, unsigned int* err) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nw) return;
+    const int64_t b0 = 32 * k;
+    const int64_t e0 = b0 / w, e1 = min((b0 + 31) / w, n_edits - 1);
+    const unsigned long long mask = (w >= 64) ? ~0ull : ((1ull << w) - 1ull);
+    uint32_t word = 0u;
+    for (int64_t e = e0; e <= e1; e++) {
+        const long long v = __ldg(q + e);
+        if (v > lim || v < -lim) atomicOr(err, 4u);
+        const unsigned long long u = (unsigned long long)v & mask;
+        const int64_t sh = e * w - b0;  // field start relative to the word, > -w and < 32
+        word |= sh >= 0 ? (uint32_t)(u << sh) : (uint32_t)(u >> (-sh));
+    }
+    words[k] = word;
+}
+
+__global__ void __launch_bounds__(CT) k_edit_unpack(int64_t n_edits, int w, const uint32_t* __restrict__ words,
+                                                    int64_t nw, long long* __restrict__ q) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n_edits) return;
+    const int64_t bit = e * w, k = bit >> 5;
+    const int off = (int)(bit & 31);
+    const unsigned long long lo = (unsigned long long)__ldg(words + k) |
+                                  (k + 1 < nw ? (unsigned long long)__ldg(words + k + 1) << 32 : 0ull);
+    unsigned long long u = lo >> off;
+    if (off + w > 64 && k + 2 < nw) u |= (unsigned long long)__ldg(words + k + 2) << (64 - off);
+    const unsigned long long mask = (1ull << w) - 1ull;
+    u &= mask;
+    if ((u >> (w - 1)) & 1ull) u |= ~mask;  // sign extension
+    q[e] = (long long)u;
+}
+
 bool aligned4(const void* p) { return ((uintptr_t)p & 3u) == 0; }
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
@@ -394,5 +431,48 @@ cc_status cc_edit_decode(cc_ctx* c, int64_t n, const float* xh0, const float* yh
     CC_CUDA(c, cudaMemcpyAsync(&tot, bsum + nb, sizeof(tot), cudaMemcpyDeviceToHost, c->stream));
     CC_CUDA(c, cudaStreamSynchronize(c->stream));
     if ((int64_t)tot != n_edits) return cc_fail(c, CC_E_DATA, "popcount(flags) != n_edits");
+    return CC_OK;
+}
+
+cc_status cc_edit_pack(cc_ctx* c, const int64_t* q, int64_t n_edits, uint32_t* words, int64_t cap_words,
+                       int64_t* n_words_h) {
+    int64_t nb = 0;
+    CC_TRY(edit_common(c, 0, &nb));
+    if (n_edits < 0 || !n_words_h) return cc_fail(c, CC_E_ARG, "n_edits < 0 or null n_words_h");
+    const int w = c->p.m + 2;
+    const int64_t nw = (n_edits * w + 31) / 32;
+    *n_words_h = nw;
+    if (nw > cap_words) return cc_fail(c, CC_E_OOM, "cap_words < ceil(n_edits (m+2) / 32)");
+    if (nw == 0) return CC_OK;
+    if (!q || !words) return cc_fail(c, CC_E_ARG, "null buffer");
+    CC_TRY(cc_ensure(c, c->codec_bsum, 2, "edit-log flags"));
+    unsigned int* err = reinterpret_cast<unsigned int*>(c->codec_bsum.p);
+    CC_CUDA(c, cudaMemsetAsync(err, 0, sizeof(unsigned int), c->stream));
+    int tok = cc_prof_begin(c, "F1_pack");
+    CCL(c, k_edit_pack<<<(unsigned)((nw + CT - 1) / CT), CT, 0, c->stream>>>(
+               n_edits, w, 1ll << c->p.m, reinterpret_cast<const long long*>(q), words, nw, err));
+    cc_prof_end(c, tok);
+    CC_CUDA(c, cudaGetLastError());
+    unsigned int e = 0;
+    CC_CUDA(c, cudaMemcpyAsync(&e, err, sizeof(e), cudaMemcpyDeviceToHost, c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (e) return cc_fail(c, CC_E_DATA, "an edit index exceeds |q| <= 2^m");
+    return CC_OK;
+}
+
+cc_status cc_edit_unpack(cc_ctx* c, const uint32_t* words, int64_t n_edits, int64_t* q) {
+    int64_t nb = 0;
+    CC_TRY(edit_common(c, 0, &nb));
+    if (n_edits < 0) return cc_fail(c, CC_E_ARG, "n_edits < 0");
+    if (n_edits == 0) return CC_OK;
+    if (!q || !words) return cc_fail(c, CC_E_ARG, "null buffer");
+    const int w = c->p.m + 2;
+    const int64_t nw = (n_edits * w + 31) / 32;
+    int tok = cc_prof_begin(c, "F1_unpack");
+    CCL(c, k_edit_unpack<<<(unsigned)((n_edits + CT - 1) / CT), CT, 0, c->stream>>>(n_edits, w, words, nw,
+                                                                                   reinterpret_cast<long long*>(q)));
+    cc_prof_end(c, tok);
+    CC_CUDA(c, cudaGetLastError());
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
     return CC_OK;
 }

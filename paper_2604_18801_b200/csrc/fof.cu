@@ -34,9 +34,8 @@ __global__ void __launch_bounds__(FOF_THREADS)
 k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ orig4, const uint32_t* __restrict__ xk,
            const uint32_t* __restrict__ cs, Grid g, Th t, double r, float thr2, uint32_t* __restrict__ par,
            unsigned long long* __restrict__ tests) {
-    const int64_t s0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool live = s0 < n;
-    const int64_t s = live ? s0 : n - 1;
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
     unsigned ntest = 0;
     const float4 o = orig4[s];
     const float4 p = P[s];
@@ -46,7 +45,6 @@ k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ o
     const bool periodic_yz = t.periodic != 0;
     uint32_t rs = (uint32_t)s;  // cached ancestor of s (uf_link)
     auto link = [&](uint32_t j) {
-        if (!live) return;
         ntest++;
         const float4 q = P[j];
         if (dist2(p, q, t) <= thr2) uf_link(par, (uint32_t)s, j, rs);

@@ -32,10 +32,9 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
               const uint32_t* __restrict__ xk, const uint32_t* __restrict__ cs, Grid g, Th t, double r, uint32_t n_own,
               uint32_t* __restrict__ deg, uint32_t* __restrict__ par_base, uint2* __restrict__ near,
               unsigned long long* __restrict__ near_n, unsigned long long near_cap, unsigned long long* __restrict__ tests) {
-    const int64_t s0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
     unsigned ntest = 0;  // pair tests (candidates evaluated), reported as tests/s
-    const int64_t s = s0 < n ? s0 : n - 1;  // a tail thread repeats the last particle's search without effects
-    const bool live = s0 < n;
     const bool multi = n_own < (uint32_t)n;
     const bool ghost = multi && __float_as_uint(dec4[s].w) >= n_own;
     const float4 p = orig4[s];
@@ -47,7 +46,6 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
     uint32_t cnt = 0;
     uint32_t rs = (uint32_t)s;  // cached ancestor of s in the stable forest (uf_link)
     auto test = [&](uint32_t j) {
-        if (!live) return;
         ntest++;
         const float4 q = orig4[j];
         const float d2 = inner ? dist2_nw(p, q) : dist2(p, q, t);
@@ -109,9 +107,8 @@ k_pairs_fill(uint32_t e_all, const uint32_t* __restrict__ slotE, const float4* _
              const uint32_t* __restrict__ eidx, uint32_t e_own, const unsigned long long* __restrict__ rowptr,
              uint32_t* __restrict__ cur, uint32_t* __restrict__ rows, uint32_t* __restrict__ par_orig,
              unsigned long long* __restrict__ tests) {
-    const uint32_t e0 = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool live = e0 < e_all;
-    const uint32_t e = live ? e0 : e_all - 1;
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= e_all) return;
     unsigned ntest = 0;
     const uint32_t s = slotE[e];
     const float4 p = orig4[s];
@@ -123,7 +120,6 @@ k_pairs_fill(uint32_t e_all, const uint32_t* __restrict__ slotE, const float4* _
     const bool inner = interior(p.x, p.y, p.z, g, t);
     uint32_t rs = (uint32_t)s;  // cached ancestor of s in the ORIG forest (uf_link)
     auto emit = [&](uint32_t j) {
-        if (!live) return;
         ntest++;
         const float4 q = orig4[j];
         const float d2 = inner ? dist2_nw(p, q) : dist2(p, q, t);
@@ -295,7 +291,7 @@ cc_status pairs_fill(cc_ctx* c) {
         CC_CUDA(c, cudaMemcpyAsync(c->parent_orig.p, c->parent_base.p, (size_t)n * sizeof(uint32_t),
                                    cudaMemcpyDeviceToDevice, c->stream));
     c->orig_valid = true;
-    CC_TRY(cc_ensure(c, c->rows, (size_t)std::max<int64_t>(c->nent, 1), "rows"));
+    CC_TRY(cc_ensure(c, c->rows, (size_t)c->nent + 8, "rows"));  // +8: k_pgd<1> reads whole 16-byte vectors
     if (n > 0 && c->nent > 0) {
         int tok = cc_prof_begin(c, "K2_fill");
         CC_TRY(cc_ensure(c, c->scratch_u32, (size_t)std::max<int64_t>(c->E, 1), "row cursors"));

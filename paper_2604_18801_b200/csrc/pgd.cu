@@ -460,20 +460,30 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
             for (uint32_t c0 = g0; c0 < g1; c0 += GC, m++) {
                 const uint32_t c1 = min(c0 + GC, g1);
                 float cx = 0.0f, cy = 0.0f, cz = 0.0f;
-                uint32_t f = c0;
-                for (; f + 4 <= c1; f += 4) {
+                // row entries as aligned 16-byte vectors (the lanes walk different rows: one L1
+                // wavefront per 4 entries instead of per entry); mis = misalignment of the chunk
+                // start, entries assembled from the previous and the next vector (the row buffer
+                // is padded so the last vector read stays inside it)
+                const unsigned long long A = k0 + c0;
+                const int mis = (int)(A & 3ull);
+                const uint4* R4 = reinterpret_cast<const uint4*>(a.rows) + (A >> 2);
+                uint4 bv = R4[0];
+                for (uint32_t f = c0; f < c1; f += 4) {
+                    const uint4 nv = R4[((f - c0) >> 2) + 1];
                     uint32_t en[4];
+                    en[0] = mis == 0 ? bv.x : mis == 1 ? bv.y : mis == 2 ? bv.z : bv.w;
+                    en[1] = mis == 0 ? bv.y : mis == 1 ? bv.z : mis == 2 ? bv.w : nv.x;
+                    en[2] = mis == 0 ? bv.z : mis == 1 ? bv.w : mis == 2 ? nv.x : nv.y;
+                    en[3] = mis == 0 ? bv.w : mis == 1 ? nv.x : mis == 2 ? nv.y : nv.z;
+                    bv = nv;
+                    const int nvalid = (int)min(4u, c1 - f);
                     float4 q[4];
 #pragma unroll
-                    for (int j = 0; j < 4; j++) en[j] = a.rows[k0 + f + j];
+                    for (int j = 0; j < 4; j++)
+                        if (j < nvalid) q[j] = ldpos<TAIL>(k.src + (en[j] & ENT_IDX));
 #pragma unroll
-                    for (int j = 0; j < 4; j++) q[j] = ldpos<TAIL>(k.src + (en[j] & ENT_IDX));
-#pragma unroll
-                    for (int j = 0; j < 4; j++) add_term<TAIL>(pair_term(p, q[j], en[j], th), en[j], k, cx, cy, cz, act);
-                }
-                for (; f < c1; f++) {
-                    const uint32_t en = a.rows[k0 + f];
-                    add_term<TAIL>(pair_term(p, ldpos<TAIL>(k.src + (en & ENT_IDX)), en, th), en, k, cx, cy, cz, act);
+                    for (int j = 0; j < 4; j++)
+                        if (j < nvalid) add_term<TAIL>(pair_term(p, q[j], en[j], th), en[j], k, cx, cy, cz, act);
                 }
                 // chunk m completes: right child at each level whose bit of m is set
 #pragma unroll
@@ -538,28 +548,35 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
     }
     if (TAIL || k.build) {  // a mover touches its owned partners for t+1
         const unsigned mv_all = __ballot_sync(0xffffffffu, (flags & 1) != 0);
-        unsigned mv = mv_all & lmask;  // long rows: the warp walks the row
-        if (KIND != 1 && (mv_all & ~lmask)) {
-            if (T <= CH) {  // the short rows' entries are still staged: each lane touches its own
-                for (uint32_t f = lane; f < T; f += 32u) {
-                    const int o = ws.seg[f];
-                    const uint32_t jj = ws.ent[f];
-                    if (((mv_all >> o) & 1u) && jj < a.E) {
-                        if (TAIL) tail_push(k, jj);
-                        else atomicOr(&k.unext[jj >> 5], 1u << (jj & 31));  // fire-and-forget (RED)
-                    }
+        // short rows whose entries are still staged (the batch fit one chunk): every lane
+        // touches the staged entries at its positions
+        const bool staged = KIND != 1 && T <= CH;
+        if (staged && (mv_all & ~lmask)) {
+            for (uint32_t f = lane; f < T; f += 32u) {
+                const int o = ws.seg[f];
+                const uint32_t jj = ws.ent[f];
+                if (((mv_all >> o) & 1u) && jj < a.E) {
+                    if (TAIL) tail_push(k, jj);
+                    else atomicOr(&k.unext[jj >> 5], 1u << (jj & 31));  // fire-and-forget (RED)
                 }
-            } else {
-                mv |= mv_all & ~lmask;
             }
         }
-        while (mv) {
-            const int sl = __ffs(mv) - 1;
-            mv &= mv - 1;
-            const unsigned long long kb = __shfl_sync(0xffffffffu, k0, sl);
-            const uint32_t ln = __shfl_sync(0xffffffffu, len, sl);
-            for (uint32_t i = lane; i < ln; i += 32) {
-                const uint32_t j = a.rows[kb + i] & ENT_IDX;
+        // the other movers walk their own rows, all lanes in parallel (4 entries in flight)
+        if ((flags & 1) && (lng || !staged)) {
+            uint32_t i = 0;
+            for (; i + 4 <= len; i += 4) {
+                uint32_t jj[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) jj[q] = a.rows[k0 + i + q] & ENT_IDX;
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    if (jj[q] < a.E) {
+                        if (TAIL) tail_push(k, jj[q]);
+                        else atomicOr(&k.unext[jj[q] >> 5], 1u << (jj[q] & 31));
+                    }
+            }
+            for (; i < len; i++) {
+                const uint32_t j = a.rows[k0 + i] & ENT_IDX;
                 if (j < a.E) {
                     if (TAIL) tail_push(k, j);
                     else atomicOr(&k.unext[j >> 5], 1u << (j & 31));

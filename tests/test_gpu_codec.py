@@ -186,3 +186,40 @@ def test_vector_and_scalar_paths(path, monkeypatch):
     for a in range(3):
         assert np.array_equal(rec[a].cpu().numpy().view(np.uint32), orec[a].view(np.uint32))
     ctx.close()
+
+
+@pytest.mark.parametrize("m", [2, 8, 16, 32, 40])
+def test_edit_pack_bit_exact(m):
+    """cc_edit_pack / cc_edit_unpack (R33): (m+2)-bit fields bit-exact against the oracle's
+    packer, ragged counts (fields straddling 2-3 words), and the round trip."""
+    rng = np.random.default_rng(100 + m)
+    c = cc.Corrector(cc.Params(box=1.0, xi=1e-3, m=m), device=0)
+    for n in (0, 1, 31, 32, 33, 1000, 65537):
+        q = rng.integers(-(2 ** m), 2 ** m + 1, n).astype(np.int64)
+        if n >= 2:
+            q[:2] = [-(2 ** m), 2 ** m]
+        w = c.edit_pack(_dev(q))
+        want = oracle.edit_pack(q, m)
+        assert np.array_equal(w.cpu().numpy().view(np.uint32), want), (m, n)
+        assert np.array_equal(c.edit_unpack(w, n).cpu().numpy(), q)
+    with pytest.raises(cc.CCError):
+        c.edit_pack(_dev(np.array([2 ** m + 1], np.int64)))
+
+
+def test_edit_pack_of_a_correction_matches_oracle():
+    """The packed index stream of a real correction (C1 recipe): GPU encode + pack == oracle
+    encode + pack, (m+2)/8 bytes per edit."""
+    w = synth.Workload("C1", "clumped", 20000, 1.0, 1e-3, seed=1)
+    arrs = [t.numpy() for t in synth.make(w)]
+    p = cc.Params(box=w.L, b=w.linking_length, xi=w.xi)
+    c = cc.Corrector(p, device=0)
+    d = [_dev(a) for a in arrs]
+    c.build_cells(*d)
+    c.find_vulnerable()
+    out, _ = c.correct()
+    fl, q = c.edit_encode(*d, *out)
+    words = c.edit_pack(q)
+    oc = oracle_cfg(p, w.n)
+    of, oq = oracle.edit_encode(*arrs, *[o.cpu().numpy() for o in out], oc)
+    assert np.array_equal(words.cpu().numpy().view(np.uint32), oracle.edit_pack(oq, p.m))
+    assert words.numel() * 4 == (len(oq) * (p.m + 2) + 31) // 32 * 4

@@ -177,3 +177,35 @@ def test_bound_safe_index_near_origin():
         r0 = np.float32(float(Fraction(float(h[i])) + q0 * s))
         plain_bad += abs(Fraction(float(r0)) - Fraction(float(x[i]))) > Fraction(xi_f)
     assert plain_bad > 0
+
+
+# --------------------------------------------------------------------------------------------
+# m-bit packing of the edits (Alg. 1 l.13; reading R33: (m+2)-bit two's-complement fields,
+# LSB first in 32-bit words)
+def test_edit_pack_worked_layout():
+    """Hand-derived: m = 2 -> 4-bit fields; q = 1,-1,3,-4,0,2,-2,4 -> nibbles 1,F,3,C,0,2,E,4 from
+    the least significant end: one word 0x4E20C3F1.  m = 8 -> 10-bit fields straddle words:
+    q = 255 (0x0FF), -1 (0x3FF), -256 (0x300), 7 -> bits 0..9, 10..19, 20..29, 30..39."""
+    w = oracle.edit_pack(np.array([1, -1, 3, -4, 0, 2, -2, 4]), 2)
+    assert w.tolist() == [0x4E20C3F1]
+    w = oracle.edit_pack(np.array([255, -1, -256, 7]), 8)
+    want = 0x0FF | (0x3FF << 10) | (0x300 << 20) | (7 << 30)
+    assert w.tolist() == [want & 0xFFFFFFFF, want >> 32]
+    assert oracle.edit_unpack(w, 4, 8).tolist() == [255, -1, -256, 7]
+
+
+@pytest.mark.parametrize("m", [2, 8, 16, 24, 32, 40])
+def test_edit_pack_round_trip_and_size(m):
+    rng = np.random.default_rng(m)
+    lim = 2 ** m
+    q = rng.integers(-lim, lim + 1, 997)
+    q[:4] = [-lim, lim, 0, -1]
+    w = oracle.edit_pack(q, m)
+    assert w.size == (q.size * (m + 2) + 31) // 32          # (m+2)/8 bytes per edit
+    assert np.array_equal(oracle.edit_unpack(w, q.size, m), q)
+    assert oracle.edit_pack(np.zeros(0, np.int64), m).size == 0
+
+
+def test_edit_pack_rejects_out_of_range():
+    with pytest.raises(ValueError):
+        oracle.edit_pack(np.array([2 ** 8 + 1]), 8)
