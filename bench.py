@@ -499,17 +499,22 @@ def main():
                 "rec_ne_corr": int(sum(int((r != o).sum()) for r, o in zip(rec, out)))}
         log(f"edit log diag: {diag}")
         ke = 3
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        ms_e = ms_d = 0.0
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ms_e = ms_d = ms_p = 0.0
+        cap = int(q.shape[0])  # known from the first encode: one pass per timed encode
         for _ in range(ke):
             ev[0].record(stream)
-            fl, q = c.edit_encode(x, y, z, xh, yh, zh, *out)
+            fl, q = c.edit_encode(x, y, z, xh, yh, zh, *out, cap=cap)
             ev[1].record(stream)
-            c.edit_decode(xh, yh, zh, fl, q, out=rec)
+            words = c.edit_pack(q)  # (m+2)-bit container (R33)
             ev[2].record(stream)
+            c.edit_decode(xh, yh, zh, fl, q, out=rec)
+            ev[3].record(stream)
             torch.cuda.synchronize(dev)
             ms_e += ev[0].elapsed_time(ev[1]) / ke
-            ms_d += ev[1].elapsed_time(ev[2]) / ke
+            ms_p += ev[1].elapsed_time(ev[2]) / ke
+            ms_d += ev[2].elapsed_time(ev[3]) / ke
+        packed_ok = bool(torch.equal(c.edit_unpack(words, int(q.shape[0])), q))
         # quantisation-safety re-check (R31): S1 + S2 on (P, x_rec) -> violated pairs
         c.build_cells(x, y, z, *rec, gid=gid)
         recheck = c.find_vulnerable()
@@ -518,7 +523,9 @@ def main():
         b_enc = 24 * n + fb + 8 * ne        # read P_hat0 and P_hat, write flags and indices
         b_dec = 12 * n + fb + 8 * ne + 12 * n
         pk = hbm or 1.0
-        line["edit_log"] = {"n_edits": ne, "flags_bytes": fb, "index_bytes": 8 * ne, "in_bound": in_bound, "diag": diag,
+        line["edit_log"] = {"n_edits": ne, "flags_bytes": fb, "index_bytes": 8 * ne,
+                            "packed_index_bytes": int(words.numel()) * 4, "packed_bits_per_edit": params.m + 2,
+                            "pack_ms": ms_p, "packed_round_trip": packed_ok, "in_bound": in_bound, "diag": diag,
                             "recheck_pairs": recheck["n_pairs"], "recheck_violated": recheck["n_violated0"],
                             "encode_ms": ms_e, "decode_ms": ms_d,
                             "encode_gbs": b_enc / (ms_e * 1e-3) / 1e9, "decode_gbs": b_dec / (ms_d * 1e-3) / 1e9,
@@ -526,7 +533,7 @@ def main():
                             "decode_frac": b_dec / (ms_d * 1e-3) / 1e9 / pk,
                             "bytes_model": "encode 24N + ceil(3N/8) + 8 n_edits; decode 24N + ceil(3N/8) + 8 n_edits"}
         log(f"edit log: {ne:,} edits, encode {ms_e:.3f} ms, decode {ms_d:.3f} ms, in_bound={in_bound}")
-        del fl, q, rec
+        del fl, q, rec, words
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(w)
         line["cpu_baseline"] = {k: v for k, v in cb.items() if k in ("value", "unit", "cores", "kind", "sample")}

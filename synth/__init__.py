@@ -196,7 +196,9 @@ CONFIGS = {
     "C2": Workload("C2", "lattice", 196_066, 1.0, 1e-3, seed=2),
     "C3": Workload("C3", "fcc", 2_869_440, 1.0, 1e-4, b=0.80 / 90.0, seed=3,
                    extra={"cells": 90, "n_vac": 46_560}),
-    "C4": Workload("C4", "clumped", 280_953_867, 256.0, 1e-5, seed=4),
+    # C4 at SURVEY §8(d)'s xi_rel = 1e-6 (the paper's HACC error bound); the bench also
+    # reports 1.2e-4 (density-matched heavy case) and 1e-5 via --xi-rel
+    "C4": Workload("C4", "clumped", 280_953_867, 256.0, 1e-6, seed=4),
     "C5": Workload("C5", "clumped", 1_073_734_015, 256.0, 1e-6, seed=5),
 }
 

@@ -32,10 +32,14 @@ def _gpu_run(arrs, p):
     return c, vp, out, info
 
 
-def test_c4_full_size_sampled_parity():
+@pytest.mark.parametrize("xi_rel", [1e-6, 1e-5])
+def test_c4_full_size_sampled_parity(xi_rel):
+    """C4 at full size in the bench configuration: xi_rel = 1e-6 (the bench default)
+    and 1e-5 (round 1's default: a 50M-editable frontier and the long tail)."""
     if torch.cuda.get_device_properties(0).total_memory < 120e9:
         pytest.skip("needs a B200-class GPU")
-    w = synth.CONFIGS["C4"]
+    w0 = synth.CONFIGS["C4"]
+    w = synth.Workload(w0.name, w0.kind, w0.n, w0.L, xi_rel, seed=w0.seed)
     dev = torch.device("cuda", 0)
     arrs = synth.make(w, device=dev)
     p = cc.Params(box=w.L, b=w.linking_length, xi=w.xi, stop_mode=cc.STOP_RESTORED)  # bench config
