@@ -110,12 +110,15 @@ def oracle_sample(w: synth.Workload, n_sample: int):
     return ws
 
 
+_ORACLE_STOP = [3, 10_000]  # the oracle arms run the bench's stop mode and T_max (set in main)
+
+
 def run_oracle(ws: synth.Workload, timeout: float = 120.0):
     """The oracle's S1-S7 on a sample, in a child process (so a slow sample cannot hang the
     bench); returns (seconds, iterations, |V|) or None on timeout."""
     cmd = [sys.executable, os.path.abspath(__file__), "--_oracle", json.dumps(
         {"name": ws.name, "kind": ws.kind, "n": ws.n, "L": ws.L, "xi_rel": ws.xi_rel, "b": ws.linking_length,
-         "seed": ws.seed, "extra": ws.extra})]
+         "seed": ws.seed, "extra": ws.extra, "stop": _ORACLE_STOP[0], "t_max": _ORACLE_STOP[1]})]
     try:
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
     except subprocess.TimeoutExpired:
@@ -133,7 +136,8 @@ def _oracle_child(spec: str) -> int:
     ws = synth.Workload(d["name"], d["kind"], d["n"], d["L"], d["xi_rel"], b=d["b"], seed=d["seed"],
                         extra=d["extra"])
     arrs = [t.numpy() for t in synth.make(ws)]
-    c = oracle.cfg(L=ws.L, b=ws.linking_length, xi=ws.xi, stop_mode=d.get("stop", oracle.STOP_RESTORED))
+    c = oracle.cfg(L=ws.L, b=ws.linking_length, xi=ws.xi, stop_mode=d.get("stop", oracle.STOP_RESTORED),
+                   t_max=d.get("t_max", 10_000))
     oracle.build()
     x, y, z, xh, yh, zh = arrs
     t0 = time.perf_counter()
@@ -164,6 +168,10 @@ def calibrated_sample(w: synth.Workload, target_s: float = 12.0, n_sample=None):
     same N in both): start at 50,000 particles of the same recipe and
     density, then scale N so the oracle's S1-S5 takes ~target_s (at most 4M particles).
     Returns (sample workload, its first timing) or (sample, None) on timeout."""
+    if n_sample is None and (w.kind != "clumped" or w.n <= 4_000_000):
+        # the lattice / crystal recipes do not rescale, and C1-C3 are small: the oracle runs the
+        # workload itself (the same N as the GPU)
+        return w, run_oracle(w, timeout=600)
     n0 = n_sample or 50_000
     ws = oracle_sample(w, n0)
     r = run_oracle(ws, timeout=6 * target_s)
@@ -277,6 +285,7 @@ def main():
 
     rank, world, local = dist_env()
     w = _workload(args)
+    _ORACLE_STOP[:] = [{"restored": 3, "active": 0, "eps": 1, "none": 2}[args.stop], args.t_max]
     if args.impl == "reference":
         return reference_arm(args, w, rank)
 

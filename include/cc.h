@@ -72,6 +72,13 @@ typedef struct {
     int profile;           /* 1: time each kernel class with CUDA events (cc_kernel_stats)   */
     int frontier;          /* 1: skip particles whose state provably cannot change (exact;   */
                            /*    perf only, results identical; 0 = sweep every editable)    */
+    /* Optional scratch allocator (e.g. torch's caching allocator): alloc_fn(bytes, user) returns
+     * device memory usable on the context's stream (NULL = failure, CC_E_OOM); free_fn(ptr,
+     * user) releases it, stream-ordered after the work already enqueued.  NULL = cudaMallocAsync
+     * / cudaFreeAsync on the context's stream.  Called only from the thread making the cc_* call. */
+    void* (*alloc_fn)(size_t bytes, void* user);
+    void (*free_fn)(void* ptr, void* user);
+    void* alloc_user;
 } cc_params;
 
 /* fill *p with the paper's defaults (eta 0.2, m 16, Adam 1e-3/.9/.999/1e-8, t_max 10000,
@@ -131,7 +138,9 @@ typedef struct {
 cc_status cc_find_vulnerable(cc_ctx* ctx, cc_vp_info* info_h);
 
 /* The canonical pair list (gi < gj, global ids) with flags bit0 = original link,
- * bit1 = decompressed link, in unspecified order; at most `cap` written, *n_out_h = |V|. */
+ * bit1 = decompressed link, sorted by (gi, gj) (a counting sort on gi: scratch of 8 B per
+ * gid up to the largest owner gid); at most `cap` written, *n_out_h = |V| (cap = 0: count only).
+ * Multi-GPU: this rank's owned pairs (R17), sorted. */
 cc_status cc_get_pairs(cc_ctx* ctx, uint32_t* gi, uint32_t* gj, uint8_t* flags, int64_t cap,
                        int64_t* n_out_h);
 

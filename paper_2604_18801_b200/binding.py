@@ -33,7 +33,11 @@ class _Params(C.Structure):
                 ("beta2", C.c_double), ("eps_adam", C.c_double), ("t_max", C.c_int), ("eps_loss", C.c_double),
                 ("stop_mode", C.c_int), ("optimizer", C.c_int), ("vanilla_step", C.c_double),
                 ("graph_batch", C.c_int), ("cells_per_particle", C.c_double), ("profile", C.c_int),
-                ("frontier", C.c_int)]
+                ("frontier", C.c_int), ("alloc_fn", C.c_void_p), ("free_fn", C.c_void_p), ("alloc_user", C.c_void_p)]
+
+
+_ALLOC_T = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+_FREE_T = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
 
 
 class _Dist(C.Structure):
@@ -147,9 +151,10 @@ class Params:
     cells_per_particle: float = 2.0
     profile: int = 0
     frontier: int = 1
+    torch_allocator: bool = False  # scratch from torch's caching allocator (cc_params.alloc_fn)
 
     def to_c(self) -> _Params:
-        return _Params(**{k: v for k, v in asdict(self).items()})
+        return _Params(**{k: v for k, v in asdict(self).items() if k != "torch_allocator"})
 
 
 def _ptr(t):
@@ -175,6 +180,21 @@ class Corrector:
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.params = params
         self._p = params.to_c()
+        if params.torch_allocator:  # scratch from torch's caching allocator, on this context's stream
+            dev, st = self.device, self.stream
+
+            def _alloc(nbytes, user):
+                try:
+                    return torch.cuda.caching_allocator_alloc(int(nbytes), dev, st)
+                except Exception:
+                    return None
+
+            def _free(ptr, user):
+                torch.cuda.caching_allocator_delete(ptr)
+
+            self._cb = (_ALLOC_T(_alloc), _FREE_T(_free))  # kept alive with the context
+            self._p.alloc_fn = C.cast(self._cb[0], C.c_void_p)
+            self._p.free_fn = C.cast(self._cb[1], C.c_void_p)
         self._d = None
         if dist is not None:
             # (rank, nranks, nccl unique id) for NCCL ranks, or (rank, nranks, None, VGroup)

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "cc_internal.cuh"
@@ -23,16 +24,33 @@ cc_status cc_cuda_check(cc_ctx* c, cudaError_t e, const char* what) {
     return cc_fail(c, CC_E_CUDA, std::string(cudaGetErrorString(e)) + " at " + what);
 }
 
+// scratch memory: the caller's allocator when cc_params supplies one (e.g. torch's caching
+// allocator, bound to the context's stream by the caller), else stream-ordered cudaMallocAsync
+static void scratch_free(cc_ctx* c, void* p) {
+    if (!p) return;
+    if (c->p.free_fn) c->p.free_fn(p, c->p.alloc_user);
+    else cudaFreeAsync(p, c->stream);
+}
+
 template <typename T>
 cc_status cc_ensure(cc_ctx* c, cc::DBuf<T>& b, size_t n, const char* name) {
     if (n == 0) n = 1;
     if (b.cap >= n) return CC_OK;
     if (b.p) {
-        cudaFreeAsync(b.p, c->stream);
+        scratch_free(c, b.p);
         b.p = nullptr;
         b.cap = 0;
     }
     void* p = nullptr;
+    if (c->p.alloc_fn) {
+        p = c->p.alloc_fn(n * sizeof(T), c->p.alloc_user);
+        if (!p)
+            return cc_fail(c, CC_E_OOM, std::string("allocator callback failed for ") + name + " (" +
+                                            std::to_string(n * sizeof(T)) + " bytes)");
+        b.p = static_cast<T*>(p);
+        b.cap = n;
+        return CC_OK;
+    }
     cudaError_t e = cudaMallocAsync(&p, n * sizeof(T), c->stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -46,7 +64,7 @@ cc_status cc_ensure(cc_ctx* c, cc::DBuf<T>& b, size_t n, const char* name) {
 
 template <typename T>
 void cc_release(cc_ctx* c, cc::DBuf<T>& b) {
-    if (b.p) cudaFreeAsync(b.p, c->stream);
+    if (b.p) scratch_free(c, b.p);
     b.p = nullptr;
     b.cap = 0;
 }
@@ -172,6 +190,17 @@ static cc_status derive_params(cc_ctx* c, int64_t n_total) {
     t.b2 = f32_nearest(B * B);                                    // R3: d <= b
     t.Lf = (float)p.box;
     t.hLf = f32_nearest((ld)p.box / 2);
+    // largest fp32 s with sqrtf(s) <= c (host sqrtf is the correctly rounded IEEE square root,
+    // the same as the device's __fsqrt_rn)
+    auto sq_thr = [](float c) -> float {
+        if (!(c > 0.0f)) return -1.0f;
+        float s2 = c * c;
+        while (std::sqrt(s2) > c) s2 = std::nextafter(s2, 0.0f);
+        while (std::sqrt(std::nextafter(s2, INFINITY)) <= c) s2 = std::nextafter(s2, INFINITY);
+        return s2;
+    };
+    t.sb2 = sq_thr(t.c_b);
+    t.sf2 = sq_thr(t.c_f);
     t.periodic = p.periodic ? 1 : 0;
 
     // Proven-link shells (cc_internal.cuh Th): every pinned fp32 d2 lies within the relative
@@ -233,6 +262,10 @@ static void choose_grid(cc_ctx* c, int64_t n_local, double x_extent, double x0, 
     c->g.ext_x = x_extent;
     c->g.xwrap = xwrap;
     c->ncell = (int64_t)nx * nyz * nyz;
+    // thread-per-cell insertion sort only where cells are tiny (K >= 1); crowded cells by a warp
+    const double per_cell = nl / (double)c->ncell;
+    c->bin_short_max = per_cell < 1.0 ? 16 : 1;
+    if (const char* e = std::getenv("CC_BIN_SHORT")) c->bin_short_max = std::max(1, std::min(16, std::atoi(e)));
 }
 
 // ------------------------------------------------------------------------------------------
@@ -259,6 +292,9 @@ void cc_default_params(cc_params* p) {
     p->cells_per_particle = 2.0;
     p->profile = 0;
     p->frontier = 1;
+    p->alloc_fn = nullptr;
+    p->free_fn = nullptr;
+    p->alloc_user = nullptr;
 }
 
 cc_status cc_create(cc_ctx** out, int device, void* stream, const cc_params* p, const cc_dist* dist) {
@@ -333,7 +369,7 @@ void cc_destroy(cc_ctx* c) {
         cc_release(c, c->rrb[d]);
     }
     cc_release(c, c->stage); cc_release(c, c->gath); cc_release(c, c->dcnt); cc_release(c, c->red); cc_release(c, c->red_sum);
-    cc_release(c, c->bnd); cc_release(c, c->near); cc_release(c, c->near_n);
+    cc_release(c, c->bnd); cc_release(c, c->near); cc_release(c, c->near_n); cc_release(c, c->gp_cnt); cc_release(c, c->gp_pos);
     cudaStreamSynchronize(c->stream);
     // the PGD graph holds NCCL work (multi-GPU): release it before the communicator
     if (c->pgd_exec) cudaGraphExecDestroy(c->pgd_exec);

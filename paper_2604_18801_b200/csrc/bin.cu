@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(BIN_THREADS)
 k_cell_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restrict__ rec, Grid g,
               float4* __restrict__ orig4, float4* __restrict__ dec4, uint32_t* __restrict__ xk,
               uint32_t* __restrict__ slot_of, uint32_t* __restrict__ long_list, uint64_t cap,
-              unsigned long long* __restrict__ n_long) {
+              unsigned long long* __restrict__ n_long, int short_max) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= ncell) return;
     const uint32_t a = cs[c], b = cs[c + 1];
@@ -116,7 +116,7 @@ k_cell_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restr
         emit(load_rec(rec, a), a, a, orig4, dec4, xk, slot_of, g);
         return;
     }
-    if (len > CELL_SHORT) {  // mid cells from the front of the list, long ones from the back
+    if (len > short_max) {  // mid cells from the front of the list, long ones from the back
         if (len <= CELL_MID) long_list[atomicAdd(n_long, 1ull)] = (uint32_t)c;
         else long_list[cap - 1 - atomicAdd(n_long + 1, 1ull)] = (uint32_t)c;
         return;
@@ -298,7 +298,7 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
         int t2 = cc_prof_begin(c, "K1_finish");
         CCL(c, k_cell_finish<<<(unsigned)((nc + BIN_THREADS - 1) / BIN_THREADS), BIN_THREADS, 0, c->stream>>>(
                    nc, c->cell_start.p, rec, c->g, c->orig4.p, c->dec4.p, c->xk.p, c->slot_of.p, c->scratch_u32.p, cap,
-                   nl));
+                   nl, c->bin_short_max));
         CCL(c, k_cell_finish_mid<<<148 * 8, BIN_THREADS, 0, c->stream>>>(c->scratch_u32.p, nl, c->cell_start.p, rec,
                                                                           c->g, c->orig4.p, c->dec4.p, c->xk.p,
                                                                           c->slot_of.p));

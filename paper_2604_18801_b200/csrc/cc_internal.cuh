@@ -44,6 +44,10 @@ struct Th {
     // _w: pairs near a periodic face (the wrap adds an absolute error u (L + 2 xi)).  Pairs in
     // (lo2s, lo2] or (hi2, hi2s] form the near-shell list re-tested on the positions.
     float lo2s_i, hi2s_i, lo2s_w, hi2s_w;
+    // Eq. 3 activity on the squared distance (K3 skips the square root of inactive pairs):
+    // sqrt_rn(s) > c_b  <=>  s > sb2,  sqrt_rn(s) <= c_f  <=>  s <= sf2 (sqrt_rn is monotone;
+    // sb2/sf2 = the largest fp32 s with sqrt_rn(s) <= c_b / c_f, found on the host)
+    float sb2, sf2;
 };
 
 // Search structure on ORIGINAL positions ("x-sorted rows"): the (y,z) plane is cut into
@@ -211,6 +215,7 @@ struct cc_ctx {
     double b = 0, xi_d = 0, eps_q = 0, mu = 0, delta = 0;
     cc::Grid g{};
     int64_t ncell = 0;
+    int bin_short_max = 16;  // K1 finish: cells up to this size sorted by one thread, larger by a warp / block
 
     // sizes
     int64_t n_in = 0;      // particles given by the caller (owned)
@@ -230,6 +235,7 @@ struct cc_ctx {
     bool base_valid = false;
     cc::DBuf<uint32_t> parent_orig;  // stable forest + original-linked band pairs = FoF(ORIG), per build
     bool orig_valid = false;
+    cc::DBuf<uint32_t> gp_cnt, gp_pos;  // cc_get_pairs: counting sort by owner gid
     cc::DBuf<uint2> near;        // near-shell pairs (slot, slot | bit 31 = linked in the original), K2 count
     cc::DBuf<unsigned long long> near_n;  // their count (may exceed near.cap: then FoF searches directly)
     int64_t near_count = 0;      // host copy after cc_find_vulnerable

@@ -324,13 +324,79 @@ cc_status mcc_run(cc_ctx* c, int which, unsigned long long* counts_dev) {
     return CC_OK;
 }
 
+// canonical order (§8(b): gi < gj, sorted by (gi, gj)) by a counting sort on the row owner's gid:
+// rows are already sorted by partner gid (R14), so placing each editable's upper entries at the
+// exclusive prefix of the per-gid counts yields the sorted list without a comparison sort.
+__global__ void k_max_gid(uint32_t E, const float4* __restrict__ posE, unsigned int* __restrict__ mx) {
+    uint32_t m = 0u;
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x)
+        m = max(m, __float_as_uint(posE[e].w));
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+}
+
+__global__ void k_count_upper(uint32_t E, const unsigned long long* __restrict__ rowptr,
+                              const uint32_t* __restrict__ rows, const float4* __restrict__ posE,
+                              uint32_t* __restrict__ cnt) {
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        uint32_t u = 0;
+        for (unsigned long long k = rowptr[e]; k < rowptr[e + 1]; k++) u += (rows[k] & ENT_UPPER) ? 1u : 0u;
+        cnt[__float_as_uint(posE[e].w)] = u;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_get_pairs_sorted(uint32_t E, const unsigned long long* __restrict__ rowptr, const uint32_t* __restrict__ rows,
+                   const float4* __restrict__ posE, const float4* __restrict__ dec4, const uint32_t* __restrict__ slotE,
+                   const uint32_t* __restrict__ pos, Th t, int64_t cap, uint32_t* __restrict__ gi,
+                   uint32_t* __restrict__ gj, uint8_t* __restrict__ fl) {
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        const float4 pd = dec4[slotE[e]];
+        const uint32_t g0 = __float_as_uint(posE[e].w);
+        int64_t q = pos[g0];
+        for (unsigned long long k = rowptr[e]; k < rowptr[e + 1]; k++) {
+            const uint32_t ent = rows[k];
+            if (!(ent & ENT_UPPER)) continue;
+            const uint32_t j = ent & ENT_IDX;
+            const float4 qd = dec4[slotE[j]];
+            if (q < cap) {
+                gi[q] = g0;
+                gj[q] = __float_as_uint(posE[j].w);
+                fl[q] = (uint8_t)(((ent & ENT_OLINK) ? 1 : 0) | (dist2(pd, qd, t) <= t.b2 ? 2 : 0));
+            }
+            q++;
+        }
+    }
+}
+
 cc_status get_pairs_run(cc_ctx* c, uint32_t* gi, uint32_t* gj, uint8_t* flags, int64_t cap, unsigned long long* n_dev) {
     CC_CUDA(c, cudaMemsetAsync(n_dev, 0, sizeof(unsigned long long), c->stream));
     if (c->E == 0) return CC_OK;
-    int nb = (int)std::min<int64_t>((c->E + 255) / 256, 148 * 8);
-    CCL(c, k_get_pairs<<<nb, 256, 0, c->stream>>>((uint32_t)c->E, reinterpret_cast<const unsigned long long*>(c->rowptr.p),
-                                           c->rows.p, c->origE.p, c->dec4.p, c->slotE.p, c->th, cap, gi, gj, flags,
-                                           n_dev));
+    const int nb = (int)std::min<int64_t>((c->E + 255) / 256, 148 * 8);
+    const unsigned long long* rowptr = reinterpret_cast<const unsigned long long*>(c->rowptr.p);
+    if (cap <= 0) {  // count only (the total is needed to size the outputs)
+        CCL(c, k_get_pairs<<<nb, 256, 0, c->stream>>>((uint32_t)c->E, rowptr, c->rows.p, c->origE.p, c->dec4.p,
+                                                       c->slotE.p, c->th, 0, gi, gj, flags, n_dev));
+        CC_CUDA(c, cudaGetLastError());
+        return CC_OK;
+    }
+    // largest owner gid -> counting-sort array size
+    CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
+    unsigned int* mx = reinterpret_cast<unsigned int*>(c->counters.p + 13);
+    CC_CUDA(c, cudaMemsetAsync(mx, 0, sizeof(unsigned int), c->stream));
+    CCL(c, k_max_gid<<<nb, 256, 0, c->stream>>>((uint32_t)c->E, c->origE.p, mx));
+    unsigned int hmx = 0;
+    CC_CUDA(c, cudaMemcpyAsync(&hmx, mx, sizeof(hmx), cudaMemcpyDeviceToHost, c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    const int64_t G = (int64_t)hmx + 1;
+    CC_TRY(cc_ensure(c, c->gp_cnt, (size_t)G, "pair sort counts"));
+    CC_TRY(cc_ensure(c, c->gp_pos, (size_t)G, "pair sort offsets"));
+    CC_CUDA(c, cudaMemsetAsync(c->gp_cnt.p, 0, (size_t)G * sizeof(uint32_t), c->stream));
+    CCL(c, k_count_upper<<<nb, 256, 0, c->stream>>>((uint32_t)c->E, rowptr, c->rows.p, c->origE.p, c->gp_cnt.p));
+    CC_CUDA(c, cudaMemsetAsync(n_dev, 0, sizeof(unsigned long long), c->stream));
+    CC_TRY(scan_u32_to_u32(c, c->gp_cnt.p, c->gp_pos.p, G, reinterpret_cast<uint64_t*>(n_dev)));
+    CCL(c, k_get_pairs_sorted<<<nb, 256, 0, c->stream>>>((uint32_t)c->E, rowptr, c->rows.p, c->origE.p, c->dec4.p,
+                                                          c->slotE.p, c->gp_pos.p, c->th, cap, gi, gj, flags));
     CC_CUDA(c, cudaGetLastError());
     return CC_OK;
 }

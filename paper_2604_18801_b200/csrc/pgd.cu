@@ -46,6 +46,7 @@ constexpr int TAIL_BLOCKS = 64;        // k_tail's co-resident blocks
 struct WarpSh {               // per-warp staging of K3's flattened row evaluation
     float4 t[CH];             // term (px, py, pz, kind bits) of each chunk entry
     float4 p[32];             // positions of the warp's 32 editables
+    unsigned char inner[32];  // the editable is interior (its row never needs the minimum image)
     unsigned long long k0[32];
     uint32_t off[32];         // exclusive scan of the row lengths
     uint32_t ent[CH];         // partner editable of each chunk entry (the movers' touches)
@@ -64,6 +65,7 @@ struct PgdArgs {
     float* __restrict__ mom;  // 6 x E SoA
     const float2* __restrict__ bc;
     Th t;
+    float imin, imax;  // a row whose owner lies in [imin, imax]^3 never wraps (min_image = identity)
     float alpha, b1, b2, omb1, omb2, eps, vstep;
     int optimizer;
     int t_max;
@@ -103,24 +105,27 @@ struct Term {
     bool viol;
 };
 
+template <bool INNER = false>
 __device__ __forceinline__ Term pair_term(const float4& p, const float4& q, uint32_t ent, const Th& th) {
     Term o;
-    const float rx = min_image(__fsub_rn(p.x, q.x), th);
-    const float ry = min_image(__fsub_rn(p.y, q.y), th);
-    const float rz = min_image(__fsub_rn(p.z, q.z), th);
+    // INNER: the row's owner is far from the periodic faces (interior()), min_image is the identity
+    const float rx = INNER ? __fsub_rn(p.x, q.x) : min_image(__fsub_rn(p.x, q.x), th);
+    const float ry = INNER ? __fsub_rn(p.y, q.y) : min_image(__fsub_rn(p.y, q.y), th);
+    const float rz = INNER ? __fsub_rn(p.z, q.z) : min_image(__fsub_rn(p.z, q.z), th);
     float s = __fmul_rn(rx, rx);
     s = __fadd_rn(s, __fmul_rn(ry, ry));
     s = __fadd_rn(s, __fmul_rn(rz, rz));
-    const float d = __fsqrt_rn(s);
     const bool ol = (ent & ENT_OLINK) != 0;
     o.viol = (s <= th.b2) != ol;  // link status differs from the original (Eq. 1 support)
     // Eq. (3): broken side (orig linked) active iff d_hat > b - 2 sqrt3 eps_q;
     //          false side (orig unlinked) active iff d_hat <= b + 2 sqrt3 eps_q
-    const bool act = ol ? (d > th.c_b) : (d <= th.c_f);
+    // decided on s = d_hat^2 against sb2 / sf2 (identical decisions, Th); d_hat only if active
+    const bool act = ol ? (s > th.sb2) : (s <= th.sf2);
     o.kind = 0;
     o.ee = 0.0f;
     o.px = o.py = o.pz = 0.0f;
     if (act) {
+        const float d = __fsqrt_rn(s);
         o.ee = __fsub_rn(d, ol ? th.c_b : th.c_f);
         const float two_e = __fmul_rn(2.0f, o.ee);
         if (d > 0.0f) {
@@ -152,6 +157,10 @@ __device__ __forceinline__ float project(float x, float o, float xip) {
 __device__ __forceinline__ float div_rn(float a, float b) {
     if (a == 0.0f) return __int_as_float((__float_as_int(a) ^ __float_as_int(b)) & 0x80000000);
     return __fdiv_rn(a, b);
+}
+
+__device__ __forceinline__ bool k3_inner(const float4& p, const PgdArgs& a) {
+    return p.x >= a.imin && p.x <= a.imax && p.y >= a.imin && p.y <= a.imax && p.z >= a.imin && p.z <= a.imax;
 }
 
 // per-editable state loads: plain, or through L2 only (k_tail: blocks read what other blocks
@@ -274,7 +283,10 @@ __device__ __forceinline__ int update(const PgdArgs& a, uint32_t e, const float4
     return flags;
 }
 
-// frontier bookkeeping after e was processed at iteration t; returns whether e stays awake
+// frontier bookkeeping after e was processed at iteration t; returns whether e stays awake.
+// any_active: some pair of e's row was L_tight-active OR violated -- when the margin 2 sqrt3 eps_q
+// is below fp32 resolution (tiny xi) a pair can be violated yet inactive; freezing e then would
+// hide a violated pair from the stop statistics (found on C3 at xi_rel = 1e-6)
 __device__ __forceinline__ bool frontier_after(const PgdArgs& a, uint32_t e, int t, int flags, bool any_active,
                                                uint32_t fz) {
     if (fz == FZ_NEVER) return true;
@@ -341,7 +353,7 @@ __device__ __forceinline__ void add_term(const Term& tm, uint32_t ent, K3Ctx& k,
         }
         if (tm.viol) k.cn[PGD_THREADS]++;
     }
-    act |= tm.kind != 0;
+    act |= tm.kind != 0 || tm.viol;  // keeps the editable awake (frontier): active OR violated
     cx = __fadd_rn(cx, tm.px);
     cy = __fadd_rn(cy, tm.py);
     cz = __fadd_rn(cz, tm.pz);
@@ -379,6 +391,8 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
     ws.off[lane] = off;
     ws.k0[lane] = k0;
     ws.p[lane] = p;
+    const bool inner = k3_inner(p, a);
+    ws.inner[lane] = inner ? 1 : 0;
     __syncwarp();
     bool any_active = false;
     float gx = 0.0f, gy = 0.0f, gz = 0.0f;
@@ -408,7 +422,8 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
         for (int j = 0; j < NB; j++) {
             if (sg[j] >= 0) {
                 ws.ent[lane + 32 * j] = ent[j] & ENT_IDX;
-                const Term tm = pair_term(ws.p[sg[j]], q[j], ent[j], th);
+                const Term tm = ws.inner[sg[j]] ? pair_term<true>(ws.p[sg[j]], q[j], ent[j], th)
+                                                : pair_term<false>(ws.p[sg[j]], q[j], ent[j], th);
                 if (ent[j] & ENT_UPPER) {  // each pair counted once, at its lower-gid endpoint
                     if (tm.kind) {
                         k.cn[0]++;
@@ -416,7 +431,7 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
                     }
                     if (tm.viol) k.cn[PGD_THREADS]++;
                 }
-                ws.t[lane + 32 * j] = make_float4(tm.px, tm.py, tm.pz, __int_as_float(tm.kind));
+                ws.t[lane + 32 * j] = make_float4(tm.px, tm.py, tm.pz, __int_as_float(tm.kind | (tm.viol ? 4 : 0)));
             }
         }
         __syncwarp();
@@ -483,7 +498,9 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
                         if (j < nvalid) q[j] = ldpos<TAIL>(k.src + (en[j] & ENT_IDX));
 #pragma unroll
                     for (int j = 0; j < 4; j++)
-                        if (j < nvalid) add_term<TAIL>(pair_term(p, q[j], en[j], th), en[j], k, cx, cy, cz, act);
+                        if (j < nvalid)
+                            add_term<TAIL>(inner ? pair_term<true>(p, q[j], en[j], th) : pair_term<false>(p, q[j], en[j], th),
+                                           en[j], k, cx, cy, cz, act);
                 }
                 // chunk m completes: right child at each level whose bit of m is set
 #pragma unroll
@@ -1030,6 +1047,18 @@ PgdArgs make_args(cc_ctx* c, int count_only) {
     a.mom = c->mom.p;
     a.bc = c->bc.p;
     a.t = c->th;
+    // owners at least 2 search radii inside the periodic box: every partner difference of the
+    // current positions (within xi_f of the originals, partners within r_pair) is far below L/2
+    if (c->p.periodic && 8.0 * c->r_pair < c->p.box) {
+        a.imin = (float)(2.0 * c->r_pair);
+        a.imax = (float)(c->p.box - 2.0 * c->r_pair);
+    } else if (!c->p.periodic) {
+        a.imin = -INFINITY;
+        a.imax = INFINITY;
+    } else {
+        a.imin = 1.0f;  // empty interval: every row takes the minimum image
+        a.imax = 0.0f;
+    }
     a.alpha = (float)c->p.alpha;
     a.b1 = (float)c->p.beta1;
     a.b2 = (float)c->p.beta2;

@@ -28,6 +28,11 @@ def gpu_pipeline(arrs, params: cc.Params, gid=None, fof=True):
     c.build_cells(*ts, gid=g)
     vp = c.find_vulnerable()
     gi, gj, fl = c.get_pairs()
+    # §8(b): canonical (gi < gj) and sorted by (gi, gj)
+    a_, b_ = to_np(gi).view(np.uint32).astype(np.int64), to_np(gj).view(np.uint32).astype(np.int64)
+    assert np.all(a_ < b_), "cc_get_pairs: not canonical"
+    key = (a_ << 32) | b_
+    assert np.all(np.diff(key) > 0), "cc_get_pairs: not sorted by (gi, gj)"
     out, info = c.correct()
     res = {"vp": vp, "info": info, "pairs": (to_np(gi).view(np.uint32), to_np(gj).view(np.uint32), to_np(fl)),
            "out": [to_np(o) for o in out]}

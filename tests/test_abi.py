@@ -68,3 +68,25 @@ def test_cc_hmf_matches_oracle():
     e1, d1 = cc.hmf(sizes[:100], 8.0, 50, lo=e2[0], hi=e2[-1])
     e2, d2 = oracle.hmf(sizes[:100], 8.0, 50, lo=e2[0], hi=e2[-1])
     assert np.allclose(d1, d2, rtol=1e-12)
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors of the ABI structs have the C compiler's sizes and field offsets."""
+    structs = {"cc_params": binding._Params, "cc_dist": binding._Dist, "cc_vp_info": binding._VP,
+               "cc_corr_info": binding._Corr, "cc_mcc_info": binding._Mcc, "cc_run_info": binding._Run,
+               "cc_thresholds": binding._Th}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "cc.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-std=c11", f"-I{os.path.join(ROOT, 'include')}", str(src), "-o", str(exe)])
+    got = dict(ln.split() for ln in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(got[cname]) == C.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert int(got[f"{cname}.{f}"]) == getattr(py, f).offset, f"{cname}.{f}"

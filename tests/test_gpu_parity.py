@@ -232,3 +232,29 @@ def test_hmf_on_gpu_catalogue_matches_oracle():
     _, d4 = cc.hmf(g["halo_orig"], 1.0, 50, lo=lo, hi=hi)
     _, d3 = cc.hmf(g["halo_cor"], 1.0, 50, lo=lo, hi=hi)
     assert np.array_equal(d4, d3)   # converged -> identical HMF on the original's bins (R22)
+
+
+@pytest.mark.parametrize("frontier", [1, 0])
+def test_margin_below_fp32_resolution_violated_but_inactive(frontier):
+    """configs[2] (C3, full size) at xi_rel = 1e-6: the Eq. 3 margin 2 sqrt3 eps_q (1.06e-10) is
+    below half an ulp of b, so c_b = fl32(b) and one pair stays violated (d_hat^2 > b2) yet
+    L_tight-inactive from iteration 3 on (oracle trace: active 2753, 9, 0, ...; violated 2754,
+    10, 1, 1, ...).  The frontier must not freeze its endpoints (round 1 did, ending the RESTORED
+    loop at t = 2): GPU trace and iteration count == oracle, not converged at T_max."""
+    w0 = synth.CONFIGS["C3"]
+    w = synth.Workload(w0.name, w0.kind, w0.n, w0.L, 1e-6, b=w0.b, seed=w0.seed, extra=w0.extra)
+    arrs = _arrs(w)
+    p = _params(w, stop_mode=cc.STOP_RESTORED, t_max=30, frontier=frontier)
+    g = gpu_pipeline(arrs, p, fof=False)
+    o = oracle_pipeline(arrs, p, fof=False)
+    assert_parity(g, o, fof=False)
+    assert o["info"]["violated_final"] > 0 and not g["info"]["converged"]
+
+
+def test_torch_caching_allocator_scratch():
+    """cc_params.alloc_fn/free_fn (§8(b)): scratch from torch's caching allocator on the
+    context's stream gives the same bit-exact results."""
+    w = synth.Workload("C1", "clumped", 30_000, 1.0, 1e-3, seed=2)
+    arrs = _arrs(w)
+    p = _params(w, torch_allocator=True)
+    assert_parity(gpu_pipeline(arrs, p), oracle_pipeline(arrs, p))
