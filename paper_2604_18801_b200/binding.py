@@ -148,7 +148,7 @@ class Params:
     optimizer: int = 0
     vanilla_step: float = 0.0
     graph_batch: int = 16
-    cells_per_particle: float = 2.0
+    cells_per_particle: float = 0.03
     profile: int = 0
     frontier: int = 1
     torch_allocator: bool = False  # scratch from torch's caching allocator (cc_params.alloc_fn)

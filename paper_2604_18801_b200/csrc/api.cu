@@ -243,7 +243,7 @@ static cc_status derive_params(cc_ctx* c, int64_t n_total) {
 // R25).  FoF on the original positions searches radius r_link = b (1 + 1e-5).
 static void choose_grid(cc_ctx* c, int64_t n_local, double x_extent, double x0, int xwrap) {
     const double L = c->p.box;
-    const double K = c->p.cells_per_particle > 0 ? c->p.cells_per_particle : 2.0;
+    const double K = c->p.cells_per_particle > 0 ? c->p.cells_per_particle : 0.03;
     const double nl = (double)std::max<int64_t>(n_local, 1);
     int64_t nyz = std::max<int64_t>(1, (int64_t)std::floor(L / c->r_pair));
     while (nyz > 1 && (double)nyz * (double)nyz > std::max(nl, 9.0)) nyz = std::max<int64_t>(1, (int64_t)(nyz * 0.97));
@@ -289,7 +289,7 @@ void cc_default_params(cc_params* p) {
     p->optimizer = CC_OPT_ADAM;
     p->vanilla_step = 0.0;
     p->graph_batch = 16;
-    p->cells_per_particle = 2.0;
+    p->cells_per_particle = 0.03;  // cells = rows of ~30 particles (measured: K1 37 vs 46 ms at C4)
     p->profile = 0;
     p->frontier = 1;
     p->alloc_fn = nullptr;

@@ -226,6 +226,7 @@ struct cc_ctx {
 
     // device buffers
     cc::DBuf<float4> orig4, dec4, cor4, posA, posB, origE;
+    bool cor4_valid = false;  // cor4 matches the last cc_correct (built on demand)
     cc::DBuf<uint32_t> key, rnk, cell_count, cell_start, slot_of, deg, eidx, rows, slotE, parent, mingid,
         gsize, scratch_u32;
     cc::DBuf<uint64_t> rowoff, rowptr, scratch_u64;
@@ -682,6 +683,7 @@ cc_status pairs_fill(cc_ctx* c);
 cc_status rows_finish(cc_ctx* c);
 cc_status pgd_run(cc_ctx* c, cc_corr_info* info);
 cc_status write_output(cc_ctx* c, const float4* pos_res, float* xo, float* yo, float* zo);
+cc_status ensure_cor4(cc_ctx* c);
 cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups);
 cc_status mcc_run(cc_ctx* c, int which, unsigned long long* counts_dev);
 cc_status get_pairs_run(cc_ctx* c, uint32_t* gi, uint32_t* gj, uint8_t* flags, int64_t cap,

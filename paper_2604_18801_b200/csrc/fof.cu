@@ -247,6 +247,7 @@ cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
     CC_TRY(cc_ensure(c, c->mingid, n1, "mingid"));
     CC_TRY(cc_ensure(c, c->gsize, n1, "gsize"));
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
+    if (which == CC_CORR) CC_TRY(ensure_cor4(c));
     const float4* P = which == CC_ORIG ? c->orig4.p : (which == CC_DECOMP ? c->dec4.p : c->cor4.p);
     // ORIG and CORR: the stable forest (provably linked in both, Th::lo2s) + the near shell
     // re-tested + the vulnerable rows (the near list overflowing its buffer: direct search)

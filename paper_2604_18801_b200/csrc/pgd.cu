@@ -1023,6 +1023,21 @@ __global__ void k_cor4(int64_t n, const float4* __restrict__ dec4, const uint32_
     cor4[s] = d;
 }
 
+// outputs in input order (owned particles), straight from the result buffer (editables) or the
+// decompressed positions (the rest): no slot-order intermediate on the S1-S5 path
+__global__ void k_output_direct(int64_t n_in, const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ eidx,
+                                const float4* __restrict__ dec4, const float4* __restrict__ res, float* __restrict__ xo,
+                                float* __restrict__ yo, float* __restrict__ zo) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_in) return;
+    const uint32_t s = slot_of[i];
+    const uint32_t e = eidx[s];
+    const float4 v = e != 0xFFFFFFFFu ? res[e] : dec4[s];
+    xo[i] = v.x;
+    yo[i] = v.y;
+    zo[i] = v.z;
+}
+
 // outputs in input order (owned particles)
 __global__ void k_output(int64_t n_in, const uint32_t* __restrict__ slot_of, const float4* __restrict__ cor4,
                          float* __restrict__ xo, float* __restrict__ yo, float* __restrict__ zo) {
@@ -1390,17 +1405,26 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
 }
 
 cc_status write_output(cc_ctx* c, const float4* res, float* xo, float* yo, float* zo) {
-    const int64_t n = c->n;
-    CC_TRY(cc_ensure(c, c->cor4, (size_t)std::max<int64_t>(n, 1), "cor4"));
+    c->cor4_valid = false;  // slot-order corrected positions are built on demand (FoF / MCC of CORR)
     int tok = cc_prof_begin(c, "K3_output");
-    if (n > 0)
-        CCL(c, k_cor4<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(n, c->dec4.p, c->eidx.p, (uint32_t)c->E,
-                                                                          res, c->cor4.p));
     if (c->n_in > 0 && xo)
-        CCL(c, k_output<<<(unsigned)((c->n_in + 255) / 256), 256, 0, c->stream>>>(c->n_in, c->slot_of.p, c->cor4.p,
-                                                                                  xo, yo, zo));
+        CCL(c, k_output_direct<<<(unsigned)((c->n_in + 255) / 256), 256, 0, c->stream>>>(
+                   c->n_in, c->slot_of.p, c->eidx.p, c->dec4.p, res, xo, yo, zo));
     cc_prof_end(c, tok);
     CC_CUDA(c, cudaGetLastError());
+    return CC_OK;
+}
+
+// corrected positions in slot order (the FoF(CORR) near-shell test), from the result buffer
+cc_status ensure_cor4(cc_ctx* c) {
+    if (c->cor4_valid) return CC_OK;
+    const int64_t n = c->n;
+    CC_TRY(cc_ensure(c, c->cor4, (size_t)std::max<int64_t>(n, 1), "cor4"));
+    if (n > 0)
+        CCL(c, k_cor4<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(n, c->dec4.p, c->eidx.p, (uint32_t)c->E,
+                                                                          pgd_result(c), c->cor4.p));
+    CC_CUDA(c, cudaGetLastError());
+    c->cor4_valid = true;
     return CC_OK;
 }
 
