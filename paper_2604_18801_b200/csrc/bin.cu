@@ -192,6 +192,96 @@ k_cell_finish_mid(const uint32_t* __restrict__ long_list, const unsigned long lo
     }
 }
 
+// warp-per-cell finish for the default grid (cells = whole rows of ~30 particles): one warp per
+// cell, grid-stride; cells of <= 32 records sort one key per lane (15-step bitonic), <= 64 two per
+// lane (k_cell_finish_mid's network), longer ones go to the block kernel's list.  No thread-per-
+// cell divergence and no list atomics for the common sizes.
+__device__ __forceinline__ void warp_sort32(unsigned long long& k, int& o, int lane) {
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            const unsigned long long pk = __shfl_xor_sync(0xffffffffu, k, j);
+            const int po = __shfl_xor_sync(0xffffffffu, o, j);
+            const bool up = (lane & kk) == 0;
+            const bool lower = (lane & j) == 0;
+            const bool take = lower ? ((k > pk) == up) : ((k < pk) == up);
+            if (take) {
+                k = pk;
+                o = po;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(BIN_THREADS)
+k_row_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restrict__ rec, Grid g,
+             float4* __restrict__ orig4, float4* __restrict__ dec4, uint32_t* __restrict__ xk,
+             uint32_t* __restrict__ slot_of, uint32_t* __restrict__ long_list, uint64_t cap,
+             unsigned long long* __restrict__ n_long) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = w0; c < ncell; c += nw) {
+        const uint32_t a = cs[c], b = cs[c + 1];
+        const int len = (int)(b - a);
+        if (len == 0) continue;
+        if (len > CELL_MID) {
+            if (lane == 0) long_list[cap - 1 - atomicAdd(n_long + 1, 1ull)] = (uint32_t)c;
+            continue;
+        }
+        if (len <= 32) {
+            Rec r;
+            unsigned long long k = ~0ull;
+            int o = lane;
+            if (lane < len) {
+                r = load_rec(rec, a + lane);
+                k = rec_key(r, g);
+            }
+            warp_sort32(k, o, lane);
+            if (lane < len) emit(load_rec(rec, a + o), a + lane, a + o, orig4, dec4, xk, slot_of, g);
+            continue;
+        }
+        // 33..64: two keys per lane, the 64-slot network of k_cell_finish_mid
+        unsigned long long k0 = rec_key(load_rec(rec, a + lane), g);
+        unsigned long long k1 = lane + 32 < len ? rec_key(load_rec(rec, a + lane + 32), g) : ~0ull;
+        int o0 = lane, o1 = lane + 32;
+        for (int kk = 2; kk <= 64; kk <<= 1) {
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                if (j == 32) {
+                    const bool up = (lane & kk) == 0;
+                    if ((k0 > k1) == up) {
+                        const unsigned long long tk = k0;
+                        k0 = k1;
+                        k1 = tk;
+                        const int to = o0;
+                        o0 = o1;
+                        o1 = to;
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        unsigned long long& kr = h ? k1 : k0;
+                        int& orr = h ? o1 : o0;
+                        const int idx = lane + 32 * h;
+                        const unsigned long long pk = __shfl_xor_sync(0xffffffffu, kr, j);
+                        const int po = __shfl_xor_sync(0xffffffffu, orr, j);
+                        const bool up = (idx & kk) == 0;
+                        const bool lower = (lane & j) == 0;
+                        const bool take = lower ? ((kr > pk) == up) : ((kr < pk) == up);
+                        if (take) {
+                            kr = pk;
+                            orr = po;
+                        }
+                    }
+                }
+            }
+        }
+        emit(load_rec(rec, a + o0), a + lane, a + o0, orig4, dec4, xk, slot_of, g);
+        if (lane + 32 < len) emit(load_rec(rec, a + o1), a + lane + 32, a + o1, orig4, dec4, xk, slot_of, g);
+    }
+}
+
 // crowded cells: one block per cell, bitonic sort of (key, local offset) in shared memory
 __global__ void __launch_bounds__(512)
 k_cell_finish_long(const uint32_t* __restrict__ long_list, uint64_t cap, const unsigned long long* __restrict__ n_long,
@@ -296,12 +386,18 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
         cc_prof_end(c, tok);
         unsigned long long* nl = reinterpret_cast<unsigned long long*>(c->scratch_u64.p);
         int t2 = cc_prof_begin(c, "K1_finish");
-        CCL(c, k_cell_finish<<<(unsigned)((nc + BIN_THREADS - 1) / BIN_THREADS), BIN_THREADS, 0, c->stream>>>(
-                   nc, c->cell_start.p, rec, c->g, c->orig4.p, c->dec4.p, c->xk.p, c->slot_of.p, c->scratch_u32.p, cap,
-                   nl, c->bin_short_max));
-        CCL(c, k_cell_finish_mid<<<148 * 8, BIN_THREADS, 0, c->stream>>>(c->scratch_u32.p, nl, c->cell_start.p, rec,
-                                                                          c->g, c->orig4.p, c->dec4.p, c->xk.p,
-                                                                          c->slot_of.p));
+        if (c->g.nx == 1) {  // cells are rows (default grid): one warp per cell
+            CCL(c, k_row_finish<<<148 * 16, BIN_THREADS, 0, c->stream>>>(nc, c->cell_start.p, rec, c->g, c->orig4.p,
+                                                                          c->dec4.p, c->xk.p, c->slot_of.p,
+                                                                          c->scratch_u32.p, cap, nl));
+        } else {
+            CCL(c, k_cell_finish<<<(unsigned)((nc + BIN_THREADS - 1) / BIN_THREADS), BIN_THREADS, 0, c->stream>>>(
+                       nc, c->cell_start.p, rec, c->g, c->orig4.p, c->dec4.p, c->xk.p, c->slot_of.p, c->scratch_u32.p,
+                       cap, nl, c->bin_short_max));
+            CCL(c, k_cell_finish_mid<<<148 * 8, BIN_THREADS, 0, c->stream>>>(c->scratch_u32.p, nl, c->cell_start.p,
+                                                                              rec, c->g, c->orig4.p, c->dec4.p,
+                                                                              c->xk.p, c->slot_of.p));
+        }
         CCL(c, k_cell_finish_long<<<148 * 2, 512, 0, c->stream>>>(c->scratch_u32.p, cap, nl, c->cell_start.p, rec,
                                                                   c->g, c->orig4.p, c->dec4.p, c->xk.p, c->slot_of.p));
         cc_prof_end(c, t2);

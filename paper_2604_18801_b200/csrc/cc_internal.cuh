@@ -584,6 +584,68 @@ __device__ __forceinline__ void for_each_pair_forward(const Grid& g, const uint3
         for_each_candidate(g, cs, xk, u, cy, cz, r, periodic_yz, fwd);
         return;
     }
+    if (g.nx == 1) {
+        // cells are whole rows (the default grid): the x-window's key bounds are the same for
+        // all 5 rows -- computed once; each row is one slot range searched by its keys
+        double a = u - r, b = u + r, a1 = 0.0, b1 = -1.0;
+        bool up = false;
+        if (g.xwrap) {
+            if (a < 0.0) {
+                a1 = a + g.L;
+                b1 = g.L;
+                a = 0.0;
+            } else if (b >= g.L) {
+                a1 = 0.0;
+                b1 = b - g.L;
+                b = g.L;
+                up = true;
+            }
+        } else {
+            if (a < 0.0) a = 0.0;
+            if (b > g.ext_x) b = g.ext_x;
+        }
+        const bool two = b1 >= a1;
+        const uint32_t klo0 = key_lo(a, g), khi0 = key_hi(b, g);
+        const uint32_t klo1 = two ? key_lo(a1, g) : 0u, khi1 = two ? key_hi(b1, g) : 0u;
+        {   // own row: forward in slot (= x) order, then the part above the seam at the row start
+            const int64_t row = (int64_t)cz * g.ny + cy;
+            const uint32_t row_end = cs[row + 1];
+            for (uint32_t j = s + 1; j < row_end; j++) {
+                if (xk[j] > khi0) break;
+                f(j);
+            }
+            if (two && up) {
+                for (uint32_t j = cs[row]; j < s; j++) {
+                    if (xk[j] > khi1) break;
+                    f(j);
+                }
+            }
+        }
+        const int rows_dz[4] = {0, 1, 1, 1};
+        const int rows_dy[4] = {1, -1, 0, 1};
+#pragma unroll 1
+        for (int k = 0; k < 4; k++) {
+            int zz = cz + rows_dz[k], yy = cy + rows_dy[k];
+            if (periodic_yz) {
+                zz = wrapi(zz, g.nz);
+                yy = wrapi(yy, g.ny);
+            } else if (zz < 0 || zz >= g.nz || yy < 0 || yy >= g.ny) {
+                continue;
+            }
+            const int64_t row = (int64_t)zz * g.ny + yy;
+            const uint32_t j0 = cs[row], j1 = cs[row + 1];
+            for (uint32_t j = lower_bound_key(xk, j0, j1, klo0); j < j1; j++) {
+                if (xk[j] > khi0) break;
+                f(j);
+            }
+            if (two)
+                for (uint32_t j = lower_bound_key(xk, j0, j1, klo1); j < j1; j++) {
+                    if (xk[j] > khi1) break;
+                    f(j);
+                }
+        }
+        return;
+    }
     {
         const int64_t rowbase = ((int64_t)cz * g.ny + cy) * g.nx;
         const double b = u + r;
