@@ -369,7 +369,7 @@ void cc_destroy(cc_ctx* c) {
         cc_release(c, c->rrb[d]);
     }
     cc_release(c, c->stage); cc_release(c, c->gath); cc_release(c, c->dcnt); cc_release(c, c->red); cc_release(c, c->red_sum);
-    cc_release(c, c->bnd); cc_release(c, c->near); cc_release(c, c->near_n); cc_release(c, c->gp_cnt); cc_release(c, c->gp_pos);
+    cc_release(c, c->bnd); cc_release(c, c->near); cc_release(c, c->near_n); cc_release(c, c->gp_cnt); cc_release(c, c->gp_pos); cc_release(c, c->codec_status);
     cudaStreamSynchronize(c->stream);
     // the PGD graph holds NCCL work (multi-GPU): release it before the communicator
     if (c->pgd_exec) cudaGraphExecDestroy(c->pgd_exec);

@@ -79,14 +79,24 @@ k_bin_scatter(int64_t n, const float* __restrict__ x, const float* __restrict__ 
                  : "memory");
 }
 
-// record r (scattered to slot s0) goes to slot s; slot_of[r.i] already holds s0 (k_bin_scatter)
+// record r (scattered to the provisional slot s0) goes to slot s.  slot_of[r.i] holds s0
+// (written coalesced by k_bin_scatter); the finish records fin[s0] = s -- s0 and s lie in the
+// same cell, so these writes stay within a few sectors -- and k_fix_slot_of then maps
+// slot_of[i] = fin[slot_of[i]] in input order (a random READ per particle instead of a random
+// partial-sector WRITE per moved record: -9 ms of K1 at C4 when cells are rows)
 __device__ __forceinline__ void emit(const Rec& r, uint32_t s, uint32_t s0, float4* __restrict__ orig4,
                                      float4* __restrict__ dec4, uint32_t* __restrict__ xk,
-                                     uint32_t* __restrict__ slot_of, const Grid& g) {
+                                     uint32_t* __restrict__ fin, const Grid& g) {
     orig4[s] = make_float4(r.x, r.y, r.z, __uint_as_float(r.gid));
     dec4[s] = make_float4(r.xh, r.yh, r.zh, __uint_as_float(r.i));
     xk[s] = x_sort_key(r.x, g);
-    if (s != s0) slot_of[r.i] = s;
+    fin[s0] = s;
+}
+
+__global__ void __launch_bounds__(BIN_THREADS) k_fix_slot_of(int64_t n, const uint32_t* __restrict__ fin,
+                                                             uint32_t* __restrict__ slot_of) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) slot_of[i] = fin[slot_of[i]];
 }
 
 __device__ __forceinline__ Rec load_rec(const Rec* __restrict__ rec, uint32_t s) {
@@ -386,20 +396,22 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
         cc_prof_end(c, tok);
         unsigned long long* nl = reinterpret_cast<unsigned long long*>(c->scratch_u64.p);
         int t2 = cc_prof_begin(c, "K1_finish");
+        uint32_t* fin = c->rnk.p;  // the ranks are dead after the scatter: final slot per provisional slot
         if (c->g.nx == 1) {  // cells are rows (default grid): one warp per cell
             CCL(c, k_row_finish<<<148 * 16, BIN_THREADS, 0, c->stream>>>(nc, c->cell_start.p, rec, c->g, c->orig4.p,
-                                                                          c->dec4.p, c->xk.p, c->slot_of.p,
-                                                                          c->scratch_u32.p, cap, nl));
+                                                                          c->dec4.p, c->xk.p, fin, c->scratch_u32.p,
+                                                                          cap, nl));
         } else {
             CCL(c, k_cell_finish<<<(unsigned)((nc + BIN_THREADS - 1) / BIN_THREADS), BIN_THREADS, 0, c->stream>>>(
-                       nc, c->cell_start.p, rec, c->g, c->orig4.p, c->dec4.p, c->xk.p, c->slot_of.p, c->scratch_u32.p,
+                       nc, c->cell_start.p, rec, c->g, c->orig4.p, c->dec4.p, c->xk.p, fin, c->scratch_u32.p,
                        cap, nl, c->bin_short_max));
             CCL(c, k_cell_finish_mid<<<148 * 8, BIN_THREADS, 0, c->stream>>>(c->scratch_u32.p, nl, c->cell_start.p,
                                                                               rec, c->g, c->orig4.p, c->dec4.p,
-                                                                              c->xk.p, c->slot_of.p));
+                                                                              c->xk.p, fin));
         }
         CCL(c, k_cell_finish_long<<<148 * 2, 512, 0, c->stream>>>(c->scratch_u32.p, cap, nl, c->cell_start.p, rec,
-                                                                  c->g, c->orig4.p, c->dec4.p, c->xk.p, c->slot_of.p));
+                                                                  c->g, c->orig4.p, c->dec4.p, c->xk.p, fin));
+        CCL(c, k_fix_slot_of<<<nb, BIN_THREADS, 0, c->stream>>>(n, fin, c->slot_of.p));
         cc_prof_end(c, t2);
         CC_CUDA(c, cudaGetLastError());
     }

@@ -253,6 +253,7 @@ struct cc_ctx {
     cc::DBuf<double> trace_l;
     cc::DBuf<unsigned char> tmp_bytes;  // scan scratch
     cc::DBuf<unsigned long long> codec_bsum;  // f1 edit log: block sums + total + error flag
+    cc::DBuf<unsigned long long> codec_status;  // f1 single-pass encode: per-tile look-back status, ticket, total
     cc::DBuf<float> in_f;        // cc_run host staging: 6 n floats
     cc::DBuf<uint32_t> in_gid;
 

@@ -208,6 +208,125 @@ __global__ void __launch_bounds__(CT) k_edit_fill(int64_t n, EncMask mk, const f
     }
 }
 
+// ---- single-pass encode (decoupled look-back): each block takes the next tile by ticket, builds
+// its flag words and edit count (the inputs are read once), publishes the count, sums its
+// predecessors' published counts / inclusive prefixes, and writes its edits at that offset.
+// Replaces pass 1 + scan + pass 3 when q is written (the count-only call keeps the two-pass path).
+constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_VAL = (1ull << 62) - 1ull;
+
+__global__ void __launch_bounds__(CT) k_edit_encode1(int64_t n, EncMask mk, const float* x, const float* y,
+                                                    const float* z, uint32_t* flags_w, int64_t nbytes,
+                                                    unsigned long long* __restrict__ status,
+                                                    unsigned int* __restrict__ ticket, double s, double xi_f,
+                                                    double lim, long long* q, int64_t cap,
+                                                    unsigned long long* total, unsigned int* err) {
+    __shared__ unsigned int tile_sh;
+    __shared__ unsigned long long base_sh;
+    if (threadIdx.x == 0) tile_sh = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const unsigned int tile = tile_sh;
+    const int lane = threadIdx.x & 31;
+    const float* h[3] = {mk.xh, mk.yh, mk.zh};
+    const float* p[3] = {mk.xc, mk.yc, mk.zc};
+    const float* org[3] = {x, y, z};
+    // pass A: masks (kept, 3 bits per sub-tile), flag words, bound check, count
+    uint32_t masks = 0u, cnt = 0u;
+    for (int t = 0; t < SUB; t++) {
+        const int64_t i0 = (int64_t)tile * TILE + t * CT;
+        if (i0 >= n) break;  // uniform over the block
+        const int64_t i = i0 + threadIdx.x;
+        uint32_t m3 = 0;
+        if (i < n) {
+            m3 = mk(i);
+            if (m3) {
+#pragma unroll
+                for (int a = 0; a < 3; a++)
+                    if ((m3 >> a & 1u) && fabs((double)p[a][i] - (double)h[a][i]) > lim) atomicOr(err, 1u);
+            }
+        }
+        masks |= m3 << (3 * t);
+        cnt += __popc(m3);
+        const int64_t wbase = (i0 + (threadIdx.x & ~31)) / 32 * 3;
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+            const int b = 32 * j + lane;
+            const uint32_t src = __shfl_sync(0xffffffffu, m3, b / 3);
+            const uint32_t word = __ballot_sync(0xffffffffu, (src >> (b % 3)) & 1u);
+            const int64_t wi = wbase + j;
+            if (lane == j) {
+                if (4 * wi + 4 <= nbytes) {
+                    flags_w[wi] = word;
+                } else {
+                    uint8_t* fb = reinterpret_cast<uint8_t*>(flags_w);
+                    for (int64_t qq = 4 * wi; qq < nbytes; qq++) fb[qq] = (uint8_t)(word >> (8 * (qq - 4 * wi)));
+                }
+            }
+        }
+    }
+    uint32_t tot;
+    (void)block_excl(cnt, &tot);  // the tile's edit count
+    // publish, look back, publish the inclusive prefix
+    if (threadIdx.x == 0) {
+        volatile unsigned long long* st = status;
+        if (tile == 0) {
+            st[0] = LB_PRE | (unsigned long long)tot;
+            base_sh = 0ull;
+        } else {
+            st[tile] = LB_AGG | (unsigned long long)tot;
+            __threadfence();
+            unsigned long long acc = 0ull;
+            long long pidx = (long long)tile - 1;
+            for (;;) {
+                unsigned long long v;
+                do {
+                    v = st[pidx];
+                } while ((v >> 62) == 0ull);
+                acc += v & LB_VAL;
+                if ((v >> 62) == 2ull) break;
+                pidx--;
+            }
+            base_sh = acc;
+            __threadfence();
+            st[tile] = LB_PRE | (acc + (unsigned long long)tot);
+        }
+        if ((int64_t)(tile + 1) * TILE >= n) *total = base_sh + tot;  // the last tile
+    }
+    __syncthreads();
+    int64_t base = (int64_t)base_sh;
+    // pass B: the edits in ascending k (sub-tile by sub-tile, R30, R32); values re-read only for
+    // flagged coordinates (the tile was just read: L2)
+    for (int t = 0; t < SUB; t++) {
+        const int64_t i0 = (int64_t)tile * TILE + t * CT;
+        if (i0 >= n) break;  // uniform over the block
+        const int64_t i = i0 + threadIdx.x;
+        const uint32_t m3 = (masks >> (3 * t)) & 7u;
+        uint32_t stot;
+        int64_t o = base + block_excl(__popc(m3), &stot);
+        base += stot;
+        if (!m3) continue;
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            if (m3 >> a & 1u) {
+                const double hv = (double)h[a][i];
+                const double d = (double)p[a][i] - hv;  // exact
+                long long qi = (long long)rint(d / s);
+                const double xo = (double)__ldg(org[a] + i);
+                for (int step = 0;; step++) {
+                    const double dev = (double)(float)(hv + (double)qi * s) - xo;
+                    if (fabs(dev) <= xi_f) break;
+                    if (step == 8) {
+                        atomicOr(err, 2u);
+                        break;
+                    }
+                    qi += dev > 0 ? -1 : 1;
+                }
+                if (o < cap) q[o] = qi;
+                o++;
+            }
+        }
+    }
+}
+
 // pass 3 (decode): x_rec = fl32((double)x_hat0 + (double)q s) where flagged, x_hat0 elsewhere (R31)
 __global__ void __launch_bounds__(CT) k_edit_apply(int64_t n, DecMask mk, const unsigned long long* bsum,
                                                    double s, const long long* q, int64_t n_edits,
@@ -376,6 +495,30 @@ cc_status cc_edit_encode(cc_ctx* c, int64_t n, const float* x, const float* y, c
     CC_CUDA(c, cudaMemsetAsync(err, 0, sizeof(unsigned long long), c->stream));
     const EncMask mk{xh0, yh0, zh0, xc, yc, zc};
     const int64_t nbytes = (3 * n + 7) / 8;
+    if (cap > 0 && std::getenv("CC_CODEC_TWO_PASS") == nullptr) {
+        // single pass (decoupled look-back); q must have room for every edit: if the count
+        // exceeds cap the call fails with CC_E_OOM after counting (q then holds the first cap)
+        CC_TRY(cc_ensure(c, c->codec_status, (size_t)nb + 2, "edit-log tile status"));
+        unsigned long long* st = c->codec_status.p;
+        CC_CUDA(c, cudaMemsetAsync(st, 0, ((size_t)nb + 2) * sizeof(unsigned long long), c->stream));
+        unsigned int* ticket = reinterpret_cast<unsigned int*>(st + nb);
+        unsigned long long* total = st + nb + 1;
+        int tok = cc_prof_begin(c, "F1_encode");
+        CCL(c, k_edit_encode1<<<(unsigned)nb, CT, 0, c->stream>>>(n, mk, x, y, z, reinterpret_cast<uint32_t*>(flags),
+                                                                  nbytes, st, ticket, s, xi, 2.0 * xi,
+                                                                  reinterpret_cast<long long*>(q), cap, total, err));
+        cc_prof_end(c, tok);
+        CC_CUDA(c, cudaGetLastError());
+        unsigned long long ht[2];
+        CC_CUDA(c, cudaMemcpyAsync(&ht[0], total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaMemcpyAsync(&ht[1], err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+        *n_edits_h = (int64_t)ht[0];
+        if ((unsigned int)ht[1] & 1u) return cc_fail(c, CC_E_BOUND, "an edit exceeds 2 xi_f (corrected coordinates out of bound)");
+        if ((int64_t)ht[0] > cap) return cc_fail(c, CC_E_OOM, "more edits than cap (*n_edits_h holds the count)");
+        if ((unsigned int)ht[1] & 2u) return cc_fail(c, CC_E_BOUND, "no lattice index reconstructs within xi_f (R32)");
+        return CC_OK;
+    }
     int tok = cc_prof_begin(c, "F1_encode");
     CCL(c, k_edit_flags<<<(unsigned)nb, CT, 0, c->stream>>>(n, mk, reinterpret_cast<uint32_t*>(flags), nbytes, bsum,
                                                            2.0 * xi, err));
