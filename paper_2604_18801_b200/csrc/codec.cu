@@ -265,31 +265,46 @@ __global__ void __launch_bounds__(CT) k_edit_encode1(int64_t n, EncMask mk, cons
     }
     uint32_t tot;
     (void)block_excl(cnt, &tot);  // the tile's edit count
-    // publish, look back, publish the inclusive prefix
-    if (threadIdx.x == 0) {
+    // publish, look back (warp 0, 32 predecessors per step), publish the inclusive prefix
+    if (threadIdx.x < 32) {
         volatile unsigned long long* st = status;
         if (tile == 0) {
-            st[0] = LB_PRE | (unsigned long long)tot;
-            base_sh = 0ull;
-        } else {
-            st[tile] = LB_AGG | (unsigned long long)tot;
-            __threadfence();
-            unsigned long long acc = 0ull;
-            long long pidx = (long long)tile - 1;
-            for (;;) {
-                unsigned long long v;
-                do {
-                    v = st[pidx];
-                } while ((v >> 62) == 0ull);
-                acc += v & LB_VAL;
-                if ((v >> 62) == 2ull) break;
-                pidx--;
+            if (lane == 0) {
+                st[0] = LB_PRE | (unsigned long long)tot;
+                base_sh = 0ull;
             }
-            base_sh = acc;
-            __threadfence();
-            st[tile] = LB_PRE | (acc + (unsigned long long)tot);
+        } else {
+            if (lane == 0) {
+                st[tile] = LB_AGG | (unsigned long long)tot;
+                __threadfence();
+            }
+            __syncwarp();
+            unsigned long long acc = 0ull;
+            long long top = (long long)tile - 1;  // predecessors top, top-1, ... in this window
+            for (;;) {
+                const long long pi = top - lane;
+                unsigned long long v = 0ull;
+                bool ready;
+                do {  // every lane waits for its predecessor to publish (they are all running)
+                    v = pi >= 0 ? st[pi] : (LB_PRE | 0ull);
+                    ready = (v >> 62) != 0ull;
+                } while (!__all_sync(0xffffffffu, ready));
+                const unsigned pre = __ballot_sync(0xffffffffu, (v >> 62) == 2ull);
+                const int stop = pre ? __ffs(pre) - 1 : 32;  // nearest predecessor with a prefix
+                unsigned long long add = lane <= stop && lane < 32 ? (v & LB_VAL) : 0ull;
+                if (stop == 32) add = v & LB_VAL;
+                for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+                acc += add;
+                if (pre) break;
+                top -= 32;
+            }
+            if (lane == 0) {
+                base_sh = acc;
+                __threadfence();
+                st[tile] = LB_PRE | (acc + (unsigned long long)tot);
+            }
         }
-        if ((int64_t)(tile + 1) * TILE >= n) *total = base_sh + tot;  // the last tile
+        if (lane == 0 && (int64_t)(tile + 1) * TILE >= n) *total = base_sh + tot;  // the last tile
     }
     __syncthreads();
     int64_t base = (int64_t)base_sh;

@@ -56,11 +56,10 @@ k_fof_link(int64_t n, const float4* __restrict__ P, const float4* __restrict__ o
 // read-only root walk: the flatten pass must not path-halve, or a halving write could land
 // after another thread's final par[x] = root and leave x pointing at a non-root
 __device__ __forceinline__ uint32_t uf_root(const uint32_t* par, uint32_t x) {
-    const volatile uint32_t* vp = par;
-    uint32_t p = vp[x];
+    uint32_t p = ld_rlx(par + x);
     while (p != x) {
         x = p;
-        p = vp[x];
+        p = ld_rlx(par + x);
     }
     return x;
 }
