@@ -5,6 +5,7 @@ OUT=gpurun_out/survey_$TAG
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || exit 1
 nvidia-smi -L > $OUT/gpu.txt; lscpu | grep -E "Model name|^CPU\(s\)" >> $OUT/gpu.txt
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout 900 > $OUT/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 $OUT/pytest_gpu.log
 run() { name=$1; shift; timeout ${TO:-900} python bench.py "$@" > $OUT/$name.json 2> $OUT/$name.err; echo "$name rc=$?"; }
 run default
 run reference --impl reference
