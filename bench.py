@@ -307,6 +307,7 @@ def main():
         gid = own.to(torch.int32)
         del own
     torch.cuda.synchronize(dev)
+    torch.cuda.empty_cache()  # the generator's fp64 temporaries (C5: ~100 GB) go back to the device
     n = x.shape[0]
     stop = {"restored": cc.STOP_RESTORED, "active": cc.STOP_ACTIVE, "eps": cc.STOP_EPS, "none": cc.STOP_NONE}[args.stop]
     params = cc.Params(box=w.L, b=w.linking_length, xi=w.xi, profile=1, t_max=args.t_max, stop_mode=stop)
@@ -344,6 +345,9 @@ def main():
         res = step()
         log(f"warmup {k}: {time.perf_counter() - t0:.3f} s wall, |V|={res[0]['n_pairs']:,} |E|={res[0]['n_editable']:,}"
             f" iterations={res[1]['iterations']} converged={res[1]['converged']} mcc={res[2]['mcc']:.6f}")
+    free_b, tot_b = torch.cuda.mem_get_info(dev)
+    log(f"device memory in use after warm-up: {(tot_b - free_b) / 2**30:.1f} GiB of {tot_b / 2**30:.1f} GiB "
+        f"({(tot_b - free_b) / max(n, 1):.0f} B per local particle)")
     c.kernel_stats(reset=True)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]

@@ -356,7 +356,7 @@ void cc_destroy(cc_ctx* c) {
     cc_release(c, c->key); cc_release(c, c->rnk); cc_release(c, c->cell_count); cc_release(c, c->cell_start);
     cc_release(c, c->slot_of); cc_release(c, c->deg); cc_release(c, c->eidx); cc_release(c, c->rows);
     cc_release(c, c->slotE); cc_release(c, c->parent); cc_release(c, c->mingid); cc_release(c, c->gsize);
-    cc_release(c, c->scratch_u32); cc_release(c, c->rowoff); cc_release(c, c->rowptr); cc_release(c, c->scratch_u64);
+    cc_release(c, c->scratch_u32); cc_release(c, c->rowptr); cc_release(c, c->scratch_u64);
     cc_release(c, c->mom); cc_release(c, c->bc); 
     cc_release(c, c->counters); cc_release(c, c->ctl); cc_release(c, c->trace_a); cc_release(c, c->trace_l);
     cc_release(c, c->trace_v); cc_release(c, c->trace_s); cc_release(c, c->parent_base); cc_release(c, c->parent_orig); cc_release(c, c->rec32);
@@ -459,12 +459,21 @@ cc_status cc_find_vulnerable(cc_ctx* c, cc_vp_info* info) {
     if (c->state < 1) return cc_fail(c, CC_E_STATE, "cc_build_cells first");
     const int64_t n = c->n;
     CC_TRY(cc::pairs_count(c));
-    CC_TRY(cc_ensure(c, c->rowoff, (size_t)std::max<int64_t>(n, 1), "rowoff"));
     CC_TRY(cc_ensure(c, c->eidx, (size_t)std::max<int64_t>(n, 1), "eidx"));
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
-    CC_TRY(cc_ensure(c, c->key, (size_t)std::max<int64_t>(n, 1), "row class"));  // key is dead after K1
+    CC_TRY(cc_ensure(c, c->key, (size_t)std::max<int64_t>(n, 1), "editable list"));  // key is dead after K1
+    // S3: the editable list (slots with deg != 0, one pass over deg), then the class scan over it
+    int64_t e_all = 0;
+    CC_TRY(cc::editable_list(c, &e_all));
+    if (e_all >= cc::MAX_LOCAL) return cc_fail(c, CC_E_DATA, "editable set beyond the 2^30 index space");
+    const size_t e1 = (size_t)std::max<int64_t>(e_all, 1);
+    CC_TRY(cc_ensure(c, c->slotE, e1, "slotE"));
+    CC_TRY(cc_ensure(c, c->rowptr, e1 + 1, "rowptr"));
+    CC_TRY(cc_ensure(c, c->origE, e1, "origE"));
+    CC_TRY(cc_ensure(c, c->posA, e1, "posA"));
+    CC_TRY(cc_ensure(c, c->posB, e1, "posB"));
     unsigned long long* tot = c->counters.p + 2;  // 56-byte VDeg total at counters[2..8]
-    CC_TRY(cc::scan_deg(c, c->deg.p, c->rowoff.p, c->eidx.p, c->key.p, n, tot));
+    CC_TRY(cc::scan_editables(c, e_all, tot));
     CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 2, tot, 7 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                c->stream));
     CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 11, c->near_n.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -474,7 +483,7 @@ cc_status cc_find_vulnerable(cc_ctx* c, cc_vp_info* info) {
     unsigned long long totals[7];
     std::memcpy(totals, c->h_counters + 2, sizeof(totals));
     CC_TRY(cc::rows_resolve(c, totals));
-    if (c->E_all >= cc::MAX_LOCAL) return cc_fail(c, CC_E_DATA, "editable set beyond the 2^30 index space");
+    if (c->E_all != e_all) return cc_fail(c, CC_E_DATA, "editable list and class scan disagree");
     CC_TRY(cc::rows_finish(c));
     if (c->nranks > 1) CC_TRY(cc::dist_setup_refresh(c));
     c->state = 2;

@@ -24,6 +24,7 @@ constexpr int BIN_THREADS = 256;
 constexpr int CELL_SHORT = 16;
 constexpr int CELL_MID = 64;    // 17..64: one warp per cell (k_cell_finish_mid)
 constexpr int CELL_LONG_MAX = 4096;
+constexpr int ROW_WIDE = 512;  // 65..512: one warp per row, bitonic in the warp's shared memory
 
 struct __align__(16) Rec {
     float x, y, z, xh;
@@ -236,8 +237,11 @@ k_row_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restri
         const uint32_t a = cs[c], b = cs[c + 1];
         const int len = (int)(b - a);
         if (len == 0) continue;
-        if (len > CELL_MID) {
-            if (lane == 0) long_list[cap - 1 - atomicAdd(n_long + 1, 1ull)] = (uint32_t)c;
+        if (len > CELL_MID) {  // 65..512: k_row_finish_wide (front of the list); longer: the block kernel
+            if (lane == 0) {
+                if (len <= ROW_WIDE) long_list[atomicAdd(n_long, 1ull)] = (uint32_t)c;
+                else long_list[cap - 1 - atomicAdd(n_long + 1, 1ull)] = (uint32_t)c;
+            }
             continue;
         }
         if (len <= 32) {
@@ -292,11 +296,63 @@ k_row_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restri
     }
 }
 
+// crowded rows of 65..512 records (halo cores): one warp per row, bitonic sort of (key, local
+// offset) in the warp's own shared-memory slice with __syncwarp steps -- a 512-thread block per
+// row idled most of its threads and synchronised the whole block every step
+constexpr int WIDE_WARPS = 8;
+
+__global__ void __launch_bounds__(32 * WIDE_WARPS)
+k_row_finish_wide(const uint32_t* __restrict__ long_list, const unsigned long long* __restrict__ n_long,
+                  const uint32_t* __restrict__ cs, const Rec* __restrict__ rec, Grid g, float4* __restrict__ orig4,
+                  float4* __restrict__ dec4, uint32_t* __restrict__ xk, uint32_t* __restrict__ slot_of) {
+    __shared__ unsigned long long shk[WIDE_WARPS][ROW_WIDE];
+    __shared__ unsigned short sho[WIDE_WARPS][ROW_WIDE];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned long long* sk = shk[w];
+    unsigned short* so = sho[w];
+    const unsigned long long nm = n_long[0];
+    const unsigned long long nw = (unsigned long long)gridDim.x * WIDE_WARPS;
+    for (unsigned long long q = (unsigned long long)blockIdx.x * WIDE_WARPS + w; q < nm; q += nw) {
+        const uint32_t c = long_list[q];
+        const uint32_t a = cs[c], b = cs[c + 1];
+        const int len = (int)(b - a);
+        int p2 = 64;
+        while (p2 < len) p2 <<= 1;
+        for (int i = lane; i < p2; i += 32) {
+            sk[i] = i < len ? rec_key(load_rec(rec, a + i), g) : ~0ull;  // unique keys (input index)
+            so[i] = (unsigned short)i;
+        }
+        __syncwarp();
+        for (int k = 2; k <= p2; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                // p2 / 2 compare-exchanges: pair index t -> lower element i (bit j of i clear)
+                for (int t = lane; t < (p2 >> 1); t += 32) {
+                    const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+                    const int ij = i | j;
+                    const bool up = (i & k) == 0;
+                    const unsigned long long x0 = sk[i], x1 = sk[ij];
+                    if ((x0 > x1) == up) {
+                        sk[i] = x1;
+                        sk[ij] = x0;
+                        const unsigned short t0 = so[i];
+                        so[i] = so[ij];
+                        so[ij] = t0;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        for (int k = lane; k < len; k += 32) emit(load_rec(rec, a + so[k]), a + k, a + so[k], orig4, dec4, xk, slot_of, g);
+        __syncwarp();
+    }
+}
+
 // crowded cells: one block per cell, bitonic sort of (key, local offset) in shared memory
 __global__ void __launch_bounds__(512)
 k_cell_finish_long(const uint32_t* __restrict__ long_list, uint64_t cap, const unsigned long long* __restrict__ n_long,
                    const uint32_t* __restrict__ cs, const Rec* __restrict__ rec, Grid g, float4* __restrict__ orig4,
-                   float4* __restrict__ dec4, uint32_t* __restrict__ xk, uint32_t* __restrict__ slot_of) {
+                   float4* __restrict__ dec4, uint32_t* __restrict__ xk, uint32_t* __restrict__ slot_of,
+                   uint32_t* __restrict__ offs) {
     __shared__ unsigned long long sh[CELL_LONG_MAX];
     __shared__ unsigned short so[CELL_LONG_MAX];
     const unsigned long long nl = n_long[1];
@@ -334,23 +390,17 @@ k_cell_finish_long(const uint32_t* __restrict__ long_list, uint64_t cap, const u
             for (int k = threadIdx.x; k < len; k += blockDim.x)
                 emit(load_rec(rec, a + so[k]), a + k, a + so[k], orig4, dec4, xk, slot_of, g);
             __syncthreads();
-        } else if (threadIdx.x == 0) {
-            // pathological crowding: selection by repeated minimum (correct, slow)
-            unsigned long long prev = 0;
-            for (int k = 0; k < len; k++) {
-                unsigned long long best = ~0ull;
-                uint32_t bq = 0;
-                for (int q2 = 0; q2 < len; q2++) {
-                    const Rec r = load_rec(rec, a + q2);
-                    const unsigned long long kk = ((unsigned long long)x_sort_key(r.x, g) << 32) | r.i;
-                    if ((k == 0 || kk > prev) && kk < best) {
-                        best = kk;
-                        bq = q2;
-                    }
-                }
-                emit(load_rec(rec, a + bq), a + k, a + bq, orig4, dec4, xk, slot_of, g);
-                prev = best;
-            }
+        } else {
+            // beyond shared memory: sort the row's local offsets in place in global memory (the
+            // row's own slot range of the dead key array), keys gathered from the records
+            uint32_t* off = offs + a;
+            for (int k = threadIdx.x; k < len; k += blockDim.x) off[k] = (uint32_t)k;
+            __syncthreads();
+            const Rec* ra = rec + a;
+            block_sort_global(off, (int64_t)len, [ra, g](uint32_t o) { return rec_key(load_rec(ra, o), g); });
+            for (int k = threadIdx.x; k < len; k += blockDim.x)
+                emit(load_rec(rec, a + off[k]), a + k, a + off[k], orig4, dec4, xk, slot_of, g);
+            __syncthreads();
         }
     }
 }
@@ -401,6 +451,10 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
             CCL(c, k_row_finish<<<148 * 16, BIN_THREADS, 0, c->stream>>>(nc, c->cell_start.p, rec, c->g, c->orig4.p,
                                                                           c->dec4.p, c->xk.p, fin, c->scratch_u32.p,
                                                                           cap, nl));
+            CCL(c, k_row_finish_wide<<<148 * 4, 32 * WIDE_WARPS, 0, c->stream>>>(c->scratch_u32.p, nl,
+                                                                                  c->cell_start.p, rec, c->g,
+                                                                                  c->orig4.p, c->dec4.p, c->xk.p,
+                                                                                  fin));
         } else {
             CCL(c, k_cell_finish<<<(unsigned)((nc + BIN_THREADS - 1) / BIN_THREADS), BIN_THREADS, 0, c->stream>>>(
                        nc, c->cell_start.p, rec, c->g, c->orig4.p, c->dec4.p, c->xk.p, fin, c->scratch_u32.p,
@@ -410,7 +464,8 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
                                                                               c->xk.p, fin));
         }
         CCL(c, k_cell_finish_long<<<148 * 2, 512, 0, c->stream>>>(c->scratch_u32.p, cap, nl, c->cell_start.p, rec,
-                                                                  c->g, c->orig4.p, c->dec4.p, c->xk.p, fin));
+                                                                  c->g, c->orig4.p, c->dec4.p, c->xk.p, fin,
+                                                                  c->key.p));
         CCL(c, k_fix_slot_of<<<nb, BIN_THREADS, 0, c->stream>>>(n, fin, c->slot_of.p));
         cc_prof_end(c, t2);
         CC_CUDA(c, cudaGetLastError());

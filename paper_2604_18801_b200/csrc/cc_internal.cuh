@@ -5,8 +5,8 @@
 //     orig4[s] = (x, y, z, gid bits)          float4, original P           (S1)
 //     dec4[s]  = (xh, yh, zh, input index i)  float4, decompressed P_hat^(0)
 //     cell_start[c]  u32 (n_cell + 1), slot_of[i] u32 (input index -> slot)
-//     deg[s] u32, rowoff[s] u64 (exclusive scan of deg), eidx[s] u32 (editable rank)
-//   per editable particle e (compacted in slot order, S3):
+//     deg[s] u32 (band partners), eidx[s] u32 (editable index or 0xFFFFFFFF)
+//   per editable particle e (class-major, slot order within a class, S3):
 //     posA/posB[e] float4 (x, y, z, gid bits) ping-pong, origE[e] float4, slotE[e] u32,
 //     rowptr[e] u64, Adam moments m,v as 6 float SoA arrays
 //   rows[k] u32 (2|V| directed entries, sorted by partner gid within a row):
@@ -229,7 +229,7 @@ struct cc_ctx {
     bool cor4_valid = false;  // cor4 matches the last cc_correct (built on demand)
     cc::DBuf<uint32_t> key, rnk, cell_count, cell_start, slot_of, deg, eidx, rows, slotE, parent, mingid,
         gsize, scratch_u32;
-    cc::DBuf<uint64_t> rowoff, rowptr, scratch_u64;
+    cc::DBuf<uint64_t> rowptr, scratch_u64;
     cc::DBuf<uint32_t> xk;       // x_sort_key of the original x per slot (the in-row search key)
     cc::DBuf<uint4> rec32;       // K1 binning records, 2 x uint4 = 32 B per particle
     cc::DBuf<uint32_t> parent_base;  // FoF forest of the stable links (d2 <= lo2), per build
@@ -685,6 +685,80 @@ __device__ __forceinline__ void for_each_pair_forward(const Grid& g, const uint3
 
 // per-warp sum of a per-thread counter into a global total (one atomic per warp; callable after
 // an early return of some lanes)
+// ascending in-place sort of v[0..len) in global memory by one block, for the rare rows too long
+// for shared memory (K1 rows, K2 rows): bitonic network in its all-ascending form (each merge
+// phase opens with the mirror comparator i <-> i ^ (kk-1), then half-cleaners i <-> i | j), so
+// every comparator puts the minimum at the lower index and the virtual +inf padding beyond len
+// never moves: comparators reaching past len are skipped.  key(x) = a unique sort key.
+// O(len log^2 len) comparators, block-synchronised per step.
+template <class T, class K>
+__device__ void block_sort_global(T* v, int64_t len, const K& key) {
+    int64_t p2 = 1;
+    while (p2 < len) p2 <<= 1;
+    for (int64_t kk = 2; kk <= p2; kk <<= 1) {
+        for (int64_t j = kk >> 1; j > 0; j >>= 1) {
+            for (int64_t t = threadIdx.x; t < (p2 >> 1); t += blockDim.x) {
+                const int64_t i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+                const int64_t q = (j == (kk >> 1)) ? (i ^ (kk - 1)) : (i | j);
+                if (q < len) {
+                    const T a = v[i], b = v[q];
+                    if (key(a) > key(b)) {
+                        v[i] = b;
+                        v[q] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// decoupled look-back of the single-pass scans (K2's editable list, f1's encode).  A tile's
+// status word = 2 flag bits (aggregate published / inclusive prefix published) | 62-bit value.
+// Called by warp 0 of the block owning `tile` with the tile's aggregate: publishes it, sums the
+// predecessors' values (32 per step) back to the nearest published inclusive prefix, publishes
+// its own inclusive prefix and returns the exclusive prefix (on every lane).  Tiles are taken in
+// ticket order, so every predecessor is running or done: the spin terminates.
+constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_VAL = (1ull << 62) - 1ull;
+
+__device__ __forceinline__ unsigned long long lookback_warp0(unsigned long long* status, unsigned tile,
+                                                             unsigned long long tot) {
+    const int lane = threadIdx.x & 31;
+    volatile unsigned long long* st = status;
+    if (tile == 0) {
+        if (lane == 0) st[0] = LB_PRE | tot;
+        return 0ull;
+    }
+    if (lane == 0) {
+        st[tile] = LB_AGG | tot;
+        __threadfence();
+    }
+    __syncwarp();
+    unsigned long long acc = 0ull;
+    long long top = (long long)tile - 1;  // predecessors top, top-1, ... in this window
+    for (;;) {
+        const long long pi = top - lane;
+        unsigned long long v = 0ull;
+        bool ready;
+        do {
+            v = pi >= 0 ? st[pi] : (LB_PRE | 0ull);
+            ready = (v >> 62) != 0ull;
+        } while (!__all_sync(0xffffffffu, ready));
+        const unsigned pre = __ballot_sync(0xffffffffu, (v >> 62) == 2ull);
+        const int stop = pre ? __ffs(pre) - 1 : 32;  // nearest predecessor with a prefix
+        unsigned long long add = lane <= stop ? (v & LB_VAL) : 0ull;
+        for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+        acc += add;
+        if (pre) break;
+        top -= 32;
+    }
+    if (lane == 0) {
+        __threadfence();
+        st[tile] = LB_PRE | (acc + tot);
+    }
+    return acc;
+}
+
 __device__ __forceinline__ void warp_count(unsigned long long* dst, unsigned v) {
     const unsigned m = __activemask();
     const unsigned x = __reduce_add_sync(m, v);
@@ -746,8 +820,8 @@ void cc_prof_end(cc_ctx* c, int token);
 // launch wrappers (each .cu file)
 namespace cc {
 cc_status scan_u32_to_u32(cc_ctx* c, const uint32_t* in, uint32_t* out, int64_t n, uint64_t* total_dev);
-cc_status scan_deg(cc_ctx* c, const uint32_t* deg, uint64_t* rowoff, uint32_t* eidx, uint32_t* cls, int64_t n,
-                   unsigned long long* totals_dev);
+cc_status editable_list(cc_ctx* c, int64_t* e_all);
+cc_status scan_editables(cc_ctx* c, int64_t e_all, unsigned long long* totals_dev);
 cc_status rows_resolve(cc_ctx* c, const unsigned long long* totals_h);
 cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* z, const float* xh,
                         const float* yh, const float* zh, const uint32_t* gid, int64_t n);

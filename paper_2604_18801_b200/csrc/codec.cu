@@ -212,7 +212,6 @@ __global__ void __launch_bounds__(CT) k_edit_fill(int64_t n, EncMask mk, const f
 // its flag words and edit count (the inputs are read once), publishes the count, sums its
 // predecessors' published counts / inclusive prefixes, and writes its edits at that offset.
 // Replaces pass 1 + scan + pass 3 when q is written (the count-only call keeps the two-pass path).
-constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_VAL = (1ull << 62) - 1ull;
 
 __global__ void __launch_bounds__(CT) k_edit_encode1(int64_t n, EncMask mk, const float* x, const float* y,
                                                     const float* z, uint32_t* flags_w, int64_t nbytes,
@@ -267,43 +266,8 @@ __global__ void __launch_bounds__(CT) k_edit_encode1(int64_t n, EncMask mk, cons
     (void)block_excl(cnt, &tot);  // the tile's edit count
     // publish, look back (warp 0, 32 predecessors per step), publish the inclusive prefix
     if (threadIdx.x < 32) {
-        volatile unsigned long long* st = status;
-        if (tile == 0) {
-            if (lane == 0) {
-                st[0] = LB_PRE | (unsigned long long)tot;
-                base_sh = 0ull;
-            }
-        } else {
-            if (lane == 0) {
-                st[tile] = LB_AGG | (unsigned long long)tot;
-                __threadfence();
-            }
-            __syncwarp();
-            unsigned long long acc = 0ull;
-            long long top = (long long)tile - 1;  // predecessors top, top-1, ... in this window
-            for (;;) {
-                const long long pi = top - lane;
-                unsigned long long v = 0ull;
-                bool ready;
-                do {  // every lane waits for its predecessor to publish (they are all running)
-                    v = pi >= 0 ? st[pi] : (LB_PRE | 0ull);
-                    ready = (v >> 62) != 0ull;
-                } while (!__all_sync(0xffffffffu, ready));
-                const unsigned pre = __ballot_sync(0xffffffffu, (v >> 62) == 2ull);
-                const int stop = pre ? __ffs(pre) - 1 : 32;  // nearest predecessor with a prefix
-                unsigned long long add = lane <= stop && lane < 32 ? (v & LB_VAL) : 0ull;
-                if (stop == 32) add = v & LB_VAL;
-                for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
-                acc += add;
-                if (pre) break;
-                top -= 32;
-            }
-            if (lane == 0) {
-                base_sh = acc;
-                __threadfence();
-                st[tile] = LB_PRE | (acc + (unsigned long long)tot);
-            }
-        }
+        const unsigned long long ex = lookback_warp0(status, tile, tot);
+        if (lane == 0) base_sh = ex;
         if (lane == 0 && (int64_t)(tile + 1) * TILE >= n) *total = base_sh + tot;  // the last tile
     }
     __syncthreads();

@@ -14,6 +14,7 @@
 // sorted by partner gid so the PGD gradient sum has one defined order on any grid / rank (R14).
 // Each unordered pair is tested from both endpoints: both see the identical pinned fp32 d2.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "cc_internal.cuh"
@@ -23,31 +24,35 @@ namespace {
 
 constexpr int PAIR_THREADS = 256;
 
-// pass 1 (each unordered pair once, for_each_pair_forward): deg[] = band partners per slot
-// (atomics for the far endpoint), ghost endpoints of band pairs with an owned partner get bit 31
-// of their deg word (multi-GPU: they become ghost editables); stable links (d2 <= lo2) are
-// united into the stable FoF forest in the same sweep.
-__global__ void __launch_bounds__(PAIR_THREADS)
-k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
-              const uint32_t* __restrict__ xk, const uint32_t* __restrict__ cs, Grid g, Th t, double r, uint32_t n_own,
-              uint32_t* __restrict__ deg, uint32_t* __restrict__ par_base, uint2* __restrict__ near,
-              unsigned long long* __restrict__ near_n, unsigned long long near_cap, unsigned long long* __restrict__ tests) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
-    unsigned ntest = 0;  // pair tests (candidates evaluated), reported as tests/s
-    const bool multi = n_own < (uint32_t)n;
-    const bool ghost = multi && __float_as_uint(dec4[s].w) >= n_own;
-    const float4 p = orig4[s];
-    double u;
-    int cx, cy, cz;
-    cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
-    const bool inner = interior(p.x, p.y, p.z, g, t);
-    const float lo2s = inner ? t.lo2s_i : t.lo2s_w, hi2s = inner ? t.hi2s_i : t.hi2s_w;
-    uint32_t cnt = 0;
-    uint32_t rs = (uint32_t)s;  // cached ancestor of s in the stable forest (uf_link)
-    auto test = [&](uint32_t j) {
+// the count sweep's per-candidate work (shared by the two count kernels): band pair -> degrees;
+// stable link -> the stable forest; near shell -> the near list
+struct CountCtx {
+    const float4* __restrict__ dec4;
+    const Th& t;  // the kernel's parameter (no copy)
+    uint32_t n_own;
+    bool multi, ghost, inner;
+    float lo2s, hi2s;
+    uint32_t s;
+    float4 p;
+    uint32_t cnt, rs, ntest;
+    uint32_t* __restrict__ deg;
+    uint32_t* __restrict__ par_base;
+    uint2* __restrict__ near;
+    unsigned long long* __restrict__ near_n;
+    unsigned long long near_cap;
+    __device__ __forceinline__ CountCtx(int64_t n, const float4* dec4_, const Grid& g, const Th& t_, uint32_t n_own_,
+                                        uint32_t* deg_, uint32_t* par_base_, uint2* near_, unsigned long long* near_n_,
+                                        unsigned long long near_cap_, uint32_t s_, const float4& p_)
+        : dec4(dec4_), t(t_), n_own(n_own_), s(s_), p(p_), cnt(0), rs(s_), ntest(0), deg(deg_), par_base(par_base_),
+          near(near_), near_n(near_n_), near_cap(near_cap_) {
+        multi = n_own < (uint32_t)n;
+        ghost = multi && __float_as_uint(dec4[s].w) >= n_own;
+        inner = interior(p.x, p.y, p.z, g, t);
+        lo2s = inner ? t.lo2s_i : t.lo2s_w;
+        hi2s = inner ? t.hi2s_i : t.hi2s_w;
+    }
+    __device__ __forceinline__ void operator()(uint32_t j, const float4& q) {
         ntest++;
-        const float4 q = orig4[j];
         const float d2 = inner ? dist2_nw(p, q) : dist2(p, q, t);
         if (t.lo2 < d2 && d2 <= t.hi2) {
             const bool gj = multi && __float_as_uint(dec4[j].w) >= n_own;
@@ -62,38 +67,207 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
         } else if (d2 <= lo2s) {
             // a stable FoF link: provably linked in the original, decompressed and corrected
             // positions alike (Th::lo2s, fof.cu), united here in the same candidate sweep
-            uf_link(par_base, (uint32_t)s, j, rs);
+            uf_link(par_base, s, j, rs);
         } else if (d2 <= hi2s) {
             // near shell (lo2s, lo2] or (hi2, hi2s]: not vulnerable, but fp32 rounding could flip
             // its link in other positions -- listed, re-tested by every FoF labelling
-            const unsigned long long q = atomicAdd(near_n, 1ull);
-            if (q < near_cap) near[q] = make_uint2((uint32_t)s, j | (d2 <= t.b2 ? 0x80000000u : 0u));
+            const unsigned long long qn = atomicAdd(near_n, 1ull);
+            if (qn < near_cap) near[qn] = make_uint2(s, j | (d2 <= t.b2 ? 0x80000000u : 0u));
         }
-    };
-    for_each_pair_forward(g, cs, xk, (uint32_t)s, u, cy, cz, r, t.periodic != 0, test);
-    if (cnt) atomicAdd(&deg[s], cnt);
-    warp_count(tests, ntest);
-}
-
-// after the scan: editable ranks and row offsets become global (class-major numbering: class
-// bases first, ghost editables after all owned ones)
-struct ClassBases {
-    uint32_t e[4];
-    unsigned long long off[4];
+    }
 };
-__global__ void k_resolve(int64_t n, const uint32_t* __restrict__ cls, ClassBases cb, uint32_t e_own,
-                          uint32_t* __restrict__ eidx, unsigned long long* __restrict__ rowoff) {
+
+// pass 1 (each unordered pair once, for_each_pair_forward): deg[] = band partners per slot
+// (atomics for the far endpoint), ghost endpoints of band pairs with an owned partner get bit 31
+// of their deg word (multi-GPU: they become ghost editables); stable links (d2 <= lo2s) are
+// united into the stable FoF forest in the same sweep.  (General grid; k_pairs_count_tiled below
+// is the default-grid form.)
+__global__ void __launch_bounds__(PAIR_THREADS)
+k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
+              const uint32_t* __restrict__ xk, const uint32_t* __restrict__ cs, Grid g, Th t, double r, uint32_t n_own,
+              uint32_t* __restrict__ deg, uint32_t* __restrict__ par_base, uint2* __restrict__ near,
+              unsigned long long* __restrict__ near_n, unsigned long long near_cap, unsigned long long* __restrict__ tests) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    const uint32_t k = cls[s];
-    if (k <= 3u) {
-        eidx[s] += cb.e[k];
-        rowoff[s] += cb.off[k];
-    } else if (k == 4u) {
-        eidx[s] += e_own;
-    } else {
-        eidx[s] = 0xFFFFFFFFu;
+    const float4 p = orig4[s];
+    double u;
+    int cx, cy, cz;
+    cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
+    CountCtx k(n, dec4, g, t, n_own, deg, par_base, near, near_n, near_cap, (uint32_t)s, p);
+    auto test = [&](uint32_t j) { k(j, orig4[j]); };
+    for_each_pair_forward(g, cs, xk, (uint32_t)s, u, cy, cz, r, t.periodic != 0, test);
+    if (k.cnt) atomicAdd(&deg[s], k.cnt);
+    warp_count(tests, k.ntest);
+}
+
+// ---- the default grid (cells = whole rows, periodic or not, >= 3 rows per axis): a block takes
+// a strip of TROWS consecutive rows of one z-row and stages in shared memory every row the strip's
+// half-shell visits -- rows y0..y0+TROWS of z-row z and y0-1..y0+TROWS of z-row z+1, contiguous
+// slot ranges loaded coalesced -- then each thread searches its home particle's windows with
+// binary searches and candidate reads in shared memory (the north_star's staged home cell).  The
+// per-particle global form is latency-bound on dependent window loads (ncu: ISETP stalls on the
+// binary-search loads).  A strip whose rows exceed the staging capacity (dense halo cores) runs
+// the global form for its home particles.
+constexpr int TROWS_MAX = 16;
+constexpr int TCAP = 2048;
+constexpr int TDIR = 2 * TROWS_MAX + 3;
+
+struct RowDir {
+    uint32_t g0;  // global slot of the row's first particle
+    uint32_t n;   // particles (0: row outside a non-periodic domain)
+    uint32_t s0;  // its first staged index
+};
+
+template <class F>
+__device__ __forceinline__ void scan_staged(const uint32_t* sxk, const float4* so4, const RowDir& d, uint32_t klo,
+                                            uint32_t khi, F& f) {
+    uint32_t lo = d.s0, hi = d.s0 + d.n;
+    while (lo < hi) {  // first staged index with key >= klo
+        const uint32_t m = (lo + hi) >> 1;
+        if (sxk[m] < klo) lo = m + 1;
+        else hi = m;
     }
+    for (uint32_t k = lo; k < d.s0 + d.n; k++) {
+        if (sxk[k] > khi) break;
+        f(d.g0 + (k - d.s0), so4[k]);
+    }
+}
+
+__global__ void __launch_bounds__(PAIR_THREADS)
+k_pairs_count_tiled(int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
+                    const uint32_t* __restrict__ xk, const uint32_t* __restrict__ cs, Grid g, Th t, double r,
+                    uint32_t n_own, uint32_t* __restrict__ deg, uint32_t* __restrict__ par_base,
+                    uint2* __restrict__ near, unsigned long long* __restrict__ near_n, unsigned long long near_cap,
+                    unsigned long long* __restrict__ tests, int64_t ntiles, int tiles_y, int trows) {
+    __shared__ float4 so4[TCAP];
+    __shared__ uint32_t sxk[TCAP];
+    __shared__ RowDir dir[TDIR];
+    __shared__ uint32_t total_sh;
+    const bool periodic = t.periodic != 0;
+    unsigned ntest = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int z = (int)(tile / tiles_y), y0 = (int)(tile % tiles_y) * trows;
+        const int ky = min(trows, g.ny - y0);
+        const int nd = 2 * ky + 3;  // dir: [0, ky] z-row z, rows y0..y0+ky; [ky+1, 2ky+2] z-row z+1, y0-1..y0+ky
+        if (threadIdx.x < nd) {
+            const int idx = threadIdx.x;
+            int zz, yy;
+            bool use = true;
+            if (idx <= ky) {
+                zz = z;
+                yy = y0 + idx;
+            } else {
+                zz = z + 1;
+                yy = y0 - 1 + (idx - ky - 1);
+            }
+            if (periodic) {
+                zz = wrapi(zz, g.nz);
+                yy = wrapi(yy, g.ny);
+            } else if (zz < 0 || zz >= g.nz || yy < 0 || yy >= g.ny) {
+                use = false;
+            }
+            RowDir d;
+            d.g0 = 0u;
+            d.n = 0u;
+            if (use) {
+                const int64_t row = (int64_t)zz * g.ny + yy;
+                d.g0 = cs[row];
+                d.n = cs[row + 1] - d.g0;
+            }
+            dir[idx] = d;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t off = 0;
+            for (int i = 0; i < nd; i++) {
+                dir[i].s0 = off;
+                off += dir[i].n;
+            }
+            total_sh = off;
+        }
+        __syncthreads();
+        const uint32_t total = total_sh;
+        const uint32_t h0 = dir[0].g0;
+        const uint32_t h1 = cs[(int64_t)z * g.ny + y0 + ky];  // home rows: contiguous slots
+        if (total > (uint32_t)TCAP) {
+            // crowded strip: the global per-particle form for its home particles
+            for (uint32_t s = h0 + threadIdx.x; s < h1; s += blockDim.x) {
+                const float4 p = orig4[s];
+                double u;
+                int cx, cy, cz;
+                cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
+                CountCtx k(n, dec4, g, t, n_own, deg, par_base, near, near_n, near_cap, s, p);
+                auto test = [&](uint32_t j) { k(j, orig4[j]); };
+                for_each_pair_forward(g, cs, xk, s, u, cy, cz, r, periodic, test);
+                if (k.cnt) atomicAdd(&deg[s], k.cnt);
+                ntest += k.ntest;
+            }
+            __syncthreads();
+            continue;
+        }
+        // stage the rows (each a contiguous slot range; a warp per row)
+        for (int i = threadIdx.x >> 5; i < nd; i += blockDim.x >> 5) {
+            const RowDir d = dir[i];
+            for (uint32_t q = threadIdx.x & 31u; q < d.n; q += 32u) {
+                so4[d.s0 + q] = orig4[d.g0 + q];
+                sxk[d.s0 + q] = xk[d.g0 + q];
+            }
+        }
+        __syncthreads();
+        for (uint32_t s = h0 + threadIdx.x; s < h1; s += blockDim.x) {
+            // home row of s: the dir entry whose slot range holds s
+            int hr = 0;
+            while (hr + 1 < ky && s >= dir[hr + 1].g0) hr++;
+            const RowDir hd = dir[hr];
+            const uint32_t si = hd.s0 + (s - hd.g0);  // staged index of s
+            const float4 p = so4[si];
+            const double u = local_u((double)p.x, g);
+            CountCtx k(n, dec4, g, t, n_own, deg, par_base, near, near_n, near_cap, s, p);
+            // x-window key bounds, once for all rows (as for_each_pair_forward)
+            double a = u - r, b = u + r, a1 = 0.0, b1 = -1.0;
+            bool up = false;
+            if (g.xwrap) {
+                if (a < 0.0) {
+                    a1 = a + g.L;
+                    b1 = g.L;
+                    a = 0.0;
+                } else if (b >= g.L) {
+                    a1 = 0.0;
+                    b1 = b - g.L;
+                    b = g.L;
+                    up = true;
+                }
+            } else {
+                if (a < 0.0) a = 0.0;
+                if (b > g.ext_x) b = g.ext_x;
+            }
+            const bool two = b1 >= a1;
+            const uint32_t klo0 = key_lo(a, g), khi0 = key_hi(b, g);
+            const uint32_t klo1 = two ? key_lo(a1, g) : 0u, khi1 = two ? key_hi(b1, g) : 0u;
+            // own row: forward in slot (= x) order, then the part above the seam at the row start
+            for (uint32_t q = si + 1; q < hd.s0 + hd.n; q++) {
+                if (sxk[q] > khi0) break;
+                k(hd.g0 + (q - hd.s0), so4[q]);
+            }
+            if (two && up)
+                for (uint32_t q = hd.s0; q < si; q++) {
+                    if (sxk[q] > khi1) break;
+                    k(hd.g0 + (q - hd.s0), so4[q]);
+                }
+            // (z, y+1), (z+1, y-1), (z+1, y), (z+1, y+1)
+#pragma unroll 1
+            for (int q = 0; q < 4; q++) {
+                const RowDir d = dir[q == 0 ? hr + 1 : ky + q + hr];
+                if (d.n == 0u) continue;
+                scan_staged(sxk, so4, d, klo0, khi0, k);
+                if (two) scan_staged(sxk, so4, d, klo1, khi1, k);
+            }
+            if (k.cnt) atomicAdd(&deg[s], k.cnt);
+            ntest += k.ntest;
+        }
+        __syncthreads();
+    }
+    warp_count(tests, ntest);
 }
 
 // pass 2 (each unordered pair once again): both entries of every band pair, placed by a
@@ -138,58 +312,123 @@ k_pairs_fill(uint32_t e_all, const uint32_t* __restrict__ slotE, const float4* _
 }
 
 // compaction: editable e -> slot, row start, original and starting position
-__global__ void __launch_bounds__(PAIR_THREADS)
-k_compact(int64_t n, const uint32_t* __restrict__ deg, const uint32_t* __restrict__ eidx,
-          const unsigned long long* __restrict__ rowoff, const float4* __restrict__ orig4,
-          const float4* __restrict__ dec4, uint32_t e_own, unsigned long long nent, uint32_t* __restrict__ slotE,
-          unsigned long long* __restrict__ rowptr, float4* __restrict__ origE, float4* __restrict__ posA) {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
-    const uint32_t e = eidx[s];
-    if (e == 0xFFFFFFFFu) return;
-    const float4 o = orig4[s], d = dec4[s];
-    slotE[e] = (uint32_t)s;
-    rowptr[e] = (e < e_own) ? rowoff[s] : nent;
-    origE[e] = o;
-    posA[e] = make_float4(d.x, d.y, d.z, o.w);
-}
-
 __global__ void k_rowptr_tail(unsigned long long* rowptr, uint32_t e_all, unsigned long long nent) {
     rowptr[e_all] = nent;
 }
 
-constexpr int SHORT_ROW = 32;
 constexpr int LONG_SORT_MAX = 4096;  // block bitonic capacity (entries)
 
 __device__ __forceinline__ unsigned long long row_key(uint32_t ent, const float4* __restrict__ posA) {
     return ((unsigned long long)__float_as_uint(posA[ent & ENT_IDX].w) << 32) | ent;
 }
 
-// sort each row by partner gid: rows of classes 0-2 (<= 32 entries) in registers (insertion
-// sort); class-3 rows by the block kernel
-__global__ void __launch_bounds__(PAIR_THREADS)
-k_sort_short(uint32_t e_end, const unsigned long long* __restrict__ rowptr, const float4* __restrict__ posA,
-             uint32_t* __restrict__ rows) {
-    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= e_end) return;
-    const unsigned long long a = rowptr[e], b = rowptr[e + 1];
-    const int len = (int)(b - a);
-    if (len <= 1 || len > SHORT_ROW) return;
-    unsigned long long v[SHORT_ROW];
-    for (int i = 0; i < len; i++) {
-        unsigned long long x = row_key(rows[a + i], posA);
-        int j = i - 1;
-        while (j >= 0 && v[j] > x) {
-            v[j + 1] = v[j];
-            j--;
+// sort each row by partner gid (R14's summation order).  The key (partner gid << 32 | entry) is
+// unique and carries the entry, so a sort of keys alone suffices.  Rows of classes 0-2 (<= 4,
+// <= 16, <= 32 entries): a group of W lanes per row, one key per lane, a W-wide bitonic network
+// of shuffles; class 3: k_sort_wide (<= 512) and the block kernel beyond.
+template <int W>
+__device__ __forceinline__ unsigned long long group_sort(unsigned long long k, int gl) {
+#pragma unroll
+    for (int kk = 2; kk <= W; kk <<= 1) {
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            const unsigned long long pk = __shfl_xor_sync(0xffffffffu, k, j);
+            const bool up = (gl & kk) == 0;
+            const bool lower = (gl & j) == 0;
+            if (lower ? ((k > pk) == up) : ((k < pk) == up)) k = pk;
         }
-        v[j + 1] = x;
     }
-    for (int i = 0; i < len; i++) rows[a + i] = (uint32_t)v[i];
+    return k;
 }
 
-// long rows: one block per row, bitonic sort in shared memory (<= LONG_SORT_MAX entries), and
-// a serial in-place insertion sort by one thread beyond that (rare: only at xi ~ spacing)
+template <int W>
+__global__ void __launch_bounds__(PAIR_THREADS)
+k_sort_group(uint32_t e_lo, uint32_t e_hi, const unsigned long long* __restrict__ rowptr,
+             const float4* __restrict__ posA, uint32_t* __restrict__ rows) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t e = e_lo + t / W;
+    const int gl = (int)(t % W);
+    int len = 0;
+    unsigned long long a = 0ull;
+    if (e < e_hi) {
+        a = rowptr[e];
+        len = (int)(rowptr[e + 1] - a);
+    }
+    unsigned long long k = gl < len ? row_key(rows[a + gl], posA) : ~0ull;
+    k = group_sort<W>(k, gl);  // every lane takes part (the shuffles span the warp)
+    if (len > 1 && gl < len) rows[a + gl] = (uint32_t)k;
+}
+
+// class-3 rows of 33..512 entries: one warp per row; <= 64 two keys per lane (register network),
+// longer ones a bitonic sort in the warp's slice of shared memory (__syncwarp steps)
+constexpr int SORT_WIDE = 512;
+constexpr int SW_WARPS = 8;
+
+__global__ void __launch_bounds__(32 * SW_WARPS)
+k_sort_wide(uint32_t e_lo, uint32_t e_hi, const unsigned long long* __restrict__ rowptr,
+            const float4* __restrict__ posA, uint32_t* __restrict__ rows) {
+    __shared__ unsigned long long shk[SW_WARPS][SORT_WIDE];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned long long* sk = shk[w];
+    const uint32_t nw = gridDim.x * SW_WARPS;
+    for (uint32_t e = e_lo + blockIdx.x * SW_WARPS + w; e < e_hi; e += nw) {
+        const unsigned long long a = rowptr[e];
+        const int len = (int)(rowptr[e + 1] - a);
+        if (len > SORT_WIDE) continue;  // the block kernel's
+        if (len <= 64) {
+            unsigned long long k0 = lane < len ? row_key(rows[a + lane], posA) : ~0ull;
+            unsigned long long k1 = lane + 32 < len ? row_key(rows[a + lane + 32], posA) : ~0ull;
+            for (int kk = 2; kk <= 64; kk <<= 1) {
+                for (int j = kk >> 1; j > 0; j >>= 1) {
+                    if (j == 32) {  // partners in the same lane: elements lane and lane + 32
+                        if (k0 > k1) {  // kk == 64: ascending
+                            const unsigned long long tk = k0;
+                            k0 = k1;
+                            k1 = tk;
+                        }
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            unsigned long long& kr = h ? k1 : k0;
+                            const int idx = lane + 32 * h;
+                            const unsigned long long pk = __shfl_xor_sync(0xffffffffu, kr, j);
+                            const bool up = (idx & kk) == 0;
+                            const bool lower = (lane & j) == 0;
+                            if (lower ? ((kr > pk) == up) : ((kr < pk) == up)) kr = pk;
+                        }
+                    }
+                }
+            }
+            if (lane < len) rows[a + lane] = (uint32_t)k0;
+            if (lane + 32 < len) rows[a + lane + 32] = (uint32_t)k1;
+            continue;
+        }
+        int p2 = 128;
+        while (p2 < len) p2 <<= 1;
+        for (int i = lane; i < p2; i += 32) sk[i] = i < len ? row_key(rows[a + i], posA) : ~0ull;
+        __syncwarp();
+        for (int kk = 2; kk <= p2; kk <<= 1) {
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                for (int t = lane; t < (p2 >> 1); t += 32) {
+                    const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+                    const int ij = i | j;
+                    const bool up = (i & kk) == 0;
+                    const unsigned long long x0 = sk[i], x1 = sk[ij];
+                    if ((x0 > x1) == up) {
+                        sk[i] = x1;
+                        sk[ij] = x0;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        for (int i = lane; i < len; i += 32) rows[a + i] = (uint32_t)sk[i];
+        __syncwarp();
+    }
+}
+
+// long rows (> SORT_WIDE): one block per row, bitonic sort in shared memory (<= LONG_SORT_MAX
+// entries), in global memory beyond that (rare: only at xi ~ spacing)
 __global__ void __launch_bounds__(512)
 k_sort_long(uint32_t e_lo, uint32_t e_hi, const unsigned long long* __restrict__ rowptr,
             const float4* __restrict__ posA, uint32_t* __restrict__ rows) {
@@ -197,6 +436,7 @@ k_sort_long(uint32_t e_lo, uint32_t e_hi, const unsigned long long* __restrict__
     for (uint32_t e = e_lo + blockIdx.x; e < e_hi; e += gridDim.x) {
         const unsigned long long a = rowptr[e], b = rowptr[e + 1];
         const int len = (int)(b - a);
+        if (len <= SORT_WIDE) continue;  // k_sort_wide's
         if (len <= LONG_SORT_MAX) {
             int p2 = 1;
             while (p2 < len) p2 <<= 1;
@@ -221,17 +461,9 @@ k_sort_long(uint32_t e_lo, uint32_t e_hi, const unsigned long long* __restrict__
             }
             for (int i = threadIdx.x; i < len; i += blockDim.x) rows[a + i] = (uint32_t)sh[i];
             __syncthreads();
-        } else if (threadIdx.x == 0) {
-            for (int i = 1; i < len; i++) {
-                uint32_t x = rows[a + i];
-                unsigned long long kx = row_key(x, posA);
-                int j = i - 1;
-                while (j >= 0 && row_key(rows[a + j], posA) > kx) {
-                    rows[a + j + 1] = rows[a + j];
-                    j--;
-                }
-                rows[a + j + 1] = x;
-            }
+        } else {  // beyond shared memory: in place in global memory, keys gathered per comparator
+            __syncthreads();
+            block_sort_global(rows + a, (int64_t)len, [posA](uint32_t x) { return row_key(x, posA); });
         }
     }
 }
@@ -249,9 +481,25 @@ cc_status pairs_count(cc_ctx* c) {
     CC_CUDA(c, cudaMemsetAsync(c->near_n.p, 0, sizeof(unsigned long long), c->stream));
     if (n > 0) {
         int tok = cc_prof_begin(c, "K2_count");
-        CCL(c, k_pairs_count<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
-            n, c->orig4.p, c->dec4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in, c->deg.p,
-            c->parent_base.p, c->near.p, c->near_n.p, (unsigned long long)c->near.cap, work_counters(c) + 2));
+        const bool half = !c->th.periodic || (c->g.ny >= 3 && c->g.nz >= 3);
+        const char* env = std::getenv("CC_K2_TILED");
+        if (c->g.nx == 1 && half && env && env[0] == '1') {  // A/B variant (slower)
+            // home strip ~240 particles (one pass of the 256-thread block)
+            const double per_row = (double)n / ((double)c->g.ny * c->g.nz);
+            const int trows = std::max(1, std::min(TROWS_MAX, (int)(240.0 / std::max(per_row, 1.0))));
+            const int tiles_y = (c->g.ny + trows - 1) / trows;
+            const int64_t ntiles = (int64_t)c->g.nz * tiles_y;
+            const unsigned nbk = (unsigned)std::min<int64_t>(ntiles, 148 * 8);
+            CCL(c, k_pairs_count_tiled<<<nbk, PAIR_THREADS, 0, c->stream>>>(
+                n, c->orig4.p, c->dec4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in, c->deg.p,
+                c->parent_base.p, c->near.p, c->near_n.p, (unsigned long long)c->near.cap, work_counters(c) + 2,
+                ntiles, tiles_y, trows));
+        } else {
+            CCL(c, k_pairs_count<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
+                n, c->orig4.p, c->dec4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in,
+                c->deg.p, c->parent_base.p, c->near.p, c->near_n.p, (unsigned long long)c->near.cap,
+                work_counters(c) + 2));
+        }
         cc_prof_end(c, tok);
         CC_CUDA(c, cudaGetLastError());
     }
@@ -264,10 +512,7 @@ cc_status rows_resolve(cc_ctx* c, const unsigned long long* totals_h) {
     std::memcpy(cnt, totals_h + 4, sizeof(cnt));
     std::memcpy(&ghosts, totals_h + 6, sizeof(ghosts));
     int64_t e = 0, ent = 0;
-    ClassBases cb;
     for (int k = 0; k < 4; k++) {
-        cb.e[k] = (uint32_t)e;
-        cb.off[k] = (unsigned long long)ent;
         c->E_cls[k] = cnt[k];
         e += cnt[k];
         ent += (int64_t)totals_h[k];
@@ -275,13 +520,7 @@ cc_status rows_resolve(cc_ctx* c, const unsigned long long* totals_h) {
     c->E = e;
     c->E_all = e + ghosts;
     c->nent = ent;
-    if (c->E_all >= MAX_LOCAL) return CC_OK;  // caller reports
-    const int64_t n = c->n;
-    if (n > 0)
-        CCL(c, k_resolve<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(
-            n, c->key.p, cb, (uint32_t)e, c->eidx.p, reinterpret_cast<unsigned long long*>(c->rowoff.p)));
-    CC_CUDA(c, cudaGetLastError());
-    return CC_OK;
+    return CC_OK;  // eidx and the per-editable arrays were written by the class scan (scan.cu)
 }
 
 cc_status pairs_fill(cc_ctx* c) {
@@ -310,32 +549,32 @@ cc_status pairs_fill(cc_ctx* c) {
 }
 
 cc_status rows_finish(cc_ctx* c) {
-    const int64_t n = c->n, Ea = c->E_all;
-    const size_t e1 = (size_t)std::max<int64_t>(Ea, 1);
-    CC_TRY(cc_ensure(c, c->slotE, e1, "slotE"));
-    CC_TRY(cc_ensure(c, c->rowptr, e1 + 1, "rowptr"));
-    CC_TRY(cc_ensure(c, c->origE, e1, "origE"));
-    CC_TRY(cc_ensure(c, c->posA, e1, "posA"));
-    CC_TRY(cc_ensure(c, c->posB, e1, "posB"));
+    const int64_t Ea = c->E_all;
     unsigned long long* rowptr = reinterpret_cast<unsigned long long*>(c->rowptr.p);
-    int tok = cc_prof_begin(c, "K2_compact");
-    if (n > 0)
-        CCL(c, k_compact<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
-            n, c->deg.p, c->eidx.p, reinterpret_cast<const unsigned long long*>(c->rowoff.p), c->orig4.p, c->dec4.p,
-            (uint32_t)c->E, (unsigned long long)c->nent, c->slotE.p, rowptr, c->origE.p, c->posA.p));
     CCL(c, k_rowptr_tail<<<1, 1, 0, c->stream>>>(rowptr, (uint32_t)Ea, (unsigned long long)c->nent));
-    cc_prof_end(c, tok);
     CC_CUDA(c, cudaGetLastError());
     CC_TRY(pairs_fill(c));
     const uint32_t e_short = (uint32_t)(c->E_cls[0] + c->E_cls[1] + c->E_cls[2]);
     if (c->E > 0 && c->nent > 0) {
         int t2 = cc_prof_begin(c, "K2_sort");
-        if (e_short > 0)
-            CCL(c, k_sort_short<<<(e_short + PAIR_THREADS - 1) / PAIR_THREADS, PAIR_THREADS, 0, c->stream>>>(
-                e_short, rowptr, c->posA.p, c->rows.p));
-        if (c->E_cls[3] > 0)
+        const uint32_t e0 = (uint32_t)c->E_cls[0], e1 = e0 + (uint32_t)c->E_cls[1];
+        auto groups = [&](uint64_t rows_n, int w) { return (unsigned)((rows_n * w + PAIR_THREADS - 1) / PAIR_THREADS); };
+        if (c->E_cls[0] > 0)
+            CCL(c, k_sort_group<4><<<groups(c->E_cls[0], 4), PAIR_THREADS, 0, c->stream>>>(0u, e0, rowptr, c->posA.p,
+                                                                                            c->rows.p));
+        if (c->E_cls[1] > 0)
+            CCL(c, k_sort_group<16><<<groups(c->E_cls[1], 16), PAIR_THREADS, 0, c->stream>>>(e0, e1, rowptr,
+                                                                                              c->posA.p, c->rows.p));
+        if (c->E_cls[2] > 0)
+            CCL(c, k_sort_group<32><<<groups(c->E_cls[2], 32), PAIR_THREADS, 0, c->stream>>>(e1, e_short, rowptr,
+                                                                                              c->posA.p, c->rows.p));
+        if (c->E_cls[3] > 0) {
+            CCL(c, k_sort_wide<<<(unsigned)std::min<int64_t>((c->E_cls[3] + SW_WARPS - 1) / SW_WARPS, 148 * 8),
+                                 32 * SW_WARPS, 0, c->stream>>>(e_short, (uint32_t)c->E, rowptr, c->posA.p,
+                                                                c->rows.p));
             CCL(c, k_sort_long<<<(unsigned)std::min<int64_t>(c->E_cls[3], 148 * 8), 512, 0, c->stream>>>(
                 e_short, (uint32_t)c->E, rowptr, c->posA.p, c->rows.p));
+        }
         cc_prof_end(c, t2);
         CC_CUDA(c, cudaGetLastError());
     }

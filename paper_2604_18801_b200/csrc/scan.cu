@@ -66,46 +66,139 @@ struct StoreU32 {
 };
 
 // deg[s] > 0 -> owned editable; deg == 0 but marked (ghost partner, dec4.w index >= n_own
-// and flagged with bit 31 of deg) -> ghost editable.
-struct LoadDeg {
+// and flagged with bit 31 of deg) -> ghost editable.  The scan runs over the editable list
+// (k_editable_list: the slots with deg != 0, in slot order), not over all n slots.
+__device__ __forceinline__ VDeg deg_value(uint32_t d) {
+    const uint32_t len = d & 0x7FFFFFFFu;
+    VDeg v = VDeg::zero();
+    if (len > 0u) {
+        const int k = row_class(len);
+        v.a[k] = len;
+        v.b[k] = 1u;
+    } else {
+        v.g = d >> 31;
+    }
+    return v;
+}
+struct LoadCand {
     const uint32_t* deg;
-    __device__ VDeg operator()(int64_t i) const {
-        const uint32_t d = deg[i];
-        const uint32_t len = d & 0x7FFFFFFFu;
-        VDeg v = VDeg::zero();
-        if (len > 0u) {
-            const int k = row_class(len);
-            v.a[k] = len;
-            v.b[k] = 1u;
-        } else {
-            v.g = d >> 31;
-        }
-        return v;
-    }
+    const uint32_t* cand;
+    __device__ VDeg operator()(int64_t i) const { return deg_value(deg[cand[i]]); }
 };
-// provisional (class, rank-in-class, row offset in class); rows_resolve adds the class bases
-struct StoreDeg {
-    unsigned long long* rowoff;
+// the editable index e of slot s = its class base + its rank in the class (classes 0..3 by row
+// length, then the ghosts): eidx[s] = e, and the compact per-editable arrays (slot, row offset,
+// original position, PGD start = decompressed position) are written at e.  The class bases come
+// from the scan total (written by k_scan_blocks before this pass).
+struct StoreEdit {
+    const uint32_t* cand;
+    const VDeg* total;
+    const float4* orig4;
+    const float4* dec4;
     uint32_t* eidx;
-    uint32_t* cls;
+    uint32_t* slotE;
+    unsigned long long* rowptr;
+    float4* origE;
+    float4* posA;
     __device__ void operator()(int64_t i, const VDeg& excl, const VDeg& self) const {
-        uint32_t k = 0xFFu, r = 0xFFFFFFFFu;
-        unsigned long long o = 0ull;
-        for (int q = 0; q < 4; q++)
+        const VDeg t = *total;
+        const uint32_t s = cand[i];
+        uint32_t e;
+        unsigned long long o;
+        uint32_t eb = 0u;
+        unsigned long long ob = 0ull;
+        e = 0u;
+        o = 0ull;
+        bool own = false;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
             if (self.b[q]) {
-                k = (uint32_t)q;
-                r = excl.b[q];
-                o = excl.a[q];
+                e = eb + excl.b[q];
+                o = ob + excl.a[q];
+                own = true;
             }
-        if (self.g) {
-            k = 4u;
-            r = excl.g;
+            eb += t.b[q];
+            ob += t.a[q];
         }
-        cls[i] = k;
-        eidx[i] = r;
-        rowoff[i] = o;
+        if (!own) {  // ghost editable: after every owned one; its row is empty
+            e = eb + excl.g;
+            o = ob;
+        }
+        const float4 p = orig4[s], d = dec4[s];
+        eidx[s] = e;
+        slotE[e] = s;
+        rowptr[e] = o;
+        origE[e] = p;
+        posA[e] = make_float4(d.x, d.y, d.z, p.w);
     }
 };
+
+// the editable list: cand[0..E_all) = the slots with deg != 0 in ascending order, eidx[s] =
+// 0xFFFFFFFF for every slot (the editables' entries are overwritten by the list scan).  Single
+// pass, decoupled look-back; a thread owns LI consecutive slots (16-byte loads and stores).
+constexpr int LT = 256, LI = 16, LTILE = LT * LI;
+
+__global__ void __launch_bounds__(LT) k_editable_list(int64_t n, const uint32_t* __restrict__ deg,
+                                                     uint32_t* __restrict__ eidx, uint32_t* __restrict__ cand,
+                                                     unsigned long long* __restrict__ status,
+                                                     unsigned int* __restrict__ ticket,
+                                                     unsigned long long* __restrict__ total) {
+    __shared__ unsigned int tile_sh;
+    __shared__ unsigned long long base_sh;
+    __shared__ uint32_t wsum[LT / 32];
+    if (threadIdx.x == 0) tile_sh = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const unsigned int tile = tile_sh;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i0 = (int64_t)tile * LTILE + (int64_t)threadIdx.x * LI;
+    uint32_t mask = 0u;
+    if (i0 + LI <= n) {
+        const uint4* d4 = reinterpret_cast<const uint4*>(deg + i0);
+        uint4* e4 = reinterpret_cast<uint4*>(eidx + i0);
+#pragma unroll
+        for (int k = 0; k < LI / 4; k++) {
+            const uint4 v = d4[k];
+            mask |= (v.x != 0u ? 1u : 0u) << (4 * k) | (v.y != 0u ? 2u : 0u) << (4 * k) |
+                    (v.z != 0u ? 4u : 0u) << (4 * k) | (v.w != 0u ? 8u : 0u) << (4 * k);
+            e4[k] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        }
+    } else {
+        for (int k = 0; k < LI; k++)
+            if (i0 + k < n) {
+                mask |= (deg[i0 + k] != 0u ? 1u : 0u) << k;
+                eidx[i0 + k] = 0xFFFFFFFFu;
+            }
+    }
+    // block-exclusive prefix of the per-thread counts (slot order = thread order)
+    const uint32_t cnt = __popc(mask);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    uint32_t wex = 0u, tot = 0u;
+#pragma unroll
+    for (int k = 0; k < LT / 32; k++) {
+        wex += k < w ? wsum[k] : 0u;
+        tot += wsum[k];
+    }
+    if (threadIdx.x < 32) {
+        const unsigned long long ex = lookback_warp0(status, tile, tot);
+        if (lane == 0) {
+            base_sh = ex;
+            if ((int64_t)(tile + 1) * LTILE >= n) *total = ex + tot;  // the last tile
+        }
+    }
+    __syncthreads();
+    unsigned long long q = base_sh + wex + inc - cnt;
+    while (mask) {
+        const int k = __ffs(mask) - 1;
+        mask &= mask - 1u;
+        cand[q++] = (uint32_t)(i0 + k);
+    }
+}
 
 // inclusive warp scan then block exclusive scan; returns exclusive prefix, *total = sum
 template <class V>
@@ -222,12 +315,35 @@ cc_status scan_u32_to_u32(cc_ctx* c, const uint32_t* in, uint32_t* out, int64_t 
     return scan_generic<VU32>(c, n, LoadU32{in}, StoreU32{out}, reinterpret_cast<VU32*>(total_dev), "K1_scan");
 }
 
-cc_status scan_deg(cc_ctx* c, const uint32_t* deg, uint64_t* rowoff, uint32_t* eidx, uint32_t* cls, int64_t n,
-                   unsigned long long* totals_dev) {
+cc_status editable_list(cc_ctx* c, int64_t* e_all) {
+    const int64_t n = c->n;
+    *e_all = 0;
+    if (n <= 0) return CC_OK;
+    const int64_t nt = (n + LTILE - 1) / LTILE;
+    CC_TRY(cc_ensure(c, c->codec_status, (size_t)nt + 2, "look-back status"));
+    unsigned long long* st = c->codec_status.p;
+    unsigned int* ticket = reinterpret_cast<unsigned int*>(st + nt);
+    unsigned long long* tot = c->counters.p + 9;
+    CC_CUDA(c, cudaMemsetAsync(st, 0, (size_t)(nt + 1) * sizeof(unsigned long long), c->stream));
+    int tok = cc_prof_begin(c, "K2_scan");
+    CCL(c, k_editable_list<<<(unsigned)nt, LT, 0, c->stream>>>(n, c->deg.p, c->eidx.p, c->key.p, st, ticket, tot));
+    cc_prof_end(c, tok);
+    CC_CUDA(c, cudaGetLastError());
+    CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 9, tot, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    *e_all = (int64_t)c->h_counters[9];
+    return CC_OK;
+}
+
+cc_status scan_editables(cc_ctx* c, int64_t e_all, unsigned long long* totals_dev) {
     static_assert(sizeof(VDeg) == 56, "");
-    return scan_generic<VDeg>(c, n, LoadDeg{deg},
-                              StoreDeg{reinterpret_cast<unsigned long long*>(rowoff), eidx, cls},
-                              reinterpret_cast<VDeg*>(totals_dev), "K2_scan");
+    VDeg* tot = reinterpret_cast<VDeg*>(totals_dev);
+    unsigned long long* rowptr = reinterpret_cast<unsigned long long*>(c->rowptr.p);
+    return scan_generic<VDeg>(c, e_all, LoadCand{c->deg.p, c->key.p},
+                              StoreEdit{c->key.p, tot, c->orig4.p, c->dec4.p, c->eidx.p, c->slotE.p, rowptr,
+                                        c->origE.p, c->posA.p},
+                              tot, "K2_scan");
 }
 
 }  // namespace cc

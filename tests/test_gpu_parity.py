@@ -165,6 +165,31 @@ def test_everything_in_one_cell_and_coincident_points():
     assert_parity(gpu_pipeline(arrs, pr), oracle_pipeline(arrs, pr))
 
 
+def test_giant_rows_bit_exact():
+    """Rows beyond shared memory on both sorts: two tight clusters of 4,200 particles one linking
+    length apart along x share one K1 row (8,400 records > 4,096) and every cross pair is in the
+    band, so each editable's K2 row holds 4,200 entries (> 4,096): the in-place global bitonic
+    paths of K1 and K2, and the K2 count's over-capacity strip, against the oracle (3 fixed
+    iterations keep the oracle's 17.6M-pair loop to seconds)."""
+    rng = np.random.default_rng(21)
+    m, b, xi = 4200, 0.02, 1e-3
+    h = 1.5e-4
+    A = np.array([0.3, 0.5, 0.5]) + rng.uniform(-h, h, (m, 3))
+    B = np.array([0.3 + b, 0.5, 0.5]) + rng.uniform(-h, h, (m, 3))
+    P = np.concatenate([A, B]).astype(np.float32)
+    perm = rng.permutation(2 * m)
+    P = P[perm]
+    x, y, z = P[:, 0].copy(), P[:, 1].copy(), P[:, 2].copy()
+    noise = [np.clip(a + rng.uniform(-xi * 0.99, xi * 0.99, 2 * m).astype(np.float32), a - np.float32(xi * 0.99),
+                     a + np.float32(xi * 0.99)).astype(np.float32) for a in (x, y, z)]
+    pr = cc.Params(box=1.0, b=b, xi=xi, t_max=3, stop_mode=cc.STOP_NONE)
+    arrs = [x, y, z, *noise]
+    g, o = gpu_pipeline(arrs, pr), oracle_pipeline(arrs, pr)
+    assert_parity(g, o)
+    assert g["info"]["iterations"] == 3
+    assert len(o["pairs"][0]) >= m * m
+
+
 def test_gid_permutation():
     """User-supplied gids: results are keyed by gid (R14, R20)."""
     w = synth.Workload("t", "clumped", 10_000, 1.0, 1e-3, seed=12)
