@@ -15,7 +15,10 @@
  *    outputs synchronise that stream before returning.
  *  - The caller owns every input/output buffer; the library owns its scratch (allocated with
  *    stream-ordered cudaMallocAsync on the context's stream, freed by cc_destroy()).  Inputs
- *    are never written; cc_build_cells() snapshots them into cell-sorted copies.
+ *    are never written; cc_build_cells() snapshots them into cell-sorted copies, and
+ *    cc_correct() reads the decompressed inputs xh,yh,zh of the last cc_build_cells() once more
+ *    (they are the output of every non-editable particle): keep those three arrays valid and
+ *    unchanged until cc_correct() has returned (cc_run() does this itself).
  *  - Every function returns a cc_status; no exception, abort or exit crosses the ABI.  On a
  *    non-OK status cc_last_error() describes it.  Calling steps out of order returns
  *    CC_E_STATE.  A CUDA failure returns CC_E_CUDA and leaves the context unusable.
@@ -148,7 +151,8 @@ cc_status cc_get_pairs(cc_ctx* ctx, uint32_t* gi, uint32_t* gj, uint8_t* flags, 
  * (Eq. 3) over the editable particles, box projection onto B(xi') around the
  * ORIGINAL positions, stop per params.stop_mode checked before every update.
  * Writes all n corrected coordinates in input order to xo,yo,zo (non-editable particles =
- * decompressed input, bit-exact).  Returns CC_NOT_CONVERGED if T_max ended the loop with
+ * decompressed input, bit-exact, copied from the xh,yh,zh of the last cc_build_cells(), which
+ * must still be valid; xo,yo,zo may alias them).  Returns CC_NOT_CONVERGED if T_max ended the loop with
  * active pairs left (outputs still valid and within xi').  Synchronises. */
 typedef struct {
     int64_t iterations;     /* updates performed (R27)                                       */

@@ -440,9 +440,15 @@ cc_status cc_build_cells(cc_ctx* c, int64_t n, const float* x, const float* y, c
         const double x0 = std::fmod(c->slab_lo - c->r_pair + c->p.box, c->p.box);
         choose_grid(c, c->n, slab + 2.0 * c->r_pair, x0, 0);
         CC_TRY(cc::bin_particles(c, f, f + cap, f + 2 * cap, f + 3 * cap, f + 4 * cap, f + 5 * cap, st + 6 * cap, c->n));
+        c->in_dec[0] = f + 3 * cap;  // owned particles first, in input order
+        c->in_dec[1] = f + 4 * cap;
+        c->in_dec[2] = f + 5 * cap;
     } else {
         choose_grid(c, n, c->p.box, 0.0, c->p.periodic ? 1 : 0);
         CC_TRY(cc::bin_particles(c, x, y, z, xh, yh, zh, gid, n));
+        c->in_dec[0] = xh;
+        c->in_dec[1] = yh;
+        c->in_dec[2] = zh;
     }
     CC_CUDA(c, cudaMemcpyAsync(c->h_counters, c->counters.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                c->stream));

@@ -466,10 +466,25 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
         CCL(c, k_cell_finish_long<<<148 * 2, 512, 0, c->stream>>>(c->scratch_u32.p, cap, nl, c->cell_start.p, rec,
                                                                   c->g, c->orig4.p, c->dec4.p, c->xk.p, fin,
                                                                   c->key.p));
-        CCL(c, k_fix_slot_of<<<nb, BIN_THREADS, 0, c->stream>>>(n, fin, c->slot_of.p));
         cc_prof_end(c, t2);
         CC_CUDA(c, cudaGetLastError());
     }
+    c->slot_of_valid = n <= 0;
+    return CC_OK;
+}
+
+// slot_of[i] = fin[slot_of[i]] (k_fix_slot_of): the input-order -> slot map is only needed to
+// write FoF labels in input order and by the multi-GPU exchanges, not by S1-S5 (cc_correct's
+// output is written from the inputs and slotE), so it is completed on first use.  fin lives in
+// the rank buffer, untouched until the next cc_build_cells.
+cc_status ensure_slot_of(cc_ctx* c) {
+    if (c->slot_of_valid) return CC_OK;
+    const int64_t n = c->n;
+    if (n > 0)
+        CCL(c, k_fix_slot_of<<<(unsigned)((n + BIN_THREADS - 1) / BIN_THREADS), BIN_THREADS, 0, c->stream>>>(
+                   n, c->rnk.p, c->slot_of.p));
+    CC_CUDA(c, cudaGetLastError());
+    c->slot_of_valid = true;
     return CC_OK;
 }
 

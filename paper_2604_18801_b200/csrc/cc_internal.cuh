@@ -227,6 +227,8 @@ struct cc_ctx {
     // device buffers
     cc::DBuf<float4> orig4, dec4, cor4, posA, posB, origE;
     bool cor4_valid = false;  // cor4 matches the last cc_correct (built on demand)
+    bool slot_of_valid = false;  // slot_of completed since the last build (ensure_slot_of)
+    const float* in_dec[3] = {nullptr, nullptr, nullptr};  // decompressed inputs of the last build (input order)
     cc::DBuf<uint32_t> key, rnk, cell_count, cell_start, slot_of, deg, eidx, rows, slotE, parent, mingid,
         gsize, scratch_u32;
     cc::DBuf<uint64_t> rowptr, scratch_u64;
@@ -826,6 +828,7 @@ cc_status rows_resolve(cc_ctx* c, const unsigned long long* totals_h);
 cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* z, const float* xh,
                         const float* yh, const float* zh, const uint32_t* gid, int64_t n);
 cc_status pairs_count(cc_ctx* c);
+cc_status ensure_slot_of(cc_ctx* c);
 cc_status pairs_fill(cc_ctx* c);
 cc_status rows_finish(cc_ctx* c);
 cc_status pgd_run(cc_ctx* c, cc_corr_info* info);

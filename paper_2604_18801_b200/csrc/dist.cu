@@ -522,6 +522,7 @@ static cc_status dist_setup_peer(cc_ctx* c) {
 }
 
 cc_status dist_setup_refresh(cc_ctx* c) {
+    CC_TRY(ensure_slot_of(c));
     const int64_t n = c->n;
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
     const int64_t ng = std::max<int64_t>(c->E_all - c->E, 1);
@@ -652,6 +653,7 @@ cc_status dist_iter_tail(cc_ctx* c, const float4* p0, const float4* p1) {
 // FoF label merge across slabs (X4): owners send their shell particles' labels; receivers lower
 // the ghosts' local components; repeat until no label changes anywhere.
 cc_status dist_fof_merge(cc_ctx* c, int64_t* n_groups) {
+    CC_TRY(ensure_slot_of(c));
     const int64_t ns0 = c->n_shell[0], ns1 = c->n_shell[1], nfl = c->n_from_left, nfr = c->n_from_right;
     for (int d = 0; d < 2; d++) {
         CC_TRY(cc_ensure(c, c->lsb[d], (size_t)std::max<int64_t>(c->n_shell[d], 1), "label send"));

@@ -240,6 +240,7 @@ cc_status fof_base_end(cc_ctx* c) {
 }
 
 cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
+    CC_TRY(ensure_slot_of(c));
     const int64_t n = c->n;
     const size_t n1 = (size_t)std::max<int64_t>(n, 1);
     CC_TRY(cc_ensure(c, c->parent, n1, "parent"));

@@ -100,6 +100,167 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
     warp_count(tests, k.ntest);
 }
 
+// ---- the default grid, warp-flattened (the default K2 count when cells are rows): a warp takes
+// 32 consecutive home slots; each lane finds its candidate slot RANGES in the 5 rows of its half
+// shell (x-window key bounds once, a binary search per row, a key scan to the window end), the
+// warp sums the range lengths, and then every lane tests one (home, candidate) pair per step
+// across the whole warp's concatenated candidate list.  The per-lane sweep left 9 of 32 lanes
+// active on average (ncu r02q: candidate loops of different lengths and the stable-forest
+// unions of halo cores serialised on single lanes); here tests and unions are spread over all
+// lanes.  Results are those of k_pairs_count (the same pair set; union order does not change
+// the forest's components; degrees are sums).
+constexpr int CW_NR = 10;       // ranges per home particle: own row (forward, wrap part), 4 rows x 2 windows
+constexpr int CW_WARPS = PAIR_THREADS / 32;
+
+__global__ void __launch_bounds__(PAIR_THREADS)
+k_pairs_count_warp(int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
+                   const uint32_t* __restrict__ xk, const uint32_t* __restrict__ cs, Grid g, Th t, double r,
+                   uint32_t n_own, uint32_t* __restrict__ deg, uint32_t* __restrict__ par_base,
+                   uint2* __restrict__ near, unsigned long long* __restrict__ near_n, unsigned long long near_cap,
+                   unsigned long long* __restrict__ tests) {
+    __shared__ uint32_t r_start[CW_WARPS][CW_NR][32];  // range starts, [range][lane]
+    __shared__ uint32_t r_cum[CW_WARPS][CW_NR + 1][32];  // exclusive running counts, [range][lane]
+    __shared__ uint32_t l_ex[CW_WARPS][33];              // warp-exclusive pair offsets per lane
+    __shared__ float4 l_p[CW_WARPS][32];
+    __shared__ uint8_t l_fl[CW_WARPS][32];               // bit 0 ghost, bit 1 interior
+    __shared__ uint32_t l_rs[CW_WARPS][32];              // per home: a cached stable-forest ancestor
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t s = ((int64_t)blockIdx.x * CW_WARPS + w) * 32 + lane;
+    const bool multi = n_own < (uint32_t)n;
+    uint32_t nr = 0u, tot = 0u;
+    auto add_range = [&](uint32_t a, uint32_t b) {
+        if (b > a) {
+            r_start[w][nr][lane] = a;
+            r_cum[w][nr][lane] = tot;
+            tot += b - a;
+            nr++;
+        }
+    };
+    if (s < n) {
+        const float4 p = orig4[s];
+        double u;
+        int cx, cy, cz;
+        cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
+        const bool ghost = multi && __float_as_uint(dec4[s].w) >= n_own;
+        const bool inner = interior(p.x, p.y, p.z, g, t);
+        l_p[w][lane] = p;
+        l_fl[w][lane] = (uint8_t)((ghost ? 1 : 0) | (inner ? 2 : 0));
+        double a = u - r, b = u + r, a1 = 0.0, b1 = -1.0;
+        bool up = false;
+        if (g.xwrap) {
+            if (a < 0.0) {
+                a1 = a + g.L;
+                b1 = g.L;
+                a = 0.0;
+            } else if (b >= g.L) {
+                a1 = 0.0;
+                b1 = b - g.L;
+                b = g.L;
+                up = true;
+            }
+        } else {
+            if (a < 0.0) a = 0.0;
+            if (b > g.ext_x) b = g.ext_x;
+        }
+        const bool two = b1 >= a1;
+        const uint32_t klo0 = key_lo(a, g), khi0 = key_hi(b, g);
+        const uint32_t klo1 = two ? key_lo(a1, g) : 0u, khi1 = two ? key_hi(b1, g) : 0u;
+        const bool periodic = t.periodic != 0;
+        {   // own row: forward in slot (= x) order, then the part above the seam at the row start
+            const int64_t row = (int64_t)cz * g.ny + cy;
+            const uint32_t r0 = cs[row], r1 = cs[row + 1];
+            uint32_t j = (uint32_t)s + 1u;
+            while (j < r1 && xk[j] <= khi0) j++;
+            add_range((uint32_t)s + 1u, j);
+            if (two && up) {
+                uint32_t j2 = r0;
+                while (j2 < (uint32_t)s && xk[j2] <= khi1) j2++;
+                add_range(r0, j2);
+            }
+        }
+        const int rows_dz[4] = {0, 1, 1, 1};
+        const int rows_dy[4] = {1, -1, 0, 1};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            int zz = cz + rows_dz[k], yy = cy + rows_dy[k];
+            if (periodic) {
+                zz = wrapi(zz, g.nz);
+                yy = wrapi(yy, g.ny);
+            } else if (zz < 0 || zz >= g.nz || yy < 0 || yy >= g.ny) {
+                continue;
+            }
+            const int64_t row = (int64_t)zz * g.ny + yy;
+            const uint32_t j0 = cs[row], j1 = cs[row + 1];
+            uint32_t lo = lower_bound_key(xk, j0, j1, klo0), hi = lo;
+            while (hi < j1 && xk[hi] <= khi0) hi++;
+            add_range(lo, hi);
+            if (two) {
+                lo = lower_bound_key(xk, j0, j1, klo1);
+                hi = lo;
+                while (hi < j1 && xk[hi] <= khi1) hi++;
+                add_range(lo, hi);
+            }
+        }
+    }
+    r_cum[w][nr][lane] = tot;
+    for (uint32_t q = nr + 1; q <= CW_NR; q++) r_cum[w][q][lane] = 0xFFFFFFFFu;  // past the last range
+    l_rs[w][lane] = (uint32_t)s;
+    // warp-exclusive offsets of the lanes' candidate lists
+    uint32_t inc = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    l_ex[w][lane] = inc - tot;
+    const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+    if (lane == 31) l_ex[w][32] = T;
+    __syncwarp();
+    // the flattened tests: pair q = (home lane o, its candidate q - ex[o])
+    for (uint32_t base = 0; base < T; base += 32u) {
+        const uint32_t q = base + (uint32_t)lane;
+        if (q < T) {
+            int o = 0;  // largest o with ex[o] <= q
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1)
+                if (l_ex[w][o + st] <= q) o += st;
+            const uint32_t qo = q - l_ex[w][o];
+            int k = 0;  // the range: largest k with cum[k] <= qo
+            while (r_cum[w][k + 1][o] <= qo) k++;
+            const uint32_t j = r_start[w][k][o] + (qo - r_cum[w][k][o]);
+            const uint32_t so = (uint32_t)(s - lane + o);
+            const float4 pp = l_p[w][o];
+            const uint8_t fl = l_fl[w][o];
+            const bool ghost = fl & 1u, inner = (fl & 2u) != 0;
+            const float4 qq = orig4[j];
+            const float d2 = inner ? dist2_nw(pp, qq) : dist2(pp, qq, t);
+            if (t.lo2 < d2 && d2 <= t.hi2) {
+                const bool gj = multi && __float_as_uint(dec4[j].w) >= n_own;
+                if (!ghost) {
+                    atomicAdd(&deg[so], 1u);
+                    if (gj) atomicOr(&deg[j], 0x80000000u);
+                    else atomicAdd(&deg[j], 1u);
+                } else if (!gj) {
+                    atomicAdd(&deg[j], 1u);
+                    atomicOr(&deg[so], 0x80000000u);
+                }
+            } else if (d2 <= (inner ? t.lo2s_i : t.lo2s_w)) {
+                // a stable FoF link (see CountCtx).  The home's cached ancestor is shared by the
+                // lanes testing its candidates: any value once an ancestor of the home stays
+                // valid for uf_link's filter (sets only merge), so the benign races are harmless
+                uint32_t rs = l_rs[w][o];
+                const uint32_t rs0 = rs;
+                uf_link(par_base, so, j, rs);
+                if (rs != rs0) l_rs[w][o] = rs;
+            } else if (d2 <= (inner ? t.hi2s_i : t.hi2s_w)) {
+                const unsigned long long qn = atomicAdd(near_n, 1ull);
+                if (qn < near_cap) near[qn] = make_uint2(so, j | (d2 <= t.b2 ? 0x80000000u : 0u));
+            }
+        }
+    }
+    if (lane == 0 && T) atomicAdd(tests, (unsigned long long)T);
+}
+
 // ---- the default grid (cells = whole rows, periodic or not, >= 3 rows per axis): a block takes
 // a strip of TROWS consecutive rows of one z-row and stages in shared memory every row the strip's
 // half-shell visits -- rows y0..y0+TROWS of z-row z and y0-1..y0+TROWS of z-row z+1, contiguous
@@ -483,7 +644,12 @@ cc_status pairs_count(cc_ctx* c) {
         int tok = cc_prof_begin(c, "K2_count");
         const bool half = !c->th.periodic || (c->g.ny >= 3 && c->g.nz >= 3);
         const char* env = std::getenv("CC_K2_TILED");
-        if (c->g.nx == 1 && half && env && env[0] == '1') {  // A/B variant (slower)
+        if (c->g.nx == 1 && half && !(env && (env[0] == '0' || env[0] == '1'))) {
+            const int64_t nwarp = (n + 31) / 32;
+            CCL(c, k_pairs_count_warp<<<(unsigned)((nwarp + CW_WARPS - 1) / CW_WARPS), PAIR_THREADS, 0, c->stream>>>(
+                n, c->orig4.p, c->dec4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in, c->deg.p,
+                c->parent_base.p, c->near.p, c->near_n.p, (unsigned long long)c->near.cap, work_counters(c) + 2));
+        } else if (c->g.nx == 1 && half && env && env[0] == '1') {  // A/B variant (slower)
             // home strip ~240 particles (one pass of the 256-thread block)
             const double per_row = (double)n / ((double)c->g.ny * c->g.nz);
             const int trows = std::max(1, std::min(TROWS_MAX, (int)(240.0 / std::max(per_row, 1.0))));

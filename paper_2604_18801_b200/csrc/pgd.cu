@@ -1023,15 +1023,18 @@ __global__ void k_cor4(int64_t n, const float4* __restrict__ dec4, const uint32_
     cor4[s] = d;
 }
 
-// outputs in input order (owned particles)
-__global__ void k_output(int64_t n_in, const uint32_t* __restrict__ slot_of, const float4* __restrict__ cor4,
-                         float* __restrict__ xo, float* __restrict__ yo, float* __restrict__ zo) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_in) return;
-    const float4 v = cor4[slot_of[i]];
-    xo[i] = v.x;
-    yo[i] = v.y;
-    zo[i] = v.z;
+// outputs in input order (owned particles): the decompressed inputs were copied first; the owned
+// editables overwrite their entries with the PGD result (x^(0) = P_hat, only editables move)
+__global__ void k_output_edits(uint32_t e_own, const uint32_t* __restrict__ slotE, const float4* __restrict__ dec4,
+                               const float4* __restrict__ res, float* __restrict__ xo, float* __restrict__ yo,
+                               float* __restrict__ zo) {
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= e_own) return;
+    const uint32_t i = __float_as_uint(dec4[slotE[e]].w);  // input index
+    const float4 r = res[e];
+    xo[i] = r.x;
+    yo[i] = r.y;
+    zo[i] = r.z;
 }
 
 PgdArgs make_args(cc_ctx* c, int count_only) {
@@ -1390,14 +1393,22 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
 }
 
 cc_status write_output(cc_ctx* c, const float4* res, float* xo, float* yo, float* zo) {
-    // slot-order corrected positions (coalesced), then one gather per output particle: measured
-    // faster than reading the result buffer directly per input particle (two random reads)
+    // every owned particle's decompressed input streamed to the output (coalesced copies), then
+    // one scattered write per owned editable: round 1 gathered all n outputs from a slot-order
+    // buffer through slot_of (a random 32-byte sector per particle, 8.3 ms at C4)
     c->cor4_valid = false;
     int tok = cc_prof_begin(c, "K3_output");
-    CC_TRY(ensure_cor4(c));
-    if (c->n_in > 0 && xo)
-        CCL(c, k_output<<<(unsigned)((c->n_in + 255) / 256), 256, 0, c->stream>>>(c->n_in, c->slot_of.p, c->cor4.p,
-                                                                                  xo, yo, zo));
+    const int64_t n = c->n_in;
+    if (n > 0 && xo) {
+        float* out[3] = {xo, yo, zo};
+        for (int a = 0; a < 3; a++)
+            if (out[a] != c->in_dec[a])
+                CC_CUDA(c, cudaMemcpyAsync(out[a], c->in_dec[a], (size_t)n * sizeof(float), cudaMemcpyDeviceToDevice,
+                                           c->stream));
+        if (c->E > 0)
+            CCL(c, k_output_edits<<<(unsigned)((c->E + 255) / 256), 256, 0, c->stream>>>(
+                       (uint32_t)c->E, c->slotE.p, c->dec4.p, res, xo, yo, zo));
+    }
     cc_prof_end(c, tok);
     CC_CUDA(c, cudaGetLastError());
     return CC_OK;

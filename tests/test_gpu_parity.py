@@ -283,3 +283,24 @@ def test_torch_caching_allocator_scratch():
     arrs = _arrs(w)
     p = _params(w, torch_allocator=True)
     assert_parity(gpu_pipeline(arrs, p), oracle_pipeline(arrs, p))
+
+
+def test_output_into_the_decompressed_input_arrays():
+    """cc_correct copies every non-editable particle's decompressed input and scatters the
+    editables (cc.h): writing the outputs over xh, yh, zh themselves gives the same corrected
+    positions as separate outputs (and the oracle's)."""
+    w = synth.Workload("alias", "clumped", 20_000, 1.0, 1e-3, seed=14)
+    arrs = _arrs(w)
+    p = _params(w)
+    o = oracle_pipeline(arrs, p, fof=False)
+    dev = torch.device("cuda", 0)
+    ts = [torch.as_tensor(a).to(dev) for a in arrs]
+    c = cc.Corrector(p, device=0)
+    c.build_cells(*ts)
+    c.find_vulnerable()
+    out, info = c.correct(out=(ts[3], ts[4], ts[5]))
+    torch.cuda.synchronize()
+    for k in range(3):
+        assert np.array_equal(out[k].cpu().numpy().view(np.uint32), o["out"][k].view(np.uint32))
+    assert info["iterations"] == o["info"]["iterations"]
+    c.close()
