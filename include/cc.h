@@ -11,8 +11,9 @@
  *    unless the parameter name ends in `_h` (host memory).  Exception: cc_run() takes host or
  *    device pointers as its `flags` say.
  *  - Particle arrays are structure-of-arrays float32 of length n, index i = input order.
- *  - All work is enqueued on the stream given to cc_create(); only functions with `_h`
- *    outputs synchronise that stream before returning.
+ *  - All work is enqueued on the stream given to cc_create(); functions with `_h` outputs
+ *    synchronise that stream before returning, and so do the steps whose status depends on
+ *    device results (cc_build_cells, cc_find_vulnerable, cc_correct, as each states).
  *  - The caller owns every input/output buffer; the library owns its scratch (allocated with
  *    stream-ordered cudaMallocAsync on the context's stream, freed by cc_destroy()).  Inputs
  *    are never written; cc_build_cells() snapshots them into cell-sorted copies, and
@@ -121,7 +122,8 @@ const char* cc_last_error(const cc_ctx* ctx);
  * P_hat^(0); gid = global particle ids (NULL: gid = i).  Multi-GPU: the n owned
  * particles of this rank (original x inside its slab); ghost shells of width
  * b + 2 sqrt3 xi are exchanged here with NCCL.  Checks |x_hat - x| <= xi_f
- * (CC_E_BOUND) and finite inputs (CC_E_DATA).  May be called again to start over. */
+ * (CC_E_BOUND) and finite inputs (CC_E_DATA).  Synchronises (the contract check is returned as
+ * the status).  May be called again to start over. */
 cc_status cc_build_cells(cc_ctx* ctx, int64_t n, const float* x, const float* y, const float* z,
                          const float* xh, const float* yh, const float* zh, const uint32_t* gid);
 

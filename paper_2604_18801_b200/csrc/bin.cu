@@ -229,11 +229,14 @@ __global__ void __launch_bounds__(BIN_THREADS)
 k_row_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restrict__ rec, Grid g,
              float4* __restrict__ orig4, float4* __restrict__ dec4, uint32_t* __restrict__ xk,
              uint32_t* __restrict__ slot_of, uint32_t* __restrict__ long_list, uint64_t cap,
-             unsigned long long* __restrict__ n_long) {
+             unsigned long long* __restrict__ n_long, const uint32_t* __restrict__ list,
+             const unsigned long long* __restrict__ n_list) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t c = w0; c < ncell; c += nw) {
+    const int64_t cnt = list ? (int64_t)*n_list : ncell;  // list mode: the rows k_row_finish_group deferred
+    for (int64_t q = w0; q < cnt; q += nw) {
+        const int64_t c = list ? (int64_t)list[q] : q;
         const uint32_t a = cs[c], b = cs[c + 1];
         const int len = (int)(b - a);
         if (len == 0) continue;
@@ -293,6 +296,60 @@ k_row_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restri
         }
         emit(load_rec(rec, a + o0), a + lane, a + o0, orig4, dec4, xk, slot_of, g);
         if (lane + 32 < len) emit(load_rec(rec, a + o1), a + lane + 32, a + o1, orig4, dec4, xk, slot_of, g);
+    }
+}
+
+// short rows (multi-GPU slabs: ~8 particles per row): a group of W lanes per row, one record per
+// lane, a W-wide register bitonic of (key, offset); longer rows are deferred to the warp kernel
+// (<= 64, list mode), k_row_finish_wide (<= 512) and the block kernel.  The warp-per-row kernel
+// left 3/4 of its lanes idle there and did not shrink with the slab (its cost is per row).
+template <int W>
+__device__ __forceinline__ void group_sort_kv(unsigned long long& k, int& o, int gl) {
+#pragma unroll
+    for (int kk = 2; kk <= W; kk <<= 1) {
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            const unsigned long long pk = __shfl_xor_sync(0xffffffffu, k, j);
+            const int po = __shfl_xor_sync(0xffffffffu, o, j);
+            const bool up = (gl & kk) == 0;
+            const bool lower = (gl & j) == 0;
+            if (lower ? ((k > pk) == up) : ((k < pk) == up)) {
+                k = pk;
+                o = po;
+            }
+        }
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(BIN_THREADS)
+k_row_finish_group(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restrict__ rec, Grid g,
+                   float4* __restrict__ orig4, float4* __restrict__ dec4, uint32_t* __restrict__ xk,
+                   uint32_t* __restrict__ slot_of, uint32_t* __restrict__ long_list, uint64_t cap,
+                   unsigned long long* __restrict__ n_long, uint32_t* __restrict__ mid_list) {
+    const int lane = threadIdx.x & 31, gl = lane % W;
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t wb = warp0 * (32 / W); wb < ncell; wb += nwarps * (32 / W)) {  // warp-uniform trips
+        const int64_t c = wb + lane / W;
+        uint32_t a = 0u;
+        int len = 0;
+        if (c < ncell) {
+            a = cs[c];
+            len = (int)(cs[c + 1] - a);
+            if (len > W) {
+                if (gl == 0) {
+                    if (len <= CELL_MID) mid_list[atomicAdd(n_long + 2, 1ull)] = (uint32_t)c;
+                    else if (len <= ROW_WIDE) long_list[atomicAdd(n_long, 1ull)] = (uint32_t)c;
+                    else long_list[cap - 1 - atomicAdd(n_long + 1, 1ull)] = (uint32_t)c;
+                }
+                len = 0;
+            }
+        }
+        unsigned long long k = gl < len ? rec_key(load_rec(rec, a + gl), g) : ~0ull;
+        int o = gl;
+        group_sort_kv<W>(k, o, gl);
+        if (gl < len) emit(load_rec(rec, a + o), a + gl, a + o, orig4, dec4, xk, slot_of, g);
     }
 }
 
@@ -421,10 +478,10 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
     CC_TRY(cc_ensure(c, c->slot_of, n1, "slot_of"));
     CC_TRY(cc_ensure(c, c->rec32, 2 * n1, "binning records"));  // 32 B per particle
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
-    CC_TRY(cc_ensure(c, c->scratch_u64, 2, "long count"));
+    CC_TRY(cc_ensure(c, c->scratch_u64, 3, "long counts"));
     CC_CUDA(c, cudaMemsetAsync(c->cell_count.p, 0, (size_t)nc * sizeof(uint32_t), c->stream));
     CC_CUDA(c, cudaMemsetAsync(c->counters.p, 0, 16 * sizeof(unsigned long long), c->stream));
-    CC_CUDA(c, cudaMemsetAsync(c->scratch_u64.p, 0, 2 * sizeof(uint64_t), c->stream));
+    CC_CUDA(c, cudaMemsetAsync(c->scratch_u64.p, 0, 3 * sizeof(uint64_t), c->stream));
     Rec* rec = reinterpret_cast<Rec*>(c->rec32.p);
     const unsigned nb = (unsigned)((n + BIN_THREADS - 1) / BIN_THREADS);
     if (n > 0) {
@@ -447,10 +504,28 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
         unsigned long long* nl = reinterpret_cast<unsigned long long*>(c->scratch_u64.p);
         int t2 = cc_prof_begin(c, "K1_finish");
         uint32_t* fin = c->rnk.p;  // the ranks are dead after the scatter: final slot per provisional slot
-        if (c->g.nx == 1) {  // cells are rows (default grid): one warp per cell
+        const double per_row = (double)n / (double)std::max<int64_t>(nc, 1);
+        if (c->g.nx == 1 && per_row <= 12.0) {  // short rows (multi-GPU slabs): W lanes per row
+            uint32_t* mid = c->cell_count.p;      // dead after the scan: the deferred 17..64 rows
+            if (per_row <= 5.0)
+                CCL(c, k_row_finish_group<8><<<148 * 16, BIN_THREADS, 0, c->stream>>>(
+                           nc, c->cell_start.p, rec, c->g, c->orig4.p, c->dec4.p, c->xk.p, fin, c->scratch_u32.p, cap,
+                           nl, mid));
+            else
+                CCL(c, k_row_finish_group<16><<<148 * 16, BIN_THREADS, 0, c->stream>>>(
+                           nc, c->cell_start.p, rec, c->g, c->orig4.p, c->dec4.p, c->xk.p, fin, c->scratch_u32.p, cap,
+                           nl, mid));
+            CCL(c, k_row_finish<<<148 * 4, BIN_THREADS, 0, c->stream>>>(nc, c->cell_start.p, rec, c->g, c->orig4.p,
+                                                                         c->dec4.p, c->xk.p, fin, c->scratch_u32.p,
+                                                                         cap, nl, mid, nl + 2));
+            CCL(c, k_row_finish_wide<<<148 * 4, 32 * WIDE_WARPS, 0, c->stream>>>(c->scratch_u32.p, nl,
+                                                                                  c->cell_start.p, rec, c->g,
+                                                                                  c->orig4.p, c->dec4.p, c->xk.p,
+                                                                                  fin));
+        } else if (c->g.nx == 1) {  // cells are rows (default grid): one warp per cell
             CCL(c, k_row_finish<<<148 * 16, BIN_THREADS, 0, c->stream>>>(nc, c->cell_start.p, rec, c->g, c->orig4.p,
                                                                           c->dec4.p, c->xk.p, fin, c->scratch_u32.p,
-                                                                          cap, nl));
+                                                                          cap, nl, nullptr, nullptr));
             CCL(c, k_row_finish_wide<<<148 * 4, 32 * WIDE_WARPS, 0, c->stream>>>(c->scratch_u32.p, nl,
                                                                                   c->cell_start.p, rec, c->g,
                                                                                   c->orig4.p, c->dec4.p, c->xk.p,
