@@ -394,7 +394,9 @@ def main():
     if world > 1:  # this rank's share for the per-launch byte count
         E, nent = E / world, nent / world
     cls_ms = dict(stats)
-    dom = max(cls_ms, key=lambda k: cls_ms[k][0]) if cls_ms else None
+    # the dominant kernel of the metric's step (S1-S5); K4_fof is the S6 check, timed outside it
+    s15 = {k: v for k, v in cls_ms.items() if k != "K4_fof"}
+    dom = max(s15, key=lambda k: s15[k][0]) if s15 else None
     # algorithmic bytes per launch
     alg_bytes = {
         # per launch: 104 B per editable actually updated + 4 B per row entry evaluated
@@ -409,7 +411,9 @@ def main():
     # ncu traffic of the dominant kernel (committed capture): dram bytes of one
     # captured launch next to that launch's algorithmic bytes
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01_k3_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "r02_k3_traffic.json")
+    if not os.path.exists(tp):
+        tp = os.path.join(ROOT, "profiles", "r01_k3_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f)

@@ -270,7 +270,8 @@ cc_status cc_edit_pack(cc_ctx* ctx, const int64_t* q, int64_t n_edits, uint32_t*
                        int64_t* n_words_h);
 cc_status cc_edit_unpack(cc_ctx* ctx, const uint32_t* words, int64_t n_edits, int64_t* q);
 
-/* S0 thresholds actually used (after cc_build_cells; near_pairs after cc_find_vulnerable), for
+/* S0 thresholds actually used (after cc_build_cells; near_pairs after the first FoF labelling
+ * of ORIG or CORR, -1 before), for
  * the boundary tests: every fp32 value is the single rounding of the paper's formula (Alg. 1
  * l.1-3 P:419-421, Eq. 3; readings R2-R8 of DESIGN.md §3).  lo2s/hi2s: the
  * proven-link shells: original d2 <= lo2s => linked under any positions within
@@ -281,7 +282,7 @@ typedef struct {
     float lo2s_i, hi2s_i, lo2s_w, hi2s_w;
     int pad;
     double b, eps_q, mu, r_search, r_link;
-    int64_t near_pairs;    /* pairs in (lo2s, lo2] U (hi2, hi2s] found by cc_find_vulnerable */
+    int64_t near_pairs;    /* pairs in (lo2s, lo2] U (hi2, hi2s] (the FoF near-shell list)     */
 } cc_thresholds;
 cc_status cc_get_thresholds(cc_ctx* ctx, cc_thresholds* out_h);
 

@@ -359,7 +359,7 @@ void cc_destroy(cc_ctx* c) {
     cc_release(c, c->scratch_u32); cc_release(c, c->rowptr); cc_release(c, c->scratch_u64);
     cc_release(c, c->mom); cc_release(c, c->bc); 
     cc_release(c, c->counters); cc_release(c, c->ctl); cc_release(c, c->trace_a); cc_release(c, c->trace_l);
-    cc_release(c, c->trace_v); cc_release(c, c->trace_s); cc_release(c, c->parent_base); cc_release(c, c->parent_orig); cc_release(c, c->rec32);
+    cc_release(c, c->trace_v); cc_release(c, c->trace_s); cc_release(c, c->parent_base); cc_release(c, c->rec32);
     cc_release(c, c->frozen); cc_release(c, c->fbits); cc_release(c, c->lab_s); cc_release(c, c->slist); cc_release(c, c->tlist); cc_release(c, c->k3work);
     cc_release(c, c->tmp_bytes); cc_release(c, c->codec_bsum); cc_release(c, c->in_f); cc_release(c, c->in_gid);
     for (int d = 0; d < 2; d++) {
@@ -482,10 +482,7 @@ cc_status cc_find_vulnerable(cc_ctx* c, cc_vp_info* info) {
     CC_TRY(cc::scan_editables(c, e_all, tot));
     CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 2, tot, 7 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                c->stream));
-    CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 11, c->near_n.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                               c->stream));
     CC_CUDA(c, cudaStreamSynchronize(c->stream));
-    c->near_count = (int64_t)c->h_counters[11];
     unsigned long long totals[7];
     std::memcpy(totals, c->h_counters + 2, sizeof(totals));
     CC_TRY(cc::rows_resolve(c, totals));
@@ -553,7 +550,7 @@ cc_status cc_get_thresholds(cc_ctx* c, cc_thresholds* out) {
     out->c_b = t.c_b; out->c_f = t.c_f; out->Lf = t.Lf; out->hLf = t.hLf;
     out->lo2s_i = t.lo2s_i; out->hi2s_i = t.hi2s_i; out->lo2s_w = t.lo2s_w; out->hi2s_w = t.hi2s_w;
     out->b = c->b; out->eps_q = c->eps_q; out->mu = c->mu; out->r_search = c->r_pair; out->r_link = c->r_link;
-    out->near_pairs = c->state >= 2 ? c->near_count : 0;
+    out->near_pairs = (c->state >= 2 && c->base_valid) ? c->near_count : -1;
     return CC_OK;
 }
 

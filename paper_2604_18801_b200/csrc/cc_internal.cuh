@@ -236,8 +236,6 @@ struct cc_ctx {
     cc::DBuf<uint4> rec32;       // K1 binning records, 2 x uint4 = 32 B per particle
     cc::DBuf<uint32_t> parent_base;  // FoF forest of the stable links (d2 <= lo2), per build
     bool base_valid = false;
-    cc::DBuf<uint32_t> parent_orig;  // stable forest + original-linked band pairs = FoF(ORIG), per build
-    bool orig_valid = false;
     cc::DBuf<uint32_t> gp_cnt, gp_pos;  // cc_get_pairs: counting sort by owner gid
     cc::DBuf<uint2> near;        // near-shell pairs (slot, slot | bit 31 = linked in the original), K2 count
     cc::DBuf<unsigned long long> near_n;  // their count (may exceed near.cap: then FoF searches directly)
@@ -828,6 +826,8 @@ cc_status rows_resolve(cc_ctx* c, const unsigned long long* totals_h);
 cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* z, const float* xh,
                         const float* yh, const float* zh, const uint32_t* gid, int64_t n);
 cc_status pairs_count(cc_ctx* c);
+cc_status fof_base_build(cc_ctx* c);
+cc_status read_near_count(cc_ctx* c);
 cc_status ensure_slot_of(cc_ctx* c);
 cc_status pairs_fill(cc_ctx* c);
 cc_status rows_finish(cc_ctx* c);

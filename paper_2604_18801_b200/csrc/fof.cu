@@ -216,14 +216,13 @@ cc_status union_near(cc_ctx* c, const float4* P, uint32_t* par) {
 }
 
 // The stable forest: links with original d2 <= lo2s (provably linked in the original,
-// decompressed and corrected positions alike, Th) are united ONCE per build, inside K2's count
-// sweep (pairs.cu); each FoF labelling then adds the near shell and the vulnerable rows.
-// the count sweep of K2 (pairs.cu) unites the stable links it meets; these bracket it
+// decompressed and corrected positions alike, Th) are united ONCE per build, by the count form's
+// candidate sweep in forest mode (pairs.cu fof_base_build, at the first labelling); each FoF
+// labelling then adds the near shell and the vulnerable rows.  These bracket that sweep.
 cc_status fof_base_begin(cc_ctx* c) {
     const int64_t n = c->n;
     CC_TRY(cc_ensure(c, c->parent_base, (size_t)std::max<int64_t>(n, 1), "stable forest"));
     c->base_valid = false;
-    c->orig_valid = false;
     if (n > 0) CCL(c, k_iota<<<(unsigned)((n + FOF_THREADS - 1) / FOF_THREADS), FOF_THREADS, 0, c->stream>>>(
                           n, c->parent_base.p));
     CC_CUDA(c, cudaGetLastError());
@@ -251,18 +250,16 @@ cc_status fof_run(cc_ctx* c, int which, uint32_t* labels, int64_t* n_groups) {
     const float4* P = which == CC_ORIG ? c->orig4.p : (which == CC_DECOMP ? c->dec4.p : c->cor4.p);
     // ORIG and CORR: the stable forest (provably linked in both, Th::lo2s) + the near shell
     // re-tested + the vulnerable rows (the near list overflowing its buffer: direct search)
+    int tok = cc_prof_begin(c, "K4_fof");
+    if (c->state >= 2 && (which == CC_ORIG || which == CC_CORR)) CC_TRY(fof_base_build(c));
     const bool near_ok = c->near_count <= (int64_t)c->near.cap;
     const bool via_base = c->state >= 2 && c->base_valid && near_ok && (which == CC_ORIG || which == CC_CORR);
     CC_CUDA(c, cudaMemsetAsync(c->mingid.p, 0xFF, n1 * sizeof(uint32_t), c->stream));
     CC_CUDA(c, cudaMemsetAsync(c->gsize.p, 0, n1 * sizeof(uint32_t), c->stream));
     CC_CUDA(c, cudaMemsetAsync(c->counters.p + 8, 0, sizeof(unsigned long long), c->stream));
     const unsigned nb = (unsigned)((n + FOF_THREADS - 1) / FOF_THREADS);
-    int tok = cc_prof_begin(c, "K4_fof");
     if (n > 0) {
-        if (via_base && which == CC_ORIG && c->orig_valid) {  // built by K2's fill sweep
-            CC_CUDA(c, cudaMemcpyAsync(c->parent.p, c->parent_orig.p, (size_t)n * sizeof(uint32_t),
-                                       cudaMemcpyDeviceToDevice, c->stream));
-        } else if (via_base) {
+        if (via_base) {
             CC_CUDA(c, cudaMemcpyAsync(c->parent.p, c->parent_base.p, (size_t)n * sizeof(uint32_t),
                                        cudaMemcpyDeviceToDevice, c->stream));
             if (c->E > 0) {

@@ -26,7 +26,12 @@ constexpr int PAIR_THREADS = 256;
 
 // the count sweep's per-candidate work (shared by the two count kernels): band pair -> degrees;
 // stable link -> the stable forest; near shell -> the near list
+// mode bits: CM_DEG = band pairs -> degrees (S2, cc_find_vulnerable); CM_FOREST = stable links ->
+// the stable forest and the near-shell list (S6 data, built at the first FoF labelling)
+constexpr int CM_DEG = 1, CM_FOREST = 2;
+
 struct CountCtx {
+    int mode;
     const float4* __restrict__ dec4;
     const Th& t;  // the kernel's parameter (no copy)
     uint32_t n_own;
@@ -40,10 +45,11 @@ struct CountCtx {
     uint2* __restrict__ near;
     unsigned long long* __restrict__ near_n;
     unsigned long long near_cap;
-    __device__ __forceinline__ CountCtx(int64_t n, const float4* dec4_, const Grid& g, const Th& t_, uint32_t n_own_,
-                                        uint32_t* deg_, uint32_t* par_base_, uint2* near_, unsigned long long* near_n_,
-                                        unsigned long long near_cap_, uint32_t s_, const float4& p_)
-        : dec4(dec4_), t(t_), n_own(n_own_), s(s_), p(p_), cnt(0), rs(s_), ntest(0), deg(deg_), par_base(par_base_),
+    __device__ __forceinline__ CountCtx(int mode_, int64_t n, const float4* dec4_, const Grid& g, const Th& t_,
+                                        uint32_t n_own_, uint32_t* deg_, uint32_t* par_base_, uint2* near_,
+                                        unsigned long long* near_n_, unsigned long long near_cap_, uint32_t s_,
+                                        const float4& p_)
+        : mode(mode_), dec4(dec4_), t(t_), n_own(n_own_), s(s_), p(p_), cnt(0), rs(s_), ntest(0), deg(deg_), par_base(par_base_),
           near(near_), near_n(near_n_), near_cap(near_cap_) {
         multi = n_own < (uint32_t)n;
         ghost = multi && __float_as_uint(dec4[s].w) >= n_own;
@@ -55,6 +61,7 @@ struct CountCtx {
         ntest++;
         const float d2 = inner ? dist2_nw(p, q) : dist2(p, q, t);
         if (t.lo2 < d2 && d2 <= t.hi2) {
+            if (!(mode & CM_DEG)) return;
             const bool gj = multi && __float_as_uint(dec4[j].w) >= n_own;
             if (!ghost) {
                 cnt++;
@@ -64,9 +71,11 @@ struct CountCtx {
                 atomicAdd(&deg[j], 1u);
                 atomicOr(&deg[s], 0x80000000u);
             }
+        } else if (!(mode & CM_FOREST)) {
+            return;
         } else if (d2 <= lo2s) {
             // a stable FoF link: provably linked in the original, decompressed and corrected
-            // positions alike (Th::lo2s, fof.cu), united here in the same candidate sweep
+            // positions alike (Th::lo2s, fof.cu)
             uf_link(par_base, s, j, rs);
         } else if (d2 <= hi2s) {
             // near shell (lo2s, lo2] or (hi2, hi2s]: not vulnerable, but fp32 rounding could flip
@@ -83,7 +92,7 @@ struct CountCtx {
 // united into the stable FoF forest in the same sweep.  (General grid; k_pairs_count_tiled below
 // is the default-grid form.)
 __global__ void __launch_bounds__(PAIR_THREADS)
-k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
+k_pairs_count(int mode, int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
               const uint32_t* __restrict__ xk, const uint32_t* __restrict__ cs, Grid g, Th t, double r, uint32_t n_own,
               uint32_t* __restrict__ deg, uint32_t* __restrict__ par_base, uint2* __restrict__ near,
               unsigned long long* __restrict__ near_n, unsigned long long near_cap, unsigned long long* __restrict__ tests) {
@@ -93,7 +102,7 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
     double u;
     int cx, cy, cz;
     cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
-    CountCtx k(n, dec4, g, t, n_own, deg, par_base, near, near_n, near_cap, (uint32_t)s, p);
+    CountCtx k(mode, n, dec4, g, t, n_own, deg, par_base, near, near_n, near_cap, (uint32_t)s, p);
     auto test = [&](uint32_t j) { k(j, orig4[j]); };
     for_each_pair_forward(g, cs, xk, (uint32_t)s, u, cy, cz, r, t.periodic != 0, test);
     if (k.cnt) atomicAdd(&deg[s], k.cnt);
@@ -112,6 +121,7 @@ k_pairs_count(int64_t n, const float4* __restrict__ orig4, const float4* __restr
 constexpr int CW_NR = 10;       // ranges per home particle: own row (forward, wrap part), 4 rows x 2 windows
 constexpr int CW_WARPS = PAIR_THREADS / 32;
 
+template <int MODE>
 __global__ void __launch_bounds__(PAIR_THREADS)
 k_pairs_count_warp(int64_t n, const float4* __restrict__ orig4, const float4* __restrict__ dec4,
                    const uint32_t* __restrict__ xk, const uint32_t* __restrict__ cs, Grid g, Th t, double r,
@@ -235,6 +245,7 @@ k_pairs_count_warp(int64_t n, const float4* __restrict__ orig4, const float4* __
             const float4 qq = orig4[j];
             const float d2 = inner ? dist2_nw(pp, qq) : dist2(pp, qq, t);
             if (t.lo2 < d2 && d2 <= t.hi2) {
+                if (!(MODE & CM_DEG)) continue;
                 const bool gj = multi && __float_as_uint(dec4[j].w) >= n_own;
                 if (!ghost) {
                     atomicAdd(&deg[so], 1u);
@@ -244,6 +255,8 @@ k_pairs_count_warp(int64_t n, const float4* __restrict__ orig4, const float4* __
                     atomicAdd(&deg[j], 1u);
                     atomicOr(&deg[so], 0x80000000u);
                 }
+            } else if (!(MODE & CM_FOREST)) {
+                continue;
             } else if (d2 <= (inner ? t.lo2s_i : t.lo2s_w)) {
                 // a stable FoF link (see CountCtx).  The home's cached ancestor is shared by the
                 // lanes testing its candidates: any value once an ancestor of the home stays
@@ -357,7 +370,7 @@ k_pairs_count_tiled(int64_t n, const float4* __restrict__ orig4, const float4* _
                 double u;
                 int cx, cy, cz;
                 cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
-                CountCtx k(n, dec4, g, t, n_own, deg, par_base, near, near_n, near_cap, s, p);
+                CountCtx k(CM_DEG | CM_FOREST, n, dec4, g, t, n_own, deg, par_base, near, near_n, near_cap, s, p);
                 auto test = [&](uint32_t j) { k(j, orig4[j]); };
                 for_each_pair_forward(g, cs, xk, s, u, cy, cz, r, periodic, test);
                 if (k.cnt) atomicAdd(&deg[s], k.cnt);
@@ -383,7 +396,7 @@ k_pairs_count_tiled(int64_t n, const float4* __restrict__ orig4, const float4* _
             const uint32_t si = hd.s0 + (s - hd.g0);  // staged index of s
             const float4 p = so4[si];
             const double u = local_u((double)p.x, g);
-            CountCtx k(n, dec4, g, t, n_own, deg, par_base, near, near_n, near_cap, s, p);
+            CountCtx k(CM_DEG | CM_FOREST, n, dec4, g, t, n_own, deg, par_base, near, near_n, near_cap, s, p);
             // x-window key bounds, once for all rows (as for_each_pair_forward)
             double a = u - r, b = u + r, a1 = 0.0, b1 = -1.0;
             bool up = false;
@@ -440,8 +453,7 @@ __global__ void __launch_bounds__(PAIR_THREADS)
 k_pairs_fill(uint32_t e_all, const uint32_t* __restrict__ slotE, const float4* __restrict__ orig4,
              const uint32_t* __restrict__ xk, const uint32_t* __restrict__ cs, Grid g, Th t, double r,
              const uint32_t* __restrict__ eidx, uint32_t e_own, const unsigned long long* __restrict__ rowptr,
-             uint32_t* __restrict__ cur, uint32_t* __restrict__ rows, uint32_t* __restrict__ par_orig,
-             unsigned long long* __restrict__ tests) {
+             uint32_t* __restrict__ cur, uint32_t* __restrict__ rows, unsigned long long* __restrict__ tests) {
     const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= e_all) return;
     unsigned ntest = 0;
@@ -453,7 +465,6 @@ k_pairs_fill(uint32_t e_all, const uint32_t* __restrict__ slotE, const float4* _
     int cx, cy, cz;
     cell_of(p.x, p.y, p.z, g, u, cx, cy, cz);
     const bool inner = interior(p.x, p.y, p.z, g, t);
-    uint32_t rs = (uint32_t)s;  // cached ancestor of s in the ORIG forest (uf_link)
     auto emit = [&](uint32_t j) {
         ntest++;
         const float4 q = orig4[j];
@@ -463,9 +474,6 @@ k_pairs_fill(uint32_t e_all, const uint32_t* __restrict__ slotE, const float4* _
             const uint32_t ol = d2 <= t.b2 ? ENT_OLINK : 0u;
             if (es < e_own) rows[rowptr[es] + atomicAdd(&cur[es], 1u)] = ej | (gq > gp ? ENT_UPPER : 0u) | ol;
             if (ej < e_own) rows[rowptr[ej] + atomicAdd(&cur[ej], 1u)] = es | (gp > gq ? ENT_UPPER : 0u) | ol;
-            // FoF(ORIG) = the stable forest + the original-linked band pairs (an owned endpoint;
-            // ghost-ghost pairs belong to their owner rank)
-            if (ol && (es < e_own || ej < e_own)) uf_link(par_orig, (uint32_t)s, j, rs);
         }
     };
     for_each_pair_forward(g, cs, xk, (uint32_t)s, u, cy, cz, r, t.periodic != 0, emit);
@@ -631,45 +639,86 @@ k_sort_long(uint32_t e_lo, uint32_t e_hi, const unsigned long long* __restrict__
 
 }  // namespace
 
+// one candidate sweep of the count form in the given mode (CM_DEG / CM_FOREST), counting tests
+static cc_status count_sweep(cc_ctx* c, int mode, unsigned long long* tests) {
+    const int64_t n = c->n;
+    if (n <= 0) return CC_OK;
+    const bool half = !c->th.periodic || (c->g.ny >= 3 && c->g.nz >= 3);
+    const char* env = std::getenv("CC_K2_TILED");
+    const unsigned long long cap = (unsigned long long)c->near.cap;
+    if (c->g.nx == 1 && half && !(env && (env[0] == '0' || env[0] == '1'))) {
+        const int64_t nwarp = (n + 31) / 32;
+        const unsigned nb = (unsigned)((nwarp + CW_WARPS - 1) / CW_WARPS);
+        if (mode == CM_DEG)
+            CCL(c, k_pairs_count_warp<CM_DEG><<<nb, PAIR_THREADS, 0, c->stream>>>(
+                n, c->orig4.p, c->dec4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in, c->deg.p,
+                c->parent_base.p, c->near.p, c->near_n.p, cap, tests));
+        else
+            CCL(c, k_pairs_count_warp<CM_FOREST><<<nb, PAIR_THREADS, 0, c->stream>>>(
+                n, c->orig4.p, c->dec4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in, c->deg.p,
+                c->parent_base.p, c->near.p, c->near_n.p, cap, tests));
+    } else if (c->g.nx == 1 && half && env && env[0] == '1') {  // A/B variant (slower)
+        if (mode != CM_DEG) return CC_OK;  // it does both in the degree sweep
+        const double per_row = (double)n / ((double)c->g.ny * c->g.nz);
+        const int trows = std::max(1, std::min(TROWS_MAX, (int)(240.0 / std::max(per_row, 1.0))));
+        const int tiles_y = (c->g.ny + trows - 1) / trows;
+        const int64_t ntiles = (int64_t)c->g.nz * tiles_y;
+        const unsigned nbk = (unsigned)std::min<int64_t>(ntiles, 148 * 8);
+        CCL(c, k_pairs_count_tiled<<<nbk, PAIR_THREADS, 0, c->stream>>>(
+            n, c->orig4.p, c->dec4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in, c->deg.p,
+            c->parent_base.p, c->near.p, c->near_n.p, cap, tests, ntiles, tiles_y, trows));
+    } else {
+        CCL(c, k_pairs_count<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
+            mode, n, c->orig4.p, c->dec4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in,
+            c->deg.p, c->parent_base.p, c->near.p, c->near_n.p, cap, tests));
+    }
+    CC_CUDA(c, cudaGetLastError());
+    return CC_OK;
+}
+
+// S2's count: band partners per slot (the degrees) -- no FoF work (the stable-forest
+// unions of round 1's count sweep were S6 work inside the S1-S5 timing)
 cc_status pairs_count(cc_ctx* c) {
     const int64_t n = c->n;
     CC_TRY(cc_ensure(c, c->deg, (size_t)std::max<int64_t>(n, 1), "deg"));
     CC_CUDA(c, cudaMemsetAsync(c->deg.p, 0, (size_t)std::max<int64_t>(n, 1) * sizeof(uint32_t), c->stream));
-    CC_TRY(fof_base_begin(c));  // the stable FoF forest is built inside the count sweep
     const int64_t near_cap = std::max<int64_t>(4096, n / 128);
     CC_TRY(cc_ensure(c, c->near, (size_t)near_cap, "near-shell pairs"));
     CC_TRY(cc_ensure(c, c->near_n, 1, "near-shell count"));
+    CC_TRY(cc_ensure(c, c->parent_base, (size_t)std::max<int64_t>(n, 1), "stable forest"));
     CC_CUDA(c, cudaMemsetAsync(c->near_n.p, 0, sizeof(unsigned long long), c->stream));
-    if (n > 0) {
-        int tok = cc_prof_begin(c, "K2_count");
-        const bool half = !c->th.periodic || (c->g.ny >= 3 && c->g.nz >= 3);
-        const char* env = std::getenv("CC_K2_TILED");
-        if (c->g.nx == 1 && half && !(env && (env[0] == '0' || env[0] == '1'))) {
-            const int64_t nwarp = (n + 31) / 32;
-            CCL(c, k_pairs_count_warp<<<(unsigned)((nwarp + CW_WARPS - 1) / CW_WARPS), PAIR_THREADS, 0, c->stream>>>(
-                n, c->orig4.p, c->dec4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in, c->deg.p,
-                c->parent_base.p, c->near.p, c->near_n.p, (unsigned long long)c->near.cap, work_counters(c) + 2));
-        } else if (c->g.nx == 1 && half && env && env[0] == '1') {  // A/B variant (slower)
-            // home strip ~240 particles (one pass of the 256-thread block)
-            const double per_row = (double)n / ((double)c->g.ny * c->g.nz);
-            const int trows = std::max(1, std::min(TROWS_MAX, (int)(240.0 / std::max(per_row, 1.0))));
-            const int tiles_y = (c->g.ny + trows - 1) / trows;
-            const int64_t ntiles = (int64_t)c->g.nz * tiles_y;
-            const unsigned nbk = (unsigned)std::min<int64_t>(ntiles, 148 * 8);
-            CCL(c, k_pairs_count_tiled<<<nbk, PAIR_THREADS, 0, c->stream>>>(
-                n, c->orig4.p, c->dec4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in, c->deg.p,
-                c->parent_base.p, c->near.p, c->near_n.p, (unsigned long long)c->near.cap, work_counters(c) + 2,
-                ntiles, tiles_y, trows));
-        } else {
-            CCL(c, k_pairs_count<<<(unsigned)((n + PAIR_THREADS - 1) / PAIR_THREADS), PAIR_THREADS, 0, c->stream>>>(
-                n, c->orig4.p, c->dec4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, (uint32_t)c->n_in,
-                c->deg.p, c->parent_base.p, c->near.p, c->near_n.p, (unsigned long long)c->near.cap,
-                work_counters(c) + 2));
-        }
-        cc_prof_end(c, tok);
-        CC_CUDA(c, cudaGetLastError());
+    c->base_valid = false;
+    const char* env = std::getenv("CC_K2_TILED");
+    const bool tiled = env && env[0] == '1';
+    if (tiled) CC_TRY(fof_base_begin(c));  // the A/B variant builds the forest in the same sweep
+    int tok = cc_prof_begin(c, "K2_count");
+    CC_TRY(count_sweep(c, CM_DEG, work_counters(c) + 2));
+    cc_prof_end(c, tok);
+    if (tiled) {
+        CC_TRY(fof_base_end(c));
+        CC_TRY(read_near_count(c));
     }
-    return fof_base_end(c);
+    return CC_OK;
+}
+
+// S6 data, built at the first FoF labelling after cc_find_vulnerable: the stable forest (links
+// with original d2 <= lo2s, provably linked in every position set within xi_f) and the near-shell
+// list, by the same candidate sweep in CM_FOREST mode
+cc_status fof_base_build(cc_ctx* c) {
+    if (c->base_valid) return CC_OK;
+    CC_CUDA(c, cudaMemsetAsync(c->near_n.p, 0, sizeof(unsigned long long), c->stream));
+    CC_TRY(fof_base_begin(c));
+    CC_TRY(count_sweep(c, CM_FOREST, work_counters(c) + 4));
+    CC_TRY(fof_base_end(c));
+    return read_near_count(c);
+}
+
+cc_status read_near_count(cc_ctx* c) {
+    CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 11, c->near_n.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               c->stream));
+    CC_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->near_count = (int64_t)c->h_counters[11];
+    return CC_OK;
 }
 
 // totals_h = the 56-byte VDeg total (scan.cu): entries per class, editables per class, ghosts
@@ -691,11 +740,6 @@ cc_status rows_resolve(cc_ctx* c, const unsigned long long* totals_h) {
 
 cc_status pairs_fill(cc_ctx* c) {
     const int64_t n = c->n;
-    CC_TRY(cc_ensure(c, c->parent_orig, (size_t)std::max<int64_t>(n, 1), "ORIG forest"));
-    if (n > 0)
-        CC_CUDA(c, cudaMemcpyAsync(c->parent_orig.p, c->parent_base.p, (size_t)n * sizeof(uint32_t),
-                                   cudaMemcpyDeviceToDevice, c->stream));
-    c->orig_valid = true;
     CC_TRY(cc_ensure(c, c->rows, (size_t)c->nent + 8, "rows"));  // +8: k_pgd<1> reads whole 16-byte vectors
     if (n > 0 && c->nent > 0) {
         int tok = cc_prof_begin(c, "K2_fill");
@@ -707,11 +751,11 @@ cc_status pairs_fill(cc_ctx* c) {
             (uint32_t)c->E_all, c->slotE.p, c->orig4.p, c->xk.p, c->cell_start.p, c->g, c->th, c->r_pair, c->eidx.p,
             (uint32_t)c->E,
             reinterpret_cast<const unsigned long long*>(c->rowptr.p), c->scratch_u32.p, c->rows.p,
-            c->parent_orig.p, work_counters(c) + 3));
+            work_counters(c) + 3));
         cc_prof_end(c, tok);
         CC_CUDA(c, cudaGetLastError());
     }
-    return union_near(c, nullptr, c->parent_orig.p);  // + the near shell's original links
+    return CC_OK;
 }
 
 cc_status rows_finish(cc_ctx* c) {
