@@ -14,6 +14,7 @@
 //     Consecutive threads own consecutive cells, so reads and writes stream.
 // The slot order is fully determined by the data (x ties broken by input index).
 #include <cmath>
+#include <cstdlib>
 
 #include "cc_internal.cuh"
 
@@ -225,7 +226,7 @@ __device__ __forceinline__ void warp_sort32(unsigned long long& k, int& o, int l
     }
 }
 
-__global__ void __launch_bounds__(BIN_THREADS)
+__global__ void __launch_bounds__(BIN_THREADS, 6)  // 6 blocks/SM (measured: -0.3 ms at C4 vs 64 registers)
 k_row_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restrict__ rec, Grid g,
              float4* __restrict__ orig4, float4* __restrict__ dec4, uint32_t* __restrict__ xk,
              uint32_t* __restrict__ slot_of, uint32_t* __restrict__ long_list, uint64_t cap,

@@ -129,7 +129,8 @@ k_pairs_count_warp(int64_t n, const float4* __restrict__ orig4, const float4* __
                    uint2* __restrict__ near, unsigned long long* __restrict__ near_n, unsigned long long near_cap,
                    unsigned long long* __restrict__ tests) {
     __shared__ uint32_t r_start[CW_WARPS][CW_NR][32];  // range starts, [range][lane]
-    __shared__ uint32_t r_cum[CW_WARPS][CW_NR + 1][32];  // exclusive running counts, [range][lane]
+    __shared__ uint32_t r_cum[CW_WARPS][CW_NR][32];      // exclusive running counts, [range][lane]
+    __shared__ uint8_t l_nr[CW_WARPS][32];               // ranges per home
     __shared__ uint32_t l_ex[CW_WARPS][33];              // warp-exclusive pair offsets per lane
     __shared__ float4 l_p[CW_WARPS][32];
     __shared__ uint8_t l_fl[CW_WARPS][32];               // bit 0 ghost, bit 1 interior
@@ -212,8 +213,7 @@ k_pairs_count_warp(int64_t n, const float4* __restrict__ orig4, const float4* __
             }
         }
     }
-    r_cum[w][nr][lane] = tot;
-    for (uint32_t q = nr + 1; q <= CW_NR; q++) r_cum[w][q][lane] = 0xFFFFFFFFu;  // past the last range
+    l_nr[w][lane] = (uint8_t)nr;
     l_rs[w][lane] = (uint32_t)s;
     // warp-exclusive offsets of the lanes' candidate lists
     uint32_t inc = tot;
@@ -236,7 +236,8 @@ k_pairs_count_warp(int64_t n, const float4* __restrict__ orig4, const float4* __
                 if (l_ex[w][o + st] <= q) o += st;
             const uint32_t qo = q - l_ex[w][o];
             int k = 0;  // the range: largest k with cum[k] <= qo
-            while (r_cum[w][k + 1][o] <= qo) k++;
+            const int nro = l_nr[w][o];
+            while (k + 1 < nro && r_cum[w][k + 1][o] <= qo) k++;
             const uint32_t j = r_start[w][k][o] + (qo - r_cum[w][k][o]);
             const uint32_t so = (uint32_t)(s - lane + o);
             const float4 pp = l_p[w][o];
