@@ -208,12 +208,13 @@ k_cell_finish_mid(const uint32_t* __restrict__ long_list, const unsigned long lo
 // cell, grid-stride; cells of <= 32 records sort one key per lane (15-step bitonic), <= 64 two per
 // lane (k_cell_finish_mid's network), longer ones go to the block kernel's list.  No thread-per-
 // cell divergence and no list atomics for the common sizes.
-__device__ __forceinline__ void warp_sort32(unsigned long long& k, int& o, int lane) {
+template <typename K>
+__device__ __forceinline__ void warp_sort32(K& k, int& o, int lane) {
 #pragma unroll
     for (int kk = 2; kk <= 32; kk <<= 1) {
 #pragma unroll
         for (int j = kk >> 1; j > 0; j >>= 1) {
-            const unsigned long long pk = __shfl_xor_sync(0xffffffffu, k, j);
+            const K pk = __shfl_xor_sync(0xffffffffu, k, j);
             const int po = __shfl_xor_sync(0xffffffffu, o, j);
             const bool up = (lane & kk) == 0;
             const bool lower = (lane & j) == 0;
@@ -224,6 +225,48 @@ __device__ __forceinline__ void warp_sort32(unsigned long long& k, int& o, int l
             }
         }
     }
+}
+
+// the 64-slot network, two (key, offset) pairs per lane: elements lane and lane + 32
+template <typename K>
+__device__ __forceinline__ void warp_sort64(K& k0, K& k1, int& o0, int& o1, int lane) {
+    for (int kk = 2; kk <= 64; kk <<= 1) {
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            if (j == 32) {
+                const bool up = (lane & kk) == 0;
+                if ((k0 > k1) == up) {
+                    const K tk = k0;
+                    k0 = k1;
+                    k1 = tk;
+                    const int to = o0;
+                    o0 = o1;
+                    o1 = to;
+                }
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    K& kr = h ? k1 : k0;
+                    int& orr = h ? o1 : o0;
+                    const int idx = lane + 32 * h;
+                    const K pk = __shfl_xor_sync(0xffffffffu, kr, j);
+                    const int po = __shfl_xor_sync(0xffffffffu, orr, j);
+                    const bool up = (idx & kk) == 0;
+                    const bool lower = (lane & j) == 0;
+                    const bool take = lower ? ((kr > pk) == up) : ((kr < pk) == up);
+                    if (take) {
+                        kr = pk;
+                        orr = po;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// a record's 32-bit x order key from its first half (x, y, z, x_hat)
+__device__ __forceinline__ uint32_t rec_xkey(const Rec* __restrict__ rec, uint32_t s, const Grid& g) {
+    const uint4 h = reinterpret_cast<const uint4*>(rec)[2 * s];
+    return x_sort_key(__uint_as_float(h.x), g);
 }
 
 __global__ void __launch_bounds__(BIN_THREADS, 6)  // 6 blocks/SM (measured: -0.3 ms at C4 vs 64 registers)
@@ -248,51 +291,37 @@ k_row_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restri
             }
             continue;
         }
+        // sort by the 32-bit x key with the record offset as payload (2 shuffles per step instead
+        // of 3); a row with two equal x keys (rare) is sorted again on the full (x key, input
+        // index) key so the order stays a pure function of the data
         if (len <= 32) {
-            Rec r;
-            unsigned long long k = ~0ull;
+            uint32_t k = lane < len ? rec_xkey(rec, a + lane, g) : 0xFFFFFFFFu;  // no real key is ~0
             int o = lane;
-            if (lane < len) {
-                r = load_rec(rec, a + lane);
-                k = rec_key(r, g);
-            }
             warp_sort32(k, o, lane);
+            const uint32_t kp = __shfl_up_sync(0xffffffffu, k, 1);
+            if (__any_sync(0xffffffffu, lane > 0 && lane < len && kp == k)) {
+                unsigned long long k64 = lane < len ? rec_key(load_rec(rec, a + lane), g) : ~0ull;
+                o = lane;
+                warp_sort32(k64, o, lane);
+            }
             if (lane < len) emit(load_rec(rec, a + o), a + lane, a + o, orig4, dec4, xk, slot_of, g);
             continue;
         }
-        // 33..64: two keys per lane, the 64-slot network of k_cell_finish_mid
-        unsigned long long k0 = rec_key(load_rec(rec, a + lane), g);
-        unsigned long long k1 = lane + 32 < len ? rec_key(load_rec(rec, a + lane + 32), g) : ~0ull;
+        // 33..64: two keys per lane, the 64-slot network
+        uint32_t k0 = rec_xkey(rec, a + lane, g);
+        uint32_t k1 = lane + 32 < len ? rec_xkey(rec, a + lane + 32, g) : 0xFFFFFFFFu;
         int o0 = lane, o1 = lane + 32;
-        for (int kk = 2; kk <= 64; kk <<= 1) {
-            for (int j = kk >> 1; j > 0; j >>= 1) {
-                if (j == 32) {
-                    const bool up = (lane & kk) == 0;
-                    if ((k0 > k1) == up) {
-                        const unsigned long long tk = k0;
-                        k0 = k1;
-                        k1 = tk;
-                        const int to = o0;
-                        o0 = o1;
-                        o1 = to;
-                    }
-                } else {
-#pragma unroll
-                    for (int h = 0; h < 2; h++) {
-                        unsigned long long& kr = h ? k1 : k0;
-                        int& orr = h ? o1 : o0;
-                        const int idx = lane + 32 * h;
-                        const unsigned long long pk = __shfl_xor_sync(0xffffffffu, kr, j);
-                        const int po = __shfl_xor_sync(0xffffffffu, orr, j);
-                        const bool up = (idx & kk) == 0;
-                        const bool lower = (lane & j) == 0;
-                        const bool take = lower ? ((kr > pk) == up) : ((kr < pk) == up);
-                        if (take) {
-                            kr = pk;
-                            orr = po;
-                        }
-                    }
-                }
+        warp_sort64(k0, k1, o0, o1, lane);
+        {
+            const uint32_t p0 = __shfl_up_sync(0xffffffffu, k0, 1), p1 = __shfl_up_sync(0xffffffffu, k1, 1);
+            const uint32_t last0 = __shfl_sync(0xffffffffu, k0, 31);
+            const bool tie = (lane > 0 && p0 == k0) || (lane + 32 < len && (lane > 0 ? p1 == k1 : last0 == k1));
+            if (__any_sync(0xffffffffu, tie)) {
+                unsigned long long q0 = rec_key(load_rec(rec, a + lane), g);
+                unsigned long long q1 = lane + 32 < len ? rec_key(load_rec(rec, a + lane + 32), g) : ~0ull;
+                o0 = lane;
+                o1 = lane + 32;
+                warp_sort64(q0, q1, o0, o1, lane);
             }
         }
         emit(load_rec(rec, a + o0), a + lane, a + o0, orig4, dec4, xk, slot_of, g);
