@@ -333,13 +333,13 @@ k_row_finish(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __restri
 // lane, a W-wide register bitonic of (key, offset); longer rows are deferred to the warp kernel
 // (<= 64, list mode), k_row_finish_wide (<= 512) and the block kernel.  The warp-per-row kernel
 // left 3/4 of its lanes idle there and did not shrink with the slab (its cost is per row).
-template <int W>
-__device__ __forceinline__ void group_sort_kv(unsigned long long& k, int& o, int gl) {
+template <int W, typename K>
+__device__ __forceinline__ void group_sort_kv(K& k, int& o, int gl) {
 #pragma unroll
     for (int kk = 2; kk <= W; kk <<= 1) {
 #pragma unroll
         for (int j = kk >> 1; j > 0; j >>= 1) {
-            const unsigned long long pk = __shfl_xor_sync(0xffffffffu, k, j);
+            const K pk = __shfl_xor_sync(0xffffffffu, k, j);
             const int po = __shfl_xor_sync(0xffffffffu, o, j);
             const bool up = (gl & kk) == 0;
             const bool lower = (gl & j) == 0;
@@ -376,9 +376,17 @@ k_row_finish_group(int64_t ncell, const uint32_t* __restrict__ cs, const Rec* __
                 len = 0;
             }
         }
-        unsigned long long k = gl < len ? rec_key(load_rec(rec, a + gl), g) : ~0ull;
+        // 32-bit x keys; a group with equal keys is sorted again on the full key (k_row_finish)
+        uint32_t k = gl < len ? rec_xkey(rec, a + gl, g) : 0xFFFFFFFFu;
         int o = gl;
         group_sort_kv<W>(k, o, gl);
+        const uint32_t kp = __shfl_up_sync(0xffffffffu, k, 1);
+        const bool tie = gl > 0 && gl < len && kp == k;
+        if (__any_sync(0xffffffffu, tie)) {  // warp-uniform redo (groups without ties re-sort identically)
+            unsigned long long k64 = gl < len ? rec_key(load_rec(rec, a + gl), g) : ~0ull;
+            o = gl;
+            group_sort_kv<W>(k64, o, gl);
+        }
         if (gl < len) emit(load_rec(rec, a + o), a + gl, a + o, orig4, dec4, xk, slot_of, g);
     }
 }
@@ -483,8 +491,7 @@ k_cell_finish_long(const uint32_t* __restrict__ long_list, uint64_t cap, const u
             uint32_t* off = offs + a;
             for (int k = threadIdx.x; k < len; k += blockDim.x) off[k] = (uint32_t)k;
             __syncthreads();
-            const Rec* ra = rec + a;
-            block_sort_global(off, (int64_t)len, [ra, g](uint32_t o) { return rec_key(load_rec(ra, o), g); });
+            block_sort_global(off, (int64_t)len, [rec, a, g](uint32_t o) { return rec_key(load_rec(rec, a + o), g); });
             for (int k = threadIdx.x; k < len; k += blockDim.x)
                 emit(load_rec(rec, a + off[k]), a + k, a + off[k], orig4, dec4, xk, slot_of, g);
             __syncthreads();
