@@ -327,9 +327,13 @@ def main():
     small = 24 * n < 512 * 2**20
     flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=dev) if small else None
 
-    def step(mid=None):
+    def step(mid=None, ph=None):
         c.build_cells(x, y, z, xh, yh, zh, gid=gid)
+        if ph is not None:
+            ph[0].record(stream)
         vp = c.find_vulnerable()
+        if ph is not None:
+            ph[1].record(stream)
         _, info = c.correct(out)
         if mid is not None:  # S1-S5 end here; S6 + S7 (the check) follow
             mid.record(stream)
@@ -351,6 +355,7 @@ def main():
     c.kernel_stats(reset=True)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    phs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
@@ -361,7 +366,7 @@ def main():
             with torch.cuda.stream(stream):
                 flush.fill_(float(k))
         evs[k][0].record(stream)
-        res = step(mids[k])
+        res = step(mids[k], phs[k])
         evs[k][1].record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
@@ -375,14 +380,22 @@ def main():
     rank_ms = None
     if world > 1:
         # every rank's own S1-S5 time and profiled-kernel sum (load balance across the slabs)
+        # phases per rank: S1 (cc_build_cells incl. the ghost exchange), S2-S3 (cc_find_vulnerable
+        # incl. the refresh lists), S4-S5 (cc_correct incl. the per-iteration exchange)
+        ph1 = sum(a[0].elapsed_time(p[0]) for a, p in zip(evs, phs)) / args.steps
+        ph2 = sum(p[0].elapsed_time(p[1]) for p in phs) / args.steps
+        ph3 = sum(p[1].elapsed_time(mm) for p, mm in zip(phs, mids)) / args.steps
         own = torch.tensor([ms_corr / args.steps, sum(v[0] for k, v in stats.items()
                                                       if k != "K4_fof" and not k.startswith("K3_work")
                                                       and k != "total_launches" and not k.endswith("_tests"))
-                            / args.steps], device=dev, dtype=torch.float64)
+                            / args.steps, ph1, ph2, ph3], device=dev, dtype=torch.float64)
         allr = [torch.zeros_like(own) for _ in range(world)]
         torch.distributed.all_gather(allr, own)
         rank_ms = {"s1_s5_ms": [round(float(a[0]), 3) for a in allr],
-                   "profiled_kernels_ms": [round(float(a[1]), 3) for a in allr]}
+                   "profiled_kernels_ms": [round(float(a[1]), 3) for a in allr],
+                   "build_ms": [round(float(a[2]), 3) for a in allr],
+                   "find_vulnerable_ms": [round(float(a[3]), 3) for a in allr],
+                   "correct_ms": [round(float(a[4]), 3) for a in allr]}
         t = torch.tensor([ms_total, ms_corr], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_total, ms_corr = float(t[0].item()), float(t[1].item())
