@@ -378,13 +378,14 @@ def main():
     ms_corr = sum(a[0].elapsed_time(mm) for a, mm in zip(evs, mids))
     stats = c.kernel_stats(reset=True)
     rank_ms = None
+    # phases: S1 (cc_build_cells incl. the ghost exchange), S2-S3 (cc_find_vulnerable incl. the
+    # refresh lists), S4-S5 (cc_correct incl. the per-iteration exchange); device time per step
+    ph1 = sum(a[0].elapsed_time(p[0]) for a, p in zip(evs, phs)) / args.steps
+    ph2 = sum(p[0].elapsed_time(p[1]) for p in phs) / args.steps
+    ph3 = sum(p[1].elapsed_time(mm) for p, mm in zip(phs, mids)) / args.steps
+    phases = {"build_ms": round(ph1, 3), "find_vulnerable_ms": round(ph2, 3), "correct_ms": round(ph3, 3)}
     if world > 1:
-        # every rank's own S1-S5 time and profiled-kernel sum (load balance across the slabs)
-        # phases per rank: S1 (cc_build_cells incl. the ghost exchange), S2-S3 (cc_find_vulnerable
-        # incl. the refresh lists), S4-S5 (cc_correct incl. the per-iteration exchange)
-        ph1 = sum(a[0].elapsed_time(p[0]) for a, p in zip(evs, phs)) / args.steps
-        ph2 = sum(p[0].elapsed_time(p[1]) for p in phs) / args.steps
-        ph3 = sum(p[1].elapsed_time(mm) for p, mm in zip(phs, mids)) / args.steps
+        # every rank's own S1-S5 time, profiled-kernel sum and phases (load balance, exchange cost)
         own = torch.tensor([ms_corr / args.steps, sum(v[0] for k, v in stats.items()
                                                       if k != "K4_fof" and not k.startswith("K3_work")
                                                       and k != "total_launches" and not k.endswith("_tests"))
@@ -507,6 +508,7 @@ def main():
         "roofline": roof, "k3_roofline": k3_roof,
         "kernels_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in cls_ms.items()},
         "pair_tests": pair_tests,
+        "phases_ms": phases,
         "per_rank": rank_ms,
         "incl_check": {"value": value_incl, "unit": UNIT, "ms_per_step": ms_incl,
                        "what": "S1-S7: + FoF labels on original and corrected positions, halo catalogues, MCC"},
