@@ -434,18 +434,16 @@ cc_status cc_build_cells(cc_ctx* c, int64_t n, const float* x, const float* y, c
         if (slab < 2.0 * c->r_pair)
             return cc_fail(c, CC_E_ARG, "x slab narrower than two ghost widths (b + 2 sqrt3 xi); use fewer GPUs");
         CC_TRY(cc::dist_exchange_ghosts(c, n, x, y, z, xh, yh, zh, gid));
-        const uint32_t* st = c->stage.p;
-        const size_t cap = (size_t)c->stage_cap;
-        const float* f = reinterpret_cast<const float*>(st);
         const double x0 = std::fmod(c->slab_lo - c->r_pair + c->p.box, c->p.box);
         choose_grid(c, c->n, slab + 2.0 * c->r_pair, x0, 0);
-        CC_TRY(cc::bin_particles(c, f, f + cap, f + 2 * cap, f + 3 * cap, f + 4 * cap, f + 5 * cap, st + 6 * cap, c->n));
-        c->in_dec[0] = f + 3 * cap;  // owned particles first, in input order
-        c->in_dec[1] = f + 4 * cap;
-        c->in_dec[2] = f + 5 * cap;
+        // owned particles read in place, the ghosts from their 7-word staging (stride stage_cap)
+        CC_TRY(cc::bin_particles(c, x, y, z, xh, yh, zh, gid, n, c->stage.p, c->stage_cap, c->n));
+        c->in_dec[0] = xh;
+        c->in_dec[1] = yh;
+        c->in_dec[2] = zh;
     } else {
         choose_grid(c, n, c->p.box, 0.0, c->p.periodic ? 1 : 0);
-        CC_TRY(cc::bin_particles(c, x, y, z, xh, yh, zh, gid, n));
+        CC_TRY(cc::bin_particles(c, x, y, z, xh, yh, zh, gid, n, nullptr, 0, n));
         c->in_dec[0] = xh;
         c->in_dec[1] = yh;
         c->in_dec[2] = zh;

@@ -33,14 +33,47 @@ struct __align__(16) Rec {
     uint32_t gid, i;
 };
 
+// the local particles: i < n_own from the caller's SoA arrays (input order), then the ghosts
+// (multi-GPU) from a small 7-word SoA staging of stride gm (x, y, z, xh, yh, zh, gid) -- the
+// owned arrays are read in place instead of being copied into a combined staging first
+struct BinSrc {
+    const float *x, *y, *z, *xh, *yh, *zh;
+    const uint32_t* gid;  // NULL: gid = input index
+    int64_t n_own;
+    const uint32_t* g7;
+    int64_t gm;
+    __device__ __forceinline__ void load(int64_t i, float& a, float& b, float& c, float& ah, float& bh,
+                                         float& ch) const {
+        if (i < n_own) {
+            a = x[i];
+            b = y[i];
+            c = z[i];
+            ah = xh[i];
+            bh = yh[i];
+            ch = zh[i];
+        } else {
+            const int64_t k = i - n_own;
+            a = __uint_as_float(g7[k]);
+            b = __uint_as_float(g7[gm + k]);
+            c = __uint_as_float(g7[2 * gm + k]);
+            ah = __uint_as_float(g7[3 * gm + k]);
+            bh = __uint_as_float(g7[4 * gm + k]);
+            ch = __uint_as_float(g7[5 * gm + k]);
+        }
+    }
+    __device__ __forceinline__ uint32_t gid_of(int64_t i) const {
+        if (i < n_own) return gid ? gid[i] : (uint32_t)i;
+        return g7[6 * gm + (i - n_own)];
+    }
+};
+
 __global__ void __launch_bounds__(BIN_THREADS)
-k_bin_key(int64_t n, const float* __restrict__ x, const float* __restrict__ y, const float* __restrict__ z,
-          const float* __restrict__ xh, const float* __restrict__ yh, const float* __restrict__ zh, Grid g,
-          float xi_f, uint32_t* __restrict__ key, uint32_t* __restrict__ rnk, uint32_t* __restrict__ count,
-          unsigned long long* __restrict__ errs) {
+k_bin_key(int64_t n, BinSrc src, Grid g, float xi_f, uint32_t* __restrict__ key, uint32_t* __restrict__ rnk,
+          uint32_t* __restrict__ count, unsigned long long* __restrict__ errs) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const float a = x[i], b = y[i], c = z[i], ah = xh[i], bh = yh[i], ch = zh[i];
+    float a, b, c, ah, bh, ch;
+    src.load(i, a, b, c, ah, bh, ch);
     unsigned int bad = 0;
     if (!(isfinite(a) && isfinite(b) && isfinite(c) && isfinite(ah) && isfinite(bh) && isfinite(ch))) bad |= 1u;
     // input contract |x_hat - x| <= xi_f per coordinate, exact in fp64
@@ -57,22 +90,15 @@ k_bin_key(int64_t n, const float* __restrict__ x, const float* __restrict__ y, c
 }
 
 __global__ void __launch_bounds__(BIN_THREADS)
-k_bin_scatter(int64_t n, const float* __restrict__ x, const float* __restrict__ y, const float* __restrict__ z,
-              const float* __restrict__ xh, const float* __restrict__ yh, const float* __restrict__ zh,
-              const uint32_t* __restrict__ gid, const uint32_t* __restrict__ key, const uint32_t* __restrict__ rnk,
+k_bin_scatter(int64_t n, BinSrc src, const uint32_t* __restrict__ key, const uint32_t* __restrict__ rnk,
               const uint32_t* __restrict__ cell_start, Rec* __restrict__ rec, uint32_t* __restrict__ slot_of) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t s = cell_start[key[i]] + rnk[i];
     slot_of[i] = s;  // provisional: k_cell_finish* rewrite only the records the in-cell sort moves
     Rec r;
-    r.x = x[i];
-    r.y = y[i];
-    r.z = z[i];
-    r.xh = xh[i];
-    r.yh = yh[i];
-    r.zh = zh[i];
-    r.gid = gid ? gid[i] : (uint32_t)i;
+    src.load(i, r.x, r.y, r.z, r.xh, r.yh, r.zh);
+    r.gid = src.gid_of(i);
     r.i = (uint32_t)i;
     // one full-sector 256-bit store (two 16-byte stores would be partial-sector writes)
     asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(rec + s), "r"(__float_as_uint(r.x)),
@@ -502,7 +528,9 @@ k_cell_finish_long(const uint32_t* __restrict__ long_list, uint64_t cap, const u
 }  // namespace
 
 cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* z, const float* xh,
-                        const float* yh, const float* zh, const uint32_t* gid, int64_t n) {
+                        const float* yh, const float* zh, const uint32_t* gid, int64_t n_own, const uint32_t* g7,
+                        int64_t gm, int64_t n) {
+    const BinSrc src{x, y, z, xh, yh, zh, gid, n_own, g7, gm};
     const int64_t nc = c->ncell;
     const size_t n1 = (size_t)std::max<int64_t>(n, 1);
     CC_TRY(cc_ensure(c, c->key, n1, "key"));
@@ -523,8 +551,8 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
     const unsigned nb = (unsigned)((n + BIN_THREADS - 1) / BIN_THREADS);
     if (n > 0) {
         int tok = cc_prof_begin(c, "K1_key");
-        CCL(c, k_bin_key<<<nb, BIN_THREADS, 0, c->stream>>>(n, x, y, z, xh, yh, zh, c->g, c->th.xi_f, c->key.p,
-                                                             c->rnk.p, c->cell_count.p, c->counters.p));
+        CCL(c, k_bin_key<<<nb, BIN_THREADS, 0, c->stream>>>(n, src, c->g, c->th.xi_f, c->key.p, c->rnk.p,
+                                                             c->cell_count.p, c->counters.p));
         cc_prof_end(c, tok);
         CC_CUDA(c, cudaGetLastError());
     }
@@ -535,8 +563,8 @@ cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* 
         const uint64_t cap = (uint64_t)std::max<int64_t>(std::min<int64_t>(nc, n), 1);  // >= crowded cells
         CC_TRY(cc_ensure(c, c->scratch_u32, (size_t)cap, "crowded cells"));
         int tok = cc_prof_begin(c, "K1_scatter");
-        CCL(c, k_bin_scatter<<<nb, BIN_THREADS, 0, c->stream>>>(n, x, y, z, xh, yh, zh, gid, c->key.p, c->rnk.p,
-                                                                 c->cell_start.p, rec, c->slot_of.p));
+        CCL(c, k_bin_scatter<<<nb, BIN_THREADS, 0, c->stream>>>(n, src, c->key.p, c->rnk.p, c->cell_start.p, rec,
+                                                                 c->slot_of.p));
         cc_prof_end(c, tok);
         unsigned long long* nl = reinterpret_cast<unsigned long long*>(c->scratch_u64.p);
         int t2 = cc_prof_begin(c, "K1_finish");

@@ -824,7 +824,8 @@ cc_status editable_list(cc_ctx* c, int64_t* e_all);
 cc_status scan_editables(cc_ctx* c, int64_t e_all, unsigned long long* totals_dev);
 cc_status rows_resolve(cc_ctx* c, const unsigned long long* totals_h);
 cc_status bin_particles(cc_ctx* c, const float* x, const float* y, const float* z, const float* xh,
-                        const float* yh, const float* zh, const uint32_t* gid, int64_t n);
+                        const float* yh, const float* zh, const uint32_t* gid, int64_t n_own, const uint32_t* g7,
+                        int64_t gm, int64_t n);
 cc_status pairs_count(cc_ctx* c);
 cc_status fof_base_build(cc_ctx* c);
 cc_status read_near_count(cc_ctx* c);

@@ -33,24 +33,82 @@ constexpr int DT = 256;
 
 inline ncclComm_t comm(cc_ctx* c) { return static_cast<ncclComm_t>(c->nccl_comm); }
 
-// flag owned particles inside the lower (dir 0) / upper (dir 1) ghost shell of the slab
-__global__ void k_shell_flags(int64_t n, const float* __restrict__ x, double lo, double hi, double gw, double L,
-                              uint32_t* __restrict__ f0, uint32_t* __restrict__ f1, unsigned long long* errs) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double xv = (double)x[i];
-    if (!(xv >= lo && xv < hi)) atomicOr(errs, 4ull);  // not in this rank's slab
-    f0[i] = (xv < lo + gw) ? 1u : 0u;
-    f1[i] = (xv >= hi - gw) ? 1u : 0u;
+
+// both shell lists in ONE pass over x (decoupled look-back, cc_internal.cuh lookback_warp0):
+// list0 = owned particles within the ghost width of the lower face, list1 = of the upper face,
+// each in ascending input order; a thread owns SL_I consecutive particles.  Replaces a flag pass,
+// two device-wide scans and two compactions.  The two running counts share one
+// look-back word (31 bits each: counts < 2^30).
+constexpr int SL_T = 256, SL_I = 16, SL_TILE = SL_T * SL_I;
+
+__global__ void __launch_bounds__(SL_T)
+k_shell_lists(int64_t n, const float* __restrict__ x, double lo, double hi, double gw, uint32_t* __restrict__ list0,
+              uint32_t* __restrict__ list1, unsigned long long* __restrict__ status, unsigned int* __restrict__ ticket,
+              unsigned long long* __restrict__ out /* [0] error bits, [1] n0, [2] n1 */) {
+    __shared__ unsigned int tile_sh;
+    __shared__ unsigned long long base_sh;
+    __shared__ unsigned long long wsum[SL_T / 32];
+    if (threadIdx.x == 0) tile_sh = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const unsigned int tile = tile_sh;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i0 = (int64_t)tile * SL_TILE + (int64_t)threadIdx.x * SL_I;
+    uint32_t m0 = 0u, m1 = 0u;
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < SL_I; k++) {
+        const int64_t i = i0 + k;
+        if (i < n) {
+            const double xv = (double)x[i];
+            bad |= !(xv >= lo && xv < hi);  // not in this rank's slab
+            m0 |= (xv < lo + gw ? 1u : 0u) << k;
+            m1 |= (xv >= hi - gw ? 1u : 0u) << k;
+        }
+    }
+    if (bad) atomicOr(&out[0], 4ull);
+    const unsigned long long cnt = (unsigned long long)__popc(m0) | ((unsigned long long)__popc(m1) << 32);
+    unsigned long long inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    unsigned long long wex = 0ull, tot = 0ull;
+#pragma unroll
+    for (int k = 0; k < SL_T / 32; k++) {
+        wex += k < w ? wsum[k] : 0ull;
+        tot += wsum[k];
+    }
+    const unsigned long long M31 = (1ull << 31) - 1ull;
+    if (threadIdx.x < 32) {
+        const unsigned long long packed = (tot & 0xFFFFFFFFull) | ((tot >> 32) << 31);
+        const unsigned long long ex = lookback_warp0(status, tile, packed);
+        if (lane == 0) {
+            base_sh = ex;
+            if ((int64_t)(tile + 1) * SL_TILE >= n) {  // the last tile
+                out[1] = (ex & M31) + (tot & 0xFFFFFFFFull);
+                out[2] = (ex >> 31) + (tot >> 32);
+            }
+        }
+    }
+    __syncthreads();
+    const unsigned long long my = wex + inc - cnt;
+    unsigned long long q0 = (base_sh & M31) + (my & 0xFFFFFFFFull);
+    unsigned long long q1 = (base_sh >> 31) + (my >> 32);
+    while (m0) {
+        const int k = __ffs(m0) - 1;
+        m0 &= m0 - 1u;
+        list0[q0++] = (uint32_t)(i0 + k);
+    }
+    while (m1) {
+        const int k = __ffs(m1) - 1;
+        m1 &= m1 - 1u;
+        list1[q1++] = (uint32_t)(i0 + k);
+    }
 }
 
-// list[pos[i]] = i for flagged i (pos = exclusive scan of the flags)
-__global__ void k_compact_list(int64_t n, const uint32_t* __restrict__ f, const uint32_t* __restrict__ pos,
-                               uint32_t* __restrict__ list) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    if (f[i]) list[pos[i]] = (uint32_t)i;
-}
 
 // pack particles of a list as 7 SoA words (x, y, z, xh, yh, zh, gid)
 __global__ void k_pack7(int64_t m, const uint32_t* __restrict__ list, const float* __restrict__ x,
@@ -69,21 +127,6 @@ __global__ void k_pack7(int64_t m, const uint32_t* __restrict__ list, const floa
     buf[6 * m + k] = gid ? gid[i] : i;
 }
 
-// copy owned arrays into the local staging (7 SoA arrays of capacity cap)
-__global__ void k_stage_owned(int64_t n, int64_t cap, const float* __restrict__ x, const float* __restrict__ y,
-                              const float* __restrict__ z, const float* __restrict__ xh, const float* __restrict__ yh,
-                              const float* __restrict__ zh, const uint32_t* __restrict__ gid, uint32_t gid_base,
-                              uint32_t* __restrict__ st) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    st[0 * cap + i] = __float_as_uint(x[i]);
-    st[1 * cap + i] = __float_as_uint(y[i]);
-    st[2 * cap + i] = __float_as_uint(z[i]);
-    st[3 * cap + i] = __float_as_uint(xh[i]);
-    st[4 * cap + i] = __float_as_uint(yh[i]);
-    st[5 * cap + i] = __float_as_uint(zh[i]);
-    st[6 * cap + i] = gid ? gid[i] : gid_base + (uint32_t)i;
-}
 
 // received block of m particles -> staging rows [off, off + m)
 __global__ void k_unstage(int64_t m, int64_t cap, int64_t off, const uint32_t* __restrict__ buf,
@@ -116,12 +159,18 @@ __global__ void k_ghost_requests(int64_t n, const uint32_t* __restrict__ eidx, c
 }
 
 // owner side: requested shell-list index -> owned editable index
+// slot_of may still hold provisional slots (bin.cu ensure_slot_of: completed on first use); the
+// few shell particles asked for here take the two-step lookup fin[slot_of[i]] instead of
+// completing the whole map inside S2-S3
 __global__ void k_map_requests(int64_t m, const uint32_t* __restrict__ req, const uint32_t* __restrict__ shell,
-                               const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ eidx,
-                               uint32_t e_own, uint32_t* __restrict__ send_e, unsigned long long* errs) {
+                               const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ fin, int fixed,
+                               const uint32_t* __restrict__ eidx, uint32_t e_own, uint32_t* __restrict__ send_e,
+                               unsigned long long* errs) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= m) return;
-    const uint32_t e = eidx[slot_of[shell[req[k]]]];
+    uint32_t sl = slot_of[shell[req[k]]];
+    if (!fixed) sl = fin[sl];
+    const uint32_t e = eidx[sl];
     if (e >= e_own) atomicOr(errs, 8ull);  // must be an owned editable
     send_e[k] = e;
 }
@@ -366,30 +415,26 @@ cc_status dist_exchange_ghosts(cc_ctx* c, int64_t n, const float* x, const float
                                const float* yh, const float* zh, const uint32_t* gid) {
     const double gw = c->r_pair;  // ghost width delta (1 + 1e-5)
     const size_t n1 = (size_t)std::max<int64_t>(n, 1);
-    CC_TRY(cc_ensure(c, c->dflag[0], n1, "shell flags"));
-    CC_TRY(cc_ensure(c, c->dflag[1], n1, "shell flags"));
-    CC_TRY(cc_ensure(c, c->dpos[0], n1 + 1, "shell positions"));
-    CC_TRY(cc_ensure(c, c->dpos[1], n1 + 1, "shell positions"));
+    CC_TRY(cc_ensure(c, c->shell[0], n1, "shell list"));
+    CC_TRY(cc_ensure(c, c->shell[1], n1, "shell list"));
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
     CC_CUDA(c, cudaMemsetAsync(c->counters.p, 0, 16 * sizeof(unsigned long long), c->stream));
-    const unsigned nb = (unsigned)((n + DT - 1) / DT);
-    if (n > 0)
-        CCL(c, k_shell_flags<<<nb, DT, 0, c->stream>>>(n, x, c->slab_lo, c->slab_hi, gw, c->p.box, c->dflag[0].p,
-                                                       c->dflag[1].p, c->counters.p));
-    uint64_t* tot = reinterpret_cast<uint64_t*>(c->counters.p + 1);
-    CC_TRY(scan_u32_to_u32(c, c->dflag[0].p, c->dpos[0].p, n, tot));
-    CC_TRY(scan_u32_to_u32(c, c->dflag[1].p, c->dpos[1].p, n, tot + 1));
+    if (n > 0) {
+        const int64_t nt = (n + SL_TILE - 1) / SL_TILE;
+        CC_TRY(cc_ensure(c, c->codec_status, (size_t)nt + 2, "look-back status"));
+        unsigned long long* st = c->codec_status.p;
+        CC_CUDA(c, cudaMemsetAsync(st, 0, (size_t)(nt + 1) * sizeof(unsigned long long), c->stream));
+        CCL(c, k_shell_lists<<<(unsigned)nt, SL_T, 0, c->stream>>>(n, x, c->slab_lo, c->slab_hi, gw, c->shell[0].p,
+                                                                   c->shell[1].p, st,
+                                                                   reinterpret_cast<unsigned int*>(st + nt),
+                                                                   c->counters.p));
+    }
     CC_CUDA(c, cudaMemcpyAsync(c->h_counters, c->counters.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                c->stream));
     CC_CUDA(c, cudaStreamSynchronize(c->stream));
     if (c->h_counters[0] & 4ull) return cc_fail(c, CC_E_DATA, "an owned particle lies outside this rank's x slab");
-    int64_t ns[2] = {(int64_t)(c->h_counters[1] & 0xFFFFFFFFull), (int64_t)(c->h_counters[2] & 0xFFFFFFFFull)};
-    for (int d = 0; d < 2; d++) {
-        CC_TRY(cc_ensure(c, c->shell[d], (size_t)std::max<int64_t>(ns[d], 1), "shell list"));
-        if (n > 0)
-            CCL(c, k_compact_list<<<nb, DT, 0, c->stream>>>(n, c->dflag[d].p, c->dpos[d].p, c->shell[d].p));
-        c->n_shell[d] = ns[d];
-    }
+    int64_t ns[2] = {(int64_t)c->h_counters[1], (int64_t)c->h_counters[2]};
+    for (int d = 0; d < 2; d++) c->n_shell[d] = ns[d];
     // counts: send dir0 -> left, dir1 -> right; receive from right (their dir0), from left (their dir1)
     CC_TRY(cc_ensure(c, c->dcnt, 4, "dist counts"));
     {
@@ -408,14 +453,14 @@ cc_status dist_exchange_ghosts(cc_ctx* c, int64_t n, const float* x, const float
     }
     const int64_t nl = n + c->n_from_left + c->n_from_right;
     if (nl >= MAX_LOCAL) return cc_fail(c, CC_E_DATA, "local particles beyond the 2^30 index space");
-    const int64_t cap = std::max<int64_t>(nl, 1);
-    CC_TRY(cc_ensure(c, c->stage, (size_t)(7 * cap), "local staging"));
+    // ghost staging only (7 SoA words, stride cap = ghost count): binning reads the owned
+    // particles from the caller's arrays in place
+    const int64_t cap = std::max<int64_t>(c->n_from_left + c->n_from_right, 1);
+    CC_TRY(cc_ensure(c, c->stage, (size_t)(7 * cap), "ghost staging"));
     for (int d = 0; d < 2; d++)
         CC_TRY(cc_ensure(c, c->sbuf7[d], (size_t)std::max<int64_t>(7 * ns[d], 1), "ghost send buffer"));
     CC_TRY(cc_ensure(c, c->rbuf7[0], (size_t)std::max<int64_t>(7 * c->n_from_left, 1), "ghost recv buffer"));
     CC_TRY(cc_ensure(c, c->rbuf7[1], (size_t)std::max<int64_t>(7 * c->n_from_right, 1), "ghost recv buffer"));
-    if (n > 0)
-        CCL(c, k_stage_owned<<<nb, DT, 0, c->stream>>>(n, cap, x, y, z, xh, yh, zh, gid, 0u, c->stage.p));
     for (int d = 0; d < 2; d++)
         if (ns[d] > 0)
             CCL(c, k_pack7<<<(unsigned)((ns[d] + DT - 1) / DT), DT, 0, c->stream>>>(ns[d], c->shell[d].p, x, y, z, xh, yh,
@@ -429,11 +474,11 @@ cc_status dist_exchange_ghosts(cc_ctx* c, int64_t n, const float* x, const float
         CC_TRY(comm_recv(c, c->rbuf7[0].p, (size_t)(7 * c->n_from_left), CT_U32, c->left));
     CC_TRY(comm_group_end(c));
     if (c->n_from_left > 0)
-        CCL(c, k_unstage<<<(unsigned)((c->n_from_left + DT - 1) / DT), DT, 0, c->stream>>>(c->n_from_left, cap, n,
+        CCL(c, k_unstage<<<(unsigned)((c->n_from_left + DT - 1) / DT), DT, 0, c->stream>>>(c->n_from_left, cap, 0,
                                                                                           c->rbuf7[0].p, c->stage.p));
     if (c->n_from_right > 0)
         CCL(c, k_unstage<<<(unsigned)((c->n_from_right + DT - 1) / DT), DT, 0, c->stream>>>(
-                   c->n_from_right, cap, n + c->n_from_left, c->rbuf7[1].p, c->stage.p));
+                   c->n_from_right, cap, c->n_from_left, c->rbuf7[1].p, c->stage.p));
     CC_CUDA(c, cudaGetLastError());
     c->stage_cap = cap;
     c->n = nl;
@@ -522,7 +567,6 @@ static cc_status dist_setup_peer(cc_ctx* c) {
 }
 
 cc_status dist_setup_refresh(cc_ctx* c) {
-    CC_TRY(ensure_slot_of(c));
     const int64_t n = c->n;
     CC_TRY(cc_ensure(c, c->counters, 16, "counters"));
     const int64_t ng = std::max<int64_t>(c->E_all - c->E, 1);
@@ -574,8 +618,8 @@ cc_status dist_setup_refresh(cc_ctx* c) {
     for (int d = 0; d < 2; d++)
         if (c->n_ref_send[d] > 0)
             CCL(c, k_map_requests<<<(unsigned)((c->n_ref_send[d] + DT - 1) / DT), DT, 0, c->stream>>>(
-                       c->n_ref_send[d], c->sreq[d].p, c->shell[d].p, c->slot_of.p, c->eidx.p, (uint32_t)c->E, c->send_e[d].p,
-                       c->counters.p + 14));
+                       c->n_ref_send[d], c->sreq[d].p, c->shell[d].p, c->slot_of.p, c->rnk.p, c->slot_of_valid ? 1 : 0,
+                       c->eidx.p, (uint32_t)c->E, c->send_e[d].p, c->counters.p + 14));
     CC_CUDA(c, cudaMemcpyAsync(c->h_counters + 14, c->counters.p + 14, sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, c->stream));
     CC_CUDA(c, cudaStreamSynchronize(c->stream));
