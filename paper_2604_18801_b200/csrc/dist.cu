@@ -25,13 +25,6 @@ namespace {
 
 constexpr int DT = 256;
 
-#define CC_NCCL(c, expr)                                                                          \
-    do {                                                                                          \
-        ncclResult_t r_ = (expr);                                                                 \
-        if (r_ != ncclSuccess) return cc_fail((c), CC_E_NCCL, std::string(ncclGetErrorString(r_)) + " at " #expr); \
-    } while (0)
-
-inline ncclComm_t comm(cc_ctx* c) { return static_cast<ncclComm_t>(c->nccl_comm); }
 
 
 // both shell lists in ONE pass over x (decoupled look-back, cc_internal.cuh lookback_warp0):
@@ -274,18 +267,6 @@ __global__ void __launch_bounds__(256) k_peer_exchange(PeerArgs a) {
     __threadfence();
 }
 
-// unpack this iteration's parity of a receive area into the ghost slots
-__global__ void k_peer_unpack(int64_t m, const uint32_t* __restrict__ recv_e, const Ctl* __restrict__ ctl,
-                              float4* __restrict__ p0, float4* __restrict__ p1, const float4* __restrict__ area,
-                              int64_t cap) {
-    if (ctl->done) return;
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= m) return;
-    const int t = ctl->t + 1;
-    float4* dst = (t & 1) ? p1 : p0;
-    dst[recv_e[k]] = __ldcv(area + (size_t)(t & 1) * cap + k);
-}
-
 // global stop decision after the allreduce of (active, loss)
 __global__ void k_decide(Ctl* ctl, const unsigned long long* __restrict__ red, int stop_mode, double eps_loss,
                          int t_max, long long* trace_a, double* trace_l, long long* trace_v) {
@@ -311,6 +292,53 @@ __global__ void k_decide(Ctl* ctl, const unsigned long long* __restrict__ red, i
         ctl->t_res = t;
     }
     ctl->t = t;
+}
+
+// the peer path's per-iteration tail after k_peer_exchange in ONE launch: unpack both receive
+// areas into the ghost slots, then the last block (ticket) applies the stop rule like k_decide.
+// Two graph nodes fewer per PGD iteration (C5 at R = 4: 662 iterations).  ctl->ticket is free
+// here: k_pgd's last block left it at 0, and this kernel's last block resets it.
+__global__ void __launch_bounds__(256)
+k_peer_finish(int64_t m0, int64_t m1, const uint32_t* __restrict__ recv0, const uint32_t* __restrict__ recv1, Ctl* ctl,
+              float4* __restrict__ p0, float4* __restrict__ p1, const float4* __restrict__ area0, int64_t cap0,
+              const float4* __restrict__ area1, int64_t cap1, const unsigned long long* __restrict__ red,
+              int stop_mode, double eps_loss, int t_max, long long* trace_a, double* trace_l, long long* trace_v) {
+    if (ctl->done) return;
+    const int t = ctl->t + 1;
+    float4* dst = (t & 1) ? p1 : p0;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < m0) dst[recv0[k]] = __ldcv(area0 + (size_t)(t & 1) * cap0 + k);
+    else if (k < m0 + m1) dst[recv1[k - m0]] = __ldcv(area1 + (size_t)(t & 1) * cap1 + (k - m0));
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&ctl->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    ctl->ticket = 0u;
+    const unsigned long long tu = red[0];
+    const double td = lfx_value(red + 2);  // exact integer sums over ranks: rank-count invariant
+    const unsigned long long tv = red[1];
+    ctl->active = tu;
+    ctl->loss = td;
+    ctl->violated = tv;
+    if (trace_a) {
+        trace_a[t - 1] = (long long)tu;
+        trace_l[t - 1] = td;
+        trace_v[t - 1] = (long long)tv;
+    }
+    if (stop_rule(stop_mode, tu, lfx_le(red + 2, eps_loss), tv)) {
+        ctl->done = 1;
+        ctl->t_res = t - 1;
+        ctl->converged = 1;
+    } else if (t >= t_max) {
+        ctl->done = 1;
+        ctl->t_res = t;
+    }
+    ctl->t = t;
+    __threadfence();
 }
 
 // FoF label exchange: labels of the shell lists (owner side) ...
@@ -656,16 +684,15 @@ cc_status dist_iter_tail(cc_ctx* c, const float4* p0, const float4* p1) {
         const int64_t ns = std::max(c->n_ref_send[0], c->n_ref_send[1]);
         const unsigned nb = (unsigned)std::min<int64_t>(std::max<int64_t>((ns + 255) / 256, 1), 148);
         CCL(c, k_peer_exchange<<<nb, 256, 0, c->stream>>>(a));
+        const int64_t mr = c->n_ref_recv[0] + c->n_ref_recv[1];
+        const float4* ar[2];
         for (int d = 0; d < 2; d++)
-            if (c->n_ref_recv[d] > 0)
-                CCL(c, k_peer_unpack<<<(unsigned)((c->n_ref_recv[d] + DT - 1) / DT), DT, 0, c->stream>>>(
-                           c->n_ref_recv[d], c->recv_e[d].p, c->ctl.p, const_cast<float4*>(p0),
-                           const_cast<float4*>(p1),
-                           reinterpret_cast<const float4*>(static_cast<unsigned char*>(c->pm_local) +
-                                                           pm_area_off(d, c->pm_cap)),
-                           c->pm_cap[d]));
-        CCL(c, k_decide<<<1, 1, 0, c->stream>>>(c->ctl.p, c->red_sum.p, c->p.stop_mode, c->p.eps_loss, c->p.t_max,
-                                                c->trace_a.p, c->trace_l.p, c->trace_v.p));
+            ar[d] = reinterpret_cast<const float4*>(static_cast<unsigned char*>(c->pm_local) + pm_area_off(d, c->pm_cap));
+        CCL(c, k_peer_finish<<<(unsigned)std::max<int64_t>((mr + 255) / 256, 1), 256, 0, c->stream>>>(
+                   c->n_ref_recv[0], c->n_ref_recv[1], c->recv_e[0].p, c->recv_e[1].p, c->ctl.p,
+                   const_cast<float4*>(p0), const_cast<float4*>(p1), ar[0], c->pm_cap[0], ar[1], c->pm_cap[1],
+                   c->red_sum.p, c->p.stop_mode, c->p.eps_loss, c->p.t_max, c->trace_a.p, c->trace_l.p,
+                   c->trace_v.p));
         return CC_OK;
     }
     for (int d = 0; d < 2; d++)
