@@ -1078,11 +1078,14 @@ __global__ void k_output_edits(uint32_t e_own, const uint32_t* __restrict__ slot
                                float* __restrict__ zo) {
     const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= e_own) return;
-    const uint32_t i = __float_as_uint(dec4[slotE[e]].w);  // input index
+    const float4 d = dec4[slotE[e]];
+    const uint32_t i = __float_as_uint(d.w);  // input index
     const float4 r = res[e];
-    xo[i] = r.x;
-    yo[i] = r.y;
-    zo[i] = r.z;
+    // only the coordinates PGD changed (bitwise): the copy already wrote the others, and most
+    // editables never move at small xi (each skipped store is a DRAM read-modify-write saved)
+    if (__float_as_uint(r.x) != __float_as_uint(d.x)) xo[i] = r.x;
+    if (__float_as_uint(r.y) != __float_as_uint(d.y)) yo[i] = r.y;
+    if (__float_as_uint(r.z) != __float_as_uint(d.z)) zo[i] = r.z;
 }
 
 PgdArgs make_args(cc_ctx* c, int count_only) {
