@@ -1253,12 +1253,14 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
     const bool tail_on = use_tail && tail_blocks > 0;
     const int k3_per_iter = tail_on ? 4 : 3;  // k_select (+ k_tail) + k_pgd<0> + k_pgd<1>
     PgdArgs a = make_args(c, 0);
-    // initial statistics of P_hat^(0) for the report
-    PgdArgs a0 = make_args(c, 1);
-    CCL(c, k_pgd<0><<<nb0, PGD_THREADS, 0, c->stream>>>(a0));
-    CCL(c, k_pgd<1><<<nb1, PGD_THREADS, 0, c->stream>>>(a0));
-    CC_CUDA(c, cudaGetLastError());
-    {
+    // initial statistics of P_hat^(0) for the report: iteration 1 evaluates exactly that state
+    // (a full sweep) and records them in the trace (entry 0); a separate counting pass only
+    // when no iteration runs
+    if (tmax <= 0) {
+        PgdArgs a0 = make_args(c, 1);
+        CCL(c, k_pgd<0><<<nb0, PGD_THREADS, 0, c->stream>>>(a0));
+        CCL(c, k_pgd<1><<<nb1, PGD_THREADS, 0, c->stream>>>(a0));
+        CC_CUDA(c, cudaGetLastError());
         double al[3];
         CC_TRY(global_check(c, al));
         info->active0 = (int64_t)al[0];
@@ -1411,23 +1413,45 @@ cc_status pgd_run(cc_ctx* c, cc_corr_info* info) {
         }
     }
     c->last_iters = iters;
-    // final evaluation of the returned state
+    const bool stopped = tmax > 0 && c->h_ctl->converged != 0;  // the stop rule held at state iters
     c->h_ctl->t_res = iters;
     CC_CUDA(c, cudaMemcpyAsync(&c->ctl.p->t_res, &c->h_ctl->t_res, sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    PgdArgs af = make_args(c, 1);
-    int tok = cc_prof_begin(c, "K3_final_check");
-    CCL(c, k_pgd<0><<<nb0, PGD_THREADS, 0, c->stream>>>(af));
-    CCL(c, k_pgd<1><<<nb1, PGD_THREADS, 0, c->stream>>>(af));
-    cc_prof_end(c, tok);
-    CC_CUDA(c, cudaGetLastError());
     double al[3];
     bool le = false;
-    CC_TRY(global_check(c, al, &le));
+    if (tmax > 0) {  // trace entry s = the statistics of state s (read by iteration s + 1)
+        long long ta[2];
+        double tl[2];
+        long long tv[2];
+        const int last = stopped ? iters : 0;
+        CC_CUDA(c, cudaMemcpyAsync(&ta[0], c->trace_a.p, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaMemcpyAsync(&tl[0], c->trace_l.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaMemcpyAsync(&tv[0], c->trace_v.p, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaMemcpyAsync(&ta[1], c->trace_a.p + last, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaMemcpyAsync(&tl[1], c->trace_l.p + last, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaMemcpyAsync(&tv[1], c->trace_v.p + last, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CC_CUDA(c, cudaStreamSynchronize(c->stream));
+        info->active0 = ta[0];
+        info->loss0 = tl[0];
+        info->violated0 = tv[0];
+        al[0] = (double)ta[1];
+        al[1] = tl[1];
+        al[2] = (double)tv[1];
+    }
+    if (!stopped) {  // T_max (or no iteration): evaluate the returned state
+        PgdArgs af = make_args(c, 1);
+        int tok = cc_prof_begin(c, "K3_final_check");
+        CCL(c, k_pgd<0><<<nb0, PGD_THREADS, 0, c->stream>>>(af));
+        CCL(c, k_pgd<1><<<nb1, PGD_THREADS, 0, c->stream>>>(af));
+        cc_prof_end(c, tok);
+        CC_CUDA(c, cudaGetLastError());
+        CC_TRY(global_check(c, al, &le));
+    }
     info->iterations = iters;
     info->active_final = (int64_t)al[0];
     info->loss_final = al[1];
     info->violated_final = (int64_t)al[2];
-    info->converged = stop_rule(c->p.stop_mode, (unsigned long long)al[0], le, (unsigned long long)al[2]) ||
+    info->converged = stopped ||
+                      stop_rule(c->p.stop_mode, (unsigned long long)al[0], le, (unsigned long long)al[2]) ||
                       (c->p.stop_mode == CC_STOP_NONE && al[0] == 0.0);
     c->final_active = (unsigned long long)al[0];
     c->final_loss = al[1];
