@@ -413,7 +413,10 @@ __device__ __forceinline__ bool process_batch(const PgdArgs& a, K3Ctx& k, const 
     __syncwarp();
     bool any_active = false;
     float gx = 0.0f, gy = 0.0f, gz = 0.0f;
-    for (uint32_t c = 0; c < (KIND == 1 ? 0u : T); c += CH) {
+    const uint32_t tflat = KIND == 1 ? 0u : T;  // KIND 1 walks every row per lane (below)
+#pragma nv_diag_suppress 186  // c < 0u for KIND 1: the loop is meant to vanish there
+    for (uint32_t c = 0; c < tflat; c += CH) {
+#pragma nv_diag_default 186
         // which lane owns each position of this chunk
         const uint32_t f0 = max(off, c), f1 = min(off + slen, c + CH);
         for (uint32_t f = f0; f < f1; f++) ws.seg[f - c] = (unsigned char)lane;

@@ -15,7 +15,6 @@ struct VU32 {
     __device__ static VU32 zero() { return {0u}; }
     __device__ VU32 operator+(const VU32& o) const { return {a + o.a}; }
     __device__ VU32 shfl_up(int d) const { return {__shfl_up_sync(0xffffffffu, a, d)}; }
-    __device__ VU32 shfl(int src) const { return {__shfl_sync(0xffffffffu, a, src)}; }
 };
 
 // degree scan value, per row-length class k (K3 work classes, cc_internal.cuh row_class):
