@@ -39,9 +39,9 @@ constexpr int PGD_MAX_BLOCKS = 148 * 8;
 constexpr int NSTAT = LFX_STATS + 5;
 constexpr int NB = 4;         // row entries per lane per chunk
 constexpr int CH = 32 * NB;   // flattened row entries per warp chunk
-constexpr uint32_t TAIL_ENTER = 4096;  // k_tail takes over when a selected list is this small
-constexpr uint32_t TAIL_CAP = 16384;   // ... and hands back when a list would exceed this
-constexpr int TAIL_BLOCKS = 64;        // k_tail's co-resident blocks
+constexpr uint32_t TAIL_ENTER = 32768;  // k_tail takes over when a selected list is this small
+constexpr uint32_t TAIL_CAP = 131072;  // ... and hands back when a list would exceed this
+constexpr int TAIL_BLOCKS = 148;       // k_tail's co-resident blocks
 
 struct WarpSh {               // per-warp staging of K3's flattened row evaluation
     float4 t[CH];             // term (px, py, pz, kind bits) of each chunk entry
