@@ -1009,7 +1009,7 @@ __global__ void k_ctl_reset(Ctl* ctl) {
     ctl->loss = 0.0;
     for (int k = 0; k < 14; k++) ctl->acc[k] = 0ull;
     ctl->sel = 0;
-    ctl->bld = 0;
+    ctl->bld = 1;  // iteration 1 (a full sweep) builds the bitmaps: iteration 2 already selects
     ctl->nsel = 0u;
     ctl->nsel_l = 0u;
     ctl->tail_nn = 0u;
